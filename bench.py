@@ -1,0 +1,484 @@
+#!/usr/bin/env python
+"""Benchmark of the SRP-map hot path (BASELINE.json metric: SRP maps/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2] [--variant sspi] [--no-variants] [--no-cpu-baseline]
+
+A step is one pass of the hot path over one batch of F frames of the workload
+(cfg2 by default: BASELINE.json configs[1], F = 1000 frames per GPU):
+    samples --(fused STFT + GCC/PHAT + iFFT sampling kernel)--> xi
+            --(SSPI ELL SpMM kernel with fused argmax)--> z [F][J] + argmax [F]
+For N > 1 (torchrun, one process per GPU) each rank maps its own contiguous
+block of frames (weak scaling) and the per-frame argmax keys are all-gathered
+over NCCL inside the timed region.  `value` = frames of all ranks / max-over-ranks
+device time.  `e2e` repeats the step through the public API from pinned host
+samples (H2D inside the timed region) and reads the argmax indices back (D2H).
+
+`--impl reference` times the reference algorithm on the host cores instead
+(the float64 NumPy port in oracle/, rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "srp_maps_per_sec"
+UNIT = "maps/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--frames", type=int, default=0, help="frames per GPU per step (default: config)")
+    ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "si"])
+    ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
+    ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------- roofline inputs
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic(workload: str, kernel: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------------- scene / operators
+
+def build_scene(args, total_frames):
+    from paper_2306_08514_b200 import workloads
+    return workloads.make(args.workload, num_frames=total_frames)
+
+
+def fit_operator(wl, variant, args):
+    import paper_2306_08514_b200 as s
+    if variant in ("sspi", "si", "slri"):
+        interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
+        if variant == "si":
+            return interp
+        if variant == "slri":
+            return s.truncate_low_rank(interp, args.rank_r)
+        keep = s.resolve_sparsity(args.nnz, wl.grid.num_points, wl.pairs.num_pairs, interp.matrix.size)
+        return s.truncate_sparse(interp, keep)
+    srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 36)
+    if variant == "conv":
+        return srp
+    return s.truncate_srp_matrix(srp, args.rank_r)
+
+
+def algorithmic_bytes(wl, variant, frames, op):
+    """Per-launch algorithmic bytes of the dominant kernels."""
+    m, hop = wl.array.num_mics, wl.frame.hop
+    p, b, j = wl.pairs.num_pairs, wl.frame.num_bins, wl.grid.num_points
+    s_tot = wl.spec.total_samples
+    out = {"frontend": frames * (4 * m * hop + (4 * s_tot if variant in ("sspi", "slri", "si") else 8 * p * b))}
+    if variant in ("sspi", "si"):
+        nnz_stored = getattr(op, "num_kept", None)
+        nnz_stored = nnz_stored if nnz_stored is not None else j * s_tot
+        out["map"] = frames * (4 * s_tot + 4 * j) + 8 * nnz_stored
+    elif variant == "slri":
+        r = op.tall.shape[1]
+        out["map"] = frames * (4 * s_tot + 4 * j) + 4 * (j * r + r * s_tot)
+    elif variant == "lr":
+        r = op.tall.shape[1]
+        out["map"] = frames * (8 * p * b + 4 * j) + 8 * r * (j + p * b)
+    return out
+
+
+def conv_flops(wl, frames):
+    return 4.0 * wl.grid.num_points * wl.pairs.num_pairs * wl.frame.num_bins * frames
+
+
+# --------------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_08514_b200 as s
+    from paper_2306_08514_b200 import _native, distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    wl0 = build_scene(args, 1)
+    per_gpu = args.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000,
+                              "cfg5": 1024}[args.workload]
+    total = per_gpu * world
+    wl = build_scene(args, total)
+    first, count = D.partition(total, world, rank)
+    hop, flen = wl.frame.hop, wl.frame.frame_len
+    host_slice = np.ascontiguousarray(wl.samples[:, first * hop:(first + count - 1) * hop + flen])
+    pinned = torch.from_numpy(host_slice).pin_memory()
+    x_dev = pinned.to(dev)
+    frames = range(0, count)
+    del wl0
+
+    def make_step(variant, op):
+        if variant in ("sspi", "si", "slri"):
+            mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
+
+            def step(x):
+                xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, frames)
+                return mapf(op, xi, argmax=True)
+        elif variant == "lr":
+            def step(x):
+                return s.lr_map(op, s.gcc_frames(x, wl.frame, wl.pairs, frames), argmax=True)
+        else:
+            def step(x):
+                return s.srp_map_exact(op, s.gcc_frames(x, wl.frame, wl.pairs, frames), argmax=True)
+        return step
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def time_steps(step, steps, warmup, gather=True):
+        for _ in range(warmup):
+            z, idx = step(x_dev)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = []
+        launches0 = _native.launch_count()
+        for _ in range(steps):
+            flush.zero_()                          # L2 flush between timed iterations
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            z, idx = step(x_dev)
+            if world > 1 and gather:
+                keys_all = D.gather_frame_keys(idx, total)
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        launches = _native.launch_count() - launches0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        return ms, launches, z, idx
+
+    # ---- headline variant
+    op = fit_operator(wl, args.variant, args)
+    step = make_step(args.variant, op)
+    clocks = ClockSampler(local)
+    with clocks:
+        ms_total, launches, z, idx = time_steps(step, args.steps, args.warmup)
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms_t.item()) / args.steps
+    value = total / (ms_per_step / 1e3)
+    launches_per_step = launches / args.steps
+
+    # ---- per-kernel times for the roofline (same stream, CUDA events)
+    def kernel_times(reps=10):
+        tf, tm = [], []
+        for _ in range(reps):
+            flush.zero_()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            if args.variant in ("sspi", "si", "slri"):
+                xi = s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames)
+                e[1].record()
+                {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[args.variant](op, xi, argmax=True)
+            else:
+                g = s.gcc_frames(x_dev, wl.frame, wl.pairs, frames)
+                e[1].record()
+                (s.lr_map if args.variant == "lr" else s.srp_map_exact)(op, g, argmax=True)
+            e[2].record()
+            torch.cuda.synchronize()
+            tf.append(e[0].elapsed_time(e[1]))
+            tm.append(e[1].elapsed_time(e[2]))
+        return statistics.median(tf), statistics.median(tm)
+
+    t_front, t_map = kernel_times()
+    hbm, bf16, peak_src = peaks()
+    abytes = algorithmic_bytes(wl, args.variant, count, op)
+    if args.variant == "conv":
+        dom_name, dom_ms = "srp_map_tc", t_map
+        achieved = conv_flops(wl, count) / (dom_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": bf16,
+                "unit": "TFLOP/s", "frac": achieved / bf16, "peak_source": f"{peak_src} bf16",
+                "traffic": ncu_traffic(args.workload, dom_name)}
+    else:
+        if t_map >= t_front:
+            dom_name, dom_ms, dom_bytes = f"{args.variant}_map", t_map, abytes["map"]
+        else:
+            dom_name, dom_ms, dom_bytes = "frontend", t_front, abytes["frontend"]
+        achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dom_bytes,
+                "traffic": ncu_traffic(args.workload, dom_name)}
+    roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
+
+    # ---- e2e through the public API from pinned host memory
+    def e2e(steps):
+        torch.cuda.synchronize()
+        out_host = torch.empty(count, dtype=torch.int64).pin_memory()
+        evs = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            xd = pinned.to(dev, non_blocking=True)
+            z_, idx_ = step(xd)
+            if world > 1:
+                D.gather_frame_keys(idx_, total)
+            out_host.copy_(idx_, non_blocking=True)
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps
+    e2e_ms = e2e(max(3, args.steps // 2))
+    e2e_block = {"value": total / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                 "h2d_bytes_per_step": int(pinned.numel() * 4), "d2h_bytes_per_step": int(count * 8)}
+
+    # ---- parity spot check on this run's output (first frames vs the float64 oracle)
+    parity = None
+    if rank == 0:
+        parity = spot_parity(wl, args.variant, op, z, idx, min(8, count))
+
+    # ---- other variants of the same workload (same timing rules, N=1 view)
+    variants = {}
+    if not args.no_variants and world == 1:
+        for v in ("sspi", "slri", "lr", "conv"):
+            if v == args.variant:
+                continue
+            try:
+                opv = fit_operator(wl, v, args)
+                ms_v, l_v, _, _ = time_steps(make_step(v, opv), max(5, args.steps // 2), 3, gather=False)
+                k = max(5, args.steps // 2)
+                entry = {"value": total / (ms_v / k / 1e3), "unit": UNIT, "ms_per_step": ms_v / k,
+                         "gpu_launches_per_step": l_v / k}
+                if v == "conv":
+                    entry["tflops"] = conv_flops(wl, count) / (ms_v / k / 1e3) / 1e12
+                    entry["precision"] = "tf32 (tcgen05)"
+                if v in ("lr", "slri"):
+                    entry["rank"] = args.rank_r
+                variants[v] = entry
+            except Exception as exc:  # report, never hide
+                variants[v] = {"error": f"{type(exc).__name__}: {exc}"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args.variant, op, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "frames_per_gpu": per_gpu, "global_frames": total,
+                       "candidates": wl.grid.num_points, "pairs": wl.pairs.num_pairs,
+                       "frame_len": wl.frame.frame_len, "total_lags": wl.spec.total_samples,
+                       "variant": args.variant,
+                       "operator": (args.nnz if args.variant == "sspi" else
+                                    f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
+                       "parallelism": f"frames/{world}", "l2": "flushed between timed steps"},
+            "candidates_per_s": value * wl.grid.num_points,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e_block,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "gpu_launches_per_step": launches_per_step,
+            "clocks": clocks.summary(), "parity": parity, "variants": variants,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def spot_parity(wl, variant, op, z, idx, nf):
+    from oracle import srp_oracle as O
+    try:
+        x = wl.samples[:, :(nf - 1) * wl.frame.hop + wl.frame.frame_len].astype(np.float64)
+        z_ref = oracle_chain(wl, variant, op, x, nf)
+        zz = z[:nf].float().cpu().numpy()
+        err = O.normalized_max_error(zz, z_ref)
+        ok = O.peak_margin(z_ref) > 1e-4
+        agree = bool(np.array_equal(idx[:nf].cpu().numpy()[ok], np.argmax(z_ref, axis=1)[ok]))
+        return {"frames": nf, "max_normalized_error": float(err.max()), "tolerance": 1e-4,
+                "argmax_agree_on_margin_frames": agree, "margin_frames": int(ok.sum())}
+    except Exception as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+# --------------------------------------------------------------------- CPU (reference algorithm)
+
+def oracle_chain(wl, variant, op, x, nf):
+    """Reference algorithm (float64 NumPy port, oracle/) for frames 0..nf-1 of x."""
+    from oracle import srp_oracle as O
+    win = O.frame_window(wl.frame.frame_len, wl.frame.window)
+    spectra = O.stft_frames(x, wl.frame.frame_len, wl.frame.hop, win, np.arange(nf))
+    psi = O.fd_gcc(spectra, wl.pairs.pairs)
+    if variant == "conv":
+        return O.srp_map_exact(op.matrix, psi)
+    if variant == "lr":
+        return O.lr_map(op.tall, op.fat, psi)
+    xi = O.td_gcc_samples(psi, wl.spec.counts, wl.frame.half_len, "ifft")
+    if variant == "sspi":
+        return O.sspi_map(op.values, op.col_indices, op.row_splits, xi)
+    if variant == "slri":
+        return O.slri_map(op.tall, op.fat, xi)
+    return O.si_map(op.matrix, xi)
+
+
+def cpu_baseline(wl, variant, op, seconds):
+    """Time the reference algorithm on a bounded sample of this workload's frames."""
+    from oracle import srp_oracle as O
+    nf_chunk = 8
+    x_all = wl.samples.astype(np.float64)
+    done, t0 = 0, time.perf_counter()
+    total_frames = wl.num_frames
+    while time.perf_counter() - t0 < seconds and done < total_frames:
+        f0 = done
+        n = min(nf_chunk, total_frames - f0)
+        seg = x_all[:, f0 * wl.frame.hop:(f0 + n - 1) * wl.frame.hop + wl.frame.frame_len]
+        z = oracle_chain(wl, variant, op, seg, n)
+        O.locate(z)
+        done += n
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{done} frames of {wl.name} ({variant}) in {el:.1f} s, float64 NumPy port "
+                      f"of the reference (oracle/srp_oracle.py), BLAS threads = all cores"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    per_gpu = args.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000,
+                              "cfg5": 1024}[args.workload]
+    wl = build_scene(args, per_gpu * world)
+    op = fit_operator(wl, args.variant, args)
+    from oracle import srp_oracle as O
+    nf = 8
+    x = wl.samples.astype(np.float64)
+    seg = x[:, :(nf - 1) * wl.frame.hop + wl.frame.frame_len]
+    for _ in range(max(1, args.warmup)):
+        O.locate(oracle_chain(wl, args.variant, op, seg, nf))
+    steps = max(1, args.steps)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        f0 = (k * nf) % max(1, wl.num_frames - nf)
+        seg = x[:, f0 * wl.frame.hop:(f0 + nf - 1) * wl.frame.hop + wl.frame.frame_len]
+        O.locate(oracle_chain(wl, args.variant, op, seg, nf))
+    el = time.perf_counter() - t0
+    value = steps * nf / el
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.workload, "frames_per_gpu": per_gpu, "variant": args.variant,
+                       "operator": args.nnz if args.variant == "sspi" else "",
+                       "step": f"{nf} frames (bounded sample of the workload)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{steps} x {nf} frames of {wl.name}, float64 NumPy port of "
+                                       f"the reference (oracle/), BLAS threads = all cores"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/*
+ * srpgpu -- C-ABI of the B200-native SRP-map hot path (sm_100a).
+ *
+ * The reference (`srpmap`, pure Python/NumPy) has no FFI; its drop-in boundary is
+ * the Python API re-exported in srpmap/__init__.py:11-34 and dispatched by
+ * cli.evaluate_map (cli.py:170-180).  Each entry point below replaces one of
+ * those functions, batched over a leading frame axis.  Conventions:
+ *
+ *   - every pointer is DEVICE memory owned by the caller (no allocation inside);
+ *   - complex arrays are interleaved float32 (re, im), i.e. complex64;
+ *   - frame-major layouts: spectra [F][M][K+1], gcc [F][P][K-1], samples [F][S],
+ *     maps z [F][J]; `keys` [F] are packed per-frame argmax keys
+ *       key = (ordered_f32_bits(z_max) << 32) | (0xFFFFFFFF - i_max)
+ *     (largest value, ties to the LOWEST index as np.argmax, srp.py:74-80);
+ *     decode with srpgpu_decode_keys;
+ *   - work is stream-ordered on `stream` (a cudaStream_t; NULL = legacy default);
+ *   - return 0 on success, a negative SRPGPU_ERR_* otherwise; no exception or
+ *     C++ type crosses the ABI; srpgpu_last_error() returns the message.
+ *     The Python layer maps codes onto the reference's exception classes
+ *     (errors.py:4-29): DIMENSION -> DimensionError, VALUE -> ValueError,
+ *     CAPACITY -> CapacityError, UNSUPPORTED -> ValueError, LAUNCH -> RuntimeError.
+ */
+#ifndef SRPGPU_H
+#define SRPGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRPGPU_ABI_VERSION 1
+
+typedef void* srpgpu_stream_t; /* cudaStream_t */
+
+#define SRPGPU_OK 0
+#define SRPGPU_ERR_DIMENSION (-1)
+#define SRPGPU_ERR_VALUE (-2)
+#define SRPGPU_ERR_CAPACITY (-3)
+#define SRPGPU_ERR_LAUNCH (-4)
+#define SRPGPU_ERR_UNSUPPORTED (-5)
+
+/* ---- housekeeping ------------------------------------------------------- */
+const char* srpgpu_last_error(void);
+int srpgpu_abi_version(void);
+/* number of kernels launched through this library since load */
+uint64_t srpgpu_launch_count(void);
+int srpgpu_device_sync(void);
+
+/* ---- frontend (srpmap/frontend.py) --------------------------------------- */
+
+/* stft_frame (frontend.py:89-107), frames first_frame .. first_frame+num_frames-1:
+ * spectra[f][m][k] = rfft(samples[m][(first+f)*hop : +frame_len] * window)[k], k = 0..K.
+ * samples: [M][ld_samples] f32 (num_samples valid per row); window: [frame_len] f32;
+ * frame_len a power of two in [4, 16384].  energy (nullable): [F] sum |Y|^2.
+ * Out-of-range frames -> SRPGPU_ERR_DIMENSION (the reference's IndexError, :102-105). */
+int srpgpu_stft(const float* samples, int32_t num_channels, int64_t num_samples, int64_t ld_samples,
+                const float* window, int32_t frame_len, int32_t hop, int64_t first_frame,
+                int64_t num_frames, float* spectra, float* energy, srpgpu_stream_t stream);
+
+/* fd_gcc (frontend.py:127-160) on spectra [F][M][K+1]:
+ * gcc[f][p][k-1] = Y_m[k] conj(Y_m'[k]) for pairs[p] = (m, m'), k = 1..K-1;
+ * weighting 1 (PHAT) divides by max(|raw|, floor), 0 where that is 0;
+ * floor_mode 0: floor = floor_value * sum_{m,k=0..K} |Y|^2 of the frame (default
+ * floor_value 1e-12, frontend.py:19,154-156); floor_mode 1: floor = floor_value.
+ * pairs: device [P][2] int32. */
+int srpgpu_fd_gcc(const float* spectra, int64_t num_frames, int32_t num_channels, int32_t half_len,
+                  const int32_t* pairs, int32_t num_pairs, int32_t weighting, int32_t floor_mode,
+                  double floor_value, float* gcc, srpgpu_stream_t stream);
+
+/* fused stft_frame + fd_gcc: samples -> gcc [F][P][K-1] (spectra stay on chip). */
+int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int64_t num_samples,
+                      int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
+                      int64_t first_frame, int64_t num_frames, const int32_t* pairs,
+                      int32_t num_pairs, int32_t weighting, int32_t floor_mode, double floor_value,
+                      float* gcc, srpgpu_stream_t stream);
+
+/* ---- sampling (srpmap/sampling.py) --------------------------------------- */
+
+/* td_gcc_samples(gcc, spec, "ifft") (sampling.py:106-134): per pair the
+ * unnormalized real inverse DFT of the two-sided spectrum (bins 0, K zero), lags
+ * kept in storage order 0..N_p, -N_p..-1 (sampling.py:62-65) at
+ * samples[f][offsets[p] + j].  counts [P], offsets [P+1] are device int32. */
+int srpgpu_td_gcc_samples(const float* gcc, int64_t num_frames, int32_t num_pairs, int32_t half_len,
+                          const int32_t* counts, const int32_t* offsets, int32_t total_samples,
+                          float* samples_out, srpgpu_stream_t stream);
+
+/* fused stft_frame + fd_gcc + td_gcc_samples: signal -> TD-GCC samples [F][S]. */
+int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t num_samples,
+                             int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
+                             int64_t first_frame, int64_t num_frames, const int32_t* pairs,
+                             int32_t num_pairs, int32_t weighting, int32_t floor_mode,
+                             double floor_value, const int32_t* counts, const int32_t* offsets,
+                             int32_t total_samples, float* samples_out, srpgpu_stream_t stream);
+
+/* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
+int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
+                              int32_t half_len, const int32_t* pairs, int32_t num_pairs,
+                              int32_t weighting, int32_t floor_mode, double floor_value,
+                              const int32_t* counts, const int32_t* offsets, int32_t total_samples,
+                              float* samples_out, srpgpu_stream_t stream);
+
+/* ---- maps (srpmap/interpolation.py, lowrank.py, srp.py) ------------------- */
+
+/* sspi_map (interpolation.py:188-195) and, with a keep-all operator, si_map
+ * (:129-136).  Pair-major ELL operator: entries of pair p at
+ * ell[ell_offsets[p] + i*widths[p] + w], each a packed {uint32 float-bits value,
+ * uint32 absolute sample index}; padding entries have value 0.
+ * offsets [P+1] (sample blocks), widths [P], ell_offsets [P+1] are device arrays;
+ * max_block = max 2N_p+1, max_width = max widths[p], sum_widths = sum widths[p].
+ * z [F][J] and keys [F] are each optional (NULL). */
+int srpgpu_sspi_map(const float* samples, int64_t num_frames, int32_t total_samples,
+                    int32_t num_pairs, const int32_t* offsets, const int32_t* widths,
+                    const int64_t* ell_offsets, const void* ell, int64_t num_candidates,
+                    int32_t max_block, int32_t max_width, int32_t sum_widths, float* z,
+                    uint64_t* keys, srpgpu_stream_t stream);
+
+/* slri_map (interpolation.py:178-185): z = tall (fat xi).  fat [R][S], tall [J][R]
+ * f32; work [F][R] scratch. */
+int srpgpu_slri_map(const float* samples, int64_t num_frames, int32_t total_samples,
+                    const float* fat, const float* tall, int32_t rank, int64_t num_candidates,
+                    float* work, float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* lr_map (lowrank.py:51-57): z = 2 Re(tall (fat psi)).  Complex factors folded
+ * into real ones once on the host: fat2 [2R][2PB] with rows r: (Re fat, -Im fat)
+ * and R+r: (Im fat, Re fat) interleaved per bin; tall2 [J][2R] = (2 Re tall | -2 Im tall).
+ * gcc [F][PB] complex64 (gcc_len = PB); work [F][2R] scratch. */
+int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_len, const float* fat2,
+                  const float* tall2, int32_t rank, int64_t num_candidates, float* work, float* z,
+                  uint64_t* keys, srpgpu_stream_t stream);
+
+/* srp_map_exact (srp.py:65-71): z = 2 Re(H psi), fp32 SIMT path.  h2 [J][2PB] holds
+ * interleaved (Re H, -Im H) per bin so that z = 2 * h2 . (re, im)(psi). */
+int srpgpu_srp_map_simt(const float* gcc, int64_t num_frames, int32_t gcc_len, const float* h2,
+                        int64_t num_candidates, float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* srp_map_exact on the 5th-gen tensor cores (tcgen05.mma kind::tf32, TMEM
+ * accumulators, TMA-staged operands): same operands as srpgpu_srp_map_simt.
+ * Requires gcc_len % 16 == 0 is NOT needed: the K tail is zero-filled by TMA.
+ * Row pitches must be 16-byte multiples (caller pads: h2_ld, gcc_ld in floats). */
+int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
+                      const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,
+                      uint64_t* keys, srpgpu_stream_t stream);
+
+/* generic fp32 product out[f][i] = alpha sum_k A[i][k] B[f][k] (+ argmax keys). */
+int srpgpu_gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
+                   int64_t rows_i, int64_t rows_f, int64_t depth, float alpha, uint64_t* keys,
+                   srpgpu_stream_t stream);
+
+/* locate (srp.py:74-80) for every frame of z [F][ldz] (first J columns). */
+int srpgpu_argmax(const float* z, int64_t num_frames, int64_t num_candidates, int64_t ldz,
+                  uint64_t* keys, srpgpu_stream_t stream);
+
+/* unpack keys -> index [F] int64 and/or value [F] f32 (either may be NULL). */
+int srpgpu_decode_keys(const uint64_t* keys, int64_t num_frames, int64_t* index, float* value,
+                       srpgpu_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRPGPU_H */

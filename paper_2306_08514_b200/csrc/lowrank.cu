@@ -1,0 +1,213 @@
+// Dense fp32 SIMT products of the SRP-map hot path on sm_100a:
+//
+//   out[f][i] = alpha * sum_k A[i][k] * B[f][k]     (+ fused per-frame argmax)
+//
+// One register-tiled kernel (64 x 64 output tile, 4 x 4 per thread, k staged
+// through shared memory) serves
+//   * slri_map  z = tall (fat xi)            interpolation.py:178-185
+//   * lr_map    z = 2 Re(tall (fat psi))     lowrank.py:51-57  (complex folded into
+//               real factors of width 2R on the host, once per operator)
+//   * the fp32 SIMT conventional map z = 2 Re(H psi)   srp.py:65-71, with H
+//               stored as interleaved (Re H, -Im H) rows against psi's (re, im).
+// The tcgen05/TMEM tensor-core conventional map lives in conv_tcgen05.cu.
+#include "common.cuh"
+
+namespace srpgpu {
+
+constexpr int kGI = 64, kGF = 64, kGK = 16;
+
+__global__ void __launch_bounds__(256)
+gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+               float* __restrict__ out, int64_t ldo, int64_t I, int64_t F, int64_t K, float alpha,
+               unsigned long long* __restrict__ keys, int64_t key_base) {
+  __shared__ __align__(16) float As[kGK][kGI + 4];
+  __shared__ __align__(16) float Bs[kGK][kGF + 4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t i0 = (int64_t)blockIdx.x * kGI, f0 = (int64_t)blockIdx.y * kGF;
+  float acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+
+  for (int64_t k0 = 0; k0 < K; k0 += kGK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + r * 256;        // 0..1023 over a 64 x 16 tile, k fastest
+      const int row = idx >> 4, kk = idx & 15;
+      const int64_t gi = i0 + row, gf = f0 + row, gk = k0 + kk;
+      As[kk][row] = (gi < I && gk < K) ? __ldg(A + gi * lda + gk) : 0.f;
+      Bs[kk][row] = (gf < F && gk < K) ? __ldg(B + gf * ldb + gk) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][tx * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][ty * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(bv[u], av[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+
+  // epilogue: rows f = f0 + 4 ty + u, columns i = i0 + 4 tx + v
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t f = f0 + ty * 4 + u;
+    unsigned long long key = 0ull;
+    if (f < F) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int64_t i = i0 + tx * 4 + v;
+        if (i < I) {
+          const float val = alpha * acc[u][v];
+          if (out) out[f * ldo + i] = val;
+          key = key_max(key, make_key(val, (uint32_t)(key_base + i)));
+        }
+      }
+    }
+    if (keys) {
+      // reduce over the 16 lanes sharing ty (half-warp)
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) key = key_max(key, __shfl_xor_sync(0xffffffffu, key, o));
+      if (tx == 0 && f < F && key) atomicMax(keys + f, key);
+    }
+  }
+}
+
+// Standalone per-frame argmax of z[f][0..J) (srp.py:74-80) into packed keys.
+__global__ void __launch_bounds__(256)
+argmax_kernel(const float* __restrict__ z, int64_t ldz, int64_t J, int64_t F,
+              unsigned long long* __restrict__ keys) {
+  const int64_t f = blockIdx.y;
+  const float* row = z + f * ldz;
+  unsigned long long key = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < J;
+       i += (int64_t)gridDim.x * blockDim.x)
+    key = key_max(key, make_key(__ldg(row + i), (uint32_t)i));
+  key = warp_key_max(key);
+  __shared__ unsigned long long red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) key = key_max(key, red[w]);
+    key = key_max(key, red[0]);
+    if (key) atomicMax(keys + f, key);
+  }
+}
+
+__global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, int64_t F,
+                                   int64_t* __restrict__ index, float* __restrict__ value) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  const unsigned long long k = keys[f];
+  const uint32_t hi = (uint32_t)(k >> 32);
+  const uint32_t bits = (hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi;
+  if (index) index[f] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
+  if (value) value[f] = __uint_as_float(bits);
+}
+
+int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
+            int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
+            const char* what) {
+  if (I <= 0 || F <= 0) return SRPGPU_OK;
+  SRPGPU_CHECK_ARG(F <= 65535ll * kGF, SRPGPU_ERR_DIMENSION, "%s: too many frames", what);
+  dim3 grid((unsigned)((I + kGI - 1) / kGI), (unsigned)((F + kGF - 1) / kGF));
+  gemm_nt_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
+                                       reinterpret_cast<unsigned long long*>(keys), 0);
+  SRPGPU_CHECK_LAUNCH(what);
+  return SRPGPU_OK;
+}
+
+int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st) {
+  if (!keys || F <= 0) return SRPGPU_OK;
+  if (cudaMemsetAsync(keys, 0, (size_t)F * sizeof(uint64_t), st) != cudaSuccess) {
+    set_error("argmax key reset failed");
+    return SRPGPU_ERR_LAUNCH;
+  }
+  return SRPGPU_OK;
+}
+
+}  // namespace srpgpu
+
+using namespace srpgpu;
+
+extern "C" int srpgpu_gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out,
+                              int64_t ldo, int64_t rows_i, int64_t rows_f, int64_t depth, float alpha,
+                              uint64_t* keys, srpgpu_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, rows_f, st);
+  if (s) return s;
+  return gemm_nt(A, lda, B, ldb, out, ldo, rows_i, rows_f, depth, alpha, keys, st, "gemm_nt");
+}
+
+extern "C" int srpgpu_slri_map(const float* samples, int64_t num_frames, int32_t total_samples,
+                               const float* fat, const float* tall, int32_t rank,
+                               int64_t num_candidates, float* work, float* z, uint64_t* keys,
+                               srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rank >= 1, SRPGPU_ERR_VALUE, "slri_map: rank must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  // work[f][r] = sum_s fat[r][s] xi[f][s]
+  s = gemm_nt(fat, total_samples, samples, total_samples, work, rank, rank, num_frames,
+              total_samples, 1.0f, nullptr, st, "slri_map(fat)");
+  if (s) return s;
+  return gemm_nt(tall, rank, work, rank, z, num_candidates, num_candidates, num_frames, rank, 1.0f,
+                 keys, st, "slri_map(tall)");
+}
+
+extern "C" int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_len,
+                             const float* fat2, const float* tall2, int32_t rank,
+                             int64_t num_candidates, float* work, float* z, uint64_t* keys,
+                             srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rank >= 1, SRPGPU_ERR_VALUE, "lr_map: rank must be >= 1");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  // work[f][0:R] = Re(fat psi_f), work[f][R:2R] = Im(fat psi_f); fat2 is (2R) x (2 PB)
+  s = gemm_nt(fat2, 2 * (int64_t)gcc_len, gcc, 2 * (int64_t)gcc_len, work, 2 * rank, 2 * rank,
+              num_frames, 2 * (int64_t)gcc_len, 1.0f, nullptr, st, "lr_map(fat)");
+  if (s) return s;
+  // z = [2 Re tall, -2 Im tall] . work
+  return gemm_nt(tall2, 2 * rank, work, 2 * rank, z, num_candidates, num_candidates, num_frames,
+                 2 * rank, 1.0f, keys, st, "lr_map(tall)");
+}
+
+extern "C" int srpgpu_srp_map_simt(const float* gcc, int64_t num_frames, int32_t gcc_len,
+                                   const float* h2, int64_t num_candidates, float* z, uint64_t* keys,
+                                   srpgpu_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  return gemm_nt(h2, 2 * (int64_t)gcc_len, gcc, 2 * (int64_t)gcc_len, z, num_candidates,
+                 num_candidates, num_frames, 2 * (int64_t)gcc_len, 2.0f, keys, st, "srp_map(simt)");
+}
+
+extern "C" int srpgpu_argmax(const float* z, int64_t num_frames, int64_t num_candidates, int64_t ldz,
+                             uint64_t* keys, srpgpu_stream_t stream) {
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  if (num_frames <= 0 || num_candidates <= 0) return SRPGPU_OK;
+  SRPGPU_CHECK_ARG(num_frames <= 65535, SRPGPU_ERR_DIMENSION, "argmax: too many frames per call");
+  const int bx = (int)std::min<int64_t>((num_candidates + 255) / 256, 64);
+  dim3 grid(bx, (unsigned)num_frames);
+  argmax_kernel<<<grid, 256, 0, st>>>(z, ldz, num_candidates, num_frames,
+                                      reinterpret_cast<unsigned long long*>(keys));
+  SRPGPU_CHECK_LAUNCH("argmax");
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_decode_keys(const uint64_t* keys, int64_t num_frames, int64_t* index,
+                                  float* value, srpgpu_stream_t stream) {
+  if (num_frames <= 0) return SRPGPU_OK;
+  decode_keys_kernel<<<(unsigned)((num_frames + 255) / 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(keys), num_frames, index, value);
+  SRPGPU_CHECK_LAUNCH("decode_keys");
+  return SRPGPU_OK;
+}

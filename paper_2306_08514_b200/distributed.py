@@ -1,0 +1,78 @@
+"""Frame- and candidate-partitioned execution across GPUs (one process per GPU).
+
+The reference evaluates frames serially (cli.py:241-258) and each frame and
+each candidate row is independent (srp.py:71, interpolation.py:116-126), so the
+path shards without any data-path exchange:
+
+* frame partition (default): rank r maps a contiguous block of frames with a
+  replicated operator; the only collective is an all-gather of the 8-byte
+  packed argmax key per frame (NCCL over NVLink on GPUs, gloo in CPU tests).
+* candidate partition (grids too large for one GPU's operator): rank r owns a
+  contiguous block of candidate rows and all frames; per-frame keys are
+  combined with an all-reduce MAX.  Keys are stored as int64 with the sign bit
+  flipped so signed MAX gives the unsigned order (largest value, lowest index).
+
+Maps stay on the GPU that computed them.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+_SIGN = -(1 << 63)
+
+
+def partition(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block (first, count) of `total` items for `rank` of `world`."""
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def keys_to_signed(keys: torch.Tensor) -> torch.Tensor:
+    """Packed uint64 keys (stored in int64) -> order-preserving signed int64."""
+    return keys ^ _SIGN
+
+
+def signed_to_keys(vals: torch.Tensor) -> torch.Tensor:
+    return vals ^ _SIGN
+
+
+def offset_keys(keys: torch.Tensor, row_offset: int) -> torch.Tensor:
+    """Re-base the candidate index packed in keys computed on a row block."""
+    if row_offset == 0:
+        return keys
+    low = keys & 0xFFFFFFFF
+    return (keys - low) | ((low - row_offset) & 0xFFFFFFFF)
+
+
+def gather_frame_keys(local_keys: torch.Tensor, total_frames: int, group=None) -> torch.Tensor:
+    """All-gather per-frame keys of a frame-partitioned run -> (total_frames,) on every rank."""
+    world = dist.get_world_size(group)
+    counts = [partition(total_frames, world, r)[1] for r in range(world)]
+    width = max(counts) if counts else 0
+    buf = torch.zeros(width, dtype=torch.int64, device=local_keys.device)
+    buf[:local_keys.shape[0]] = local_keys
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[:c] for o, c in zip(out, counts)])
+
+
+def reduce_candidate_keys(local_keys: torch.Tensor, group=None) -> torch.Tensor:
+    """All-reduce MAX of per-frame keys of a candidate-partitioned run."""
+    vals = keys_to_signed(local_keys.clone())
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=group)
+    return signed_to_keys(vals)
+
+
+def decode_host_keys(keys: torch.Tensor):
+    """(index, value) from packed keys on any device (CPU-side helper for tests/bench)."""
+    k = keys.to(torch.int64)
+    low = k & 0xFFFFFFFF
+    index = 0xFFFFFFFF - low
+    hi = (k >> 32) & 0xFFFFFFFF
+    pos = (hi & 0x80000000) != 0
+    bits = torch.where(pos, hi & 0x7FFFFFFF, (~hi) & 0xFFFFFFFF)
+    value = bits.to(torch.int32).view(torch.float32)
+    return index, value

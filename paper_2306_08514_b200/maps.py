@@ -1,0 +1,378 @@
+"""SRP map backends on the GPU: conventional, LR, SI, SLRI, SSPI, and argmax.
+
+Drop-ins for srp.srp_map_exact (srp.py:65-71), srp.locate (:74-80),
+lowrank.lr_map (lowrank.py:51-57), interpolation.si_map / slri_map / sspi_map
+(interpolation.py:129-136, 178-195) and cli.evaluate_map (cli.py:170-180).
+Same arguments and DimensionError checks; inputs may carry a leading frame
+axis; maps are returned as device tensors (J,) or (F, J) float32.
+
+Every map function also takes keyword-only `argmax=True` to return
+(z, index) with the per-frame argmax fused into the map kernel (index int64,
+ties to the lowest candidate index), and `out_map=False` to skip writing z
+(argmax-only output).
+
+Operators are converted to device layouts once per operator object
+(`_device.CACHE`): the SSPI operator becomes a pair-major ELL array, low-rank
+factors are cast to float32 (complex factors folded into real ones), and the
+steering matrix is stored as interleaved (Re H, -Im H) rows for the
+tensor-core GEMM.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _native as nat
+from .errors import DimensionError
+from .sampling import TdGccSamples, spec_offsets
+
+
+# ----------------------------------------------------------------- helpers
+
+def _new_keys(frames: int, want: bool):
+    if not want:
+        return None
+    return torch.empty(frames, dtype=torch.int64, device=dev.device())
+
+
+def decode_keys(keys: torch.Tensor):
+    """Packed argmax keys -> (index int64, value float32) device tensors."""
+    idx = torch.empty(keys.shape[0], dtype=torch.int64, device=keys.device)
+    val = torch.empty(keys.shape[0], dtype=torch.float32, device=keys.device)
+    nat.call("srpgpu_decode_keys", dev.ptr(keys), keys.shape[0], dev.ptr(idx), dev.ptr(val),
+             dev.stream_ptr())
+    return idx, val
+
+
+def _finish(z, keys, batched: bool, argmax: bool):
+    zz = None if z is None else (z if batched else z[0])
+    if not argmax:
+        return zz
+    idx, _ = decode_keys(keys)
+    return zz, (idx if batched else idx[0])
+
+
+def _gcc_matrix(gcc, num_pairs: int, num_bins: int):
+    """(F, P*B) complex64 device tensor + batched flag, with the reference shape check."""
+    vals = gcc.values if hasattr(gcc, "values") else gcc
+    v = dev.as_c64(vals)
+    batched = v.dim() == 2
+    if v.shape[-1] != num_pairs * num_bins:
+        raise DimensionError(f"cross-spectrum of shape {tuple(v.shape)} does not match "
+                             f"{num_pairs} pairs x {num_bins} bins")
+    return v.reshape(-1, num_pairs * num_bins), batched
+
+
+def _sample_matrix(samples, num_cols: int):
+    vals = samples.values if isinstance(samples, TdGccSamples) or hasattr(samples, "spec") else samples
+    x = dev.as_f32(vals)
+    batched = x.dim() == 2
+    if x.shape[-1] != num_cols or x.dim() > 2:
+        raise DimensionError(f"sample vector of shape {tuple(x.shape)} does not match operator "
+                             f"with {num_cols} columns")
+    return x.reshape(-1, num_cols), batched
+
+
+def _sample_offsets(samples, num_cols: int) -> np.ndarray:
+    spec = getattr(samples, "spec", None)
+    if spec is not None:
+        off = spec_offsets(spec)
+        if int(off[-1]) == num_cols:
+            return off
+    return np.array([0, num_cols], dtype=np.int64)   # no pair structure: one block
+
+
+# ----------------------------------------------------------------- SSPI / SI
+
+class EllOperator:
+    """Pair-major ELL image of a CSR interpolation operator (device + host index).
+
+    For pair p: width W_p = max_i (entries of row i inside pair p's column block);
+    entry (i, w) at ell_off[p] + i*W_p + w, packed (float32 value bits, absolute
+    column).  `counts[p, i]` (host) records the real entries so the ELL decodes
+    back to the reference CSR exactly (padding entries have value 0).
+    """
+
+    def __init__(self, values, cols, splits, num_cols: int, offsets: np.ndarray):
+        values = np.asarray(values, dtype=np.float64)
+        cols = np.asarray(cols, dtype=np.int64)
+        splits = np.asarray(splits, dtype=np.int64)
+        j = splits.shape[0] - 1
+        p_count = offsets.shape[0] - 1
+        rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
+        pair = np.searchsorted(offsets, cols, side="right") - 1
+        counts = np.zeros((p_count, j), dtype=np.int64)
+        np.add.at(counts, (pair, rows), 1)
+        widths = counts.max(axis=1) if j else np.zeros(p_count, np.int64)
+        widths = np.maximum(widths, 0)
+        ell_off = np.concatenate([[0], np.cumsum(widths * j)]).astype(np.int64)
+        # rank of each entry inside its (pair, row) group; CSR order is (row, col)
+        order = np.lexsort((cols, rows, pair))
+        grp = pair[order] * j + rows[order]
+        start = np.r_[0, np.flatnonzero(np.diff(grp)) + 1]
+        rank = np.empty(order.size, dtype=np.int64)
+        if order.size:
+            first = np.repeat(start, np.diff(np.r_[start, order.size]))
+            rank[order] = np.arange(order.size) - first
+        packed = np.zeros((int(ell_off[-1]), 2), dtype=np.uint32)
+        for p in range(p_count):   # padding: value 0, column = first column of the block
+            packed[ell_off[p]:ell_off[p + 1], 1] = offsets[p]
+        slot = ell_off[pair] + rows * widths[pair] + rank
+        packed[slot, 0] = values.astype(np.float32).view(np.uint32)
+        packed[slot, 1] = cols.astype(np.uint32)
+        self.num_rows, self.num_cols, self.num_pairs = j, num_cols, p_count
+        self.offsets = offsets
+        self.widths = widths
+        self.counts = counts
+        self.ell_off = ell_off
+        self.host_packed = packed
+        self.max_block = int(np.max(np.diff(offsets))) if p_count else 0
+        self.d_packed = torch.from_numpy(packed.reshape(-1).view(np.int32)).to(dev.device()) \
+            if packed.size else torch.zeros(2, dtype=torch.int32, device=dev.device())
+        self.d_offsets = dev.as_i32(offsets)
+        self.d_widths = dev.as_i32(widths)
+        self.d_ell_off = dev.as_i64(ell_off)
+
+    def to_csr(self):
+        """Decode back to (values float32, col_indices int64, row_splits int64)."""
+        vals, cols, per_row = [], [], np.zeros(self.num_rows, dtype=np.int64)
+        entries = []
+        for p in range(self.num_pairs):
+            w = int(self.widths[p])
+            if w == 0:
+                continue
+            blk = self.host_packed[self.ell_off[p]:self.ell_off[p + 1]].reshape(self.num_rows, w, 2)
+            mask = np.arange(w)[None, :] < self.counts[p][:, None]
+            r, k = np.nonzero(mask)
+            entries.append((r, blk[r, k, 1].astype(np.int64), blk[r, k, 0]))
+        if entries:
+            r = np.concatenate([e[0] for e in entries])
+            c = np.concatenate([e[1] for e in entries])
+            v = np.concatenate([e[2] for e in entries])
+            order = np.lexsort((c, r))
+            r, c, v = r[order], c[order], v[order]
+            per_row = np.bincount(r, minlength=self.num_rows)
+            vals, cols = v.view(np.float32), c
+        else:
+            vals, cols = np.zeros(0, np.float32), np.zeros(0, np.int64)
+        splits = np.concatenate([[0], np.cumsum(per_row)]).astype(np.int64)
+        return vals, cols, splits
+
+
+def ell_from_sparse(sp, offsets: np.ndarray) -> EllOperator:
+    key = ("ell", tuple(int(o) for o in offsets))
+    return dev.CACHE.get(sp, key, lambda: EllOperator(sp.values, sp.col_indices, sp.row_splits,
+                                                      int(sp.num_cols), offsets))
+
+
+def ell_from_dense(interp, offsets: np.ndarray) -> EllOperator:
+    """Keep-all ELL of a dense InterpMatrix: identical to the keep-all CSR's ELL."""
+    def build():
+        mat = np.asarray(interp.matrix)
+        j, s = mat.shape
+        splits = np.arange(j + 1, dtype=np.int64) * s
+        cols = np.tile(np.arange(s, dtype=np.int64), j)
+        return EllOperator(mat.ravel(), cols, splits, s, offsets)
+    return dev.CACHE.get(interp, ("ell_dense", tuple(int(o) for o in offsets)), build)
+
+
+def _ell_map(ell: EllOperator, samples, argmax: bool, out_map: bool):
+    x, batched = _sample_matrix(samples, ell.num_cols)
+    f = x.shape[0]
+    z = torch.empty((f, ell.num_rows), dtype=torch.float32, device=x.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    if ell.num_rows == 0:
+        return _finish(z, keys, batched, argmax)
+    nat.call("srpgpu_sspi_map", dev.ptr(x), f, ell.num_cols, ell.num_pairs, dev.ptr(ell.d_offsets),
+             dev.ptr(ell.d_widths), dev.ptr(ell.d_ell_off), dev.ptr(ell.d_packed), ell.num_rows,
+             ell.max_block, int(ell.widths.max()) if ell.num_pairs else 0, int(ell.widths.sum()),
+             dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True):
+    """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195)."""
+    _sample_matrix(samples, int(sp.num_cols))      # reference DimensionError check first
+    ell = ell_from_sparse(sp, _sample_offsets(samples, int(sp.num_cols)))
+    return _ell_map(ell, samples, argmax, out_map)
+
+
+def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
+    """Dense sampling+interpolation map z = Lambda xi (interpolation.py:129-136).
+
+    Runs the SSPI kernel on the keep-all ELL, so sspi_map(keep=all) == si_map
+    bit for bit, as in the reference (interpolation.py:112-126).
+    """
+    num_cols = int(np.asarray(interp.matrix).shape[1])
+    _sample_matrix(samples, num_cols)
+    offsets = spec_offsets(interp.spec)
+    if int(offsets[-1]) != num_cols:
+        offsets = np.array([0, num_cols], dtype=np.int64)
+    return _ell_map(ell_from_dense(interp, offsets), samples, argmax, out_map)
+
+
+# ----------------------------------------------------------------- low rank
+
+def _slri_device(lr):
+    def build():
+        return (dev.as_f32(np.asarray(lr.fat, dtype=np.float64)),
+                dev.as_f32(np.asarray(lr.tall, dtype=np.float64)))
+    return dev.CACHE.get(lr, "slri_f32", build)
+
+
+def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True):
+    """Low-rank interpolation map z = tall (fat xi) (interpolation.py:178-185)."""
+    fat = np.asarray(lr.fat)
+    x, batched = _sample_matrix(samples, fat.shape[1])
+    d_fat, d_tall = _slri_device(lr)
+    r, j, f = fat.shape[0], d_tall.shape[0], x.shape[0]
+    work = torch.empty((f, r), dtype=torch.float32, device=x.device)
+    z = torch.empty((f, j), dtype=torch.float32, device=x.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    nat.call("srpgpu_slri_map", dev.ptr(x), f, fat.shape[1], dev.ptr(d_fat), dev.ptr(d_tall), r, j,
+             dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+def _lr_device(lr):
+    def build():
+        fat = np.asarray(lr.fat, dtype=np.complex128)
+        tall = np.asarray(lr.tall, dtype=np.complex128)
+        r, n = fat.shape
+        fat2 = np.empty((2 * r, 2 * n))
+        fat2[:r, 0::2], fat2[:r, 1::2] = fat.real, -fat.imag      # Re(fat psi)
+        fat2[r:, 0::2], fat2[r:, 1::2] = fat.imag, fat.real       # Im(fat psi)
+        tall2 = np.concatenate([2.0 * tall.real, -2.0 * tall.imag], axis=1)
+        return dev.as_f32(fat2), dev.as_f32(tall2)
+    return dev.CACHE.get(lr, "lr_f32", build)
+
+
+def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True):
+    """Low-rank SRP map z = 2 Re(tall (fat psi)) (lowrank.py:51-57)."""
+    fat = np.asarray(lr.fat)
+    vals = gcc.values if hasattr(gcc, "values") else gcc
+    v = dev.as_c64(vals)
+    if v.shape[-1] != fat.shape[1] or v.dim() > 2:
+        raise DimensionError(f"cross-spectrum of shape {tuple(v.shape)} does not match factor "
+                             f"with {fat.shape[1]} columns")
+    batched = v.dim() == 2
+    v = v.reshape(-1, fat.shape[1])
+    d_fat2, d_tall2 = _lr_device(lr)
+    r, j, f = fat.shape[0], d_tall2.shape[0], v.shape[0]
+    work = torch.empty((f, 2 * r), dtype=torch.float32, device=v.device)
+    z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    nat.call("srpgpu_lr_map", dev.ptr(v), f, fat.shape[1], dev.ptr(d_fat2), dev.ptr(d_tall2), r, j,
+             dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+# ----------------------------------------------------------------- conventional
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def steering_device(srp) -> torch.Tensor:
+    """(J, ld) float32: interleaved (Re H, -Im H) per bin, row pitch padded to 16 B."""
+    def build():
+        h = np.asarray(srp.matrix)
+        j, n = h.shape
+        ld = _pad4(2 * n)
+        out = torch.zeros((j, ld), dtype=torch.float32, device=dev.device())
+        step = max(1, (64 << 20) // max(1, 8 * n))       # upload in row blocks (bounded host RAM)
+        for r0 in range(0, j, step):
+            blk = np.conj(h[r0:r0 + step]).astype(np.complex64).view(np.float32)
+            out[r0:r0 + blk.shape[0], :2 * n] = torch.from_numpy(blk).to(out.device)
+        return out
+    return dev.CACHE.get(srp, "h2_f32", build)
+
+
+def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, out_map: bool = True):
+    """Conventional SRP map z = 2 Re(H psi) (srp.py:65-71).
+
+    precision "tf32": tcgen05 tensor-core GEMM (kind::tf32, fp32 accumulate in TMEM),
+    normalized max error ~1e-5 vs float64 (within the 1e-4 parity bound);
+    "fp32": SIMT fp32 GEMM.
+    """
+    if (gcc.num_pairs, gcc.num_bins) != (srp.num_pairs, srp.num_bins):
+        raise DimensionError(f"cross-spectra for {gcc.num_pairs} pairs x {gcc.num_bins} bins do not "
+                             f"match a {srp.num_pairs} x {srp.num_bins} transform")
+    if precision not in ("tf32", "fp32"):
+        raise ValueError(f"unknown precision {precision!r}")
+    v, batched = _gcc_matrix(gcc, srp.num_pairs, srp.num_bins)
+    h2 = steering_device(srp)
+    n = srp.num_pairs * srp.num_bins
+    j, f = h2.shape[0], v.shape[0]
+    z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    if precision == "fp32":
+        if h2.shape[1] != 2 * n:
+            h2 = h2[:, :2 * n].contiguous()
+        nat.call("srpgpu_srp_map_simt", dev.ptr(v), f, n, dev.ptr(h2), j, dev.ptr(z), dev.ptr(keys),
+                 dev.stream_ptr())
+    else:
+        ld = h2.shape[1]
+        if ld != 2 * n:   # pad psi rows to the same 16-byte pitch
+            vp = torch.zeros((f, ld), dtype=torch.float32, device=v.device)
+            vp[:, :2 * n] = torch.view_as_real(v).reshape(f, 2 * n)
+        else:
+            vp = v
+        nat.call("srpgpu_srp_map_tc", dev.ptr(vp), ld, f, n, dev.ptr(h2), ld, j, dev.ptr(z),
+                 dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+# ----------------------------------------------------------------- argmax
+
+def map_argmax(z) -> torch.Tensor:
+    """Per-frame argmax of z (J,) or (F, J) on the device (first index of the max)."""
+    zz = dev.as_f32(z)
+    batched = zz.dim() == 2
+    zz = zz.reshape(-1, zz.shape[-1])
+    idx = []
+    for f0 in range(0, zz.shape[0], 65535):
+        part = zz[f0:f0 + 65535]
+        keys = torch.empty(part.shape[0], dtype=torch.int64, device=zz.device)
+        nat.call("srpgpu_argmax", dev.ptr(part), part.shape[0], part.shape[1], part.shape[1],
+                 dev.ptr(keys), dev.stream_ptr())
+        idx.append(decode_keys(keys)[0])
+    out = torch.cat(idx)
+    return out if batched else out[0]
+
+
+def locate(z, grid):
+    """Index and coordinates of the map maximum; ties go to the lowest index (srp.py:74-80).
+
+    z (J,) -> (int, (3,) array); z (F, J) -> ((F,) int64 array, (F, 3) array).
+    """
+    shape = tuple(z.shape) if hasattr(z, "shape") else np.shape(z)
+    if shape[-1:] != (grid.num_points,) or len(shape) > 2:
+        raise DimensionError(f"map of length {shape} does not match grid with "
+                             f"{grid.num_points} points")
+    idx = map_argmax(z).cpu().numpy()
+    if idx.ndim == 0:
+        i = int(idx)
+        return i, np.asarray(grid.points)[i].copy()
+    return idx, np.asarray(grid.points)[idx].copy()
+
+
+def evaluate_map(kind, op, spec, frame, gcc, path="ifft", **kw):
+    """Backend dispatch of the reference (cli.py:170-180); the GPU always samples by iFFT."""
+    from .sampling import td_gcc_samples
+    if kind == "conv":
+        return srp_map_exact(op, gcc, **kw)
+    if kind == "lr":
+        return lr_map(op, gcc, **kw)
+    if path not in ("auto", "ifft", "matrix"):
+        raise ValueError(f"unknown sampling path {path!r}")
+    xi = td_gcc_samples(gcc, spec, "ifft")
+    if kind == "si":
+        return si_map(op, xi, **kw)
+    if kind == "slri":
+        return slri_map(op, xi, **kw)
+    if kind == "sspi":
+        return sspi_map(op, xi, **kw)
+    raise ValueError(f"unknown map kind {kind!r}")

@@ -1,0 +1,248 @@
+"""Host-side operator construction (precomputed once, then uploaded).
+
+Same operators and semantics as the reference builders:
+  SrpMatrix / build_srp_matrix          srp.py:22-62
+  LowRankSrp / truncate_srp_matrix      lowrank.py:19-48
+  InterpMatrix / build_interp_matrix    interpolation.py:27-44, 93-105
+  LowRankInterp / truncate_low_rank     interpolation.py:47-65, 139-152
+  SparseInterp / truncate_sparse        interpolation.py:68-90, 155-175
+plus `truncate_sparse_fixed`, the fixed-nnz-per-(candidate, pair) fit used by
+the BASELINE nnz sweep (its map is still the reference `sspi_map` applied to
+the resulting CSR).  These stay float64 NumPy: they are fitted once per scene
+and are not on the per-frame device path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CapacityError, DimensionError
+
+DEFAULT_MATRIX_CAP_BYTES = 2 * 1024 ** 3
+
+
+def check_capacity(shape, itemsize: int, max_bytes: int, what: str) -> None:
+    need = shape[0] * shape[1] * itemsize
+    if need > max_bytes:
+        raise CapacityError(f"{what} of shape {shape} needs {need / 1e9:.2f} GB, above the cap "
+                            f"of {max_bytes / 1e9:.2f} GB")
+
+
+# ---------------------------------------------------------------- conventional
+
+@dataclass(frozen=True)
+class SrpMatrix:
+    matrix: np.ndarray   # (J, P*B) complex
+    num_pairs: int
+    num_bins: int
+
+    @property
+    def num_candidates(self) -> int:
+        return self.matrix.shape[0]
+
+    def pair_block(self, p: int) -> np.ndarray:
+        return self.matrix[:, p * self.num_bins:(p + 1) * self.num_bins]
+
+
+def srp_matrix_shape(tdoa, frame):
+    return tdoa.num_candidates, tdoa.num_pairs * frame.num_bins
+
+
+def build_srp_matrix(tdoa, frame, max_bytes: int = DEFAULT_MATRIX_CAP_BYTES) -> SrpMatrix:
+    """H[i, p B + k - 1] = exp(j w_k dt_p(i))."""
+    shape = srp_matrix_shape(tdoa, frame)
+    check_capacity(shape, 16, max_bytes, "SRP matrix")
+    b = frame.num_bins
+    w = frame.bin_freqs
+    out = np.empty(shape, dtype=np.complex128)
+    for p in range(tdoa.num_pairs):
+        np.exp(1j * tdoa.delta_t[:, p:p + 1] * w[None, :], out=out[:, p * b:(p + 1) * b])
+    return SrpMatrix(matrix=out, num_pairs=tdoa.num_pairs, num_bins=b)
+
+
+@dataclass(frozen=True)
+class LowRankSrp:
+    tall: np.ndarray            # (J, R) complex = U[:, :R] s[:R]
+    fat: np.ndarray             # (R, P*B) complex = Vh[:R]
+    singular_values: np.ndarray
+
+    @property
+    def rank(self) -> int:
+        return self.tall.shape[1]
+
+    def to_dense(self) -> np.ndarray:
+        return self.tall @ self.fat
+
+
+def low_rank_srp_from_svd(u, s, vt, rank: int) -> LowRankSrp:
+    return LowRankSrp(tall=u[:, :rank] * s[:rank], fat=vt[:rank], singular_values=s[:rank].copy())
+
+
+def truncate_srp_matrix(srp, rank: int) -> LowRankSrp:
+    full = min(srp.matrix.shape)
+    if not 1 <= rank <= full:
+        raise ValueError(f"rank must be in [1, {full}], got {rank}")
+    u, s, vt = np.linalg.svd(srp.matrix, full_matrices=False)
+    return low_rank_srp_from_svd(u, s, vt, rank)
+
+
+# ---------------------------------------------------------------- interpolation
+
+@dataclass(frozen=True)
+class InterpMatrix:
+    matrix: np.ndarray   # (J, S) float64
+    spec: object
+
+    @property
+    def num_candidates(self) -> int:
+        return self.matrix.shape[0]
+
+    @property
+    def num_samples(self) -> int:
+        return self.matrix.shape[1]
+
+    def pair_block(self, p: int) -> np.ndarray:
+        off = _offsets(self.spec)
+        return self.matrix[:, off[p]:off[p + 1]]
+
+
+def _offsets(spec) -> np.ndarray:
+    counts = np.asarray(spec.counts, dtype=np.int64)
+    return np.concatenate([[0], np.cumsum(2 * counts + 1)]).astype(np.int64)
+
+
+def _lags(count: int) -> np.ndarray:
+    return np.concatenate([np.arange(count + 1), np.arange(-count, 0)])
+
+
+def build_interp_matrix(tdoa, spec, frame, max_bytes: int = DEFAULT_MATRIX_CAP_BYTES) -> InterpMatrix:
+    """Lambda[:, off_p + s] = sinc(dt_p(i)/T - lag_s) (normalized sinc)."""
+    if tdoa.num_pairs != spec.num_pairs:
+        raise DimensionError("TDOA table and sample spec disagree on pair count")
+    off = _offsets(spec)
+    shape = (tdoa.num_candidates, int(off[-1]))
+    check_capacity(shape, 8, max_bytes, "interpolation matrix")
+    out = np.empty(shape)
+    for p in range(spec.num_pairs):
+        frac = tdoa.delta_t[:, p] / frame.sample_period
+        out[:, off[p]:off[p + 1]] = np.sinc(frac[:, None] - _lags(int(spec.counts[p]))[None, :])
+    return InterpMatrix(matrix=out, spec=spec)
+
+
+@dataclass(frozen=True)
+class LowRankInterp:
+    tall: np.ndarray            # (J, R)
+    fat: np.ndarray             # (R, S)
+    singular_values: np.ndarray
+
+    @property
+    def rank(self) -> int:
+        return self.tall.shape[1]
+
+    def to_dense(self) -> np.ndarray:
+        return self.tall @ self.fat
+
+
+def low_rank_interp_from_svd(u, s, vt, rank: int) -> LowRankInterp:
+    return LowRankInterp(tall=u[:, :rank] * s[:rank], fat=vt[:rank], singular_values=s[:rank].copy())
+
+
+def truncate_low_rank(interp, rank: int) -> LowRankInterp:
+    full = min(interp.matrix.shape)
+    if not 1 <= rank <= full:
+        raise ValueError(f"rank must be in [1, {full}], got {rank}")
+    u, s, vt = np.linalg.svd(interp.matrix, full_matrices=False)
+    return low_rank_interp_from_svd(u, s, vt, rank)
+
+
+@dataclass(frozen=True)
+class SparseInterp:
+    values: np.ndarray        # (Q,)
+    col_indices: np.ndarray   # (Q,) int64
+    row_splits: np.ndarray    # (J+1,) int64
+    num_cols: int
+
+    @property
+    def num_rows(self) -> int:
+        return self.row_splits.shape[0] - 1
+
+    @property
+    def num_kept(self) -> int:
+        return self.values.shape[0]
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.num_rows, self.num_cols))
+        rows = np.repeat(np.arange(self.num_rows), np.diff(self.row_splits))
+        out[rows, self.col_indices] = self.values
+        return out
+
+
+def _csr_from_flat(mat: np.ndarray, sel: np.ndarray) -> SparseInterp:
+    sel = np.sort(sel)
+    rows = sel // mat.shape[1]
+    cols = sel % mat.shape[1]
+    splits = np.zeros(mat.shape[0] + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=mat.shape[0]), out=splits[1:])
+    return SparseInterp(values=mat.ravel()[sel], col_indices=cols.astype(np.int64),
+                        row_splits=splits, num_cols=mat.shape[1])
+
+
+def truncate_sparse(interp, keep: int) -> SparseInterp:
+    """Global top-`keep` magnitudes; ties go to the lower row-major flat index.
+
+    Same selection as the reference's stable argsort of -|Lambda|
+    (interpolation.py:166-170), computed by thresholding: everything strictly
+    above the keep-th largest magnitude, then the first ties in flat order.
+    """
+    mat = interp.matrix
+    size = mat.size
+    if not 0 <= keep <= size:
+        raise ValueError(f"keep must be in [0, {size}], got {keep}")
+    mag = np.abs(mat).ravel()
+    if keep == 0:
+        sel = np.zeros(0, dtype=np.int64)
+    elif keep == size:
+        sel = np.arange(size, dtype=np.int64)
+    else:
+        thresh = np.partition(mag, size - keep)[size - keep]
+        above = np.flatnonzero(mag > thresh)
+        ties = np.flatnonzero(mag == thresh)[:keep - above.size]
+        sel = np.concatenate([above, ties])
+    return _csr_from_flat(mat, sel)
+
+
+def truncate_sparse_fixed(interp, nnz: int) -> SparseInterp:
+    """Keep the `nnz` largest |entries| of every (candidate, pair) block.
+
+    Ties go to the lower column (stable).  Blocks narrower than nnz are kept
+    whole, so Q = sum_p min(nnz, 2 N_p + 1) * J.  This is the fixed-width
+    ELL fit of the BASELINE nnz sweep; at nnz = 1 it coincides with the
+    reference's global fit at keep = J*P whenever that fit keeps exactly one
+    entry per (candidate, pair).
+    """
+    if nnz < 0:
+        raise ValueError("nnz must be >= 0")
+    mat = interp.matrix
+    off = _offsets(interp.spec)
+    j = mat.shape[0]
+    picks = []
+    for p in range(len(off) - 1):
+        block = np.abs(mat[:, off[p]:off[p + 1]])
+        k = min(nnz, block.shape[1])
+        if k == 0:
+            continue
+        idx = np.argsort(-block, axis=1, kind="stable")[:, :k] + off[p]
+        picks.append((np.arange(j)[:, None] * mat.shape[1] + idx).ravel())
+    sel = np.concatenate(picks) if picks else np.zeros(0, dtype=np.int64)
+    return _csr_from_flat(mat, sel)
+
+
+def resolve_sparsity(token, num_candidates: int, num_pairs: int, size: int) -> int:
+    """"all" | "<x>jp" | int -> kept count (config.py:245-262)."""
+    if token == "all":
+        return size
+    if isinstance(token, str) and token.endswith("jp"):
+        return int(round(float(token[:-2]) * num_candidates * num_pairs))
+    return int(token)

@@ -1,0 +1,165 @@
+"""Critical sampling of the TD GCCs on the GPU (batched real inverse FFT).
+
+Drop-in for srpmap/sampling.py: `SampleSpec` (:31-65), `sample_spec` (:68-84),
+`TdGccSamples` (:87-96) and `td_gcc_samples` (:106-134).  The GPU always uses
+the iFFT path (the reference's "matrix" path agrees with it to <= 1e-12,
+sampling.py:1-16, tests/test_sampling.py:81-88), so `path` only selects the
+validation: "matrix" | "ifft" are accepted, anything else is a ValueError.
+
+Output layout matches the reference: per frame the S = sum_p (2 N_p + 1) lags,
+pair-major, each block in storage order 0..N_p, -N_p..-1.  Batched calls
+return (F, S).  `frames_to_samples` is the fused signal -> samples chain.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from . import _native as nat
+from .errors import ConfigError, DimensionError
+from .frontend import (FdGcc, _check_range, _floor_args, _frame_range, _pairs_device, _signal,
+                       _window_device, num_frames)
+
+
+@dataclass(frozen=True)
+class SampleSpec:
+    counts: np.ndarray   # (P,) N_p
+    n_aux: int
+    half_len: int
+
+    @property
+    def num_pairs(self) -> int:
+        return self.counts.shape[0]
+
+    @property
+    def samples_per_pair(self) -> np.ndarray:
+        return 2 * self.counts + 1
+
+    @property
+    def total_samples(self) -> int:
+        return int(np.sum(self.samples_per_pair))
+
+    @property
+    def mean_samples(self) -> float:
+        return self.total_samples / self.num_pairs
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.samples_per_pair)])
+
+    def lag_indices(self, p: int) -> np.ndarray:
+        c = int(self.counts[p])
+        return np.concatenate([np.arange(c + 1), np.arange(-c, 0)])
+
+
+def spec_offsets(spec) -> np.ndarray:
+    counts = np.asarray(spec.counts, dtype=np.int64)
+    return np.concatenate([[0], np.cumsum(2 * counts + 1)]).astype(np.int64)
+
+
+def sample_spec(tdoa, frame, n_aux: int = 2) -> SampleSpec:
+    """N_p = floor(limit_p / T) + n_aux; ConfigError if 2 N_p + 1 > frame_len."""
+    if n_aux < 0:
+        raise ConfigError("n_aux must be non-negative")
+    counts = np.floor(tdoa.limits / frame.sample_period).astype(np.int64) + n_aux
+    worst = int(np.argmax(counts))
+    if 2 * counts[worst] + 1 > frame.frame_len:
+        raise ConfigError(f"frame length {frame.frame_len} too short: pair {worst} needs "
+                          f"{2 * counts[worst] + 1} lag samples")
+    return SampleSpec(counts=counts, n_aux=n_aux, half_len=frame.half_len)
+
+
+@dataclass(frozen=True)
+class TdGccSamples:
+    """TD GCC samples: values (S,) or (F, S) float32 on the device."""
+
+    values: torch.Tensor
+    spec: object
+
+    @property
+    def num_frames(self) -> int:
+        return 1 if self.values.dim() == 1 else self.values.shape[0]
+
+    def per_pair(self, p: int) -> torch.Tensor:
+        off = spec_offsets(self.spec)
+        return self.values[..., off[p]:off[p + 1]]
+
+
+def _spec_device(spec):
+    def build():
+        off = spec_offsets(spec)
+        return dev.as_i32(np.asarray(spec.counts)), dev.as_i32(off)
+    return dev.CACHE.get(spec, "spec_i32", build)
+
+
+def _check_gcc(gcc, spec) -> None:
+    if gcc.num_pairs != spec.num_pairs or gcc.num_bins != spec.half_len - 1:
+        raise DimensionError(
+            f"cross-spectra ({gcc.num_pairs} pairs x {gcc.num_bins} bins) do not match "
+            f"sampling for {spec.num_pairs} pairs at K={spec.half_len}")
+
+
+def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
+    """Unnormalized real iDFT per pair, kept lags only (sampling.py:106-134)."""
+    _check_gcc(gcc, spec)
+    if path not in ("matrix", "ifft"):
+        raise ValueError(f"unknown sampling path {path!r}")
+    vals = dev.as_c64(gcc.values)
+    batched = vals.dim() == 2
+    vals = vals.reshape(-1, gcc.num_pairs * gcc.num_bins)
+    counts, offsets = _spec_device(spec)
+    s_total = int(spec_offsets(spec)[-1])
+    out = torch.empty((vals.shape[0], s_total), dtype=torch.float32, device=vals.device)
+    nat.call("srpgpu_td_gcc_samples", dev.ptr(vals), vals.shape[0], gcc.num_pairs, spec.half_len,
+             dev.ptr(counts), dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
+    return TdGccSamples(values=out if batched else out[0], spec=spec)
+
+
+def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
+                      floor=None) -> TdGccSamples:
+    """Fused stft_frame -> fd_gcc -> td_gcc_samples for a range of frames.
+
+    Neither the spectra nor the cross-spectra touch HBM; one kernel launch.
+    """
+    x = _signal(samples)
+    if x.shape[0] != pairs.num_mics:
+        raise DimensionError(f"expected {pairs.num_mics} channels, got {x.shape[0]}")
+    if spec.num_pairs != pairs.num_pairs or spec.half_len != frame.half_len:
+        raise DimensionError("sample spec does not match the pairs / frame")
+    first, count, batched = _frame_range(frames, num_frames(frame, x.shape[1]))
+    _check_range(frame, first, count, x.shape[1])
+    w, mode, fval = _floor_args(weighting, floor)
+    counts, offsets = _spec_device(spec)
+    s_total = int(spec_offsets(spec)[-1])
+    out = torch.empty((count, s_total), dtype=torch.float32, device=x.device)
+    nat.call("srpgpu_frames_to_samples", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
+             dev.ptr(_window_device(frame)), frame.frame_len, frame.hop, first, count,
+             dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
+             dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
+    return TdGccSamples(values=out if batched else out[0], spec=spec)
+
+
+def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:
+    """Fused fd_gcc -> td_gcc_samples on precomputed spectra (M, K+1) / (F, M, K+1)."""
+    y = dev.as_c64(spectra)
+    batched = y.dim() == 3
+    if y.dim() == 2:
+        y = y.unsqueeze(0)
+    if y.dim() != 3 or y.shape[1] != pairs.num_mics or y.shape[2] != spec.half_len + 1:
+        raise DimensionError(f"spectra of shape {tuple(y.shape)} do not match the pairs / spec")
+    w, mode, fval = _floor_args(weighting, floor)
+    counts, offsets = _spec_device(spec)
+    s_total = int(spec_offsets(spec)[-1])
+    out = torch.empty((y.shape[0], s_total), dtype=torch.float32, device=y.device)
+    nat.call("srpgpu_spectra_to_samples", dev.ptr(y), y.shape[0], y.shape[1], spec.half_len,
+             dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
+             dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
+    return TdGccSamples(values=out if batched else out[0], spec=spec)
+
+
+__all__ = ["SampleSpec", "TdGccSamples", "sample_spec", "td_gcc_samples", "frames_to_samples",
+           "spectra_to_samples", "spec_offsets", "FdGcc"]

@@ -1,0 +1,287 @@
+"""GPU parity of every hot-path entry point against the reference's golden vectors.
+
+Tolerances (BASELINE.json north_star): FP32 maps within a normalized max error
+of 1e-4 of the reference float64 maps, argmax identical wherever the float64
+map's peak margin exceeds 1e-4, sparse structure bit-exact.  Intermediate
+stages are held tighter (they are fp32 transforms of unit-magnitude data).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2306_08514_b200 as s
+from oracle import srp_oracle as O
+from conftest import keep_tags, load_golden, scene_objects, sparse_from_golden
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def assert_map_close(z_gpu, z_ref, tol=MAP_TOL):
+    err = O.normalized_max_error(np_(z_gpu), z_ref)
+    assert np.all(err <= tol), f"normalized max error {err.max():.3e} > {tol:.0e}"
+    return err
+
+
+def assert_argmax_agrees(idx_gpu, z_ref, margin=MAP_TOL):
+    idx_gpu = np.atleast_1d(np_(idx_gpu))
+    z_ref = np.atleast_2d(z_ref)
+    ok = O.peak_margin(z_ref) > margin
+    assert np.array_equal(idx_gpu[ok], np.argmax(z_ref, axis=1)[ok])
+
+
+# ------------------------------------------------------------------ frontend
+
+def test_stft_matches_reference(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["spectra"].shape[0]
+    y = np_(s.stft_frame(g["samples"], frame, range(F)))
+    scale = np.abs(g["spectra"]).max(axis=(1, 2), keepdims=True)
+    assert np.max(np.abs(y - g["spectra"]) / scale) < 2e-6
+    y0 = np_(s.stft_frame(g["samples"], frame, 1))
+    assert np.array_equal(y0, y[1])                       # batched == per-frame, bit for bit
+
+
+def test_fd_gcc_matches_reference(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    psi = np_(s.fd_gcc(g["spectra"], pairs).values)
+    d = np.abs(psi - g["psi"])
+    assert np.quantile(d, 0.999) < 1e-5 and d.max() < 1e-3
+    assert np.allclose(np.abs(psi), 1.0, atol=1e-5)       # PHAT: unit magnitude
+    raw = np_(s.fd_gcc(g["spectra"], pairs, weighting="none").values)
+    rel = np.abs(raw - g["psi_none"]) / np.abs(g["psi_none"]).max()
+    assert rel.max() < 1e-6
+    one = s.fd_gcc(g["spectra"][0], pairs)
+    assert one.values.shape == (pairs.num_pairs * frame.num_bins,)
+    assert np.array_equal(np_(one.values), psi[0])
+
+
+def test_fused_gcc_frames(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    psi = np_(s.gcc_frames(g["samples"], frame, pairs, range(F)).values)
+    d = np.abs(psi - g["psi"])
+    assert np.quantile(d, 0.999) < 2e-5 and d.max() < 2e-3
+
+
+def test_td_gcc_samples_matches_reference(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    gcc = s.FdGcc(torch.from_numpy(g["psi"].astype(np.complex64)).cuda(), pairs.num_pairs,
+                  frame.num_bins, "phat")
+    for path in ("ifft", "matrix"):
+        xi = np_(s.td_gcc_samples(gcc, spec, path).values)
+        ref = g["xi_ifft"] if path == "ifft" else g["xi_matrix"]
+        err = np.abs(xi - ref).max(axis=1) / np.abs(ref).max(axis=1)
+        assert err.max() < 1e-5
+    with pytest.raises(ValueError):
+        s.td_gcc_samples(gcc, spec, "dft")
+
+
+def test_fused_frames_to_samples(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    xi = np_(s.frames_to_samples(g["samples"], frame, pairs, spec, range(F)).values)
+    err = np.abs(xi - g["xi_ifft"]).max(axis=1) / np.abs(g["xi_ifft"]).max(axis=1)
+    assert err.max() < 2e-5
+    y = s.stft_frame(g["samples"], frame, range(F))
+    xi2 = np_(s.spectra_to_samples(y, pairs, spec).values)
+    err2 = np.abs(xi2 - g["xi_ifft"]).max(axis=1) / np.abs(g["xi_ifft"]).max(axis=1)
+    assert err2.max() < 2e-5
+
+
+# ------------------------------------------------------------------ maps
+
+def test_sspi_and_si_maps(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    xi = s.TdGccSamples(torch.from_numpy(g["xi_ifft"].astype(np.float32)).cuda(), spec)
+    for tag in keep_tags(g):
+        sp = sparse_from_golden(g, tag)
+        z, idx = s.sspi_map(sp, xi, argmax=True)
+        ref = g[f"z_sspi_{tag}"]
+        if np.abs(ref).max() == 0:
+            assert np.all(np_(z) == 0)
+            continue
+        assert_map_close(z, ref)
+        assert_argmax_agrees(idx, ref)
+    interp = s.InterpMatrix(g["interp"], spec)
+    z_si = s.si_map(interp, xi)
+    assert_map_close(z_si, g["z_si"])
+    z_all = s.sspi_map(sparse_from_golden(g, "all"), xi)
+    assert torch.equal(z_all, z_si)                        # bitwise, as in the reference
+
+
+def test_sspi_tile_and_row_kernels_agree(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    x = np.tile(g["xi_ifft"].astype(np.float32), (12, 1))     # >= 32 frames: tile kernel
+    zt = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x).cuda(), spec))
+    zr = torch.stack([s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[f]).cuda(), spec))
+                      for f in range(g["xi_ifft"].shape[0])])
+    assert torch.equal(zt[:zr.shape[0]], zr)
+
+
+def test_sspi_empty_operator_and_dimension_error(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    interp = s.InterpMatrix(g["interp"], spec)
+    sp0 = s.truncate_sparse(interp, 0)
+    z = s.sspi_map(sp0, torch.ones(spec.total_samples, device="cuda"))
+    assert torch.count_nonzero(z) == 0
+    with pytest.raises(s.DimensionError):
+        s.sspi_map(sp0, torch.ones(spec.total_samples + 1, device="cuda"))
+
+
+def test_slri_map(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    xi = torch.from_numpy(g["xi_ifft"].astype(np.float32)).cuda()
+    for r in g["ranks"]:
+        lr = s.LowRankInterp(g[f"slri_{r}_tall"], g[f"slri_{r}_fat"], np.zeros(r))
+        z, idx = s.slri_map(lr, xi, argmax=True)
+        assert_map_close(z, g[f"z_slri_{r}"])
+        assert_argmax_agrees(idx, g[f"z_slri_{r}"])
+    with pytest.raises(s.DimensionError):
+        s.slri_map(lr, torch.zeros(3, device="cuda"))
+
+
+def test_lr_map(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    psi = torch.from_numpy(g["psi"].astype(np.complex64)).cuda()
+    for r in g["ranks"]:
+        lr = s.LowRankSrp(g[f"lr_{r}_tall"], g[f"lr_{r}_fat"], np.zeros(r))
+        gcc = s.FdGcc(psi, pairs.num_pairs, frame.num_bins, "phat")
+        z, idx = s.lr_map(lr, gcc, argmax=True)
+        assert_map_close(z, g[f"z_lr_{r}"])
+        assert_argmax_agrees(idx, g[f"z_lr_{r}"])
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_conventional_map(golden_scene, precision):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    srp = s.build_srp_matrix(tdoa, frame, max_bytes=1 << 34)
+    gcc = s.FdGcc(torch.from_numpy(g["psi"].astype(np.complex64)).cuda(), pairs.num_pairs,
+                  frame.num_bins, "phat")
+    z, idx = s.srp_map_exact(srp, gcc, precision=precision, argmax=True)
+    err = assert_map_close(z, g["z_conv"])
+    if precision == "fp32":
+        assert err.max() < 1e-5
+    assert_argmax_agrees(idx, g["z_conv"])
+    z1 = s.srp_map_exact(srp, s.FdGcc(gcc.values[0], gcc.num_pairs, gcc.num_bins, "phat"),
+                         precision=precision)
+    assert z1.shape == (grid.num_points,)
+    with pytest.raises(s.DimensionError):
+        s.srp_map_exact(srp, s.FdGcc(gcc.values, gcc.num_pairs + 1, gcc.num_bins, "phat"))
+
+
+def test_locate_and_argmax_ties(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    i, q = s.locate(torch.from_numpy(g["z_conv"][0].astype(np.float32)).cuda(), grid)
+    zf = g["z_conv"][0].astype(np.float32)
+    assert i == int(np.argmax(zf))
+    np.testing.assert_array_equal(q, grid.points[i])
+    tie = torch.tensor([0.0, 5.0, 5.0, 1.0], device="cuda")
+    g4 = s.CandidateGrid("nf", np.arange(12.0).reshape(4, 3))
+    assert s.locate(tie, g4)[0] == 1
+    neg = torch.tensor([[-3.0, -1.0, -1.0, -2.0], [-0.0, 0.0, -5.0, -0.0]], device="cuda")
+    assert s.map_argmax(neg).tolist() == [1, 0]
+    with pytest.raises(s.DimensionError):
+        s.locate(torch.zeros(5, device="cuda"), g4)
+
+
+def test_full_chain_argmax(golden_scene):
+    """samples -> fused GCC+iFFT -> SSPI with fused argmax == reference argmax (margin rule)."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    xi = s.frames_to_samples(g["samples"], frame, pairs, spec, range(F))
+    tag = keep_tags(g)[-2] if len(keep_tags(g)) > 1 else keep_tags(g)[0]
+    z, idx = s.sspi_map(sparse_from_golden(g, tag), xi, argmax=True)
+    assert_map_close(z, g[f"z_sspi_{tag}"])
+    assert_argmax_agrees(idx, g[f"z_sspi_{tag}"])
+    zc, ic = s.srp_map_exact(s.build_srp_matrix(tdoa, frame, max_bytes=1 << 34),
+                             s.gcc_frames(g["samples"], frame, pairs, range(F)), argmax=True)
+    assert_map_close(zc, g["z_conv"])
+    assert_argmax_agrees(ic, g["z_conv"])
+
+
+# ------------------------------------------------------------------ known answers / edges
+
+def test_known_answers_on_gpu(known):
+    # single active bin -> z = 2 cos(w_k dt)   (test_srp.py:56-65)
+    frame = s.FrameSpec(frame_len=8, sample_rate=800)
+    srp = s.build_srp_matrix(s.TdoaTable(known["ka_cos_dt"], np.array([2e-3])), frame)
+    v = torch.zeros(3, dtype=torch.complex64, device="cuda")
+    v[0] = 1.0
+    z = s.srp_map_exact(srp, s.FdGcc(v, 1, 3, "none"), precision="fp32")
+    np.testing.assert_allclose(np_(z), known["ka_cos_z"], atol=1e-6)
+    # single bin -> sampled cosine            (test_sampling.py:67-79)
+    f32 = s.FrameSpec(frame_len=32, sample_rate=1000)
+    spec = s.SampleSpec(known["ka_cos_counts"], 0, 16)
+    per = torch.zeros((3, 15), dtype=torch.complex64, device="cuda")
+    per[:, 4] = 1.0
+    xi = s.td_gcc_samples(s.FdGcc(per.reshape(-1), 3, 15, "none"), spec)
+    np.testing.assert_allclose(np_(xi.values), known["ka_cos_xi"], atol=1e-5)
+    # integer circular delay -> exact phase ramp (rect window)   (test_frontend.py:89-100)
+    arr = s.MicrophoneArray(np.array([[0.0, 0, 0], [0.1, 0, 0]]))
+    pairs = s.enumerate_pairs(arr)
+    rect = s.FrameSpec(frame_len=32, sample_rate=1000, window="rect")
+    psi = s.fd_gcc(s.stft_frame(known["ka_ramp_signal"], rect, 0), pairs)
+    np.testing.assert_allclose(np_(psi.values), known["ka_ramp_psi"], atol=2e-6)
+    # floored bin is exactly 0                (test_frontend.py:137-145)
+    fl = np_(s.fd_gcc(known["ka_floor_spectra"], pairs).values)
+    assert fl[4] == 0.0
+    np.testing.assert_allclose(np.abs(np.delete(fl, 4)), 1.0, atol=1e-6)
+    # explicit floor on all-zero spectra gives 0 (test_frontend.py:102-105)
+    zero = s.fd_gcc(np.zeros((2, 9), complex), pairs, floor=1e-9)
+    assert torch.count_nonzero(zero.values) == 0
+
+
+def test_frontend_errors():
+    arr = s.MicrophoneArray(np.array([[0.0, 0, 0], [0.1, 0, 0]]))
+    pairs = s.enumerate_pairs(arr)
+    spec = s.FrameSpec(frame_len=16, sample_rate=100, hop=4)
+    x = np.random.default_rng(0).standard_normal((1, 40))
+    out = np_(s.stft_frame(x, spec, 2))
+    np.testing.assert_allclose(out[0], np.fft.rfft(x[0, 8:24] * s.frame_window(spec)), atol=1e-5)
+    assert s.num_frames(spec, 40) == 7
+    with pytest.raises(IndexError):
+        s.stft_frame(x, spec, 7)
+    with pytest.raises(IndexError):
+        s.stft_frame(x, spec, -1)
+    with pytest.raises(s.DimensionError):
+        s.fd_gcc(np.zeros((3, 9), complex), pairs)
+    with pytest.raises(ValueError):
+        s.fd_gcc(np.zeros((2, 9), complex), pairs, weighting="scot")
+    # identical channels give unit phase     (test_frontend.py:83-87)
+    y = np.random.default_rng(3).standard_normal(9) + 1j * np.random.default_rng(4).standard_normal(9)
+    np.testing.assert_allclose(np_(s.fd_gcc(np.stack([y, y]), pairs).values), 1.0, atol=1e-6)
+
+
+def test_evaluate_map_dispatch(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    gcc = s.FdGcc(torch.from_numpy(g["psi"].astype(np.complex64)).cuda(), pairs.num_pairs,
+                  frame.num_bins, "phat")
+    tag = keep_tags(g)[0]
+    z = s.evaluate_map("sspi", sparse_from_golden(g, tag), spec, frame, gcc, "auto")
+    assert_map_close(z, g[f"z_sspi_{tag}"])
+    z = s.evaluate_map("si", s.InterpMatrix(g["interp"], spec), spec, frame, gcc, "matrix")
+    assert_map_close(z, g["z_si"])
+    with pytest.raises(ValueError):
+        s.evaluate_map("xyz", None, spec, frame, gcc, "ifft")

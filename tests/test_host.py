@@ -1,0 +1,180 @@
+"""Host-side logic of the product (no GPU): geometry, operator fits, ELL layout.
+
+Operator fitting stays on the host and is uploaded once; these tests pin it
+bit-exactly to reference-generated golden vectors (sparse structure, TDOA,
+lag counts) and check the pair-major ELL encoding decodes back to the
+reference CSR exactly.
+"""
+
+import numpy as np
+import pytest
+from numpy.testing import assert_allclose, assert_array_equal
+
+import paper_2306_08514_b200 as s
+from paper_2306_08514_b200 import operators, scene
+from paper_2306_08514_b200.distributed import decode_host_keys, offset_keys, partition
+from conftest import keep_tags, scene_objects, sparse_from_golden
+
+
+def test_scene_matches_reference(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    assert_array_equal(pairs.pairs, g["pairs"])
+    assert_array_equal(pairs.distances, g["distances"])
+    assert_array_equal(tdoa.delta_t, g["delta_t"])
+    assert_array_equal(tdoa.limits, g["limits"])
+    assert_array_equal(spec.counts, g["counts"])
+    assert_array_equal(spec.offsets, g["offsets"])
+    assert_array_equal(s.frame_window(frame), g["window"])
+
+
+def test_grids():
+    g = s.build_nf_grid((0, 0, 0), (4, 4, 0), 0.1)
+    assert g.num_points == 1681
+    assert_allclose(g.points[1], [0.1, 0, 0])          # x fastest
+    ff = s.build_ff_grid(1.0, collapse_poles=False)
+    assert ff.num_points == 32760
+    assert np.all(ff.points[-360:] == np.array([0.0, 0.0, -1.0]))
+    assert s.build_ff_grid(1.0).num_points == 32401      # reference layout (pole once)
+    big = s.build_nf_grid((0, 0, 0), (4, 4, 2.5), 0.05)
+    assert big.num_points == 334611
+
+
+def test_operators_match_reference(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    interp = s.build_interp_matrix(tdoa, spec, frame)
+    assert_array_equal(interp.matrix, g["interp"])
+    for tag in keep_tags(g):
+        sp = s.truncate_sparse(interp, int(g[f"sp_{tag}_keep"]))
+        ref = sparse_from_golden(g, tag)
+        assert_array_equal(sp.values, ref.values)
+        assert_array_equal(sp.col_indices, ref.col_indices)
+        assert_array_equal(sp.row_splits, ref.row_splits)
+    srp = s.build_srp_matrix(tdoa, frame, max_bytes=1 << 34)
+    z = 2.0 * (g["psi"] @ srp.matrix.T).real
+    assert_allclose(z, g["z_conv"], rtol=1e-12, atol=1e-9)
+
+
+def test_truncate_sparse_ties_and_bounds():
+    mk = lambda m: s.InterpMatrix(np.asarray(m, float), s.SampleSpec(np.zeros(np.shape(m)[1], np.int64), 0, 64))
+    sp = s.truncate_sparse(mk([[0.5, -0.5], [0.5, 0.5]]), 2)
+    assert_array_equal(sp.to_dense(), [[0.5, -0.5], [0.0, 0.0]])
+    sp = s.truncate_sparse(mk([[0.9, -0.5, 0.1], [0.2, -0.8, 0.3]]), 2)
+    assert_array_equal(sp.to_dense(), [[0.9, 0, 0], [0, -0.8, 0]])
+    assert s.truncate_sparse(mk([[1.0, 2.0]]), 0).num_kept == 0
+    with pytest.raises(ValueError):
+        s.truncate_sparse(mk([[1.0, 2.0]]), 3)
+    with pytest.raises(ValueError):
+        s.truncate_sparse(mk([[1.0, 2.0]]), -1)
+
+
+def test_fixed_nnz_fit_keeps_nearest_lags(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    interp = s.build_interp_matrix(tdoa, spec, frame)
+    off = spec.offsets
+    for nnz in (1, 2, 4):
+        sp = s.truncate_sparse_fixed(interp, nnz)
+        expect = sum(min(nnz, int(2 * c + 1)) for c in spec.counts) * grid.num_points
+        assert sp.num_kept == expect
+        dense = sp.to_dense()
+        kept = np.zeros(interp.matrix.shape, bool)
+        kept[np.repeat(np.arange(grid.num_points), np.diff(sp.row_splits)), sp.col_indices] = True
+        mag = np.abs(interp.matrix)
+        for p in range(spec.num_pairs):
+            blk, kb = mag[:, off[p]:off[p + 1]], kept[:, off[p]:off[p + 1]]
+            lo = np.where(kb, blk, np.inf).min(axis=1)
+            hi = np.where(kb, -np.inf, blk).max(axis=1)
+            assert np.all(lo >= hi)                       # top-k of every (i, p) block
+        assert_array_equal(dense[kept], interp.matrix[kept])
+    # nnz = 1 equals the reference global fit at keep = J*P whenever that fit is one-per-(i, p)
+    sp1 = s.truncate_sparse_fixed(interp, 1)
+    glob = s.truncate_sparse(interp, grid.num_points * spec.num_pairs)
+    pair_g = np.searchsorted(off, glob.col_indices, side="right") - 1
+    rows_g = np.repeat(np.arange(grid.num_points), np.diff(glob.row_splits))
+    per = np.zeros((grid.num_points, spec.num_pairs), int)
+    np.add.at(per, (rows_g, pair_g), 1)
+    if np.all(per == 1):
+        assert_array_equal(sp1.col_indices, glob.col_indices)
+
+
+def _ell(sp, off):
+    # EllOperator needs a device for its upload; build the host image only
+    from paper_2306_08514_b200 import maps
+    import torch
+
+    class HostEll(maps.EllOperator):
+        pass
+    orig = maps.dev.device
+    maps.dev.device = lambda: torch.device("cpu")
+    try:
+        return maps.EllOperator(sp.values, sp.col_indices, sp.row_splits, int(sp.num_cols), off)
+    finally:
+        maps.dev.device = orig
+
+
+def test_ell_roundtrip_bit_exact(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    for tag in keep_tags(g):
+        ref = sparse_from_golden(g, tag)
+        ell = _ell(ref, spec.offsets)
+        vals, cols, splits = ell.to_csr()
+        assert_array_equal(cols, ref.col_indices)
+        assert_array_equal(splits, ref.row_splits)
+        assert_array_equal(vals, ref.values.astype(np.float32))
+        assert np.all(ell.widths <= np.diff(spec.offsets))
+        # padding entries are zero-valued and point inside their pair block
+        packed = ell.host_packed
+        assert np.all(packed[:, 1] < spec.offsets[-1])
+
+
+def test_ell_empty_and_keep_all(golden_scene):
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    interp = s.build_interp_matrix(tdoa, spec, frame)
+    empty = _ell(s.truncate_sparse(interp, 0), spec.offsets)
+    assert empty.widths.sum() == 0
+    full = _ell(s.truncate_sparse(interp, interp.matrix.size), spec.offsets)
+    assert_array_equal(full.widths, np.diff(spec.offsets))
+
+
+def test_errors_mirror_reference():
+    assert issubclass(s.DimensionError, ValueError) and issubclass(s.DimensionError, s.SrpMapError)
+    assert issubclass(s.ConfigError, ValueError)
+    assert not issubclass(s.CapacityError, ValueError)
+    with pytest.raises(s.InvalidGeometryError):
+        s.MicrophoneArray(np.zeros((1, 3)))
+    with pytest.raises(s.InvalidGridError):
+        s.CandidateGrid("ff", np.array([[2.0, 0, 0]]))
+    with pytest.raises(s.CapacityError):
+        tdoa = s.TdoaTable(np.zeros((1000, 6)), np.ones(6))
+        s.build_srp_matrix(tdoa, s.FrameSpec(512, 4000), max_bytes=10_000)
+    with pytest.raises(s.ConfigError):
+        s.sample_spec(s.TdoaTable(np.zeros((1, 1)), np.array([1.0])), s.FrameSpec(64, 8000))
+    with pytest.raises(ValueError):
+        s.FrameSpec(5, 100)
+
+
+def test_partition_and_keys():
+    import torch
+    assert [partition(10, 3, r) for r in range(3)] == [(0, 4), (4, 3), (7, 3)]
+    assert sum(partition(1000, 8, r)[1] for r in range(8)) == 1000
+    # a key for value 2.5 at index 7, re-based by an offset of 100
+    v = np.float32(2.5).view(np.uint32)
+    hi = int(v) | 0x80000000
+    key = torch.tensor([(hi << 32 | (0xFFFFFFFF - 7)) - (1 << 64)], dtype=torch.int64)
+    idx, val = decode_host_keys(key)
+    assert idx.item() == 7 and val.item() == 2.5
+    idx, _ = decode_host_keys(offset_keys(key, 100))
+    assert idx.item() == 107
+
+
+def test_workloads_deterministic():
+    from paper_2306_08514_b200 import workloads
+    a = workloads.make("cfg1", num_frames=8)
+    b = workloads.make("cfg1", num_frames=8)
+    assert_array_equal(a.samples, b.samples)
+    assert a.grid.num_points == 1681 and a.pairs.num_pairs == 6
+    assert a.samples.shape == (4, 7 * 512 + 1024)
