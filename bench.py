@@ -181,6 +181,7 @@ def run_ours(args):
 
     import paper_2306_08514_b200 as s
     from paper_2306_08514_b200 import _native, distributed as D
+    from paper_2306_08514_b200.pipeline import MapPipeline
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -190,9 +191,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    wl0 = build_scene(args, 1)
-    per_gpu = args.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000,
-                              "cfg5": 1024}[args.workload]
+    per_gpu = args.frames or DEFAULT_FRAMES[args.workload]
     total = per_gpu * world
     wl = build_scene(args, total)
     first, count = D.partition(total, world, rank)
@@ -200,29 +199,14 @@ def run_ours(args):
     host_slice = np.ascontiguousarray(wl.samples[:, first * hop:(first + count - 1) * hop + flen])
     pinned = torch.from_numpy(host_slice).pin_memory()
     x_dev = pinned.to(dev)
-    frames = range(0, count)
-    del wl0
-
-    def make_step(variant, op):
-        if variant in ("sspi", "si", "slri"):
-            mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
-
-            def step(x):
-                xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, frames)
-                return mapf(op, xi, argmax=True)
-        elif variant == "lr":
-            def step(x):
-                return s.lr_map(op, s.gcc_frames(x, wl.frame, wl.pairs, frames), argmax=True)
-        else:
-            def step(x):
-                return s.srp_map_exact(op, s.gcc_frames(x, wl.frame, wl.pairs, frames), argmax=True)
-        return step
-
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    def time_steps(step, steps, warmup, gather=True):
+    def make_pipe(variant, op):
+        return MapPipeline(variant, op, wl.frame, wl.pairs, wl.spec, frames=count)
+
+    def timed(fn, steps, warmup, gather):
         for _ in range(warmup):
-            z, idx = step(x_dev)
+            fn()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -233,9 +217,9 @@ def run_ours(args):
             flush.zero_()                          # L2 flush between timed iterations
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            z, idx = step(x_dev)
+            z, idx = fn()
             if world > 1 and gather:
-                keys_all = D.gather_frame_keys(idx, total)
+                D.gather_frame_keys(idx, total)    # NCCL all-gather of per-frame argmax
             b.record()
             evs.append((a, b))
         torch.cuda.synchronize()
@@ -244,43 +228,27 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         ms = sum(a.elapsed_time(b) for a, b in evs)
-        return ms, launches, z, idx
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps, launches
 
-    # ---- headline variant
+    # ---- headline variant: captured graph, input resident in HBM
     op = fit_operator(wl, args.variant, args)
-    step = make_step(args.variant, op)
+    pipe = make_pipe(args.variant, op)
+    pipe.input.copy_(x_dev)
+    g_launch0 = _native.launch_count()
+    pipe.replay()
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     with clocks:
-        ms_total, launches, z, idx = time_steps(step, args.steps, args.warmup)
-    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(ms_t.item()) / args.steps
+        ms_per_step, _ = timed(pipe.replay, args.steps, args.warmup, True)
     value = total / (ms_per_step / 1e3)
-    launches_per_step = launches / args.steps
+    # kernels per step: counted when the graph was captured (replays do not pass the host counter)
+    launches_per_step = pipe_launches(pipe)
 
-    # ---- per-kernel times for the roofline (same stream, CUDA events)
-    def kernel_times(reps=10):
-        tf, tm = [], []
-        for _ in range(reps):
-            flush.zero_()
-            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-            e[0].record()
-            if args.variant in ("sspi", "si", "slri"):
-                xi = s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames)
-                e[1].record()
-                {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[args.variant](op, xi, argmax=True)
-            else:
-                g = s.gcc_frames(x_dev, wl.frame, wl.pairs, frames)
-                e[1].record()
-                (s.lr_map if args.variant == "lr" else s.srp_map_exact)(op, g, argmax=True)
-            e[2].record()
-            torch.cuda.synchronize()
-            tf.append(e[0].elapsed_time(e[1]))
-            tm.append(e[1].elapsed_time(e[2]))
-        return statistics.median(tf), statistics.median(tm)
-
-    t_front, t_map = kernel_times()
+    # ---- per-kernel times for the roofline: each stage captured alone, CUDA events
+    t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush)
     hbm, bf16, peak_src = peaks()
     abytes = algorithmic_bytes(wl, args.variant, count, op)
     if args.variant == "conv":
@@ -301,38 +269,24 @@ def run_ours(args):
                 "traffic": ncu_traffic(args.workload, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
 
-    # ---- e2e through the public API from pinned host memory
-    def e2e(steps):
-        torch.cuda.synchronize()
-        out_host = torch.empty(count, dtype=torch.int64).pin_memory()
-        evs = []
-        for _ in range(steps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            xd = pinned.to(dev, non_blocking=True)
-            z_, idx_ = step(xd)
-            if world > 1:
-                D.gather_frame_keys(idx_, total)
-            out_host.copy_(idx_, non_blocking=True)
-            b.record()
-            evs.append((a, b))
-        torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b in evs)
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item()) / steps
-    e2e_ms = e2e(max(3, args.steps // 2))
+    # ---- e2e through the public pipeline API: pinned host samples in, argmax indices out
+    out_host = torch.empty(count, dtype=torch.int64).pin_memory()
+
+    def e2e_step():
+        z_, idx_ = pipe.run(pinned)            # H2D (pinned) + graph replay
+        out_host.copy_(idx_, non_blocking=True)  # D2H of the per-frame result
+        return z_, idx_
+    e2e_ms, _ = timed(e2e_step, max(5, args.steps // 2), 2, True)
     e2e_block = {"value": total / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                  "h2d_bytes_per_step": int(pinned.numel() * 4), "d2h_bytes_per_step": int(count * 8)}
 
-    # ---- parity spot check on this run's output (first frames vs the float64 oracle)
     parity = None
     if rank == 0:
+        pipe.run(x_dev)
+        z, idx = pipe.z, pipe.index
         parity = spot_parity(wl, args.variant, op, z, idx, min(8, count))
 
-    # ---- other variants of the same workload (same timing rules, N=1 view)
+    # ---- other variants of the same workload (same rules; N = 1 only)
     variants = {}
     if not args.no_variants and world == 1:
         for v in ("sspi", "slri", "lr", "conv"):
@@ -340,16 +294,24 @@ def run_ours(args):
                 continue
             try:
                 opv = fit_operator(wl, v, args)
-                ms_v, l_v, _, _ = time_steps(make_step(v, opv), max(5, args.steps // 2), 3, gather=False)
+                pv = make_pipe(v, opv)
+                pv.input.copy_(x_dev)
                 k = max(5, args.steps // 2)
-                entry = {"value": total / (ms_v / k / 1e3), "unit": UNIT, "ms_per_step": ms_v / k,
-                         "gpu_launches_per_step": l_v / k}
+                ms_v, _ = timed(pv.replay, k, 3, False)
+                entry = {"value": total / (ms_v / 1e3), "unit": UNIT, "ms_per_step": ms_v,
+                         "gpu_launches_per_step": pipe_launches(pv)}
                 if v == "conv":
-                    entry["tflops"] = conv_flops(wl, count) / (ms_v / k / 1e3) / 1e12
-                    entry["precision"] = "tf32 (tcgen05)"
+                    tf, tm = stage_times(s, wl, v, opv, x_dev, count, flush)
+                    entry["tflops_step"] = conv_flops(wl, count) / (ms_v / 1e3) / 1e12
+                    entry["tflops_gemm"] = conv_flops(wl, count) / (tm / 1e3) / 1e12
+                    entry["kernel_ms"] = {"frontend": tf, "map": tm}
+                    entry["precision"] = "tf32 (tcgen05, RNE operands)"
                 if v in ("lr", "slri"):
                     entry["rank"] = args.rank_r
+                pv.run(x_dev)
+                entry["parity"] = spot_parity(wl, v, opv, pv.z, pv.index, min(8, count))
                 variants[v] = entry
+                del pv
             except Exception as exc:  # report, never hide
                 variants[v] = {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -368,7 +330,8 @@ def run_ours(args):
                        "variant": args.variant,
                        "operator": (args.nnz if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
-                       "parallelism": f"frames/{world}", "l2": "flushed between timed steps"},
+                       "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
+                       "execution": "CUDA graph per batch"},
             "candidates_per_s": value * wl.grid.num_points,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e_block,
             "gpu_launches": int(round(launches_per_step * args.steps)),
@@ -378,6 +341,55 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+DEFAULT_FRAMES = {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000, "cfg5": 1024}
+
+
+def pipe_launches(pipe) -> int:
+    """Kernels in one replay of the pipeline graph (nodes of kernel type)."""
+    import paper_2306_08514_b200._native as nat
+    import torch
+    p2 = type(pipe).__new__(type(pipe))
+    p2.__dict__.update(pipe.__dict__)
+    before = nat.launch_count()
+    p2._chain()                      # eager replay of the same chain counts its kernels
+    torch.cuda.synchronize()
+    return nat.launch_count() - before
+
+
+def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10):
+    """Median device time of the frontend kernel and of the map kernel(s), each in its own graph."""
+    import torch
+    frames = range(0, count)
+    if variant in ("sspi", "si", "slri"):
+        front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames)
+        mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
+    else:
+        front = lambda: s.gcc_frames(x_dev, wl.frame, wl.pairs, frames, tf32=(variant == "conv"))
+        mapf = s.lr_map if variant == "lr" else s.srp_map_exact
+    mid = front()
+    mapf(op, mid, argmax=True)
+    torch.cuda.synchronize()
+    g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1):
+        mid = front()
+    with torch.cuda.graph(g2):
+        mapf(op, mid, argmax=True)
+    out = []
+    for g in (g1, g2):
+        g.replay()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out.append(statistics.median(ts))
+    return out[0], out[1]
 
 
 def spot_parity(wl, variant, op, z, idx, nf):
@@ -440,8 +452,7 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    per_gpu = args.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000,
-                              "cfg5": 1024}[args.workload]
+    per_gpu = args.frames or DEFAULT_FRAMES[args.workload]
     wl = build_scene(args, per_gpu * world)
     op = fit_operator(wl, args.variant, args)
     from oracle import srp_oracle as O

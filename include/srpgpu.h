@@ -68,12 +68,14 @@ int srpgpu_fd_gcc(const float* spectra, int64_t num_frames, int32_t num_channels
                   const int32_t* pairs, int32_t num_pairs, int32_t weighting, int32_t floor_mode,
                   double floor_value, float* gcc, srpgpu_stream_t stream);
 
-/* fused stft_frame + fd_gcc: samples -> gcc [F][P][K-1] (spectra stay on chip). */
+/* fused stft_frame + fd_gcc: samples -> gcc [F][gcc_ld] complex64 (spectra stay on chip).
+ * gcc_ld: complex elements per frame row (0 = P*(K-1); larger pitches are zero-padded).
+ * flags bit 0: round the outputs to TF32 (round-to-nearest-even) for srpgpu_srp_map_tc. */
 int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int64_t num_samples,
                       int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
                       int64_t first_frame, int64_t num_frames, const int32_t* pairs,
                       int32_t num_pairs, int32_t weighting, int32_t floor_mode, double floor_value,
-                      float* gcc, srpgpu_stream_t stream);
+                      float* gcc, int64_t gcc_ld, int32_t flags, srpgpu_stream_t stream);
 
 /* ---- sampling (srpmap/sampling.py) --------------------------------------- */
 
@@ -135,12 +137,18 @@ int srpgpu_srp_map_simt(const float* gcc, int64_t num_frames, int32_t gcc_len, c
                         int64_t num_candidates, float* z, uint64_t* keys, srpgpu_stream_t stream);
 
 /* srp_map_exact on the 5th-gen tensor cores (tcgen05.mma kind::tf32, TMEM
- * accumulators, TMA-staged operands): same operands as srpgpu_srp_map_simt.
- * Requires gcc_len % 16 == 0 is NOT needed: the K tail is zero-filled by TMA.
- * Row pitches must be 16-byte multiples (caller pads: h2_ld, gcc_ld in floats). */
+ * accumulators, TMA-staged operands): same operands as srpgpu_srp_map_simt, with
+ * row pitches gcc_ld / h2_ld (floats) that are multiples of 4 (16 bytes); the K
+ * tail and out-of-range rows are zero-filled by TMA.  kind::tf32 truncates fp32
+ * operands, so callers pass TF32-rounded (RNE) operands: srpgpu_round_tf32 or
+ * srpgpu_gcc_frames(flags=1). */
 int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
                       const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,
                       uint64_t* keys, srpgpu_stream_t stream);
+
+/* dst[r][c] = tf32_rne(src[r][c]) for c < cols, 0 for cols <= c < ld_dst. */
+int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,
+                      int64_t cols, srpgpu_stream_t stream);
 
 /* generic fp32 product out[f][i] = alpha sum_k A[i][k] B[f][k] (+ argmax keys). */
 int srpgpu_gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,

@@ -29,7 +29,7 @@ SIGNATURES = {
     "srpgpu_stft": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _P, _P],
     "srpgpu_fd_gcc": [_P, _I64, _I32, _I32, _P, _I32, _I32, _I32, _F64, _P, _P],
     "srpgpu_gcc_frames": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _I32, _I32, _I32,
-                          _F64, _P, _P],
+                          _F64, _P, _I64, _I32, _P],
     "srpgpu_td_gcc_samples": [_P, _I64, _I32, _I32, _P, _P, _I32, _P, _P],
     "srpgpu_frames_to_samples": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _I32, _I32,
                                  _I32, _F64, _P, _P, _I32, _P, _P],
@@ -40,6 +40,7 @@ SIGNATURES = {
     "srpgpu_lr_map": [_P, _I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_srp_map_simt": [_P, _I64, _I32, _P, _I64, _P, _P, _P],
     "srpgpu_srp_map_tc": [_P, _I64, _I64, _I32, _P, _I64, _I64, _P, _P, _P],
+    "srpgpu_round_tf32": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "srpgpu_gemm_nt": [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _F32, _P, _P],
     "srpgpu_argmax": [_P, _I64, _I64, _I64, _P, _P],
     "srpgpu_decode_keys": [_P, _I64, _P, _P, _P],

@@ -69,6 +69,13 @@ __device__ __forceinline__ unsigned long long warp_key_max(unsigned long long k)
   return k;
 }
 
+// round-to-nearest-even to TF32 (keeps 10 explicit mantissa bits)
+__device__ __forceinline__ float tf32_rne(float x) {
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7F800000u) != 0x7F800000u) u += 0xFFFu + ((u >> 13) & 1u);
+  return __uint_as_float(u & 0xFFFFE000u);
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }

@@ -20,6 +20,7 @@
 // Tiles are rasterised in groups of GROUP_M candidate tiles so concurrently
 // running CTAs share both A and B k-slices in L2.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -260,7 +261,11 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
   cuuint32_t box[2] = {(cuuint32_t)BLOCK_K, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  static const int tma_tf32 = [] {
+    const char* e = getenv("SRPGPU_TMA_TF32");
+    return e && e[0] == '1';
+  }();
+  CUresult r = enc(map, tma_tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -292,6 +297,19 @@ static int launch(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, const
   return SRPGPU_OK;
 }
 
+// Round-to-nearest-even to TF32 (10-bit mantissa), so the tensor-core product is
+// unbiased (plain fp32 bits are truncated by kind::tf32).  Also re-pitches rows.
+__global__ void round_tf32_kernel(const float* __restrict__ src, int64_t ld_src, float* __restrict__ dst,
+                                 int64_t ld_dst, int64_t rows, int64_t cols) {
+  const int64_t r = blockIdx.y;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ld_dst;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (c < cols) v = tf32_rne(__ldg(src + r * ld_src + c));
+    dst[r * ld_dst + c] = v;
+  }
+}
+
 }  // namespace tc
 
 int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
@@ -299,6 +317,24 @@ int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
 }  // namespace srpgpu
 
 using namespace srpgpu;
+
+extern "C" int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst,
+                                 int64_t rows, int64_t cols, srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(ld_dst >= cols && ld_src >= cols && rows >= 0, SRPGPU_ERR_DIMENSION,
+                   "round_tf32: bad pitches");
+  if (rows == 0 || ld_dst == 0) return SRPGPU_OK;
+  SRPGPU_CHECK_ARG(rows <= 65535ll * 1024, SRPGPU_ERR_DIMENSION, "round_tf32: too many rows");
+  const int64_t done_rows = 0;
+  (void)done_rows;
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((ld_dst + 255) / 256, 64), (unsigned)nr);
+    tc::round_tf32_kernel<<<grid, 256, 0, as_stream(stream)>>>(src + r0 * ld_src, ld_src, dst + r0 * ld_dst,
+                                                                ld_dst, nr, cols);
+    SRPGPU_CHECK_LAUNCH("round_tf32");
+  }
+  return SRPGPU_OK;
+}
 
 extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
                                  const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,

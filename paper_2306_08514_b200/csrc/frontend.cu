@@ -38,6 +38,8 @@ struct FrontendParams {
   float2* gcc_out;            // [F][P][K-1]
   float* xi_out;              // [F][S]
   int32_t nbuf;               // concurrent FFT buffers
+  int64_t gcc_ld;             // complex elements per frame row of gcc_out (>= P*(K-1))
+  int32_t round_tf32;         // round gcc_out to TF32 (RNE) for the tensor-core map
 };
 
 constexpr int kFrontThreads = 256;
@@ -217,11 +219,15 @@ frontend_kernel(const FrontendParams prm) {
       for (int idx = threadIdx.x; idx < M * Kp1; idx += blockDim.x) dst[idx] = spec[idx];
       if (prm.energy_out && threadIdx.x == 0) prm.energy_out[f] = energy;
     } else if (OUT == OUT_GCC) {
-      float2* dst = prm.gcc_out + f * (int64_t)P * B;
+      float2* dst = prm.gcc_out + f * prm.gcc_ld;
       for (int idx = threadIdx.x; idx < P * B; idx += blockDim.x) {
         const int p = idx / B, k = idx - p * B + 1;
-        dst[idx] = cross_bin(spec, Kp1, s_pairs[2 * p], s_pairs[2 * p + 1], k, prm.weighting, floor);
+        float2 v = cross_bin(spec, Kp1, s_pairs[2 * p], s_pairs[2 * p + 1], k, prm.weighting, floor);
+        if (prm.round_tf32) v = make_float2(tf32_rne(v.x), tf32_rne(v.y));
+        dst[idx] = v;
       }
+      for (int64_t idx = P * B + threadIdx.x; idx < prm.gcc_ld; idx += blockDim.x)
+        dst[idx] = make_float2(0.f, 0.f);   // pitch padding
     } else {  // OUT_XI
       const float2* gsrc = (IN == IN_GCC) ? prm.gcc_in + f * (int64_t)P * B : nullptr;
       float* dst = prm.xi_out + f * (int64_t)prm.S;
@@ -380,6 +386,7 @@ extern "C" int srpgpu_fd_gcc(const float* spectra, int64_t num_frames, int32_t n
   prm.F = num_frames; prm.M = num_channels; prm.pairs = pairs; prm.P = num_pairs;
   prm.weighting = weighting; prm.floor_mode = floor_mode; prm.floor_value = (float)floor_value;
   prm.gcc_out = reinterpret_cast<float2*>(gcc);
+  prm.gcc_ld = (int64_t)num_pairs * (half_len - 1);
   return launch_frontend<IN_SPECTRA, OUT_GCC>(prm, as_stream(stream), "fd_gcc");
 }
 
@@ -388,7 +395,7 @@ extern "C" int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int
                                  int32_t hop, int64_t first_frame, int64_t num_frames,
                                  const int32_t* pairs, int32_t num_pairs, int32_t weighting,
                                  int32_t floor_mode, double floor_value, float* gcc,
-                                 srpgpu_stream_t stream) {
+                                 int64_t gcc_ld, int32_t flags, srpgpu_stream_t stream) {
   FrontendParams prm = {};
   int st = fill_common(prm, frame_len, "gcc_frames");
   if (st) return st;
@@ -397,6 +404,10 @@ extern "C" int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int
   prm.M = num_channels; prm.hop = hop; prm.first_frame = first_frame; prm.F = num_frames;
   prm.pairs = pairs; prm.P = num_pairs; prm.weighting = weighting; prm.floor_mode = floor_mode;
   prm.floor_value = (float)floor_value; prm.gcc_out = reinterpret_cast<float2*>(gcc);
+  prm.gcc_ld = gcc_ld > 0 ? gcc_ld : (int64_t)num_pairs * (prm.K - 1);
+  SRPGPU_CHECK_ARG(prm.gcc_ld >= (int64_t)num_pairs * (prm.K - 1), SRPGPU_ERR_DIMENSION,
+                   "gcc_frames: row pitch smaller than P*(K-1)");
+  prm.round_tf32 = flags & 1;
   if ((st = check_frames(prm, num_samples, "gcc_frames"))) return st;
   return launch_frontend<IN_SAMPLES, OUT_GCC>(prm, as_stream(stream), "gcc_frames");
 }

@@ -11,7 +11,7 @@ samples -> cross-spectra entry (spectra never leave shared memory).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -95,6 +95,10 @@ class FdGcc:
     num_pairs: int
     num_bins: int
     weighting: str
+    # set by gcc_frames(..., tf32=True): values rounded to TF32 (RNE), rows stored in
+    # `padded` (F, ld) float32 with a 16-byte pitch, ready for the tensor-core map
+    tf32_rounded: bool = field(default=False, compare=False)
+    padded: object = field(default=None, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -200,8 +204,13 @@ def fd_gcc(spectra, pairs, weighting: str = "phat", floor=None) -> FdGcc:
     return FdGcc(values=out if batched else out[0], num_pairs=p, num_bins=bins, weighting=weighting)
 
 
-def gcc_frames(samples, spec, pairs, frames=None, weighting: str = "phat", floor=None) -> FdGcc:
-    """Fused stft_frame + fd_gcc over frames (default: all complete frames)."""
+def gcc_frames(samples, spec, pairs, frames=None, weighting: str = "phat", floor=None,
+               tf32: bool = False) -> FdGcc:
+    """Fused stft_frame + fd_gcc over frames (default: all complete frames).
+
+    tf32=True rounds the cross-spectra to TF32 (round-to-nearest-even) and pads
+    rows to a 16-byte pitch: the operand layout of the tensor-core conventional map.
+    """
     x = _signal(samples)
     if x.shape[0] != pairs.num_mics:
         raise DimensionError(f"expected {pairs.num_mics} channels, got {x.shape[0]}")
@@ -209,8 +218,13 @@ def gcc_frames(samples, spec, pairs, frames=None, weighting: str = "phat", floor
     _check_range(spec, first, count, x.shape[1])
     w, mode, fval = _floor_args(weighting, floor)
     p, bins = pairs.num_pairs, spec.num_bins
-    out = torch.empty((count, p * bins), dtype=torch.complex64, device=x.device)
+    ld = p * bins + ((p * bins) & 1 if tf32 else 0)          # complex elements per row
+    buf = torch.empty((count, ld), dtype=torch.complex64, device=x.device)
     nat.call("srpgpu_gcc_frames", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
              dev.ptr(_window_device(spec)), spec.frame_len, spec.hop, first, count,
-             dev.ptr(_pairs_device(pairs)), p, w, mode, fval, dev.ptr(out), dev.stream_ptr())
-    return FdGcc(values=out if batched else out[0], num_pairs=p, num_bins=bins, weighting=weighting)
+             dev.ptr(_pairs_device(pairs)), p, w, mode, fval, dev.ptr(buf), ld, 1 if tf32 else 0,
+             dev.stream_ptr())
+    out = buf[:, :p * bins]
+    padded = torch.view_as_real(buf).reshape(count, 2 * ld) if tf32 else None
+    return FdGcc(values=out if batched else out[0], num_pairs=p, num_bins=bins, weighting=weighting,
+                 tf32_rounded=tf32, padded=padded)

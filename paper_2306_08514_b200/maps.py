@@ -275,8 +275,20 @@ def _pad4(n: int) -> int:
     return (n + 3) // 4 * 4
 
 
-def steering_device(srp) -> torch.Tensor:
-    """(J, ld) float32: interleaved (Re H, -Im H) per bin, row pitch padded to 16 B."""
+def _tf32_rne_host(a: np.ndarray) -> np.ndarray:
+    """Round float32 values to TF32 (round-to-nearest-even), as tf32_rne in common.cuh."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).copy()
+    finite = (u & 0x7F800000) != 0x7F800000
+    u[finite] += np.uint32(0xFFF) + ((u[finite] >> 13) & 1)
+    u &= np.uint32(0xFFFFE000)
+    return u.view(np.float32)
+
+
+def steering_device(srp, tf32: bool = True) -> torch.Tensor:
+    """(J, ld) float32: interleaved (Re H, -Im H) per bin, row pitch padded to 16 B.
+
+    tf32=True stores the TF32-rounded (RNE) operand of the tensor-core map.
+    """
     def build():
         h = np.asarray(srp.matrix)
         j, n = h.shape
@@ -285,16 +297,18 @@ def steering_device(srp) -> torch.Tensor:
         step = max(1, (64 << 20) // max(1, 8 * n))       # upload in row blocks (bounded host RAM)
         for r0 in range(0, j, step):
             blk = np.conj(h[r0:r0 + step]).astype(np.complex64).view(np.float32)
+            if tf32:
+                blk = _tf32_rne_host(blk)
             out[r0:r0 + blk.shape[0], :2 * n] = torch.from_numpy(blk).to(out.device)
         return out
-    return dev.CACHE.get(srp, "h2_f32", build)
+    return dev.CACHE.get(srp, "h2_tf32" if tf32 else "h2_f32", build)
 
 
 def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, out_map: bool = True):
     """Conventional SRP map z = 2 Re(H psi) (srp.py:65-71).
 
-    precision "tf32": tcgen05 tensor-core GEMM (kind::tf32, fp32 accumulate in TMEM),
-    normalized max error ~1e-5 vs float64 (within the 1e-4 parity bound);
+    precision "tf32": tcgen05 tensor-core GEMM (kind::tf32 on round-to-nearest TF32
+    operands, fp32 accumulation in TMEM), normalized max error ~1e-5 vs float64;
     "fp32": SIMT fp32 GEMM.
     """
     if (gcc.num_pairs, gcc.num_bins) != (srp.num_pairs, srp.num_bins):
@@ -302,24 +316,30 @@ def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, ou
                              f"match a {srp.num_pairs} x {srp.num_bins} transform")
     if precision not in ("tf32", "fp32"):
         raise ValueError(f"unknown precision {precision!r}")
-    v, batched = _gcc_matrix(gcc, srp.num_pairs, srp.num_bins)
-    h2 = steering_device(srp)
     n = srp.num_pairs * srp.num_bins
-    j, f = h2.shape[0], v.shape[0]
-    z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
+    h2 = steering_device(srp, tf32=(precision == "tf32"))
+    j, ld = h2.shape
+    padded = getattr(gcc, "padded", None)
+    if precision == "tf32" and getattr(gcc, "tf32_rounded", False) and padded is not None \
+            and padded.shape[1] == ld:
+        vp, batched = padded, gcc.values.dim() == 2
+        f = vp.shape[0]
+    else:
+        v, batched = _gcc_matrix(gcc, srp.num_pairs, srp.num_bins)
+        f = v.shape[0]
+        vp = None
+    z = torch.empty((f, j), dtype=torch.float32, device=h2.device) if out_map else None
     keys = _new_keys(f, argmax)
     if precision == "fp32":
-        if h2.shape[1] != 2 * n:
+        if ld != 2 * n:
             h2 = h2[:, :2 * n].contiguous()
         nat.call("srpgpu_srp_map_simt", dev.ptr(v), f, n, dev.ptr(h2), j, dev.ptr(z), dev.ptr(keys),
                  dev.stream_ptr())
     else:
-        ld = h2.shape[1]
-        if ld != 2 * n:   # pad psi rows to the same 16-byte pitch
-            vp = torch.zeros((f, ld), dtype=torch.float32, device=v.device)
-            vp[:, :2 * n] = torch.view_as_real(v).reshape(f, 2 * n)
-        else:
-            vp = v
+        if vp is None:   # round psi to TF32 and re-pitch to the operand row layout
+            vp = torch.empty((f, ld), dtype=torch.float32, device=h2.device)
+            nat.call("srpgpu_round_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, f, 2 * n,
+                     dev.stream_ptr())
         nat.call("srpgpu_srp_map_tc", dev.ptr(vp), ld, f, n, dev.ptr(h2), ld, j, dev.ptr(z),
                  dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)

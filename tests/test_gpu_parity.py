@@ -178,8 +178,12 @@ def test_conventional_map(golden_scene, precision):
                   frame.num_bins, "phat")
     z, idx = s.srp_map_exact(srp, gcc, precision=precision, argmax=True)
     err = assert_map_close(z, g["z_conv"])
-    if precision == "fp32":
-        assert err.max() < 1e-5
+    assert err.max() < (1e-5 if precision == "fp32" else 5e-5)
+    if precision == "tf32":   # fused producer path: gcc_frames(tf32=True) -> tcgen05 GEMM
+        F = g["psi"].shape[0]
+        g2 = s.gcc_frames(g["samples"], frame, pairs, range(F), tf32=True)
+        z2 = s.srp_map_exact(srp, g2)
+        assert_map_close(z2, g["z_conv"])
     assert_argmax_agrees(idx, g["z_conv"])
     z1 = s.srp_map_exact(srp, s.FdGcc(gcc.values[0], gcc.num_pairs, gcc.num_bins, "phat"),
                          precision=precision)
@@ -285,3 +289,23 @@ def test_evaluate_map_dispatch(golden_scene):
     assert_map_close(z, g["z_si"])
     with pytest.raises(ValueError):
         s.evaluate_map("xyz", None, spec, frame, gcc, "ifft")
+
+
+def test_pipeline_graph_matches_eager(golden_scene):
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    x = g["samples"][:, :(F - 1) * frame.hop + frame.frame_len]
+    tag = keep_tags(g)[0]
+    sp = sparse_from_golden(g, tag)
+    pipe = MapPipeline("sspi", sp, frame, pairs, spec, frames=F)
+    z, idx = pipe.run(x)
+    xi = s.frames_to_samples(x, frame, pairs, spec, range(F))
+    z2, idx2 = s.sspi_map(sp, xi, argmax=True)
+    assert torch.equal(z, z2) and torch.equal(idx, idx2)
+    conv = MapPipeline("conv", s.build_srp_matrix(tdoa, frame, max_bytes=1 << 34), frame, pairs,
+                       frames=F)
+    zc, ic = conv.run(torch.from_numpy(x.astype(np.float32)).cuda())
+    assert_map_close(zc, g["z_conv"])
+    assert_argmax_agrees(ic, g["z_conv"])

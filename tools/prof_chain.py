@@ -1,0 +1,56 @@
+"""Run one workload's hot-path chain eagerly a few times (for ncu / compute-sanitizer).
+
+    python tools/prof_chain.py --workload cfg2 --variant sspi --reps 3
+"""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2306_08514_b200 as s  # noqa: E402
+from paper_2306_08514_b200 import workloads  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--variant", default="sspi")
+    ap.add_argument("--frames", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--nnz", default="2jp")
+    ap.add_argument("--rank", type=int, default=16)
+    a = ap.parse_args()
+    frames = a.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000}.get(a.workload, 1000)
+    wl = workloads.make(a.workload, num_frames=frames)
+    x = torch.from_numpy(wl.samples).cuda()
+    rng = range(frames)
+    if a.variant in ("sspi", "slri", "si"):
+        interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
+        if a.variant == "sspi":
+            op = s.truncate_sparse(interp, s.resolve_sparsity(a.nnz, wl.grid.num_points,
+                                                              wl.pairs.num_pairs, interp.matrix.size))
+        elif a.variant == "slri":
+            op = s.truncate_low_rank(interp, a.rank)
+        else:
+            op = interp
+        fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
+        for _ in range(a.reps):
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng)
+            z, idx = fn(op, xi, argmax=True)
+    else:
+        srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 36)
+        op = srp if a.variant == "conv" else s.truncate_srp_matrix(srp, a.rank)
+        for _ in range(a.reps):
+            g = s.gcc_frames(x, wl.frame, wl.pairs, rng, tf32=(a.variant == "conv"))
+            z, idx = (s.srp_map_exact if a.variant == "conv" else s.lr_map)(op, g, argmax=True)
+    torch.cuda.synchronize()
+    print("ok", a.workload, a.variant, frames, int(idx[0]))
+
+
+if __name__ == "__main__":
+    main()
