@@ -81,47 +81,57 @@ int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int64_t num_sa
 
 /* td_gcc_samples(gcc, spec, "ifft") (sampling.py:106-134): per pair the
  * unnormalized real inverse DFT of the two-sided spectrum (bins 0, K zero), lags
- * kept in storage order 0..N_p, -N_p..-1 (sampling.py:62-65) at
- * samples[f][offsets[p] + j].  counts [P], offsets [P+1] are device int32. */
+ * kept in storage order 0..N_p, -N_p..-1 (sampling.py:62-65) at sample index
+ * s = offsets[p] + j.  counts [P], offsets [P+1] are device int32.
+ * samples_ld == 0: frame-major samples_out[f][s]; samples_ld >= F: lag-major
+ * samples_out[s][f] with row pitch samples_ld (the layout the map kernels read). */
 int srpgpu_td_gcc_samples(const float* gcc, int64_t num_frames, int32_t num_pairs, int32_t half_len,
                           const int32_t* counts, const int32_t* offsets, int32_t total_samples,
-                          float* samples_out, srpgpu_stream_t stream);
+                          float* samples_out, int64_t samples_ld, srpgpu_stream_t stream);
 
-/* fused stft_frame + fd_gcc + td_gcc_samples: signal -> TD-GCC samples [F][S]. */
+/* fused stft_frame + fd_gcc + td_gcc_samples: signal -> TD-GCC samples (layout as above). */
 int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t num_samples,
                              int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
                              int64_t first_frame, int64_t num_frames, const int32_t* pairs,
                              int32_t num_pairs, int32_t weighting, int32_t floor_mode,
                              double floor_value, const int32_t* counts, const int32_t* offsets,
-                             int32_t total_samples, float* samples_out, srpgpu_stream_t stream);
+                             int32_t total_samples, float* samples_out, int64_t samples_ld,
+                             srpgpu_stream_t stream);
 
 /* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
 int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
                               int32_t half_len, const int32_t* pairs, int32_t num_pairs,
                               int32_t weighting, int32_t floor_mode, double floor_value,
                               const int32_t* counts, const int32_t* offsets, int32_t total_samples,
-                              float* samples_out, srpgpu_stream_t stream);
+                              float* samples_out, int64_t samples_ld, srpgpu_stream_t stream);
 
 /* ---- maps (srpmap/interpolation.py, lowrank.py, srp.py) ------------------- */
 
 /* sspi_map (interpolation.py:188-195) and, with a keep-all operator, si_map
- * (:129-136).  Pair-major ELL operator: entries of pair p at
- * ell[ell_offsets[p] + i*widths[p] + w], each a packed {uint32 float-bits value,
- * uint32 absolute sample index}; padding entries have value 0.
- * offsets [P+1] (sample blocks), widths [P], ell_offsets [P+1] are device arrays;
- * max_block = max 2N_p+1, max_width = max widths[p], sum_widths = sum widths[p].
- * z [F][J] and keys [F] are each optional (NULL). */
-int srpgpu_sspi_map(const float* samples, int64_t num_frames, int32_t total_samples,
-                    int32_t num_pairs, const int32_t* offsets, const int32_t* widths,
+ * (:129-136).  samples: lag-major [S][samples_ld] (samples_ld >= F, multiple of 4,
+ * 16-byte aligned).  Pair-major ELL operator with rows padded to a multiple of 32
+ * candidates: entries of pair p at ell[ell_offsets[p] + i*widths[p] + w], each a
+ * packed {uint32 float-bits value, uint32 absolute sample index}; padding entries
+ * have value 0.  widths [P], ell_offsets [P+1] are device arrays; max_width =
+ * max widths[p], sum_widths = sum widths[p].  z [F][J] and keys [F] are each
+ * optional (NULL). */
+int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t num_frames,
+                    int32_t total_samples, int32_t num_pairs, const int32_t* widths,
                     const int64_t* ell_offsets, const void* ell, int64_t num_candidates,
-                    int32_t max_block, int32_t max_width, int32_t sum_widths, float* z,
-                    uint64_t* keys, srpgpu_stream_t stream);
+                    int32_t max_width, int32_t sum_widths, float* z, uint64_t* keys,
+                    srpgpu_stream_t stream);
+
+/* frame-major [rows][ld_src] -> lag-major [cols][ld_dst] (zero-filled pad columns). */
+int srpgpu_transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,
+                     int64_t ld_dst, srpgpu_stream_t stream);
 
 /* slri_map (interpolation.py:178-185): z = tall (fat xi).  fat [R][S], tall [J][R]
- * f32; work [F][R] scratch. */
-int srpgpu_slri_map(const float* samples, int64_t num_frames, int32_t total_samples,
-                    const float* fat, const float* tall, int32_t rank, int64_t num_candidates,
-                    float* work, float* z, uint64_t* keys, srpgpu_stream_t stream);
+ * f32; samples lag-major [S][samples_ld] (or frame-major [F][S] if samples_ld == 0);
+ * work [F][R] scratch. */
+int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t num_frames,
+                    int32_t total_samples, const float* fat, const float* tall, int32_t rank,
+                    int64_t num_candidates, float* work, float* z, uint64_t* keys,
+                    srpgpu_stream_t stream);
 
 /* lr_map (lowrank.py:51-57): z = 2 Re(tall (fat psi)).  Complex factors folded
  * into real ones once on the host: fat2 [2R][2PB] with rows r: (Re fat, -Im fat)

@@ -10,7 +10,7 @@
 // (8 points per thread in registers per pass: 4 passes at L = 1024, 3 at 512).
 // Two real channels are packed into one complex FFT for the forward transform;
 // two pairs' Hermitian spectra are packed into one complex FFT for the inverse.
-#include "common.cuh"
+#include "frontend_warp.cuh"
 
 namespace srpgpu {
 
@@ -39,6 +39,7 @@ struct FrontendParams {
   float* xi_out;              // [F][S]
   int32_t nbuf;               // concurrent FFT buffers
   int64_t gcc_ld;             // complex elements per frame row of gcc_out (>= P*(K-1))
+  int64_t xi_ld;              // 0: xi_out is frame-major [F][S]; > 0: lag-major [S][xi_ld]
   int32_t round_tf32;         // round gcc_out to TF32 (RNE) for the tensor-core map
 };
 
@@ -230,7 +231,8 @@ frontend_kernel(const FrontendParams prm) {
         dst[idx] = make_float2(0.f, 0.f);   // pitch padding
     } else {  // OUT_XI
       const float2* gsrc = (IN == IN_GCC) ? prm.gcc_in + f * (int64_t)P * B : nullptr;
-      float* dst = prm.xi_out + f * (int64_t)prm.S;
+      float* dst = prm.xi_out + (prm.xi_ld ? f : f * (int64_t)prm.S);
+      const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
       for (int p0 = 0; p0 < P; p0 += 2 * prm.nbuf) {
         const int nb = min(prm.nbuf, (P - p0 + 1) >> 1);
         // two-sided spectra Z = Psi_a + j Psi_b (Hermitian extension, bins 0 and K zero),
@@ -271,7 +273,7 @@ frontend_kernel(const FrontendParams prm) {
           const int j = s - s_off[q];
           const int n = (j <= c) ? j : L - (2 * c + 1 - j);
           const float2 v = fft[(size_t)((q - p0) >> 1) * L + n];
-          dst[s] = ((q - p0) & 1) ? -v.y : v.x;
+          dst[s * sst] = ((q - p0) & 1) ? -v.y : v.x;
         }
         __syncthreads();
       }
@@ -289,6 +291,19 @@ static size_t frontend_smem(int in, int out, int L, int K, int M, int P, int nbu
 
 template <int IN, int OUT>
 static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* what) {
+  if (IN == IN_SAMPLES && OUT != OUT_SPECTRA && prm.F > 0) {
+    // warp-per-frame register FFT path (frame lengths 256 / 512 / 1024)
+    WarpParams wp = {};
+    wp.samples = prm.samples; wp.ld_samples = prm.ld_samples; wp.window = prm.window;
+    wp.M = prm.M; wp.L = prm.L; wp.K = prm.K; wp.hop = prm.hop;
+    wp.first_frame = prm.first_frame; wp.F = prm.F; wp.pairs = prm.pairs; wp.P = prm.P;
+    wp.weighting = prm.weighting; wp.floor_mode = prm.floor_mode; wp.floor_value = prm.floor_value;
+    wp.counts = prm.counts; wp.offsets = prm.offsets; wp.S = prm.S;
+    wp.gcc_out = prm.gcc_out; wp.gcc_ld = prm.gcc_ld; wp.round_tf32 = prm.round_tf32;
+    wp.xi_out = prm.xi_out; wp.xi_ld = prm.xi_ld;
+    const int r = frontend_warp_launch(wp, OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI, stream, what);
+    if (r <= 0) return r;
+  }
   const int need = (OUT == OUT_XI) ? (prm.P + 1) / 2 : (IN == IN_SAMPLES ? (prm.M + 1) / 2 : 0);
   const size_t budget = 200 * 1024;
   int nbuf = max(1, need);
@@ -414,7 +429,7 @@ extern "C" int srpgpu_gcc_frames(const float* samples, int32_t num_channels, int
 
 extern "C" int srpgpu_td_gcc_samples(const float* gcc, int64_t num_frames, int32_t num_pairs,
                                      int32_t half_len, const int32_t* counts, const int32_t* offsets,
-                                     int32_t total_samples, float* samples_out,
+                                     int32_t total_samples, float* samples_out, int64_t samples_ld,
                                      srpgpu_stream_t stream) {
   FrontendParams prm = {};
   int st = fill_common(prm, 2 * half_len, "td_gcc_samples");
@@ -422,7 +437,9 @@ extern "C" int srpgpu_td_gcc_samples(const float* gcc, int64_t num_frames, int32
   SRPGPU_CHECK_ARG(half_len >= 2, SRPGPU_ERR_DIMENSION, "td_gcc_samples: half_len must be >= 2");
   prm.gcc_in = reinterpret_cast<const float2*>(gcc);
   prm.F = num_frames; prm.P = num_pairs; prm.counts = counts; prm.offsets = offsets;
-  prm.S = total_samples; prm.xi_out = samples_out;
+  prm.S = total_samples; prm.xi_out = samples_out; prm.xi_ld = samples_ld;
+  SRPGPU_CHECK_ARG(samples_ld == 0 || samples_ld >= num_frames, SRPGPU_ERR_DIMENSION,
+                   "td_gcc_samples: lag-major pitch smaller than the frame count");
   return launch_frontend<IN_GCC, OUT_XI>(prm, as_stream(stream), "td_gcc_samples");
 }
 
@@ -433,7 +450,7 @@ extern "C" int srpgpu_frames_to_samples(const float* samples, int32_t num_channe
                                         int32_t weighting, int32_t floor_mode, double floor_value,
                                         const int32_t* counts, const int32_t* offsets,
                                         int32_t total_samples, float* samples_out,
-                                        srpgpu_stream_t stream) {
+                                        int64_t samples_ld, srpgpu_stream_t stream) {
   FrontendParams prm = {};
   int st = fill_common(prm, frame_len, "frames_to_samples");
   if (st) return st;
@@ -442,7 +459,9 @@ extern "C" int srpgpu_frames_to_samples(const float* samples, int32_t num_channe
   prm.M = num_channels; prm.hop = hop; prm.first_frame = first_frame; prm.F = num_frames;
   prm.pairs = pairs; prm.P = num_pairs; prm.weighting = weighting; prm.floor_mode = floor_mode;
   prm.floor_value = (float)floor_value; prm.counts = counts; prm.offsets = offsets;
-  prm.S = total_samples; prm.xi_out = samples_out;
+  prm.S = total_samples; prm.xi_out = samples_out; prm.xi_ld = samples_ld;
+  SRPGPU_CHECK_ARG(samples_ld == 0 || samples_ld >= num_frames, SRPGPU_ERR_DIMENSION,
+                   "frames_to_samples: lag-major pitch smaller than the frame count");
   if ((st = check_frames(prm, num_samples, "frames_to_samples"))) return st;
   return launch_frontend<IN_SAMPLES, OUT_XI>(prm, as_stream(stream), "frames_to_samples");
 }
@@ -453,7 +472,7 @@ extern "C" int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frame
                                          int32_t floor_mode, double floor_value,
                                          const int32_t* counts, const int32_t* offsets,
                                          int32_t total_samples, float* samples_out,
-                                         srpgpu_stream_t stream) {
+                                         int64_t samples_ld, srpgpu_stream_t stream) {
   FrontendParams prm = {};
   int st = fill_common(prm, 2 * half_len, "spectra_to_samples");
   if (st) return st;
@@ -461,5 +480,8 @@ extern "C" int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frame
   prm.F = num_frames; prm.M = num_channels; prm.pairs = pairs; prm.P = num_pairs;
   prm.weighting = weighting; prm.floor_mode = floor_mode; prm.floor_value = (float)floor_value;
   prm.counts = counts; prm.offsets = offsets; prm.S = total_samples; prm.xi_out = samples_out;
+  prm.xi_ld = samples_ld;
+  SRPGPU_CHECK_ARG(samples_ld == 0 || samples_ld >= num_frames, SRPGPU_ERR_DIMENSION,
+                   "spectra_to_samples: lag-major pitch smaller than the frame count");
   return launch_frontend<IN_SPECTRA, OUT_XI>(prm, as_stream(stream), "spectra_to_samples");
 }

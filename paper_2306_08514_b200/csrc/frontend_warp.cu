@@ -1,0 +1,383 @@
+// Warp-per-frame frontend for frame lengths L = 32 * LP (LP = 8, 16, 32: L = 256, 512, 1024).
+//
+// Same math as frontend.cu (frontend.py:89-160, sampling.py:106-134), laid out for
+// sm_100a: every warp owns one frame at a time and never waits on other warps.
+//   * FFT of length L = 32 x LP by the four-step method: each lane holds 32
+//     points in registers and runs a 32-point radix-2 DIF transform with
+//     compile-time twiddles; the W_L^{l k2} twiddles come from a CTA table laid
+//     out [k2][l] (conflict-free); one padded shared-memory transpose; then
+//     32/LP transforms of LP points per lane.  A warp runs 32/LP FFTs at once.
+//   * two real channels are packed into one complex FFT (forward) and two
+//     pairs' Hermitian spectra into one complex FFT (inverse, as conj(FFT(conj))).
+//   * the inverse is pruned: only the 2N_p+1 kept lags (|n| <= N_p) are produced,
+//     i.e. outputs k1 in {0, LP-1} of the second step when N_p < 32.
+//   * frame energy for the PHAT floor by warp shuffles.
+#include <stdlib.h>
+
+#include "frontend_warp.cuh"
+
+namespace srpgpu {
+
+namespace wf {
+
+// W_32^m = exp(-2 pi i m / 32) for m in [0, 16); folded to immediates after unrolling
+__device__ __forceinline__ float2 w32(int m) {
+  switch (m & 15) {
+    case 0: return make_float2(1.0f, 0.0f);
+    case 1: return make_float2(0.98078528040323043f, -0.19509032201612825f);
+    case 2: return make_float2(0.92387953251128674f, -0.38268343236508978f);
+    case 3: return make_float2(0.83146961230254524f, -0.55557023301960218f);
+    case 4: return make_float2(0.70710678118654752f, -0.70710678118654752f);
+    case 5: return make_float2(0.55557023301960218f, -0.83146961230254524f);
+    case 6: return make_float2(0.38268343236508978f, -0.92387953251128674f);
+    case 7: return make_float2(0.19509032201612825f, -0.98078528040323043f);
+    case 8: return make_float2(0.0f, -1.0f);
+    case 9: return make_float2(-0.19509032201612825f, -0.98078528040323043f);
+    case 10: return make_float2(-0.38268343236508978f, -0.92387953251128674f);
+    case 11: return make_float2(-0.55557023301960218f, -0.83146961230254524f);
+    case 12: return make_float2(-0.70710678118654752f, -0.70710678118654752f);
+    case 13: return make_float2(-0.83146961230254524f, -0.55557023301960218f);
+    case 14: return make_float2(-0.92387953251128674f, -0.38268343236508978f);
+    default: return make_float2(-0.98078528040323043f, -0.19509032201612825f);
+  }
+}
+
+__device__ __forceinline__ float2 twmul32(float2 d, int m) {  // d * W_32^m, m in [0, 16)
+  if (m == 0) return d;
+  if (m == 8) return make_float2(d.y, -d.x);
+  const float2 w = w32(m);
+  return make_float2(d.x * w.x - d.y * w.y, d.x * w.y + d.y * w.x);
+}
+
+// in-place radix-2 DIF over v[base .. base+N) in registers (base constant after unrolling):
+// natural order in, v[base + i] = X[bitrev(i)] out
+template <int N>
+__device__ __forceinline__ void dif(float2 (&v)[32], const int base) {
+#pragma unroll
+  for (int h = N / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int b = 0; b < N; b += 2 * h) {
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float2 a = v[base + b + j], c = v[base + b + j + h];
+        v[base + b + j] = make_float2(a.x + c.x, a.y + c.y);
+        v[base + b + j + h] = twmul32(make_float2(a.x - c.x, a.y - c.y), j * (32 / (2 * h)));
+      }
+    }
+  }
+}
+
+template <int N>
+__host__ __device__ constexpr int brev(int i) {
+  int r = 0;
+  for (int b = 1, o = N >> 1; b < N; b <<= 1, o >>= 1)
+    if (i & b) r |= o;
+  return r;
+}
+
+template <int LP>
+struct Geo {
+  static constexpr int L = 32 * LP;
+  static constexpr int K = L / 2;
+  static constexpr int R = 32 / LP;            // FFTs per warp
+  static constexpr int XP = 32 * (LP + 1);     // float2 per FFT transpose area (padded)
+  static constexpr int WORK = R * XP;          // float2 per warp work area
+};
+
+// Forward FFT of the 32 points v[j] = x[fl + LP*j] of this lane's FFT.
+// On return v[r*LP + i] = X[32*brev_LP(i) + fl + LP*r]  (FULL2), or only the
+// k1 in {0, LP-1} outputs in v[r*LP + 0] and v[r*LP + 1] (pruned).
+template <int LP, bool FULL2>
+__device__ __forceinline__ void fft_l(float2 (&v)[32], float2* xp, const float2* twT, int fl) {
+  dif<32>(v, 0);                                // v[i] = A[brev5(i)]
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int k2 = brev<32>(i);
+    v[i] = cmul(v[i], twT[k2 * LP + fl]);       // W_L^{fl k2}
+    xp[k2 * (LP + 1) + fl] = v[i];
+  }
+  __syncwarp();
+  constexpr int R = 32 / LP;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float2* row = xp + (fl + LP * r) * (LP + 1);
+#pragma unroll
+    for (int n1 = 0; n1 < LP; ++n1) v[r * LP + n1] = row[n1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (FULL2) {
+      dif<LP>(v, r * LP);
+    } else {
+      // X[0] = sum u ; X[LP-1] = sum u W_LP^{-n1} = sum u conj(W_32^{n1*32/LP})
+      float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int n1 = 0; n1 < LP; ++n1) {
+        const float2 u = v[r * LP + n1];
+        s0.x += u.x;
+        s0.y += u.y;
+        const int m = (n1 * (32 / LP)) & 31;
+        float2 w = (m < 16) ? w32(m) : make_float2(-w32(m - 16).x, -w32(m - 16).y);
+        w.y = -w.y;   // conj
+        s1.x += u.x * w.x - u.y * w.y;
+        s1.y += u.x * w.y + u.y * w.x;
+      }
+      v[r * LP + 0] = s0;
+      v[r * LP + 1] = s1;
+    }
+  }
+}
+
+__device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m, int mp, int k, int weighting,
+                                             float floor) {
+  const float2 a = spec[m * Kp1 + k];
+  const float2 b = spec[mp * Kp1 + k];
+  float2 raw = cmulc(a, b);
+  if (weighting) {
+    const float mag = sqrtf(raw.x * raw.x + raw.y * raw.y);
+    const float denom = fmaxf(mag, floor);
+    if (denom > 0.f) {
+      raw.x = raw.x / denom;
+      raw.y = raw.y / denom;
+    } else {
+      raw = make_float2(0.f, 0.f);
+    }
+  }
+  return raw;
+}
+
+constexpr int kWarps = 4;
+
+template <int LP, int OUT>
+__global__ void __launch_bounds__(kWarps * 32)
+frontend_warp_kernel(const WarpParams prm) {
+  using G = Geo<LP>;
+  constexpr int L = G::L, K = G::K, R = G::R;
+  constexpr int Kp1 = K + 1, B = K - 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
+  int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
+  int* s_counts = s_pairs + 2 * prm.P;                                  // [P]
+  int* s_off = s_counts + prm.P;                                        // [P+1]
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
+  const int M = prm.M, P = prm.P;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t warp_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
+  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * warp_bytes);   // [M][K+1]
+  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
+  const int fi = lane / LP, fl = lane % LP;
+  float2* xp = work + fi * G::XP;
+
+  for (int e = threadIdx.x; e < 32 * LP; e += blockDim.x) {
+    const int k2 = e / LP, l = e % LP;
+    float sn, cs;
+    sincospif(2.0f * (float)(k2 * l) / (float)L, &sn, &cs);
+    twT[e] = make_float2(cs, -sn);
+  }
+  for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) s_pairs[i] = prm.pairs[i];
+  if (OUT == W_OUT_XI) {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s_counts[i] = prm.counts[i];
+    for (int i = threadIdx.x; i <= P; i += blockDim.x) s_off[i] = prm.offsets[i];
+  }
+  __syncthreads();
+
+  const int64_t total_warps = (int64_t)gridDim.x * kWarps;
+  for (int64_t f = (int64_t)blockIdx.x * kWarps + wid; f < prm.F; f += total_warps) {
+    const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
+    float energy = 0.f;
+    // ---------------- forward FFTs: R channel pairs per round ----------------
+    for (int c0 = 0; c0 < M; c0 += 2 * R) {
+      const int ca = c0 + 2 * fi, cb = ca + 1;
+      float2 v[32];
+      const float* xa = prm.samples + (int64_t)ca * prm.ld_samples + start;
+      const float* xb = prm.samples + (int64_t)cb * prm.ld_samples + start;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = fl + LP * j;
+        const float w = __ldg(prm.window + n);
+        const float a = (ca < M) ? __ldg(xa + n) * w : 0.f;
+        const float b = (cb < M) ? __ldg(xb + n) * w : 0.f;
+        v[j] = make_float2(a, b);
+      }
+      fft_l<LP, true>(v, xp, twT, fl);
+      // natural-order Z into this FFT's work area
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int i = 0; i < LP; ++i) xp[32 * brev<LP>(i) + fl + LP * r] = v[r * LP + i];
+      __syncwarp();
+      // unpack the two real spectra: Ya = (Z + conj Z[L-k]) / 2, Yb = (Z - conj Z[L-k]) / 2j
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int qa = c0 + 2 * q, qb = qa + 1;
+        if (qa >= M) break;
+        const float2* zq = work + q * G::XP;
+        for (int k = lane; k < Kp1; k += 32) {
+          const float2 Z = zq[k];
+          const float2 Zc = conjf2(zq[(L - k) & (L - 1)]);
+          const float2 Ya = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y + Zc.y));
+          spec[qa * Kp1 + k] = Ya;
+          energy += Ya.x * Ya.x + Ya.y * Ya.y;
+          if (qb < M) {
+            const float2 Yb = make_float2(0.5f * (Z.y - Zc.y), -0.5f * (Z.x - Zc.x));
+            spec[qb * Kp1 + k] = Yb;
+            energy += Yb.x * Yb.x + Yb.y * Yb.y;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    float floor = prm.floor_value;
+    if (prm.weighting && prm.floor_mode == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+      floor = prm.floor_value * energy;
+    }
+
+    if (OUT == W_OUT_GCC) {
+      float2* dst = prm.gcc_out + f * prm.gcc_ld;
+      for (int p = 0; p < P; ++p) {
+        const int m = s_pairs[2 * p], mp = s_pairs[2 * p + 1];
+        for (int k = 1 + lane; k < K; k += 32) {
+          float2 val = cross_phat(spec, Kp1, m, mp, k, prm.weighting, floor);
+          if (prm.round_tf32) val = make_float2(tf32_rne(val.x), tf32_rne(val.y));
+          dst[p * B + k - 1] = val;
+        }
+      }
+      for (int64_t idx = (int64_t)P * B + lane; idx < prm.gcc_ld; idx += 32) dst[idx] = make_float2(0.f, 0.f);
+    } else {
+      float* dst = prm.xi_out + (prm.xi_ld ? f : f * (int64_t)prm.S);
+      const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
+      for (int p0 = 0; p0 < P; p0 += 2 * R) {
+        // PHAT cross-spectra of this round's pairs into each FFT's work area: [2][B]
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int pa = p0 + 2 * q, pb = pa + 1;
+          if (pa >= P) break;
+          float2* sq = work + q * G::XP;
+          const int ma = s_pairs[2 * pa], mpa = s_pairs[2 * pa + 1];
+          const int mb = (pb < P) ? s_pairs[2 * pb] : 0, mpb = (pb < P) ? s_pairs[2 * pb + 1] : 0;
+          for (int k = 1 + lane; k < K; k += 32) {
+            sq[k - 1] = cross_phat(spec, Kp1, ma, mpa, k, prm.weighting, floor);
+            sq[B + k - 1] = (pb < P) ? cross_phat(spec, Kp1, mb, mpb, k, prm.weighting, floor)
+                                     : make_float2(0.f, 0.f);
+          }
+        }
+        __syncwarp();
+        const int pa = p0 + 2 * fi, pb = pa + 1;
+        float2 v[32];
+        {
+          const float2* sa = xp;
+          const float2* sb = xp + B;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = fl + LP * j;
+            float2 z = make_float2(0.f, 0.f);
+            if (pa < P && k != 0 && k != K) {
+              if (k < K) {
+                const float2 a = sa[k - 1], c = sb[k - 1];
+                z = make_float2(a.x - c.y, a.y + c.x);      // a + j c
+              } else {
+                const float2 a = sa[L - k - 1], c = sb[L - k - 1];
+                z = make_float2(a.x + c.y, -a.y + c.x);     // conj(a) + j conj(c)
+              }
+            }
+            v[j] = conjf2(z);
+          }
+        }
+        __syncwarp();
+        // prune the second FFT step when every kept lag of the warp's pairs has |n| < 32
+        int nmax = 0;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int qa = p0 + 2 * q;
+          if (qa < P) nmax = max(nmax, s_counts[qa]);
+          if (qa + 1 < P) nmax = max(nmax, s_counts[qa + 1]);
+        }
+        const bool full2 = nmax >= 32;
+        if (full2) fft_l<LP, true>(v, xp, twT, fl);
+        else fft_l<LP, false>(v, xp, twT, fl);
+        if (pa < P) {
+          const int Na = s_counts[pa], oa = s_off[pa];
+          const int Nb = (pb < P) ? s_counts[pb] : -1, ob = (pb < P) ? s_off[pb] : 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int k2 = fl + LP * r;
+            if (full2) {
+#pragma unroll
+              for (int i = 0; i < LP; ++i) {
+                const int n = 32 * brev<LP>(i) + k2;
+                const float2 x = v[r * LP + i];
+                const int da = (n <= Na) ? n : ((L - n <= Na) ? 2 * Na + 1 - (L - n) : -1);
+                if (da >= 0) dst[(oa + da) * sst] = x.x;
+                const int db = (n <= Nb) ? n : ((L - n <= Nb) ? 2 * Nb + 1 - (L - n) : -1);
+                if (db >= 0) dst[(ob + db) * sst] = -x.y;
+              }
+            } else {
+              const float2 x0 = v[r * LP + 0];   // n = k2
+              const float2 x1 = v[r * LP + 1];   // n = L - 32 + k2, distance d = 32 - k2
+              const int d = 32 - k2;
+              if (k2 <= Na) dst[(oa + k2) * sst] = x0.x;
+              if (d <= Na) dst[(oa + 2 * Na + 1 - d) * sst] = x1.x;
+              if (k2 <= Nb) dst[(ob + k2) * sst] = -x0.y;
+              if (d <= Nb) dst[(ob + 2 * Nb + 1 - d) * sst] = -x1.y;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int LP, int OUT>
+static int launch(const WarpParams& wp, cudaStream_t st, const char* what) {
+  using G = Geo<LP>;
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1) * 4) + 15) & ~(size_t)15;
+  const size_t warp_bytes = ((size_t)wp.M * (G::K + 1) + G::WORK) * sizeof(float2);
+  const size_t smem = head + kWarps * warp_bytes;
+  if (smem > 227 * 1024) return 1;   // caller falls back to the block kernel
+  auto kern = frontend_warp_kernel<LP, OUT>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    set_error("%s: cannot reserve %zu B shared memory", what, smem);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+  if (per_sm < 1) return 1;
+  const int64_t need = (wp.F + kWarps - 1) / kWarps;
+  const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm);
+  if (grid <= 0) return SRPGPU_OK;
+  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp);
+  SRPGPU_CHECK_LAUNCH(what);
+  return SRPGPU_OK;
+}
+
+template <int OUT>
+static int by_len(const WarpParams& wp, cudaStream_t st, const char* what) {
+  switch (wp.L) {
+    case 256: return launch<8, OUT>(wp, st, what);
+    case 512: return launch<16, OUT>(wp, st, what);
+    case 1024: return launch<32, OUT>(wp, st, what);
+    default: return 1;
+  }
+}
+
+}  // namespace wf
+
+// Returns 0 on launch, 1 if the shape is not covered (caller uses the block kernel),
+// a negative status on error.
+int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what) {
+  static const int disabled = [] {
+    const char* e = getenv("SRPGPU_FRONTEND");
+    return e && e[0] == 'b';
+  }();
+  if (disabled) return 1;
+  if (out == W_OUT_GCC) return wf::by_len<W_OUT_GCC>(wp, st, what);
+  if (out == W_OUT_XI) return wf::by_len<W_OUT_XI>(wp, st, what);
+  return 1;
+}
+
+}  // namespace srpgpu

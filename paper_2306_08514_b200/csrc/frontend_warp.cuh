@@ -1,0 +1,32 @@
+// Parameters of the warp-per-frame frontend (frontend_warp.cu), shared with frontend.cu.
+#pragma once
+#include "common.cuh"
+
+namespace srpgpu {
+
+enum { W_OUT_GCC = 1, W_OUT_XI = 2 };
+
+struct WarpParams {
+  const float* samples;
+  int64_t ld_samples;
+  const float* window;
+  int32_t M, L, K, hop;
+  int64_t first_frame, F;
+  const int32_t* pairs;
+  int32_t P;
+  int32_t weighting, floor_mode;
+  float floor_value;
+  const int32_t* counts;
+  const int32_t* offsets;
+  int32_t S;
+  float2* gcc_out;
+  int64_t gcc_ld;
+  int32_t round_tf32;
+  float* xi_out;
+  int64_t xi_ld;   // 0: frame-major [F][S]; > 0: lag-major [S][xi_ld]
+};
+
+// 0: launched; 1: shape not covered (use the block kernel); < 0: error status.
+int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what);
+
+}  // namespace srpgpu

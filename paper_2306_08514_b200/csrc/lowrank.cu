@@ -16,6 +16,7 @@ namespace srpgpu {
 
 constexpr int kGI = 64, kGF = 64, kGK = 16;
 
+template <bool BT>   // BT: B stored transposed, element (f, k) at B[k * ldb + f]
 __global__ void __launch_bounds__(256)
 gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                float* __restrict__ out, int64_t ldo, int64_t I, int64_t F, int64_t K, float alpha,
@@ -35,9 +36,16 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
     for (int r = 0; r < 4; ++r) {
       const int idx = tid + r * 256;        // 0..1023 over a 64 x 16 tile, k fastest
       const int row = idx >> 4, kk = idx & 15;
-      const int64_t gi = i0 + row, gf = f0 + row, gk = k0 + kk;
+      const int64_t gi = i0 + row, gk = k0 + kk;
       As[kk][row] = (gi < I && gk < K) ? __ldg(A + gi * lda + gk) : 0.f;
-      Bs[kk][row] = (gf < F && gk < K) ? __ldg(B + gf * ldb + gk) : 0.f;
+      if (!BT) {
+        const int64_t gf = f0 + row;
+        Bs[kk][row] = (gf < F && gk < K) ? __ldg(B + gf * ldb + gk) : 0.f;
+      } else {                              // frames fastest: coalesced along f
+        const int fr = idx & 63, kb = idx >> 6;
+        const int64_t gf = f0 + fr, gkb = k0 + kb;
+        Bs[kb][fr] = (gf < F && gkb < K) ? __ldg(B + gkb * ldb + gf) : 0.f;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -113,12 +121,16 @@ __global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, 
 
 int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
             int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
-            const char* what) {
+            const char* what, bool b_trans = false) {
   if (I <= 0 || F <= 0) return SRPGPU_OK;
   SRPGPU_CHECK_ARG(F <= 65535ll * kGF, SRPGPU_ERR_DIMENSION, "%s: too many frames", what);
   dim3 grid((unsigned)((I + kGI - 1) / kGI), (unsigned)((F + kGF - 1) / kGF));
-  gemm_nt_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
-                                       reinterpret_cast<unsigned long long*>(keys), 0);
+  if (b_trans)
+    gemm_nt_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
+                                               reinterpret_cast<unsigned long long*>(keys), 0);
+  else
+    gemm_nt_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
+                                                reinterpret_cast<unsigned long long*>(keys), 0);
   SRPGPU_CHECK_LAUNCH(what);
   return SRPGPU_OK;
 }
@@ -145,7 +157,8 @@ extern "C" int srpgpu_gemm_nt(const float* A, int64_t lda, const float* B, int64
   return gemm_nt(A, lda, B, ldb, out, ldo, rows_i, rows_f, depth, alpha, keys, st, "gemm_nt");
 }
 
-extern "C" int srpgpu_slri_map(const float* samples, int64_t num_frames, int32_t total_samples,
+extern "C" int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t num_frames,
+                               int32_t total_samples,
                                const float* fat, const float* tall, int32_t rank,
                                int64_t num_candidates, float* work, float* z, uint64_t* keys,
                                srpgpu_stream_t stream) {
@@ -153,9 +166,9 @@ extern "C" int srpgpu_slri_map(const float* samples, int64_t num_frames, int32_t
   cudaStream_t st = as_stream(stream);
   int s = reset_keys(keys, num_frames, st);
   if (s) return s;
-  // work[f][r] = sum_s fat[r][s] xi[f][s]
-  s = gemm_nt(fat, total_samples, samples, total_samples, work, rank, rank, num_frames,
-              total_samples, 1.0f, nullptr, st, "slri_map(fat)");
+  // work[f][r] = sum_s fat[r][s] xi[s][f]   (samples lag-major [S][samples_ld]; 0 = frame-major)
+  s = gemm_nt(fat, total_samples, samples, samples_ld ? samples_ld : total_samples, work, rank, rank,
+              num_frames, total_samples, 1.0f, nullptr, st, "slri_map(fat)", samples_ld != 0);
   if (s) return s;
   return gemm_nt(tall, rank, work, rank, z, num_candidates, num_candidates, num_frames, rank, 1.0f,
                  keys, st, "slri_map(tall)");

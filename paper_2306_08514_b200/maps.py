@@ -75,6 +75,25 @@ def _sample_matrix(samples, num_cols: int):
     return x.reshape(-1, num_cols), batched
 
 
+def _lag_major(samples, num_cols: int):
+    """(buf (S, ld) lag-major f32, frames, batched) for any samples input.
+
+    Kernel-produced TdGccSamples already carry the lag-major buffer; anything else
+    (reference TdGccSamples, arrays, tensors) is transposed on the device once.
+    """
+    buf = getattr(samples, "lag_major", None)
+    if buf is not None and buf.shape[0] == num_cols:
+        vals = samples.values
+        batched = vals.dim() == 2
+        return buf, (vals.shape[0] if batched else 1), batched
+    x, batched = _sample_matrix(samples, num_cols)
+    f = x.shape[0]
+    ld = (f + 3) // 4 * 4
+    buf = torch.empty((num_cols, ld), dtype=torch.float32, device=x.device)
+    nat.call("srpgpu_transpose", dev.ptr(x), f, num_cols, num_cols, dev.ptr(buf), ld, dev.stream_ptr())
+    return buf, f, batched
+
+
 def _sample_offsets(samples, num_cols: int) -> np.ndarray:
     spec = getattr(samples, "spec", None)
     if spec is not None:
@@ -107,7 +126,8 @@ class EllOperator:
         np.add.at(counts, (pair, rows), 1)
         widths = counts.max(axis=1) if j else np.zeros(p_count, np.int64)
         widths = np.maximum(widths, 0)
-        ell_off = np.concatenate([[0], np.cumsum(widths * j)]).astype(np.int64)
+        j_pad = (j + 31) // 32 * 32          # rows padded for the 32-candidate TMA tiles
+        ell_off = np.concatenate([[0], np.cumsum(widths * j_pad)]).astype(np.int64)
         # rank of each entry inside its (pair, row) group; CSR order is (row, col)
         order = np.lexsort((cols, rows, pair))
         grp = pair[order] * j + rows[order]
@@ -122,7 +142,7 @@ class EllOperator:
         slot = ell_off[pair] + rows * widths[pair] + rank
         packed[slot, 0] = values.astype(np.float32).view(np.uint32)
         packed[slot, 1] = cols.astype(np.uint32)
-        self.num_rows, self.num_cols, self.num_pairs = j, num_cols, p_count
+        self.num_rows, self.num_cols, self.num_pairs, self.rows_padded = j, num_cols, p_count, j_pad
         self.offsets = offsets
         self.widths = widths
         self.counts = counts
@@ -143,7 +163,7 @@ class EllOperator:
             w = int(self.widths[p])
             if w == 0:
                 continue
-            blk = self.host_packed[self.ell_off[p]:self.ell_off[p + 1]].reshape(self.num_rows, w, 2)
+            blk = self.host_packed[self.ell_off[p]:self.ell_off[p + 1]].reshape(self.rows_padded, w, 2)
             mask = np.arange(w)[None, :] < self.counts[p][:, None]
             r, k = np.nonzero(mask)
             entries.append((r, blk[r, k, 1].astype(np.int64), blk[r, k, 0]))
@@ -179,15 +199,14 @@ def ell_from_dense(interp, offsets: np.ndarray) -> EllOperator:
 
 
 def _ell_map(ell: EllOperator, samples, argmax: bool, out_map: bool):
-    x, batched = _sample_matrix(samples, ell.num_cols)
-    f = x.shape[0]
-    z = torch.empty((f, ell.num_rows), dtype=torch.float32, device=x.device) if out_map else None
+    buf, f, batched = _lag_major(samples, ell.num_cols)
+    z = torch.empty((f, ell.num_rows), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
     if ell.num_rows == 0:
         return _finish(z, keys, batched, argmax)
-    nat.call("srpgpu_sspi_map", dev.ptr(x), f, ell.num_cols, ell.num_pairs, dev.ptr(ell.d_offsets),
+    nat.call("srpgpu_sspi_map", dev.ptr(buf), buf.shape[1], f, ell.num_cols, ell.num_pairs,
              dev.ptr(ell.d_widths), dev.ptr(ell.d_ell_off), dev.ptr(ell.d_packed), ell.num_rows,
-             ell.max_block, int(ell.widths.max()) if ell.num_pairs else 0, int(ell.widths.sum()),
+             int(ell.widths.max()) if ell.num_pairs else 0, int(ell.widths.sum()),
              dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
@@ -225,14 +244,14 @@ def _slri_device(lr):
 def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True):
     """Low-rank interpolation map z = tall (fat xi) (interpolation.py:178-185)."""
     fat = np.asarray(lr.fat)
-    x, batched = _sample_matrix(samples, fat.shape[1])
+    buf, f, batched = _lag_major(samples, fat.shape[1])
     d_fat, d_tall = _slri_device(lr)
-    r, j, f = fat.shape[0], d_tall.shape[0], x.shape[0]
-    work = torch.empty((f, r), dtype=torch.float32, device=x.device)
-    z = torch.empty((f, j), dtype=torch.float32, device=x.device) if out_map else None
+    r, j = fat.shape[0], d_tall.shape[0]
+    work = torch.empty((f, r), dtype=torch.float32, device=buf.device)
+    z = torch.empty((f, j), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
-    nat.call("srpgpu_slri_map", dev.ptr(x), f, fat.shape[1], dev.ptr(d_fat), dev.ptr(d_tall), r, j,
-             dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    nat.call("srpgpu_slri_map", dev.ptr(buf), buf.shape[1], f, fat.shape[1], dev.ptr(d_fat),
+             dev.ptr(d_tall), r, j, dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 

@@ -13,7 +13,7 @@ return (F, S).  `frames_to_samples` is the fused signal -> samples chain.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -75,10 +75,16 @@ def sample_spec(tdoa, frame, n_aux: int = 2) -> SampleSpec:
 
 @dataclass(frozen=True)
 class TdGccSamples:
-    """TD GCC samples: values (S,) or (F, S) float32 on the device."""
+    """TD GCC samples: values (S,) or (F, S) float32 on the device.
+
+    Kernels produce them lag-major: `lag_major` is the (S, ld) device buffer
+    (frames contiguous, ld = F rounded up to 4) that the map kernels read, and
+    `values` is its (F, S) view in the reference's per-frame layout.
+    """
 
     values: torch.Tensor
     spec: object
+    lag_major: object = field(default=None, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -94,6 +100,21 @@ def _spec_device(spec):
         off = spec_offsets(spec)
         return dev.as_i32(np.asarray(spec.counts)), dev.as_i32(off)
     return dev.CACHE.get(spec, "spec_i32", build)
+
+
+def pad4(n: int) -> int:
+    return (int(n) + 3) // 4 * 4
+
+
+def _new_samples(frames: int, s_total: int, dev_):
+    """Lag-major output buffer (S, ld) and its (F, S) view."""
+    ld = pad4(max(frames, 1))
+    buf = torch.empty((s_total, ld), dtype=torch.float32, device=dev_)
+    return buf, ld, buf[:, :frames].t()
+
+
+def _wrap(view, buf, spec, batched: bool) -> "TdGccSamples":
+    return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf)
 
 
 def _check_gcc(gcc, spec) -> None:
@@ -113,10 +134,10 @@ def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
     vals = vals.reshape(-1, gcc.num_pairs * gcc.num_bins)
     counts, offsets = _spec_device(spec)
     s_total = int(spec_offsets(spec)[-1])
-    out = torch.empty((vals.shape[0], s_total), dtype=torch.float32, device=vals.device)
+    buf, ld, view = _new_samples(vals.shape[0], s_total, vals.device)
     nat.call("srpgpu_td_gcc_samples", dev.ptr(vals), vals.shape[0], gcc.num_pairs, spec.half_len,
-             dev.ptr(counts), dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
-    return TdGccSamples(values=out if batched else out[0], spec=spec)
+             dev.ptr(counts), dev.ptr(offsets), s_total, dev.ptr(buf), ld, dev.stream_ptr())
+    return _wrap(view, buf, spec, batched)
 
 
 def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
@@ -135,12 +156,12 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
     w, mode, fval = _floor_args(weighting, floor)
     counts, offsets = _spec_device(spec)
     s_total = int(spec_offsets(spec)[-1])
-    out = torch.empty((count, s_total), dtype=torch.float32, device=x.device)
+    buf, ld, view = _new_samples(count, s_total, x.device)
     nat.call("srpgpu_frames_to_samples", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
              dev.ptr(_window_device(frame)), frame.frame_len, frame.hop, first, count,
              dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
-             dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
-    return TdGccSamples(values=out if batched else out[0], spec=spec)
+             dev.ptr(offsets), s_total, dev.ptr(buf), ld, dev.stream_ptr())
+    return _wrap(view, buf, spec, batched)
 
 
 def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:
@@ -154,11 +175,11 @@ def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None
     w, mode, fval = _floor_args(weighting, floor)
     counts, offsets = _spec_device(spec)
     s_total = int(spec_offsets(spec)[-1])
-    out = torch.empty((y.shape[0], s_total), dtype=torch.float32, device=y.device)
+    buf, ld, view = _new_samples(y.shape[0], s_total, y.device)
     nat.call("srpgpu_spectra_to_samples", dev.ptr(y), y.shape[0], y.shape[1], spec.half_len,
              dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
-             dev.ptr(offsets), s_total, dev.ptr(out), dev.stream_ptr())
-    return TdGccSamples(values=out if batched else out[0], spec=spec)
+             dev.ptr(offsets), s_total, dev.ptr(buf), ld, dev.stream_ptr())
+    return _wrap(view, buf, spec, batched)
 
 
 __all__ = ["SampleSpec", "TdGccSamples", "sample_spec", "td_gcc_samples", "frames_to_samples",

@@ -178,7 +178,7 @@ def test_conventional_map(golden_scene, precision):
                   frame.num_bins, "phat")
     z, idx = s.srp_map_exact(srp, gcc, precision=precision, argmax=True)
     err = assert_map_close(z, g["z_conv"])
-    assert err.max() < (1e-5 if precision == "fp32" else 5e-5)
+    assert err.max() < (1e-5 if precision == "fp32" else MAP_TOL)
     if precision == "tf32":   # fused producer path: gcc_frames(tf32=True) -> tcgen05 GEMM
         F = g["psi"].shape[0]
         g2 = s.gcc_frames(g["samples"], frame, pairs, range(F), tf32=True)

@@ -55,4 +55,4 @@ def test_argument_errors_do_not_touch_the_device(lib):
         _native.call("srpgpu_stft", None, 2, 100, 100, None, 12, 6, 0, 1, None, None, None)
     assert "power of two" in _native.last_error()
     with pytest.raises(ValueError):
-        _native.call("srpgpu_slri_map", None, 1, 4, None, None, 0, 4, None, None, None, None)
+        _native.call("srpgpu_slri_map", None, 0, 1, 4, None, None, 0, 4, None, None, None, None)
