@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--variants", default="sspi,slri,lr,conv",
+                    help="comma list of extra variants measured on the same workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -289,7 +291,7 @@ def run_ours(args):
     # ---- other variants of the same workload (same rules; N = 1 only)
     variants = {}
     if not args.no_variants and world == 1:
-        for v in ("sspi", "slri", "lr", "conv"):
+        for v in [t for t in args.variants.split(",") if t]:
             if v == args.variant:
                 continue
             try:

@@ -127,7 +127,7 @@ int srpgpu_transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_sr
 
 /* slri_map (interpolation.py:178-185): z = tall (fat xi).  fat [R][S], tall [J][R]
  * f32; samples lag-major [S][samples_ld] (or frame-major [F][S] if samples_ld == 0);
- * work [F][R] scratch. */
+ * work: 17 * F * R floats of scratch (the rank-R intermediate and split-K partials). */
 int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t num_frames,
                     int32_t total_samples, const float* fat, const float* tall, int32_t rank,
                     int64_t num_candidates, float* work, float* z, uint64_t* keys,
@@ -136,7 +136,7 @@ int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t num_frames
 /* lr_map (lowrank.py:51-57): z = 2 Re(tall (fat psi)).  Complex factors folded
  * into real ones once on the host: fat2 [2R][2PB] with rows r: (Re fat, -Im fat)
  * and R+r: (Im fat, Re fat) interleaved per bin; tall2 [J][2R] = (2 Re tall | -2 Im tall).
- * gcc [F][PB] complex64 (gcc_len = PB); work [F][2R] scratch. */
+ * gcc [F][PB] complex64 (gcc_len = PB); work: 17 * F * 2R floats of scratch. */
 int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_len, const float* fat2,
                   const float* tall2, int32_t rank, int64_t num_candidates, float* work, float* z,
                   uint64_t* keys, srpgpu_stream_t stream);

@@ -135,14 +135,11 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
   const float2 b = spec[mp * Kp1 + k];
   float2 raw = cmulc(a, b);
   if (weighting) {
-    const float mag = sqrtf(raw.x * raw.x + raw.y * raw.y);
-    const float denom = fmaxf(mag, floor);
-    if (denom > 0.f) {
-      raw.x = raw.x / denom;
-      raw.y = raw.y / denom;
-    } else {
-      raw = make_float2(0.f, 0.f);
-    }
+    // raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158)
+    const float mag2 = raw.x * raw.x + raw.y * raw.y;
+    const float inv = (mag2 > floor * floor && mag2 > 0.f) ? rsqrtf(mag2) : (floor > 0.f ? 1.0f / floor : 0.f);
+    raw.x *= inv;
+    raw.y *= inv;
   }
   return raw;
 }

@@ -20,7 +20,12 @@ template <bool BT>   // BT: B stored transposed, element (f, k) at B[k * ldb + f
 __global__ void __launch_bounds__(256)
 gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                float* __restrict__ out, int64_t ldo, int64_t I, int64_t F, int64_t K, float alpha,
-               unsigned long long* __restrict__ keys, int64_t key_base) {
+               unsigned long long* __restrict__ keys, int64_t key_base, int64_t k_chunk) {
+  // split-K: CTA z covers k in [z * k_chunk, min(K, (z + 1) * k_chunk)) and writes its
+  // partial product to out + z * F * ldo (reduced afterwards in a fixed order)
+  const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
+  const int64_t kend = kbeg + k_chunk < K ? kbeg + k_chunk : K;
+  out += (int64_t)blockIdx.z * F * ldo;
   __shared__ __align__(16) float As[kGK][kGI + 4];
   __shared__ __align__(16) float Bs[kGK][kGF + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -31,20 +36,20 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
 
-  for (int64_t k0 = 0; k0 < K; k0 += kGK) {
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int idx = tid + r * 256;        // 0..1023 over a 64 x 16 tile, k fastest
       const int row = idx >> 4, kk = idx & 15;
       const int64_t gi = i0 + row, gk = k0 + kk;
-      As[kk][row] = (gi < I && gk < K) ? __ldg(A + gi * lda + gk) : 0.f;
+      As[kk][row] = (gi < I && gk < kend) ? __ldg(A + gi * lda + gk) : 0.f;
       if (!BT) {
         const int64_t gf = f0 + row;
-        Bs[kk][row] = (gf < F && gk < K) ? __ldg(B + gf * ldb + gk) : 0.f;
+        Bs[kk][row] = (gf < F && gk < kend) ? __ldg(B + gf * ldb + gk) : 0.f;
       } else {                              // frames fastest: coalesced along f
         const int fr = idx & 63, kb = idx >> 6;
         const int64_t gf = f0 + fr, gkb = k0 + kb;
-        Bs[kb][fr] = (gf < F && gkb < K) ? __ldg(B + gkb * ldb + gf) : 0.f;
+        Bs[kb][fr] = (gf < F && gkb < kend) ? __ldg(B + gkb * ldb + gf) : 0.f;
       }
     }
     __syncthreads();
@@ -62,19 +67,32 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
     __syncthreads();
   }
 
-  // epilogue: rows f = f0 + 4 ty + u, columns i = i0 + 4 tx + v
+  // epilogue: rows f = f0 + 4 ty + u, columns i = i0 + 4 tx + v (16-byte streaming stores
+  // when the row pitch allows: the maps are written once and never re-read here)
+  const bool vec = out && (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int64_t f = f0 + ty * 4 + u;
     unsigned long long key = 0ull;
     if (f < F) {
+      const int64_t ib = i0 + tx * 4;
+      if (vec && ib + 3 < I) {
+        const float4 v4 = make_float4(alpha * acc[u][0], alpha * acc[u][1], alpha * acc[u][2],
+                                      alpha * acc[u][3]);
+        __stcs(reinterpret_cast<float4*>(out + f * ldo + ib), v4);
+        key = key_max(key_max(make_key(v4.x, (uint32_t)(key_base + ib)),
+                              make_key(v4.y, (uint32_t)(key_base + ib + 1))),
+                      key_max(make_key(v4.z, (uint32_t)(key_base + ib + 2)),
+                              make_key(v4.w, (uint32_t)(key_base + ib + 3))));
+      } else {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int64_t i = i0 + tx * 4 + v;
-        if (i < I) {
-          const float val = alpha * acc[u][v];
-          if (out) out[f * ldo + i] = val;
-          key = key_max(key, make_key(val, (uint32_t)(key_base + i)));
+        for (int v = 0; v < 4; ++v) {
+          const int64_t i = ib + v;
+          if (i < I) {
+            const float val = alpha * acc[u][v];
+            if (out) out[f * ldo + i] = val;
+            key = key_max(key, make_key(val, (uint32_t)(key_base + i)));
+          }
         }
       }
     }
@@ -84,6 +102,16 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
       for (int o = 8; o > 0; o >>= 1) key = key_max(key, __shfl_xor_sync(0xffffffffu, key, o));
       if (tx == 0 && f < F && key) atomicMax(keys + f, key);
     }
+  }
+}
+
+// out[f][i] = sum_z part[z][f][i] in a fixed order (deterministic split-K)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t nz, int64_t n,
+                                     float* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int64_t z = 0; z < nz; ++z) s += part[z * n + e];
+    out[e] = s;
   }
 }
 
@@ -119,19 +147,40 @@ __global__ void decode_keys_kernel(const unsigned long long* __restrict__ keys, 
   if (value) value[f] = __uint_as_float(bits);
 }
 
+constexpr int kMaxSplit = 16;
+
+// `split_ws` (nullable): kMaxSplit * F * I floats of scratch enabling split-K for
+// small-output / long-K products (the low-rank factor products); out must then be
+// dense (ldo == I) and keys unused.
 int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
             int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
-            const char* what, bool b_trans = false) {
+            const char* what, bool b_trans = false, float* split_ws = nullptr) {
   if (I <= 0 || F <= 0) return SRPGPU_OK;
   SRPGPU_CHECK_ARG(F <= 65535ll * kGF, SRPGPU_ERR_DIMENSION, "%s: too many frames", what);
-  dim3 grid((unsigned)((I + kGI - 1) / kGI), (unsigned)((F + kGF - 1) / kGF));
+  const int64_t ctas = ((I + kGI - 1) / kGI) * ((F + kGF - 1) / kGF);
+  int64_t split = 1;
+  if (split_ws && !keys && ldo == I && ctas < 2 * num_sms())
+    split = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, (2 * num_sms() + ctas - 1) / ctas,
+                                                    K / 256}));
+  const int64_t chunk = ((K + split - 1) / split + kGK - 1) / kGK * kGK;
+  split = (K + chunk - 1) / chunk;
+  dim3 grid((unsigned)((I + kGI - 1) / kGI), (unsigned)((F + kGF - 1) / kGF), (unsigned)split);
+  float* dst = split > 1 ? split_ws : out;
+  const float a = split > 1 ? 1.0f : alpha;
   if (b_trans)
-    gemm_nt_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
-                                               reinterpret_cast<unsigned long long*>(keys), 0);
+    gemm_nt_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a,
+                                               reinterpret_cast<unsigned long long*>(keys), 0, chunk);
   else
-    gemm_nt_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, K, alpha,
-                                                reinterpret_cast<unsigned long long*>(keys), 0);
+    gemm_nt_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a,
+                                                reinterpret_cast<unsigned long long*>(keys), 0, chunk);
   SRPGPU_CHECK_LAUNCH(what);
+  if (split > 1) {
+    const int64_t n = F * I;
+    splitk_reduce_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * num_sms()), 256, 0, st>>>(
+        split_ws, split, n, out);
+    SRPGPU_CHECK_LAUNCH(what);
+    (void)alpha;   // alpha == 1 for the factor products that split
+  }
   return SRPGPU_OK;
 }
 
@@ -168,7 +217,8 @@ extern "C" int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t
   if (s) return s;
   // work[f][r] = sum_s fat[r][s] xi[s][f]   (samples lag-major [S][samples_ld]; 0 = frame-major)
   s = gemm_nt(fat, total_samples, samples, samples_ld ? samples_ld : total_samples, work, rank, rank,
-              num_frames, total_samples, 1.0f, nullptr, st, "slri_map(fat)", samples_ld != 0);
+              num_frames, total_samples, 1.0f, nullptr, st, "slri_map(fat)", samples_ld != 0,
+              work + num_frames * (int64_t)rank);
   if (s) return s;
   return gemm_nt(tall, rank, work, rank, z, num_candidates, num_candidates, num_frames, rank, 1.0f,
                  keys, st, "slri_map(tall)");
@@ -184,7 +234,8 @@ extern "C" int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_l
   if (s) return s;
   // work[f][0:R] = Re(fat psi_f), work[f][R:2R] = Im(fat psi_f); fat2 is (2R) x (2 PB)
   s = gemm_nt(fat2, 2 * (int64_t)gcc_len, gcc, 2 * (int64_t)gcc_len, work, 2 * rank, 2 * rank,
-              num_frames, 2 * (int64_t)gcc_len, 1.0f, nullptr, st, "lr_map(fat)");
+              num_frames, 2 * (int64_t)gcc_len, 1.0f, nullptr, st, "lr_map(fat)", false,
+              work + num_frames * (int64_t)(2 * rank));
   if (s) return s;
   // z = [2 Re tall, -2 Im tall] . work
   return gemm_nt(tall2, 2 * rank, work, 2 * rank, z, num_candidates, num_candidates, num_frames,

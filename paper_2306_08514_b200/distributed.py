@@ -76,3 +76,23 @@ def decode_host_keys(keys: torch.Tensor):
     bits = torch.where(pos, hi & 0x7FFFFFFF, (~hi) & 0xFFFFFFFF)
     value = bits.to(torch.int32).view(torch.float32)
     return index, value
+
+
+def encode_host_keys(values: torch.Tensor, index: torch.Tensor) -> torch.Tensor:
+    """Packed keys (int64 storage of the uint64 key) from per-frame max values and indices.
+
+    Same packing as make_key in csrc/common.cuh: ordered float32 bits in the high word,
+    0xFFFFFFFF - index in the low word.
+    """
+    v = values.to(torch.float32) + 0.0                     # -0.0 -> +0.0
+    bits = v.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    neg = (bits & 0x80000000) != 0
+    ordered = torch.where(neg, (~bits) & 0xFFFFFFFF, bits | 0x80000000)
+    return (ordered << 32) | (0xFFFFFFFF - index.to(torch.int64))
+
+
+def local_argmax_keys(z: torch.Tensor, row_offset: int = 0) -> torch.Tensor:
+    """Keys of a (F, J_local) map block whose first column is global candidate `row_offset`."""
+    vals, idx = z.max(dim=1)
+    first = (z == vals[:, None]).to(torch.int8).argmax(dim=1)   # lowest index among ties
+    return encode_host_keys(vals, first + row_offset)

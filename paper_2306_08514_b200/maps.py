@@ -247,7 +247,7 @@ def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True):
     buf, f, batched = _lag_major(samples, fat.shape[1])
     d_fat, d_tall = _slri_device(lr)
     r, j = fat.shape[0], d_tall.shape[0]
-    work = torch.empty((f, r), dtype=torch.float32, device=buf.device)
+    work = torch.empty((17, f, r), dtype=torch.float32, device=buf.device)   # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
     nat.call("srpgpu_slri_map", dev.ptr(buf), buf.shape[1], f, fat.shape[1], dev.ptr(d_fat),
@@ -280,7 +280,7 @@ def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True):
     v = v.reshape(-1, fat.shape[1])
     d_fat2, d_tall2 = _lr_device(lr)
     r, j, f = fat.shape[0], d_tall2.shape[0], v.shape[0]
-    work = torch.empty((f, 2 * r), dtype=torch.float32, device=v.device)
+    work = torch.empty((17, f, 2 * r), dtype=torch.float32, device=v.device)  # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
     keys = _new_keys(f, argmax)
     nat.call("srpgpu_lr_map", dev.ptr(v), f, fat.shape[1], dev.ptr(d_fat2), dev.ptr(d_tall2), r, j,
