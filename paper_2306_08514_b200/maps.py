@@ -181,7 +181,34 @@ class EllOperator:
         return vals, cols, splits
 
 
+    @classmethod
+    def from_fixed(cls, fx, offsets: np.ndarray) -> "EllOperator":
+        """ELL image of a FixedNnzInterp without going through a CSR (cfg4-size operators)."""
+        self = cls.__new__(cls)
+        p_count, j, k = fx.values.shape
+        j_pad = (j + 31) // 32 * 32
+        packed = np.zeros((p_count, j_pad, k, 2), dtype=np.uint32)
+        packed[:, :, :, 1] = np.asarray(offsets[:-1], dtype=np.uint32)[:, None, None]
+        packed[:, :j, :, 0] = fx.values.astype(np.float32).view(np.uint32)
+        packed[:, :j, :, 1] = fx.cols.astype(np.uint32)
+        self.num_rows, self.num_cols, self.num_pairs, self.rows_padded = j, int(fx.num_cols), p_count, j_pad
+        self.offsets = offsets
+        self.widths = np.full(p_count, k, dtype=np.int64)
+        self.counts = np.repeat(np.asarray(fx.kept, dtype=np.int64)[:, None], j, axis=1)
+        self.ell_off = np.arange(p_count + 1, dtype=np.int64) * j_pad * k
+        self.host_packed = packed.reshape(-1, 2)
+        self.max_block = int(np.max(np.diff(offsets))) if p_count else 0
+        self.d_packed = torch.from_numpy(self.host_packed.reshape(-1).view(np.int32)).to(dev.device())
+        self.d_offsets = dev.as_i32(offsets)
+        self.d_widths = dev.as_i32(self.widths)
+        self.d_ell_off = dev.as_i64(self.ell_off)
+        return self
+
+
 def ell_from_sparse(sp, offsets: np.ndarray) -> EllOperator:
+    if hasattr(sp, "kept") and getattr(sp, "cols", None) is not None and np.ndim(sp.cols) == 3:
+        return dev.CACHE.get(sp, ("ell_fixed", tuple(int(o) for o in offsets)),
+                             lambda: EllOperator.from_fixed(sp, offsets))
     key = ("ell", tuple(int(o) for o in offsets))
     return dev.CACHE.get(sp, key, lambda: EllOperator(sp.values, sp.col_indices, sp.row_splits,
                                                       int(sp.num_cols), offsets))
@@ -211,9 +238,18 @@ def _ell_map(ell: EllOperator, samples, argmax: bool, out_map: bool):
     return _finish(z, keys, batched, argmax)
 
 
+def _check_cols(samples, num_cols: int) -> None:
+    """The reference's DimensionError check (interpolation.py:191-194) without touching data."""
+    vals = samples.values if hasattr(samples, "values") else samples
+    shape = tuple(vals.shape) if hasattr(vals, "shape") else np.shape(vals)
+    if len(shape) not in (1, 2) or shape[-1] != num_cols:
+        raise DimensionError(f"sample vector of shape {shape} does not match operator with "
+                             f"{num_cols} columns")
+
+
 def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True):
     """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195)."""
-    _sample_matrix(samples, int(sp.num_cols))      # reference DimensionError check first
+    _check_cols(samples, int(sp.num_cols))         # reference DimensionError check first
     ell = ell_from_sparse(sp, _sample_offsets(samples, int(sp.num_cols)))
     return _ell_map(ell, samples, argmax, out_map)
 
@@ -225,7 +261,7 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
     bit for bit, as in the reference (interpolation.py:112-126).
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
-    _sample_matrix(samples, num_cols)
+    _check_cols(samples, num_cols)
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
         offsets = np.array([0, num_cols], dtype=np.int64)

@@ -246,3 +246,96 @@ def resolve_sparsity(token, num_candidates: int, num_pairs: int, size: int) -> i
     if isinstance(token, str) and token.endswith("jp"):
         return int(round(float(token[:-2]) * num_candidates * num_pairs))
     return int(token)
+
+
+@dataclass(frozen=True)
+class FixedNnzInterp:
+    """Fixed-nnz-per-(candidate, pair) sparse interpolation operator, pair-blocked.
+
+    cols[p, i, :] are absolute sample indices (ascending), values[p, i, :] the
+    float64 sinc weights; every (candidate, pair) keeps min(nnz, 2 N_p + 1)
+    entries (shorter pair blocks are padded with value 0 at their first column).
+    It is exactly `truncate_sparse_fixed(build_interp_matrix(...), nnz)` but is
+    built pair by pair from the TDOA table, so the dense J x S operator (18.7 GB at
+    BASELINE cfg4) never exists.  `to_csr()` gives the reference `SparseInterp`.
+    """
+
+    values: np.ndarray      # (P, J, k) float64
+    cols: np.ndarray        # (P, J, k) int32
+    kept: np.ndarray        # (P,) entries really kept per (i, p)
+    num_cols: int
+
+    @property
+    def num_rows(self) -> int:
+        return self.values.shape[1]
+
+    @property
+    def num_kept(self) -> int:
+        return int(np.sum(self.kept)) * self.num_rows
+
+    def to_csr(self) -> SparseInterp:
+        p_count, j, _ = self.values.shape
+        rows, cols, vals = [], [], []
+        for p in range(p_count):
+            k = int(self.kept[p])
+            rows.append(np.repeat(np.arange(j), k))
+            cols.append(self.cols[p, :, :k].ravel().astype(np.int64))
+            vals.append(self.values[p, :, :k].ravel())
+        r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+        order = np.lexsort((c, r))
+        splits = np.zeros(j + 1, dtype=np.int64)
+        np.cumsum(np.bincount(r, minlength=j), out=splits[1:])
+        return SparseInterp(values=v[order], col_indices=c[order], row_splits=splits,
+                            num_cols=self.num_cols)
+
+
+def sparse_interp_fixed(tdoa, spec, frame, nnz: int, rows=None) -> FixedNnzInterp:
+    """Per (candidate, pair): the `nnz` largest |sinc(dt fs - n)|, ties to the lower column.
+
+    |sinc(x - n)| = |sin(pi x)| / (pi |x - n|) decreases with |x - n|, so the winners
+    lie among the nnz + 2 lags nearest to x; those are evaluated exactly as
+    build_interp_matrix does (np.sinc on float64) and ranked by a stable sort on
+    (-|value|, column), which reproduces the full-block argsort of
+    truncate_sparse_fixed.  `rows` optionally restricts to a candidate subset.
+    """
+    if nnz < 1:
+        raise ValueError("nnz must be >= 1")
+    off = _offsets(spec)
+    delta = tdoa.delta_t if rows is None else tdoa.delta_t[rows]
+    j, p_count = delta.shape
+    kmax = int(min(nnz, np.max(2 * np.asarray(spec.counts) + 1)))
+    values = np.zeros((p_count, j, kmax))
+    cols = np.zeros((p_count, j, kmax), dtype=np.int32)
+    kept = np.zeros(p_count, dtype=np.int64)
+    for p in range(p_count):
+        c = int(spec.counts[p])
+        width = 2 * c + 1
+        k = min(nnz, width)
+        kept[p] = k
+        cols[p, :, :] = off[p]
+        x = delta[:, p] / frame.sample_period
+        span = min(width, k + 2)
+        base = np.floor(x).astype(np.int64) - (span - 1) // 2
+        base = np.clip(base, -c, c - span + 1)
+        lags = base[:, None] + np.arange(span)[None, :]                 # signed lags, ascending
+        vals = np.sinc(x[:, None] - lags)
+        colid = np.where(lags >= 0, lags, width + lags)                  # storage order 0..N, -N..-1
+        # stable ranking per row: primary -|v|, secondary column id
+        key = np.argsort(colid, axis=1, kind="stable")
+        v_s = np.take_along_axis(vals, key, 1)
+        c_s = np.take_along_axis(colid, key, 1)
+        rank = np.argsort(-np.abs(v_s), axis=1, kind="stable")[:, :k]
+        sel_c = np.take_along_axis(c_s, rank, 1)
+        sel_v = np.take_along_axis(v_s, rank, 1)
+        # near-integer x: the off-peak sinc values are rounding noise (sin(pi n) != 0 in
+        # floating point) and not monotone in |x - n|; rank those rows over the whole block
+        odd = np.flatnonzero(np.min(np.abs(sel_v), axis=1) < 1e-9) if k > 1 else np.zeros(0, int)
+        if odd.size:
+            full = np.sinc(x[odd, None] - _lags(c)[None, :])          # storage order
+            r2 = np.argsort(-np.abs(full), axis=1, kind="stable")[:, :k]
+            sel_c[odd] = r2
+            sel_v[odd] = np.take_along_axis(full, r2, 1)
+        back = np.argsort(sel_c, axis=1, kind="stable")
+        cols[p, :, :k] = np.take_along_axis(sel_c, back, 1) + off[p]
+        values[p, :, :k] = np.take_along_axis(sel_v, back, 1)
+    return FixedNnzInterp(values=values, cols=cols, kept=kept, num_cols=int(off[-1]))

@@ -1,0 +1,152 @@
+"""GPU parity at the BASELINE.json configurations' full grids (cfg2, cfg3, cfg4).
+
+Frame counts are reduced where the float64 oracle would take too long; the
+checks are size-independent: per-frame normalized max error <= 1e-4 against the
+oracle on a frame subset, argmax agreement on margin-qualified frames, bitwise
+invariance of the maps under frame partitioning (the multi-GPU split), and the
+nnz / rank sweeps of BASELINE configs[1].
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2306_08514_b200 as s
+from paper_2306_08514_b200 import workloads
+from paper_2306_08514_b200.operators import low_rank_interp_from_svd, low_rank_srp_from_svd
+from oracle import srp_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def oracle_psi(wl, nf):
+    win = O.frame_window(wl.frame.frame_len, wl.frame.window)
+    spectra = O.stft_frames(wl.samples.astype(np.float64), wl.frame.frame_len, wl.frame.hop, win,
+                            np.arange(nf))
+    return O.fd_gcc(spectra, wl.pairs.pairs)
+
+
+def check(z_gpu, z_ref, idx_gpu=None):
+    z = z_gpu.detach().float().cpu().numpy()[: z_ref.shape[0]]
+    err = O.normalized_max_error(z, z_ref)
+    assert err.max() <= TOL, f"normalized max error {err.max():.3e}"
+    if idx_gpu is not None:
+        ok = O.peak_margin(z_ref) > TOL
+        idx = idx_gpu.cpu().numpy()[: z_ref.shape[0]]
+        assert np.array_equal(idx[ok], np.argmax(z_ref, axis=1)[ok])
+    return float(err.max())
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    wl = workloads.make("cfg2")
+    x = torch.from_numpy(wl.samples).cuda()
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec)
+    psi_ref = oracle_psi(wl, 32)
+    xi_ref = O.td_gcc_samples(psi_ref, wl.spec.counts, wl.frame.half_len)
+    return wl, x, xi, psi_ref, xi_ref
+
+
+def test_cfg2_samples_and_sspi_global_fit(cfg2):
+    wl, x, xi, psi_ref, xi_ref = cfg2
+    got = xi.values[:32].cpu().numpy()
+    err = np.abs(got - xi_ref).max(axis=1) / np.abs(xi_ref).max(axis=1)
+    assert err.max() < 2e-5
+    interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame)
+    sp = s.truncate_sparse(interp, 2 * wl.grid.num_points * wl.pairs.num_pairs)
+    z, idx = s.sspi_map(sp, xi, argmax=True)
+    z_ref = O.sspi_map(sp.values, sp.col_indices, sp.row_splits, xi_ref)
+    check(z, z_ref, idx)
+    # frame partition (the multi-GPU split) leaves every map bit-identical
+    half = wl.num_frames // 2
+    xa = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(0, half))
+    xb = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(half, wl.num_frames))
+    za, ia = s.sspi_map(sp, xa, argmax=True)
+    zb, ib = s.sspi_map(sp, xb, argmax=True)
+    assert torch.equal(torch.cat([za, zb]), z) and torch.equal(torch.cat([ia, ib]), idx)
+
+
+@pytest.mark.parametrize("nnz", [1, 2, 4, 8, 16])
+def test_cfg2_sspi_nnz_sweep(cfg2, nnz):
+    wl, x, xi, psi_ref, xi_ref = cfg2
+    fx = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, nnz)
+    z, idx = s.sspi_map(fx, xi, argmax=True)
+    csr = fx.to_csr()
+    z_ref = O.sspi_map(csr.values, csr.col_indices, csr.row_splits, xi_ref)
+    check(z, z_ref, idx)
+
+
+def test_cfg2_rank_sweeps(cfg2):
+    wl, x, xi, psi_ref, xi_ref = cfg2
+    interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame)
+    u, sv, vt = np.linalg.svd(interp.matrix, full_matrices=False)
+    srp = s.build_srp_matrix(wl.tdoa, wl.frame)
+    hu, hs, hvt = np.linalg.svd(srp.matrix, full_matrices=False)
+    gcc = s.gcc_frames(x, wl.frame, wl.pairs)
+    for r in (1, 2, 4, 8, 16, 32):
+        lri = low_rank_interp_from_svd(u, sv, vt, r)
+        z, idx = s.slri_map(lri, xi, argmax=True)
+        check(z, O.slri_map(lri.tall, lri.fat, xi_ref), idx)
+        lrs = low_rank_srp_from_svd(hu, hs, hvt, r)
+        z, idx = s.lr_map(lrs, gcc, argmax=True)
+        check(z, O.lr_map(lrs.tall, lrs.fat, psi_ref), idx)
+
+
+def test_cfg2_conventional(cfg2):
+    wl, x, xi, psi_ref, xi_ref = cfg2
+    srp = s.build_srp_matrix(wl.tdoa, wl.frame)
+    z_ref = O.srp_map_exact(srp.matrix, psi_ref)
+    for prec in ("tf32", "fp32"):
+        gcc = s.gcc_frames(x, wl.frame, wl.pairs, tf32=(prec == "tf32"))
+        z, idx = s.srp_map_exact(srp, gcc, precision=prec, argmax=True)
+        check(z, z_ref, idx)
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    wl = workloads.make("cfg3", num_frames=256)
+    x = torch.from_numpy(wl.samples).cuda()
+    psi_ref = oracle_psi(wl, 8)
+    xi_ref = O.td_gcc_samples(psi_ref, wl.spec.counts, wl.frame.half_len)
+    return wl, x, psi_ref, xi_ref
+
+
+def test_cfg3_full_grid(cfg3):
+    wl, x, psi_ref, xi_ref = cfg3
+    assert wl.grid.num_points == 32760 and wl.pairs.num_pairs == 28
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec)
+    interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame)
+    sp = s.truncate_sparse(interp, 2 * wl.grid.num_points * wl.pairs.num_pairs)
+    z, idx = s.sspi_map(sp, xi, argmax=True)
+    check(z, O.sspi_map(sp.values, sp.col_indices, sp.row_splits, xi_ref), idx)
+    lr = s.truncate_low_rank(interp, 16)
+    z, idx = s.slri_map(lr, xi, argmax=True)
+    check(z, O.slri_map(lr.tall, lr.fat, xi_ref), idx)
+    # pole rows (polar 180 deg, 360 azimuths) are exact duplicates -> identical map values
+    zz = z[:, -360:]
+    assert torch.equal(zz, zz[:, :1].expand_as(zz))
+
+
+def test_cfg3_conventional_tf32(cfg3):
+    wl, x, psi_ref, xi_ref = cfg3
+    srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 34)
+    gcc = s.gcc_frames(x, wl.frame, wl.pairs, tf32=True)
+    z, idx = s.srp_map_exact(srp, gcc, argmax=True)
+    check(z, O.srp_map_exact(srp.matrix, psi_ref), idx)
+
+
+def test_cfg4_full_grid_sspi():
+    wl = workloads.make("cfg4", num_frames=64)
+    assert wl.grid.num_points == 334611 and wl.pairs.num_pairs == 120
+    x = torch.from_numpy(wl.samples).cuda()
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec)
+    fx = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
+    z, idx = s.sspi_map(fx, xi, argmax=True)
+    nf = 4
+    xi_ref = O.td_gcc_samples(oracle_psi(wl, nf), wl.spec.counts, wl.frame.half_len)
+    z_ref = np.zeros((nf, wl.grid.num_points))
+    for p in range(wl.pairs.num_pairs):
+        k = int(fx.kept[p])
+        z_ref += np.einsum("jk,fjk->fj", fx.values[p, :, :k], xi_ref[:, fx.cols[p, :, :k]])
+    check(z, z_ref, idx)

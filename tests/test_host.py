@@ -178,3 +178,31 @@ def test_workloads_deterministic():
     assert_array_equal(a.samples, b.samples)
     assert a.grid.num_points == 1681 and a.pairs.num_pairs == 6
     assert a.samples.shape == (4, 7 * 512 + 1024)
+
+
+def test_fixed_nnz_from_tdoa_matches_dense_fit(golden_scene):
+    """The cfg4-scale builder (no dense Lambda) equals the dense per-(i, p) top-k fit bit for bit."""
+    from paper_2306_08514_b200.operators import sparse_interp_fixed
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    interp = s.build_interp_matrix(tdoa, spec, frame)
+    for nnz in (1, 2, 3, 8):
+        a = s.truncate_sparse_fixed(interp, nnz)
+        fx = sparse_interp_fixed(tdoa, spec, frame, nnz)
+        b = fx.to_csr()
+        assert_array_equal(a.col_indices, b.col_indices)
+        assert_array_equal(a.row_splits, b.row_splits)
+        assert_array_equal(a.values, b.values)
+        assert fx.num_kept == a.num_kept
+        from paper_2306_08514_b200 import maps
+        import torch
+        orig = maps.dev.device
+        maps.dev.device = lambda: torch.device("cpu")
+        try:
+            ell = maps.EllOperator.from_fixed(fx, spec.offsets)
+        finally:
+            maps.dev.device = orig
+        vals, cols, splits = ell.to_csr()
+        assert_array_equal(cols, a.col_indices)
+        assert_array_equal(splits, a.row_splits)
+        assert_array_equal(vals, a.values.astype(np.float32))
