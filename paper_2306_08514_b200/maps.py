@@ -56,7 +56,7 @@ def _finish(z, keys, batched: bool, argmax: bool):
 
 def _gcc_matrix(gcc, num_pairs: int, num_bins: int):
     """(F, P*B) complex64 device tensor + batched flag, with the reference shape check."""
-    vals = gcc.values if hasattr(gcc, "values") else gcc
+    vals = gcc if isinstance(gcc, (torch.Tensor, np.ndarray)) else gcc.values
     v = dev.as_c64(vals)
     batched = v.dim() == 2
     if v.shape[-1] != num_pairs * num_bins:
@@ -66,7 +66,8 @@ def _gcc_matrix(gcc, num_pairs: int, num_bins: int):
 
 
 def _sample_matrix(samples, num_cols: int):
-    vals = samples.values if isinstance(samples, TdGccSamples) or hasattr(samples, "spec") else samples
+    vals = samples.values if (not isinstance(samples, (torch.Tensor, np.ndarray, list, tuple))
+                               and hasattr(samples, "spec")) else samples
     x = dev.as_f32(vals)
     batched = x.dim() == 2
     if x.shape[-1] != num_cols or x.dim() > 2:
@@ -240,7 +241,8 @@ def _ell_map(ell: EllOperator, samples, argmax: bool, out_map: bool):
 
 def _check_cols(samples, num_cols: int) -> None:
     """The reference's DimensionError check (interpolation.py:191-194) without touching data."""
-    vals = samples.values if hasattr(samples, "values") else samples
+    plain = isinstance(samples, (torch.Tensor, np.ndarray, list, tuple))
+    vals = samples if plain else samples.values
     shape = tuple(vals.shape) if hasattr(vals, "shape") else np.shape(vals)
     if len(shape) not in (1, 2) or shape[-1] != num_cols:
         raise DimensionError(f"sample vector of shape {shape} does not match operator with "
@@ -307,7 +309,7 @@ def _lr_device(lr):
 def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True):
     """Low-rank SRP map z = 2 Re(tall (fat psi)) (lowrank.py:51-57)."""
     fat = np.asarray(lr.fat)
-    vals = gcc.values if hasattr(gcc, "values") else gcc
+    vals = gcc if isinstance(gcc, (torch.Tensor, np.ndarray)) else gcc.values
     v = dev.as_c64(vals)
     if v.shape[-1] != fat.shape[1] or v.dim() > 2:
         raise DimensionError(f"cross-spectrum of shape {tuple(v.shape)} does not match factor "
