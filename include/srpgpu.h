@@ -109,17 +109,17 @@ int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t 
 
 /* sspi_map (interpolation.py:188-195) and, with a keep-all operator, si_map
  * (:129-136).  samples: lag-major [S][samples_ld] (samples_ld >= F, multiple of 4,
- * 16-byte aligned).  Pair-major ELL operator with rows padded to a multiple of 32
- * candidates: entries of pair p at ell[ell_offsets[p] + i*widths[p] + w], each a
- * packed {uint32 float-bits value, uint32 absolute sample index}; padding entries
- * have value 0.  widths [P], ell_offsets [P+1] are device arrays; max_width =
- * max widths[p], sum_widths = sum widths[p].  z [F][J] and keys [F] are each
- * optional (NULL). */
+ * 16-byte aligned).  Operator: tiled band image (tiles of 32 candidates, groups of 4):
+ * tile t's blob starts at byte tile_offsets[t] of `blob` and holds
+ *   meta[P][8] u32 = (record offset << 8) | record count, padded to 16 bytes,
+ *   records {u32 sample index, u32 pad[3], f32 weight[4]} for each (pair, group),
+ *   pair-major, then group, then ascending sample index;
+ * max_pair_records / max_tile_records = largest record count of one (tile, pair) / of one
+ * tile (shared-memory staging size).  z [F][J] and keys [F] are each optional (NULL). */
 int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t num_frames,
-                    int32_t total_samples, int32_t num_pairs, const int32_t* widths,
-                    const int64_t* ell_offsets, const void* ell, int64_t num_candidates,
-                    int32_t max_width, int32_t sum_widths, float* z, uint64_t* keys,
-                    srpgpu_stream_t stream);
+                    int32_t total_samples, int32_t num_pairs, const int64_t* tile_offsets,
+                    const void* blob, int64_t num_candidates, int64_t max_pair_records,
+                    int64_t max_tile_records, float* z, uint64_t* keys, srpgpu_stream_t stream);
 
 /* frame-major [rows][ld_src] -> lag-major [cols][ld_dst] (zero-filled pad columns). */
 int srpgpu_transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,

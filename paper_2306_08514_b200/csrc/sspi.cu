@@ -1,159 +1,177 @@
 // Sparse interpolation map (SSPI-SRP) on sm_100a:
-//   z[f][i] = sum_p sum_{w < W_p} v[p][i][w] * xi[s[p][i][w]][f]
-// restating interpolation.py:188-195 (_dot_sparse_rows :121-126).  With a
-// keep-all operator the same kernel is si_map (:129-136), so sspi(all) == si
-// bit-for-bit as in the reference (interpolation.py:112-126).
+//   z[f][i] = sum_p sum_{kept (i,p,n)} Lambda[i][p,n] * xi[(p,n)][f]
+// restating interpolation.py:188-195 (_dot_sparse_rows :121-126).  With a keep-all
+// operator the same kernel is si_map (:129-136), so sspi(all) == si bit-for-bit as in
+// the reference (interpolation.py:112-126).
 //
-// Operator (built once on the host from the reference CSR): pair-major ELL with
-// rows padded to a multiple of 32 candidates.  Entries of pair p live at
-// ell[ell_off[p] + i * W_p + w] as packed (float value bits, absolute sample index);
-// padding entries carry value 0.  Each (candidate, pair) keeps the reference's
-// entries in ascending column order.
+// Operator layout: "tiled band" (built once on the host from the reference CSR).
+// Candidates are cut into tiles of 32 and each tile into 8 groups of 4.  For every
+// (tile, pair, group) the union of the lags kept by the group's 4 candidates becomes a
+// run of records {u32 sample index, 3 x pad, f32 weight[4]} (weight 0 where a candidate
+// does not keep that lag).  A tile's blob is contiguous:
+//     meta[P][8] : u32 (record offset << 8 | record count)      (16-byte padded)
+//     records    : pair-major, then group, then ascending sample index
+// so one TMA bulk copy stages a tile's operator (chunked by pairs when it exceeds the
+// shared-memory budget).
 //
-// Samples are lag-major: xi[s][f] with row pitch `ld` (frames contiguous), as
-// written by the fused frontend.  Tile kernel: a CTA owns 32 candidates x 128
-// frames.  The CTA's operator rows (one contiguous run per pair) are staged in
-// shared memory by TMA bulk copies (cp.async.bulk + mbarrier); each lane owns
-// 4 consecutive frames and each warp 4 candidates, so every kept entry is one
-// broadcast shared-memory read of (value, lag), one coalesced 16-byte read of
-// xi[lag][f..f+3] (L1-resident across the CTA) and 4 FMAs into registers.  The
-// pair sum stays in registers; z is written through a shared-memory transpose as
-// coalesced rows z[f][i0 : i0+32] and the per-frame argmax is folded into packed
-// 64-bit keys (one atomicMax per frame per CTA).
+// Samples are lag-major xi[s][f] (row pitch ld, frames contiguous).  CTA = 32
+// candidates x 128 frames; lane = 4 consecutive frames, warp = one group of 4
+// candidates.  Per record: one broadcast shared-memory read (index + 4 weights), one
+// coalesced 16-byte L1 read of xi[s][f..f+3], 16 FMAs into registers -- the xi value is
+// reused from registers by all 4 candidates of the group.  z leaves through a
+// shared-memory transpose as coalesced rows z[f][i0 : i0+32]; the per-frame argmax is
+// folded into packed 64-bit keys (one atomicMax per frame per CTA).
 #include "common.cuh"
 
 namespace srpgpu {
 
-constexpr int kSspiWarps = 8;
-constexpr int kSspiG = 4;                          // candidates per warp
-constexpr int kSspiTI = kSspiWarps * kSspiG;       // 32 candidates per CTA
-constexpr int kSspiTF = 128;                       // frames per CTA (4 per lane)
-constexpr int kSspiOpsBudget = 96 * 1024;          // bytes of staged operator rows per chunk
+constexpr int kWarps = 8;
+constexpr int kGroup = 4;                          // candidates per warp
+constexpr int kTileI = kWarps * kGroup;            // 32 candidates per CTA
+constexpr int kTileF = 128;                        // frames per CTA (4 per lane)
+constexpr int kRecBudget = 160 * 1024;             // bytes of staged records per chunk
 
-struct SspiParams {
-  const float* xi;           // [S][ld]
+struct __align__(16) BandRec {
+  uint32_t s, pad0, pad1, pad2;
+  float4 w;
+};
+
+struct BandParams {
+  const float* xi;            // [S][ld]
   int64_t ld;
   int64_t F;
   int32_t S;
   int32_t P;
-  const int32_t* widths;     // [P]
-  const int64_t* ell_off;    // [P+1]
-  const uint2* ell;          // packed entries, rows padded to a multiple of 32
+  const int64_t* tile_off;    // [T+1] byte offsets of the tile blobs
+  const unsigned char* blob;
   int64_t J;
-  float* z;                  // [F][J] or null
-  unsigned long long* keys;  // [F] or null
-  int32_t ent_max;           // max sum of widths per staged chunk
+  float* z;                   // [F][J] or null
+  unsigned long long* keys;   // [F] or null
+  int32_t rec_cap;            // records per staged chunk
 };
 
 __device__ __forceinline__ uint32_t s_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(kSspiWarps * 32)
-sspi_tile_kernel(const SspiParams prm) {
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          s_addr(dst)),
+      "l"(src), "r"(bytes), "r"(s_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(s_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ size_t meta_bytes(int P) { return ((size_t)P * kWarps * 4 + 15) & ~(size_t)15; }
+
+__global__ void __launch_bounds__(kWarps * 32)
+sspi_band_kernel(const BandParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
-  int* s_w = reinterpret_cast<int*>(smem_raw);                                  // [P]
-  float* zs = reinterpret_cast<float*>(smem_raw + (((size_t)prm.P * 4 + 127) & ~(size_t)127));  // [TF][TI+1]
-  uint2* ops = reinterpret_cast<uint2*>(
-      reinterpret_cast<unsigned char*>(zs) + (((size_t)kSspiTF * (kSspiTI + 1) * 4 + 127) & ~(size_t)127));
+  const int P = prm.P;
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem_raw);                          // [P][8]
+  float* zs = reinterpret_cast<float*>(smem_raw + ((meta_bytes(P) + 127) & ~(size_t)127));   // [TF][TI+1]
+  BandRec* recs = reinterpret_cast<BandRec*>(
+      reinterpret_cast<unsigned char*>(zs) + (((size_t)kTileF * (kTileI + 1) * 4 + 127) & ~(size_t)127));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = (int64_t)blockIdx.x * kSspiTI;
-  const int64_t f0 = (int64_t)blockIdx.y * kSspiTF;
-  const int P = prm.P;
-  for (int i = tid; i < P; i += blockDim.x) s_w[i] = prm.widths[i];
+  const int64_t tile = blockIdx.x;
+  const int64_t i0 = tile * kTileI;
+  const int64_t f0 = (int64_t)blockIdx.y * kTileF;
+  const unsigned char* tb = prm.blob + prm.tile_off[tile];
+  const BandRec* grec = reinterpret_cast<const BandRec*>(tb + meta_bytes(P));
+
+  uint32_t phase = 0;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t mb = (uint32_t)meta_bytes(P);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(&bar)), "r"(mb)
+                 : "memory");
+    bulk_copy(meta, tb, mb, &bar);
   }
   __syncthreads();
+  mbar_wait(&bar, phase);
+  phase ^= 1u;
 
-  float acc[kSspiG][4];
+  float acc[kGroup][4];
 #pragma unroll
-  for (int c = 0; c < kSspiG; ++c)
+  for (int c = 0; c < kGroup; ++c)
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[c][t] = 0.f;
   const int64_t fl = f0 + 4 * lane;
   const bool lane_ok = fl < prm.ld;
   const float* xcol = prm.xi + fl;
+  const uint32_t total_recs =
+      (uint32_t)((prm.tile_off[tile + 1] - prm.tile_off[tile] - (int64_t)meta_bytes(P)) / sizeof(BandRec));
 
-  uint32_t phase = 0;
   int pc0 = 0;
   while (pc0 < P) {
-    int pc1 = pc0, ents = 0;
-    while (pc1 < P && (pc1 == pc0 || ents + s_w[pc1] <= prm.ent_max)) ents += s_w[pc1++];
-    if (ents > 0) {
+    // records of pairs [pc0, pc1) are contiguous: [start(pc0), start(pc1))
+    const uint32_t r0 = meta[pc0 * kWarps] >> 8;
+    int pc1 = pc0 + 1;   // at least one pair (the host checks a single pair fits)
+    while (pc1 < P && ((pc1 + 1 < P) ? (meta[(pc1 + 1) * kWarps] >> 8) : total_recs) - r0 <=
+                          (uint32_t)prm.rec_cap)
+      ++pc1;
+    const uint32_t r1 = (pc1 < P) ? (meta[pc1 * kWarps] >> 8) : total_recs;
+    if (r1 > r0) {
       if (tid == 0) {
-        // TMA bulk copies: this CTA's rows of every pair in the chunk
-        const uint32_t bytes = (uint32_t)ents * kSspiTI * 8u;
+        const uint32_t bytes = (r1 - r0) * (uint32_t)sizeof(BandRec);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(&bar)), "r"(bytes)
                      : "memory");
-        int e = 0;
-        for (int p = pc0; p < pc1; ++p) {
-          const int W = s_w[p];
-          if (W == 0) continue;
-          const uint2* src = prm.ell + prm.ell_off[p] + i0 * W;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  s_addr(ops + (size_t)e * kSspiTI)),
-              "l"(src), "r"((uint32_t)(W * kSspiTI * 8)), "r"(s_addr(&bar))
-              : "memory");
-          e += W;
-        }
+        bulk_copy(recs, grec + r0, bytes, &bar);
       }
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "WAIT_%=:\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-          "@!p bra WAIT_%=;\n\t}" ::"r"(s_addr(&bar)),
-          "r"(phase)
-          : "memory");
+      mbar_wait(&bar, phase);
       phase ^= 1u;
       if (lane_ok) {
-        const uint2* opp = ops;
         for (int p = pc0; p < pc1; ++p) {
-          const int W = s_w[p];
-          const uint2* rowb = opp + (warp * kSspiG) * W;
-#pragma unroll 2
-          for (int w = 0; w < W; ++w) {
-            uint2 en[kSspiG];
-            float4 x[kSspiG];
-#pragma unroll
-            for (int c = 0; c < kSspiG; ++c) en[c] = rowb[c * W + w];
-#pragma unroll
-            for (int c = 0; c < kSspiG; ++c)
-              x[c] = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)en[c].y * prm.ld));
-#pragma unroll
-            for (int c = 0; c < kSspiG; ++c) {
-              const float v = __uint_as_float(en[c].x);
-              acc[c][0] = fmaf(v, x[c].x, acc[c][0]);
-              acc[c][1] = fmaf(v, x[c].y, acc[c][1]);
-              acc[c][2] = fmaf(v, x[c].z, acc[c][2]);
-              acc[c][3] = fmaf(v, x[c].w, acc[c][3]);
-            }
+          const uint32_t m = meta[p * kWarps + warp];
+          const BandRec* rr = recs + ((m >> 8) - r0);
+          const int n = (int)(m & 0xFFu);
+#pragma unroll 4
+          for (int r = 0; r < n; ++r) {
+            const uint32_t s = rr[r].s;
+            const float4 w = rr[r].w;
+            const float4 x = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)s * prm.ld));
+            acc[0][0] = fmaf(w.x, x.x, acc[0][0]); acc[0][1] = fmaf(w.x, x.y, acc[0][1]);
+            acc[0][2] = fmaf(w.x, x.z, acc[0][2]); acc[0][3] = fmaf(w.x, x.w, acc[0][3]);
+            acc[1][0] = fmaf(w.y, x.x, acc[1][0]); acc[1][1] = fmaf(w.y, x.y, acc[1][1]);
+            acc[1][2] = fmaf(w.y, x.z, acc[1][2]); acc[1][3] = fmaf(w.y, x.w, acc[1][3]);
+            acc[2][0] = fmaf(w.z, x.x, acc[2][0]); acc[2][1] = fmaf(w.z, x.y, acc[2][1]);
+            acc[2][2] = fmaf(w.z, x.z, acc[2][2]); acc[2][3] = fmaf(w.z, x.w, acc[2][3]);
+            acc[3][0] = fmaf(w.w, x.x, acc[3][0]); acc[3][1] = fmaf(w.w, x.y, acc[3][1]);
+            acc[3][2] = fmaf(w.w, x.z, acc[3][2]); acc[3][3] = fmaf(w.w, x.w, acc[3][3]);
           }
-          opp += (size_t)W * kSspiTI;
         }
       }
-      __syncthreads();   // the next chunk overwrites `ops`
+      __syncthreads();   // the next chunk overwrites `recs`
     }
     pc0 = pc1;
   }
 
   // epilogue: transpose through shared memory -> coalesced rows of z, fused argmax
 #pragma unroll
-  for (int c = 0; c < kSspiG; ++c)
+  for (int c = 0; c < kGroup; ++c)
 #pragma unroll
-    for (int t = 0; t < 4; ++t) zs[(4 * lane + t) * (kSspiTI + 1) + warp * kSspiG + c] = acc[c][t];
+    for (int t = 0; t < 4; ++t) zs[(4 * lane + t) * (kTileI + 1) + warp * kGroup + c] = acc[c][t];
   __syncthreads();
-  const int ti_valid = (int)(prm.J - i0 < kSspiTI ? prm.J - i0 : kSspiTI);
-  for (int row = warp; row < kSspiTF; row += kSspiWarps) {
+  const int ti_valid = (int)(prm.J - i0 < kTileI ? prm.J - i0 : kTileI);
+  for (int row = warp; row < kTileF; row += kWarps) {
     const int64_t fg = f0 + row;
     if (fg >= prm.F) break;
     unsigned long long key = 0ull;
     if (lane < ti_valid) {
-      const float v = zs[row * (kSspiTI + 1) + lane];
+      const float v = zs[row * (kTileI + 1) + lane];
       if (prm.z) prm.z[fg * prm.J + i0 + lane] = v;
       key = make_key(v, (uint32_t)(i0 + lane));
     }
@@ -165,19 +183,27 @@ sspi_tile_kernel(const SspiParams prm) {
 }
 
 // Small-frame-count path (e.g. the per-frame reference call): a thread per
-// (candidate, frame), entries read straight from global memory.
-__global__ void sspi_rows_kernel(const SspiParams prm) {
+// (candidate, frame) walking its group's records; same accumulation order as the
+// tile kernel, so both give bit-identical maps.
+__global__ void sspi_band_rows_kernel(const BandParams prm) {
   const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t f = blockIdx.y;
   const bool live = gi < prm.J;
   float acc = 0.f;
   if (live) {
+    const int64_t tile = gi / kTileI;
+    const int g = (int)((gi % kTileI) / kGroup), c = (int)(gi % kGroup);
+    const unsigned char* tb = prm.blob + prm.tile_off[tile];
+    const uint32_t* meta = reinterpret_cast<const uint32_t*>(tb);
+    const BandRec* grec = reinterpret_cast<const BandRec*>(tb + meta_bytes(prm.P));
     for (int p = 0; p < prm.P; ++p) {
-      const int W = prm.widths[p];
-      const uint2* e = prm.ell + prm.ell_off[p] + gi * W;
-      for (int w = 0; w < W; ++w) {
-        const uint2 en = e[w];
-        acc = fmaf(__uint_as_float(en.x), __ldg(prm.xi + (int64_t)en.y * prm.ld + f), acc);
+      const uint32_t m = meta[p * kWarps + g];
+      const BandRec* rr = grec + (m >> 8);
+      const int n = (int)(m & 0xFFu);
+      for (int r = 0; r < n; ++r) {
+        const float4 w = rr[r].w;
+        const float wc = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
+        acc = fmaf(wc, __ldg(prm.xi + (int64_t)rr[r].s * prm.ld + f), acc);
       }
     }
     if (prm.z) prm.z[f * prm.J + gi] = acc;
@@ -210,24 +236,23 @@ __global__ void transpose_kernel(const float* __restrict__ in, int64_t rows, int
 using namespace srpgpu;
 
 extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t num_frames,
-                               int32_t total_samples, int32_t num_pairs, const int32_t* widths,
-                               const int64_t* ell_offsets, const void* ell, int64_t num_candidates,
-                               int32_t max_width, int32_t sum_widths, float* z, uint64_t* keys,
+                               int32_t total_samples, int32_t num_pairs, const int64_t* tile_offsets,
+                               const void* blob, int64_t num_candidates, int64_t max_pair_records,
+                               int64_t max_tile_records, float* z, uint64_t* keys,
                                srpgpu_stream_t stream) {
   SRPGPU_CHECK_ARG(num_pairs >= 1 && num_candidates >= 1 && total_samples >= 1, SRPGPU_ERR_DIMENSION,
                    "sspi_map: empty operator");
   SRPGPU_CHECK_ARG(num_candidates < 0xFFFFFFFFll, SRPGPU_ERR_DIMENSION, "sspi_map: too many candidates");
   SRPGPU_CHECK_ARG(samples_ld >= num_frames && samples_ld % 4 == 0, SRPGPU_ERR_VALUE,
                    "sspi_map: lag-major pitch must cover the frames and be a multiple of 4");
-  SRPGPU_CHECK_ARG(((uintptr_t)samples & 15) == 0 && ((uintptr_t)ell & 15) == 0, SRPGPU_ERR_VALUE,
+  SRPGPU_CHECK_ARG(((uintptr_t)samples & 15) == 0 && ((uintptr_t)blob & 15) == 0, SRPGPU_ERR_VALUE,
                    "sspi_map: operands must be 16-byte aligned");
   if (num_frames <= 0) return SRPGPU_OK;
   cudaStream_t st = as_stream(stream);
-  SspiParams prm = {};
+  BandParams prm = {};
   prm.xi = samples; prm.ld = samples_ld; prm.F = num_frames; prm.S = total_samples; prm.P = num_pairs;
-  prm.widths = widths; prm.ell_off = ell_offsets;
-  prm.ell = reinterpret_cast<const uint2*>(ell); prm.J = num_candidates; prm.z = z;
-  prm.keys = reinterpret_cast<unsigned long long*>(keys);
+  prm.tile_off = tile_offsets; prm.blob = reinterpret_cast<const unsigned char*>(blob);
+  prm.J = num_candidates; prm.z = z; prm.keys = reinterpret_cast<unsigned long long*>(keys);
   if (keys) {
     if (cudaMemsetAsync(keys, 0, (size_t)num_frames * sizeof(uint64_t), st) != cudaSuccess) {
       set_error("sspi_map: key reset failed");
@@ -236,27 +261,29 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
   }
   if (num_frames < 32) {
     dim3 grid((unsigned)((num_candidates + 255) / 256), (unsigned)num_frames);
-    sspi_rows_kernel<<<grid, 256, 0, st>>>(prm);
+    sspi_band_rows_kernel<<<grid, 256, 0, st>>>(prm);
     SRPGPU_CHECK_LAUNCH("sspi_map(rows)");
     return SRPGPU_OK;
   }
-  const int ent_cap = kSspiOpsBudget / (kSspiTI * 8);
-  prm.ent_max = std::max(std::max(max_width, 1), std::min(std::max(sum_widths, 1), ent_cap));
-  const size_t smem = (((size_t)num_pairs * 4 + 127) & ~(size_t)127) +
-                      (((size_t)kSspiTF * (kSspiTI + 1) * 4 + 127) & ~(size_t)127) +
-                      (size_t)prm.ent_max * kSspiTI * 8;
-  SRPGPU_CHECK_ARG(smem <= 227 * 1024, SRPGPU_ERR_UNSUPPORTED,
-                   "sspi_map: ELL width %d needs %zu B shared memory", max_width, smem);
-  if (cudaFuncSetAttribute(sspi_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  const int64_t cap = kRecBudget / (int64_t)sizeof(BandRec);
+  SRPGPU_CHECK_ARG(max_pair_records <= cap, SRPGPU_ERR_UNSUPPORTED,
+                   "sspi_map: %lld records of one pair exceed the shared-memory chunk",
+                   (long long)max_pair_records);
+  // stage whole tiles when they fit (one bulk copy), else pair chunks; size the buffer
+  // to the operator so that several CTAs stay resident per SM
+  prm.rec_cap = (int32_t)std::max<int64_t>(std::min<int64_t>(cap, max_tile_records), std::max<int64_t>(max_pair_records, 1));
+  const size_t smem = ((((size_t)num_pairs * kWarps * 4 + 15) & ~(size_t)15) + 127 & ~(size_t)127) +
+                      (((size_t)kTileF * (kTileI + 1) * 4 + 127) & ~(size_t)127) +
+                      (size_t)prm.rec_cap * sizeof(BandRec);
+  if (cudaFuncSetAttribute(sspi_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("sspi_map: cannot reserve %zu B shared memory", smem);
     return SRPGPU_ERR_LAUNCH;
   }
-  SRPGPU_CHECK_ARG((num_frames + kSspiTF - 1) / kSspiTF <= 65535, SRPGPU_ERR_DIMENSION,
+  SRPGPU_CHECK_ARG((num_frames + kTileF - 1) / kTileF <= 65535, SRPGPU_ERR_DIMENSION,
                    "sspi_map: too many frames per call");
-  dim3 grid((unsigned)((num_candidates + kSspiTI - 1) / kSspiTI),
-            (unsigned)((num_frames + kSspiTF - 1) / kSspiTF));
-  sspi_tile_kernel<<<grid, kSspiWarps * 32, smem, st>>>(prm);
+  dim3 grid((unsigned)((num_candidates + kTileI - 1) / kTileI), (unsigned)((num_frames + kTileF - 1) / kTileF));
+  sspi_band_kernel<<<grid, kWarps * 32, smem, st>>>(prm);
   SRPGPU_CHECK_LAUNCH("sspi_map");
   return SRPGPU_OK;
 }

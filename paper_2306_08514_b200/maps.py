@@ -206,36 +206,132 @@ class EllOperator:
         return self
 
 
-def ell_from_sparse(sp, offsets: np.ndarray) -> EllOperator:
+class BandOperator:
+    """Tiled band image of a sparse interpolation operator (what the SSPI kernel reads).
+
+    Candidates are cut into tiles of 32 and groups of 4.  For each (tile, pair, group)
+    the union of the sample indices kept by the group's candidates becomes records
+    {u32 sample index, 3 pad, f32 weight[4]}.  Tile blob = meta[P][8] (u32
+    `offset << 8 | count`, 16-byte padded) + records (pair-major, then group, then
+    ascending sample index); `tile_off` holds the blob byte offsets.  `mask` (host)
+    marks the (record, candidate) slots that are real kept entries, so the image
+    decodes back to the reference CSR exactly (`to_csr`).
+    """
+
+    TILE, GROUP = 32, 4
+
+    def __init__(self, rows, cols, vals, num_rows: int, num_cols: int, offsets: np.ndarray):
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.float64)
+        p_count = offsets.shape[0] - 1
+        ngrp = self.TILE // self.GROUP
+        tiles = max(1, (num_rows + self.TILE - 1) // self.TILE)
+        pair = np.searchsorted(offsets, cols, side="right") - 1
+        t = rows // self.TILE
+        g = (rows % self.TILE) // self.GROUP
+        c = rows % self.GROUP
+        key = ((t * p_count + pair) * ngrp + g) * num_cols + cols
+        uniq, inv = np.unique(key, return_inverse=True)
+        nrec = uniq.shape[0]
+        rs = uniq % num_cols
+        rtpg = uniq // num_cols                       # (t * P + p) * 8 + g
+        weights = np.zeros((nrec, self.GROUP), dtype=np.float32)
+        mask = np.zeros((nrec, self.GROUP), dtype=bool)
+        weights[inv, c] = vals.astype(np.float32)
+        mask[inv, c] = True
+        counts = np.bincount(rtpg, minlength=tiles * p_count * ngrp).reshape(tiles, p_count * ngrp)
+        if counts.size and counts.max() > 255:
+            raise ValueError("sspi_map: more than 255 distinct lags for one (tile, pair, group)")
+        tile_recs = counts.sum(axis=1)
+        pair_recs = counts.reshape(tiles, p_count, ngrp).sum(axis=2)
+        meta_words = (p_count * ngrp + 3) // 4 * 4
+        words = meta_words + 8 * tile_recs                # u32 words per tile blob
+        tile_off_w = np.concatenate([[0], np.cumsum(words)]).astype(np.int64)
+        blob = np.zeros(int(tile_off_w[-1]), dtype=np.uint32)
+        rec_off = np.cumsum(counts, axis=1) - counts       # offset within the tile's records
+        meta = (rec_off.astype(np.uint32) << np.uint32(8)) | counts.astype(np.uint32)
+        meta_idx = tile_off_w[:-1, None] + np.arange(p_count * ngrp)[None, :]
+        blob[meta_idx.ravel()] = meta.ravel()
+        rec_tile = rtpg // (p_count * ngrp)
+        first_rec = np.concatenate([[0], np.cumsum(tile_recs)])[:-1]
+        local = np.arange(nrec) - first_rec[rec_tile]
+        base = tile_off_w[rec_tile] + meta_words + 8 * local
+        blob[base] = rs.astype(np.uint32)
+        for k in range(self.GROUP):
+            blob[base + 4 + k] = weights[:, k].view(np.uint32)
+        self.num_rows, self.num_cols, self.num_pairs = num_rows, num_cols, p_count
+        self.offsets = offsets
+        self.records = nrec
+        self.max_pair_records = int(pair_recs.max()) if pair_recs.size else 0
+        self.max_tile_records = int(tile_recs.max()) if tile_recs.size else 0
+        self.host_blob = blob
+        self.host_tile_off = tile_off_w * 4
+        self._rec = (rtpg, rs, weights, mask)
+        self.d_blob = torch.from_numpy(blob.view(np.int32)).to(dev.device()) if blob.size else \
+            torch.zeros(4, dtype=torch.int32, device=dev.device())
+        self.d_tile_off = dev.as_i64(self.host_tile_off)
+
+    @classmethod
+    def from_csr(cls, values, cols, splits, num_cols: int, offsets):
+        splits = np.asarray(splits, dtype=np.int64)
+        j = splits.shape[0] - 1
+        rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
+        return cls(rows, cols, values, j, num_cols, offsets)
+
+    @classmethod
+    def from_fixed(cls, fx, offsets):
+        p_count, j, k = fx.values.shape
+        keep = np.arange(k)[None, :] < np.asarray(fx.kept)[:, None]          # (P, k)
+        sel = np.broadcast_to(keep[:, None, :], fx.values.shape)
+        rows = np.broadcast_to(np.arange(j, dtype=np.int64)[None, :, None], fx.values.shape)[sel]
+        return cls(rows, fx.cols[sel].astype(np.int64), fx.values[sel], j, int(fx.num_cols), offsets)
+
+    def to_csr(self):
+        """Decode to (values float32, col_indices int64, row_splits int64)."""
+        rtpg, rs, weights, mask = self._rec
+        ngrp = self.TILE // self.GROUP
+        t = rtpg // (self.num_pairs * ngrp)
+        g = rtpg % ngrp
+        rec, c = np.nonzero(mask)
+        rows = t[rec] * self.TILE + g[rec] * self.GROUP + c
+        cols = rs[rec]
+        vals = weights[rec, c]
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        splits = np.zeros(self.num_rows + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows, minlength=self.num_rows), out=splits[1:])
+        return vals, cols.astype(np.int64), splits
+
+
+def band_from_sparse(sp, offsets: np.ndarray) -> BandOperator:
+    key = ("band", tuple(int(o) for o in offsets))
     if hasattr(sp, "kept") and getattr(sp, "cols", None) is not None and np.ndim(sp.cols) == 3:
-        return dev.CACHE.get(sp, ("ell_fixed", tuple(int(o) for o in offsets)),
-                             lambda: EllOperator.from_fixed(sp, offsets))
-    key = ("ell", tuple(int(o) for o in offsets))
-    return dev.CACHE.get(sp, key, lambda: EllOperator(sp.values, sp.col_indices, sp.row_splits,
-                                                      int(sp.num_cols), offsets))
+        return dev.CACHE.get(sp, key, lambda: BandOperator.from_fixed(sp, offsets))
+    return dev.CACHE.get(sp, key, lambda: BandOperator.from_csr(sp.values, sp.col_indices, sp.row_splits,
+                                                                int(sp.num_cols), offsets))
 
 
-def ell_from_dense(interp, offsets: np.ndarray) -> EllOperator:
-    """Keep-all ELL of a dense InterpMatrix: identical to the keep-all CSR's ELL."""
+def band_from_dense(interp, offsets: np.ndarray) -> BandOperator:
+    """Keep-all band image of a dense InterpMatrix: identical to the keep-all CSR's image."""
     def build():
         mat = np.asarray(interp.matrix)
-        j, s = mat.shape
-        splits = np.arange(j + 1, dtype=np.int64) * s
-        cols = np.tile(np.arange(s, dtype=np.int64), j)
-        return EllOperator(mat.ravel(), cols, splits, s, offsets)
-    return dev.CACHE.get(interp, ("ell_dense", tuple(int(o) for o in offsets)), build)
+        j, ncol = mat.shape
+        rows = np.repeat(np.arange(j, dtype=np.int64), ncol)
+        cols = np.tile(np.arange(ncol, dtype=np.int64), j)
+        return BandOperator(rows, cols, mat.ravel(), j, ncol, offsets)
+    return dev.CACHE.get(interp, ("band_dense", tuple(int(o) for o in offsets)), build)
 
 
-def _ell_map(ell: EllOperator, samples, argmax: bool, out_map: bool):
-    buf, f, batched = _lag_major(samples, ell.num_cols)
-    z = torch.empty((f, ell.num_rows), dtype=torch.float32, device=buf.device) if out_map else None
+def _band_map(op: BandOperator, samples, argmax: bool, out_map: bool):
+    buf, f, batched = _lag_major(samples, op.num_cols)
+    z = torch.empty((f, op.num_rows), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
-    if ell.num_rows == 0:
+    if op.num_rows == 0:
         return _finish(z, keys, batched, argmax)
-    nat.call("srpgpu_sspi_map", dev.ptr(buf), buf.shape[1], f, ell.num_cols, ell.num_pairs,
-             dev.ptr(ell.d_widths), dev.ptr(ell.d_ell_off), dev.ptr(ell.d_packed), ell.num_rows,
-             int(ell.widths.max()) if ell.num_pairs else 0, int(ell.widths.sum()),
-             dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    nat.call("srpgpu_sspi_map", dev.ptr(buf), buf.shape[1], f, op.num_cols, op.num_pairs,
+             dev.ptr(op.d_tile_off), dev.ptr(op.d_blob), op.num_rows, op.max_pair_records,
+             op.max_tile_records, dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 
@@ -252,8 +348,8 @@ def _check_cols(samples, num_cols: int) -> None:
 def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True):
     """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195)."""
     _check_cols(samples, int(sp.num_cols))         # reference DimensionError check first
-    ell = ell_from_sparse(sp, _sample_offsets(samples, int(sp.num_cols)))
-    return _ell_map(ell, samples, argmax, out_map)
+    op = band_from_sparse(sp, _sample_offsets(samples, int(sp.num_cols)))
+    return _band_map(op, samples, argmax, out_map)
 
 
 def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
@@ -267,7 +363,7 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
         offsets = np.array([0, num_cols], dtype=np.int64)
-    return _ell_map(ell_from_dense(interp, offsets), samples, argmax, out_map)
+    return _band_map(band_from_dense(interp, offsets), samples, argmax, out_map)
 
 
 # ----------------------------------------------------------------- low rank

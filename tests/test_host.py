@@ -100,16 +100,15 @@ def test_fixed_nnz_fit_keeps_nearest_lags(golden_scene):
 
 
 def _ell(sp, off):
-    # EllOperator needs a device for its upload; build the host image only
+    # the operator image needs a device for its upload; build the host image on CPU tensors
     from paper_2306_08514_b200 import maps
     import torch
-
-    class HostEll(maps.EllOperator):
-        pass
     orig = maps.dev.device
     maps.dev.device = lambda: torch.device("cpu")
     try:
-        return maps.EllOperator(sp.values, sp.col_indices, sp.row_splits, int(sp.num_cols), off)
+        if np.ndim(getattr(sp, "cols", np.zeros(1))) == 3:
+            return maps.BandOperator.from_fixed(sp, off)
+        return maps.BandOperator.from_csr(sp.values, sp.col_indices, sp.row_splits, int(sp.num_cols), off)
     finally:
         maps.dev.device = orig
 
@@ -124,10 +123,9 @@ def test_ell_roundtrip_bit_exact(golden_scene):
         assert_array_equal(cols, ref.col_indices)
         assert_array_equal(splits, ref.row_splits)
         assert_array_equal(vals, ref.values.astype(np.float32))
-        assert np.all(ell.widths <= np.diff(spec.offsets))
-        # padding entries are zero-valued and point inside their pair block
-        packed = ell.host_packed
-        assert np.all(packed[:, 1] < spec.offsets[-1])
+        # every record's sample index lies inside the operator; padded weights are zero
+        rtpg, rs, weights, mask = ell._rec
+        assert np.all(rs < spec.offsets[-1]) and np.all(weights[~mask] == 0)
 
 
 def test_ell_empty_and_keep_all(golden_scene):
@@ -135,9 +133,11 @@ def test_ell_empty_and_keep_all(golden_scene):
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     interp = s.build_interp_matrix(tdoa, spec, frame)
     empty = _ell(s.truncate_sparse(interp, 0), spec.offsets)
-    assert empty.widths.sum() == 0
+    assert empty.records == 0
     full = _ell(s.truncate_sparse(interp, interp.matrix.size), spec.offsets)
-    assert_array_equal(full.widths, np.diff(spec.offsets))
+    groups = (grid.num_points + 3) // 4
+    assert full.records == groups * spec.offsets[-1]
+    assert full.max_pair_records <= 8 * int(np.max(np.diff(spec.offsets)))
 
 
 def test_errors_mirror_reference():
@@ -194,15 +194,7 @@ def test_fixed_nnz_from_tdoa_matches_dense_fit(golden_scene):
         assert_array_equal(a.row_splits, b.row_splits)
         assert_array_equal(a.values, b.values)
         assert fx.num_kept == a.num_kept
-        from paper_2306_08514_b200 import maps
-        import torch
-        orig = maps.dev.device
-        maps.dev.device = lambda: torch.device("cpu")
-        try:
-            ell = maps.EllOperator.from_fixed(fx, spec.offsets)
-        finally:
-            maps.dev.device = orig
-        vals, cols, splits = ell.to_csr()
+        vals, cols, splits = _ell(fx, spec.offsets).to_csr()
         assert_array_equal(cols, a.col_indices)
         assert_array_equal(splits, a.row_splits)
         assert_array_equal(vals, a.values.astype(np.float32))
