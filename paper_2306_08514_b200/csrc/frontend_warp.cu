@@ -144,25 +144,43 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
   return raw;
 }
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 4;   // per CTA
 
-template <int LP, int OUT>
+// named barrier of the kWpf warps sharing one frame (kWpf == 1: the warp itself)
+template <int kWpf>
+__device__ __forceinline__ void frame_sync(int fg) {
+  if (kWpf == 1) {
+    __syncwarp();
+  } else if (kWpf == 2) {
+    if (fg == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
+    else asm volatile("bar.sync 2, 64;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+// kWpf warps per frame share its spectra: 1 (latency-bound small batches: a warp per
+// frame) or 2 (large batches: half the spectra buffers per warp -> more resident warps)
+template <int LP, int OUT, int kWpf>
 __global__ void __launch_bounds__(kWarps * 32)
 frontend_warp_kernel(const WarpParams prm) {
   using G = Geo<LP>;
   constexpr int L = G::L, K = G::K, R = G::R;
   constexpr int Kp1 = K + 1, B = K - 1;
+  constexpr int kFpc = kWarps / kWpf;                                   // frames per CTA
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
   int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
   int* s_counts = s_pairs + 2 * prm.P;                                  // [P]
   int* s_off = s_counts + prm.P;                                        // [P+1]
-  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
+  float* s_energy = reinterpret_cast<float*>(s_off + prm.P + 1);        // [kWarps]
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1 + kWarps) * 4) + 15) & ~(size_t)15;
   const int M = prm.M, P = prm.P;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t warp_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
-  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * warp_bytes);   // [M][K+1]
-  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
+  const int fg = wid / kWpf, mi = wid % kWpf;
+  const size_t frame_bytes = ((size_t)M * Kp1 + kWpf * G::WORK) * sizeof(float2);
+  float2* spec = reinterpret_cast<float2*>(smem_raw + head + fg * frame_bytes);   // [M][K+1], shared
+  float2* work = spec + (size_t)M * Kp1 + mi * G::WORK;                           // [R][XP], per warp
   const int fi = lane / LP, fl = lane % LP;
   float2* xp = work + fi * G::XP;
 
@@ -179,12 +197,12 @@ frontend_warp_kernel(const WarpParams prm) {
   }
   __syncthreads();
 
-  const int64_t total_warps = (int64_t)gridDim.x * kWarps;
-  for (int64_t f = (int64_t)blockIdx.x * kWarps + wid; f < prm.F; f += total_warps) {
+  const int64_t total_groups = (int64_t)gridDim.x * kFpc;
+  for (int64_t f = (int64_t)blockIdx.x * kFpc + fg; f < prm.F; f += total_groups) {
     const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
     float energy = 0.f;
-    // ---------------- forward FFTs: R channel pairs per round ----------------
-    for (int c0 = 0; c0 < M; c0 += 2 * R) {
+    // ---------------- forward FFTs: R channel pairs per round, rounds split over the warps ----
+    for (int c0 = 2 * R * mi; c0 < M; c0 += 2 * R * kWpf) {
       const int ca = c0 + 2 * fi, cb = ca + 1;
       float2 v[32];
       const float* xa = prm.samples + (int64_t)ca * prm.ld_samples + start;
@@ -198,7 +216,6 @@ frontend_warp_kernel(const WarpParams prm) {
         v[j] = make_float2(a, b);
       }
       fft_l<LP, true>(v, xp, twT, fl);
-      // natural-order Z into this FFT's work area
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -225,16 +242,21 @@ frontend_warp_kernel(const WarpParams prm) {
       }
       __syncwarp();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+    if (lane == 0) s_energy[wid] = energy;
+    frame_sync<kWpf>(fg);                            // spectra + energy of the frame complete
     float floor = prm.floor_value;
     if (prm.weighting && prm.floor_mode == 0) {
+      float e = 0.f;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
-      floor = prm.floor_value * energy;
+      for (int w = 0; w < kWpf; ++w) e += s_energy[fg * kWpf + w];
+      floor = prm.floor_value * e;
     }
 
     if (OUT == W_OUT_GCC) {
       float2* dst = prm.gcc_out + f * prm.gcc_ld;
-      for (int p = 0; p < P; ++p) {
+      for (int p = mi; p < P; p += kWpf) {
         const int m = s_pairs[2 * p], mp = s_pairs[2 * p + 1];
         for (int k = 1 + lane; k < K; k += 32) {
           float2 val = cross_phat(spec, Kp1, m, mp, k, prm.weighting, floor);
@@ -242,11 +264,12 @@ frontend_warp_kernel(const WarpParams prm) {
           dst[p * B + k - 1] = val;
         }
       }
-      for (int64_t idx = (int64_t)P * B + lane; idx < prm.gcc_ld; idx += 32) dst[idx] = make_float2(0.f, 0.f);
+      for (int64_t idx = (int64_t)P * B + lane + 32 * mi; idx < prm.gcc_ld; idx += 32 * kWpf)
+        dst[idx] = make_float2(0.f, 0.f);
     } else {
       float* dst = prm.xi_out + (prm.xi_ld ? f : f * (int64_t)prm.S);
       const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
-      for (int p0 = 0; p0 < P; p0 += 2 * R) {
+      for (int p0 = 2 * R * mi; p0 < P; p0 += 2 * R * kWpf) {
         // PHAT cross-spectra of this round's pairs into each FFT's work area: [2][B]
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -325,18 +348,18 @@ frontend_warp_kernel(const WarpParams prm) {
         __syncwarp();
       }
     }
-    __syncwarp();
+    frame_sync<kWpf>(fg);                            // spectra free for the next frame
   }
 }
 
-template <int LP, int OUT>
+template <int LP, int OUT, int kWpf>
 static int launch(const WarpParams& wp, cudaStream_t st, const char* what) {
   using G = Geo<LP>;
-  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1) * 4) + 15) & ~(size_t)15;
-  const size_t warp_bytes = ((size_t)wp.M * (G::K + 1) + G::WORK) * sizeof(float2);
-  const size_t smem = head + kWarps * warp_bytes;
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1 + kWarps) * 4) + 15) & ~(size_t)15;
+  const size_t frame_bytes = ((size_t)wp.M * (G::K + 1) + kWpf * G::WORK) * sizeof(float2);
+  const size_t smem = head + (kWarps / kWpf) * frame_bytes;
   if (smem > 227 * 1024) return 1;   // caller falls back to the block kernel
-  auto kern = frontend_warp_kernel<LP, OUT>;
+  auto kern = frontend_warp_kernel<LP, OUT, kWpf>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("%s: cannot reserve %zu B shared memory", what, smem);
     return SRPGPU_ERR_LAUNCH;
@@ -344,7 +367,7 @@ static int launch(const WarpParams& wp, cudaStream_t st, const char* what) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
   if (per_sm < 1) return 1;
-  const int64_t need = (wp.F + kWarps - 1) / kWarps;
+  const int64_t need = (wp.F + kWarps / kWpf - 1) / (kWarps / kWpf);
   const int64_t grid = std::min<int64_t>(need, (int64_t)num_sms() * per_sm);
   if (grid <= 0) return SRPGPU_OK;
   kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp);
@@ -352,12 +375,12 @@ static int launch(const WarpParams& wp, cudaStream_t st, const char* what) {
   return SRPGPU_OK;
 }
 
-template <int OUT>
+template <int OUT, int kWpf>
 static int by_len(const WarpParams& wp, cudaStream_t st, const char* what) {
   switch (wp.L) {
-    case 256: return launch<8, OUT>(wp, st, what);
-    case 512: return launch<16, OUT>(wp, st, what);
-    case 1024: return launch<32, OUT>(wp, st, what);
+    case 256: return launch<8, OUT, kWpf>(wp, st, what);
+    case 512: return launch<16, OUT, kWpf>(wp, st, what);
+    case 1024: return launch<32, OUT, kWpf>(wp, st, what);
     default: return 1;
   }
 }
@@ -372,8 +395,11 @@ int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const c
     return e && e[0] == 'b';
   }();
   if (disabled) return 1;
-  if (out == W_OUT_GCC) return wf::by_len<W_OUT_GCC>(wp, st, what);
-  if (out == W_OUT_XI) return wf::by_len<W_OUT_XI>(wp, st, what);
+  // a warp per frame while there are fewer frames than resident warps (latency-bound),
+  // two warps per frame for large batches (throughput-bound)
+  const bool small = wp.F <= (int64_t)num_sms() * 8;
+  if (out == W_OUT_GCC) return small ? wf::by_len<W_OUT_GCC, 1>(wp, st, what) : wf::by_len<W_OUT_GCC, 2>(wp, st, what);
+  if (out == W_OUT_XI) return small ? wf::by_len<W_OUT_XI, 1>(wp, st, what) : wf::by_len<W_OUT_XI, 2>(wp, st, what);
   return 1;
 }
 

@@ -6,21 +6,23 @@
 //
 // Operator layout: "tiled band" (built once on the host from the reference CSR).
 // Candidates are cut into tiles of 32 and each tile into 8 groups of 4.  For every
-// (tile, pair, group) the union of the lags kept by the group's 4 candidates becomes a
+// (tile, group, pair) the union of the lags kept by the group's 4 candidates becomes a
 // run of records {u32 sample index, 3 x pad, f32 weight[4]} (weight 0 where a candidate
-// does not keep that lag).  A tile's blob is contiguous:
-//     meta[P][8] : u32 (record offset << 8 | record count)      (16-byte padded)
-//     records    : pair-major, then group, then ascending sample index
-// so one TMA bulk copy stages a tile's operator (chunked by pairs when it exceeds the
-// shared-memory budget).
+// does not keep that lag).  A tile's blob is contiguous and group-major:
+//     meta[16] : u32 start record of groups 0..7, meta[8] = record total (64 bytes)
+//     records  : group 0 (pairs ascending, then sample index), group 1, ...
+// so each warp walks one flat record range and one TMA bulk copy stages the tile
+// (record-range chunks when it exceeds the shared-memory budget).
 //
 // Samples are lag-major xi[s][f] (row pitch ld, frames contiguous).  CTA = 32
-// candidates x 128 frames; lane = 4 consecutive frames, warp = one group of 4
+// candidates x (n x 128) frames: the operator tile is staged once, then the CTA
+// walks its frame tiles.  Lane = 4 consecutive frames, warp = one group of 4
 // candidates.  Per record: one broadcast shared-memory read (index + 4 weights), one
 // coalesced 16-byte L1 read of xi[s][f..f+3], 16 FMAs into registers -- the xi value is
-// reused from registers by all 4 candidates of the group.  z leaves through a
-// shared-memory transpose as coalesced rows z[f][i0 : i0+32]; the per-frame argmax is
-// folded into packed 64-bit keys (one atomicMax per frame per CTA).
+// reused from registers by the group's 4 candidates.  z is stored straight from
+// registers (16-byte streaming stores when rows are aligned); the per-frame argmax
+// is reduced in registers (4 candidates), across warps in shared memory, and
+// folded into packed 64-bit keys with one atomicMax per frame per CTA.
 #include "common.cuh"
 
 namespace srpgpu {
@@ -28,8 +30,9 @@ namespace srpgpu {
 constexpr int kWarps = 8;
 constexpr int kGroup = 4;                          // candidates per warp
 constexpr int kTileI = kWarps * kGroup;            // 32 candidates per CTA
-constexpr int kTileF = 128;                        // frames per CTA (4 per lane)
-constexpr int kRecBudget = 160 * 1024;             // bytes of staged records per chunk
+constexpr int kTileF = 128;                        // frames per frame tile (4 per lane)
+constexpr int kRecBudget = 160 * 1024;             // max bytes of staged records
+constexpr int kMetaBytes = 64;
 
 struct __align__(16) BandRec {
   uint32_t s, pad0, pad1, pad2;
@@ -48,6 +51,7 @@ struct BandParams {
   float* z;                   // [F][J] or null
   unsigned long long* keys;   // [F] or null
   int32_t rec_cap;            // records per staged chunk
+  int32_t ftiles_per_cta;     // frame tiles walked by one CTA
 };
 
 __device__ __forceinline__ uint32_t s_addr(const void* p) {
@@ -62,6 +66,11 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -72,119 +81,140 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-__device__ __forceinline__ size_t meta_bytes(int P) { return ((size_t)P * kWarps * 4 + 15) & ~(size_t)15; }
+__device__ __forceinline__ void accumulate(float (&acc)[kGroup][4], const BandRec* rr, int n,
+                                           const float* xcol, int64_t ld) {
+#pragma unroll 4
+  for (int r = 0; r < n; ++r) {
+    const uint32_t s = rr[r].s;
+    const float4 w = rr[r].w;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)s * ld));
+    acc[0][0] = fmaf(w.x, x.x, acc[0][0]); acc[0][1] = fmaf(w.x, x.y, acc[0][1]);
+    acc[0][2] = fmaf(w.x, x.z, acc[0][2]); acc[0][3] = fmaf(w.x, x.w, acc[0][3]);
+    acc[1][0] = fmaf(w.y, x.x, acc[1][0]); acc[1][1] = fmaf(w.y, x.y, acc[1][1]);
+    acc[1][2] = fmaf(w.y, x.z, acc[1][2]); acc[1][3] = fmaf(w.y, x.w, acc[1][3]);
+    acc[2][0] = fmaf(w.z, x.x, acc[2][0]); acc[2][1] = fmaf(w.z, x.y, acc[2][1]);
+    acc[2][2] = fmaf(w.z, x.z, acc[2][2]); acc[2][3] = fmaf(w.z, x.w, acc[2][3]);
+    acc[3][0] = fmaf(w.w, x.x, acc[3][0]); acc[3][1] = fmaf(w.w, x.y, acc[3][1]);
+    acc[3][2] = fmaf(w.w, x.z, acc[3][2]); acc[3][3] = fmaf(w.w, x.w, acc[3][3]);
+  }
+}
 
 __global__ void __launch_bounds__(kWarps * 32)
 sspi_band_kernel(const BandParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
-  const int P = prm.P;
-  uint32_t* meta = reinterpret_cast<uint32_t*>(smem_raw);                          // [P][8]
-  float* zs = reinterpret_cast<float*>(smem_raw + ((meta_bytes(P) + 127) & ~(size_t)127));   // [TF][TI+1]
-  BandRec* recs = reinterpret_cast<BandRec*>(
-      reinterpret_cast<unsigned char*>(zs) + (((size_t)kTileF * (kTileI + 1) * 4 + 127) & ~(size_t)127));
+  __shared__ uint32_t meta[16];
+  unsigned long long* kred = reinterpret_cast<unsigned long long*>(smem_raw);        // [TF][8]
+  float* zs = reinterpret_cast<float*>(smem_raw + (size_t)kTileF * kWarps * 8);      // [TF][TI+1]
+  BandRec* recs = reinterpret_cast<BandRec*>(smem_raw + (size_t)kTileF * kWarps * 8 +
+                                             (size_t)kTileF * (kTileI + 1) * 4);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tile = blockIdx.x;
   const int64_t i0 = tile * kTileI;
-  const int64_t f0 = (int64_t)blockIdx.y * kTileF;
   const unsigned char* tb = prm.blob + prm.tile_off[tile];
-  const BandRec* grec = reinterpret_cast<const BandRec*>(tb + meta_bytes(P));
+  const uint32_t tile_bytes = (uint32_t)(prm.tile_off[tile + 1] - prm.tile_off[tile]);
+  const BandRec* grec = reinterpret_cast<const BandRec*>(tb + kMetaBytes);
 
-  uint32_t phase = 0;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t mb = (uint32_t)meta_bytes(P);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(&bar)), "r"(mb)
-                 : "memory");
-    bulk_copy(meta, tb, mb, &bar);
   }
+  if (tid < 16) meta[tid] = reinterpret_cast<const uint32_t*>(tb)[tid];
   __syncthreads();
-  mbar_wait(&bar, phase);
-  phase ^= 1u;
+  const uint32_t total = meta[8];
+  const uint32_t g0 = meta[warp], g1 = (warp + 1 < kWarps) ? meta[warp + 1] : total;
+  const bool whole = total <= (uint32_t)prm.rec_cap;
+  uint32_t phase = 0;
+  if (whole && total > 0) {   // one TMA bulk copy for the whole operator tile, reused by all frame tiles
+    if (tid == 0) {
+      mbar_arm(&bar, tile_bytes - kMetaBytes);
+      bulk_copy(recs, grec, tile_bytes - kMetaBytes, &bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+  }
 
-  float acc[kGroup][4];
+  const int64_t ftile0 = (int64_t)blockIdx.y * prm.ftiles_per_cta;
+  for (int64_t ft = ftile0; ft < ftile0 + prm.ftiles_per_cta; ++ft) {
+    const int64_t f0 = ft * kTileF;
+    if (f0 >= prm.F) break;
+    float acc[kGroup][4];
 #pragma unroll
-  for (int c = 0; c < kGroup; ++c)
+    for (int c = 0; c < kGroup; ++c)
 #pragma unroll
-    for (int t = 0; t < 4; ++t) acc[c][t] = 0.f;
-  const int64_t fl = f0 + 4 * lane;
-  const bool lane_ok = fl < prm.ld;
-  const float* xcol = prm.xi + fl;
-  const uint32_t total_recs =
-      (uint32_t)((prm.tile_off[tile + 1] - prm.tile_off[tile] - (int64_t)meta_bytes(P)) / sizeof(BandRec));
-
-  int pc0 = 0;
-  while (pc0 < P) {
-    // records of pairs [pc0, pc1) are contiguous: [start(pc0), start(pc1))
-    const uint32_t r0 = meta[pc0 * kWarps] >> 8;
-    int pc1 = pc0 + 1;   // at least one pair (the host checks a single pair fits)
-    while (pc1 < P && ((pc1 + 1 < P) ? (meta[(pc1 + 1) * kWarps] >> 8) : total_recs) - r0 <=
-                          (uint32_t)prm.rec_cap)
-      ++pc1;
-    const uint32_t r1 = (pc1 < P) ? (meta[pc1 * kWarps] >> 8) : total_recs;
-    if (r1 > r0) {
-      if (tid == 0) {
-        const uint32_t bytes = (r1 - r0) * (uint32_t)sizeof(BandRec);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(&bar)), "r"(bytes)
-                     : "memory");
-        bulk_copy(recs, grec + r0, bytes, &bar);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-      if (lane_ok) {
-        for (int p = pc0; p < pc1; ++p) {
-          const uint32_t m = meta[p * kWarps + warp];
-          const BandRec* rr = recs + ((m >> 8) - r0);
-          const int n = (int)(m & 0xFFu);
-#pragma unroll 4
-          for (int r = 0; r < n; ++r) {
-            const uint32_t s = rr[r].s;
-            const float4 w = rr[r].w;
-            const float4 x = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)s * prm.ld));
-            acc[0][0] = fmaf(w.x, x.x, acc[0][0]); acc[0][1] = fmaf(w.x, x.y, acc[0][1]);
-            acc[0][2] = fmaf(w.x, x.z, acc[0][2]); acc[0][3] = fmaf(w.x, x.w, acc[0][3]);
-            acc[1][0] = fmaf(w.y, x.x, acc[1][0]); acc[1][1] = fmaf(w.y, x.y, acc[1][1]);
-            acc[1][2] = fmaf(w.y, x.z, acc[1][2]); acc[1][3] = fmaf(w.y, x.w, acc[1][3]);
-            acc[2][0] = fmaf(w.z, x.x, acc[2][0]); acc[2][1] = fmaf(w.z, x.y, acc[2][1]);
-            acc[2][2] = fmaf(w.z, x.z, acc[2][2]); acc[2][3] = fmaf(w.z, x.w, acc[2][3]);
-            acc[3][0] = fmaf(w.w, x.x, acc[3][0]); acc[3][1] = fmaf(w.w, x.y, acc[3][1]);
-            acc[3][2] = fmaf(w.w, x.z, acc[3][2]); acc[3][3] = fmaf(w.w, x.w, acc[3][3]);
-          }
+      for (int t = 0; t < 4; ++t) acc[c][t] = 0.f;
+    const int64_t fl = f0 + 4 * lane;
+    const bool lane_ok = fl < prm.ld;
+    const float* xcol = prm.xi + fl;
+    if (whole) {
+      if (lane_ok) accumulate(acc, recs + g0, (int)(g1 - g0), xcol, prm.ld);
+    } else {
+      for (uint32_t c0 = 0; c0 < total; c0 += (uint32_t)prm.rec_cap) {
+        const uint32_t c1 = min(total, c0 + (uint32_t)prm.rec_cap);
+        __syncthreads();   // previous chunk fully consumed
+        if (tid == 0) {
+          mbar_arm(&bar, (c1 - c0) * (uint32_t)sizeof(BandRec));
+          bulk_copy(recs, grec + c0, (c1 - c0) * (uint32_t)sizeof(BandRec), &bar);
         }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        const uint32_t a = max(g0, c0), b = min(g1, c1);
+        if (lane_ok && b > a) accumulate(acc, recs + (a - c0), (int)(b - a), xcol, prm.ld);
       }
-      __syncthreads();   // the next chunk overwrites `recs`
     }
-    pc0 = pc1;
-  }
 
-  // epilogue: transpose through shared memory -> coalesced rows of z, fused argmax
+    // ---- outputs: z from registers, per-frame argmax keys
+    const int64_t ib = i0 + warp * kGroup;
+    const int nvalid = (int)(prm.J - ib < kGroup ? (prm.J - ib > 0 ? prm.J - ib : 0) : kGroup);
+    const bool aligned = (prm.J % 4 == 0);
+    const bool vec = prm.z && nvalid == kGroup && aligned;
 #pragma unroll
-  for (int c = 0; c < kGroup; ++c)
+    for (int t = 0; t < 4; ++t) {
+      const int64_t f = fl + t;
+      unsigned long long key = 0ull;
+      if (f < prm.F && nvalid > 0) {
+        float best = acc[0][t];
+        int bi = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) zs[(4 * lane + t) * (kTileI + 1) + warp * kGroup + c] = acc[c][t];
-  __syncthreads();
-  const int ti_valid = (int)(prm.J - i0 < kTileI ? prm.J - i0 : kTileI);
-  for (int row = warp; row < kTileF; row += kWarps) {
-    const int64_t fg = f0 + row;
-    if (fg >= prm.F) break;
-    unsigned long long key = 0ull;
-    if (lane < ti_valid) {
-      const float v = zs[row * (kTileI + 1) + lane];
-      if (prm.z) prm.z[fg * prm.J + i0 + lane] = v;
-      key = make_key(v, (uint32_t)(i0 + lane));
+        for (int c = 1; c < kGroup; ++c)
+          if (c < nvalid && acc[c][t] > best) { best = acc[c][t]; bi = c; }
+        key = make_key(best, (uint32_t)(ib + bi));
+        if (vec)   // 16-byte rows: store straight from registers
+          __stcs(reinterpret_cast<float4*>(prm.z + f * prm.J + ib),
+                 make_float4(acc[0][t], acc[1][t], acc[2][t], acc[3][t]));
+      }
+      kred[(4 * lane + t) * kWarps + warp] = key;
+      if (prm.z && !aligned) {
+#pragma unroll
+        for (int c = 0; c < kGroup; ++c) zs[(4 * lane + t) * (kTileI + 1) + warp * kGroup + c] = acc[c][t];
+      }
     }
-    if (prm.keys) {
-      key = warp_key_max(key);
-      if (lane == 0) atomicMax(prm.keys + fg, key);
+    __syncthreads();
+    if (prm.z && !aligned) {   // unaligned rows: transpose through shared memory, coalesced rows
+      const int ti_valid = (int)(prm.J - i0 < kTileI ? prm.J - i0 : kTileI);
+      for (int row = warp; row < kTileF; row += kWarps) {
+        const int64_t fg = f0 + row;
+        if (fg >= prm.F) break;
+        if (lane < ti_valid) prm.z[fg * prm.J + i0 + lane] = zs[row * (kTileI + 1) + lane];
+      }
     }
+    if (prm.keys && tid < kTileF) {
+      const int64_t f = f0 + tid;
+      if (f < prm.F) {
+        unsigned long long k = kred[tid * kWarps];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) k = key_max(k, kred[tid * kWarps + w]);
+        if (k) atomicMax(prm.keys + f, k);
+      }
+    }
+    __syncthreads();   // kred reused by the next frame tile
   }
 }
 
 // Small-frame-count path (e.g. the per-frame reference call): a thread per
-// (candidate, frame) walking its group's records; same accumulation order as the
-// tile kernel, so both give bit-identical maps.
+// (candidate, frame) walking its group's records in the tile kernel's order, so
+// both kernels give bit-identical maps.
 __global__ void sspi_band_rows_kernel(const BandParams prm) {
   const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t f = blockIdx.y;
@@ -195,16 +225,12 @@ __global__ void sspi_band_rows_kernel(const BandParams prm) {
     const int g = (int)((gi % kTileI) / kGroup), c = (int)(gi % kGroup);
     const unsigned char* tb = prm.blob + prm.tile_off[tile];
     const uint32_t* meta = reinterpret_cast<const uint32_t*>(tb);
-    const BandRec* grec = reinterpret_cast<const BandRec*>(tb + meta_bytes(prm.P));
-    for (int p = 0; p < prm.P; ++p) {
-      const uint32_t m = meta[p * kWarps + g];
-      const BandRec* rr = grec + (m >> 8);
-      const int n = (int)(m & 0xFFu);
-      for (int r = 0; r < n; ++r) {
-        const float4 w = rr[r].w;
-        const float wc = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
-        acc = fmaf(wc, __ldg(prm.xi + (int64_t)rr[r].s * prm.ld + f), acc);
-      }
+    const BandRec* grec = reinterpret_cast<const BandRec*>(tb + kMetaBytes);
+    const uint32_t r1 = (g + 1 < kWarps) ? meta[g + 1] : meta[8];
+    for (uint32_t r = meta[g]; r < r1; ++r) {
+      const float4 w = grec[r].w;
+      const float wc = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
+      acc = fmaf(wc, __ldg(prm.xi + (int64_t)grec[r].s * prm.ld + f), acc);
     }
     if (prm.z) prm.z[f * prm.J + gi] = acc;
   }
@@ -266,23 +292,23 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
     return SRPGPU_OK;
   }
   const int64_t cap = kRecBudget / (int64_t)sizeof(BandRec);
-  SRPGPU_CHECK_ARG(max_pair_records <= cap, SRPGPU_ERR_UNSUPPORTED,
-                   "sspi_map: %lld records of one pair exceed the shared-memory chunk",
-                   (long long)max_pair_records);
-  // stage whole tiles when they fit (one bulk copy), else pair chunks; size the buffer
-  // to the operator so that several CTAs stay resident per SM
-  prm.rec_cap = (int32_t)std::max<int64_t>(std::min<int64_t>(cap, max_tile_records), std::max<int64_t>(max_pair_records, 1));
-  const size_t smem = ((((size_t)num_pairs * kWarps * 4 + 15) & ~(size_t)15) + 127 & ~(size_t)127) +
-                      (((size_t)kTileF * (kTileI + 1) * 4 + 127) & ~(size_t)127) +
+  (void)max_pair_records;
+  prm.rec_cap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(cap, max_tile_records));
+  const size_t smem = (size_t)kTileF * kWarps * 8 + (size_t)kTileF * (kTileI + 1) * 4 +
                       (size_t)prm.rec_cap * sizeof(BandRec);
   if (cudaFuncSetAttribute(sspi_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     set_error("sspi_map: cannot reserve %zu B shared memory", smem);
     return SRPGPU_ERR_LAUNCH;
   }
-  SRPGPU_CHECK_ARG((num_frames + kTileF - 1) / kTileF <= 65535, SRPGPU_ERR_DIMENSION,
-                   "sspi_map: too many frames per call");
-  dim3 grid((unsigned)((num_candidates + kTileI - 1) / kTileI), (unsigned)((num_frames + kTileF - 1) / kTileF));
+  const int64_t ctiles = (num_candidates + kTileI - 1) / kTileI;
+  const int64_t ftiles = (num_frames + kTileF - 1) / kTileF;
+  // walk several frame tiles per CTA (operator staged once) while keeping >= ~8 CTAs per SM
+  int64_t per = std::max<int64_t>(1, std::min<int64_t>(8, (ctiles * ftiles) / (8 * (int64_t)num_sms())));
+  prm.ftiles_per_cta = (int32_t)per;
+  const int64_t gy = (ftiles + per - 1) / per;
+  SRPGPU_CHECK_ARG(gy <= 65535, SRPGPU_ERR_DIMENSION, "sspi_map: too many frames per call");
+  dim3 grid((unsigned)ctiles, (unsigned)gy);
   sspi_band_kernel<<<grid, kWarps * 32, smem, st>>>(prm);
   SRPGPU_CHECK_LAUNCH("sspi_map");
   return SRPGPU_OK;

@@ -209,16 +209,16 @@ class EllOperator:
 class BandOperator:
     """Tiled band image of a sparse interpolation operator (what the SSPI kernel reads).
 
-    Candidates are cut into tiles of 32 and groups of 4.  For each (tile, pair, group)
+    Candidates are cut into tiles of 32 and groups of 4.  For each (tile, group, pair)
     the union of the sample indices kept by the group's candidates becomes records
-    {u32 sample index, 3 pad, f32 weight[4]}.  Tile blob = meta[P][8] (u32
-    `offset << 8 | count`, 16-byte padded) + records (pair-major, then group, then
-    ascending sample index); `tile_off` holds the blob byte offsets.  `mask` (host)
-    marks the (record, candidate) slots that are real kept entries, so the image
-    decodes back to the reference CSR exactly (`to_csr`).
+    {u32 sample index, 3 pad, f32 weight[4]}.  Tile blob = meta[16] u32 (start record
+    of groups 0..7, then the record total; 64 bytes) + records, group-major (then pair,
+    then ascending sample index); `tile_off` holds the blob byte offsets.  `mask`
+    (host) marks the (record, candidate) slots that are real kept entries, so the
+    image decodes back to the reference CSR exactly (`to_csr`).
     """
 
-    TILE, GROUP = 32, 4
+    TILE, GROUP, META_WORDS = 32, 4, 16
 
     def __init__(self, rows, cols, vals, num_rows: int, num_cols: int, offsets: np.ndarray):
         rows = np.asarray(rows, dtype=np.int64)
@@ -231,45 +231,41 @@ class BandOperator:
         t = rows // self.TILE
         g = (rows % self.TILE) // self.GROUP
         c = rows % self.GROUP
-        key = ((t * p_count + pair) * ngrp + g) * num_cols + cols
+        key = ((t * ngrp + g) * p_count + pair) * num_cols + cols
         uniq, inv = np.unique(key, return_inverse=True)
         nrec = uniq.shape[0]
         rs = uniq % num_cols
-        rtpg = uniq // num_cols                       # (t * P + p) * 8 + g
+        rtg = uniq // num_cols // p_count                 # t * 8 + g
         weights = np.zeros((nrec, self.GROUP), dtype=np.float32)
         mask = np.zeros((nrec, self.GROUP), dtype=bool)
         weights[inv, c] = vals.astype(np.float32)
         mask[inv, c] = True
-        counts = np.bincount(rtpg, minlength=tiles * p_count * ngrp).reshape(tiles, p_count * ngrp)
-        if counts.size and counts.max() > 255:
-            raise ValueError("sspi_map: more than 255 distinct lags for one (tile, pair, group)")
+        counts = np.bincount(rtg, minlength=tiles * ngrp).reshape(tiles, ngrp)
         tile_recs = counts.sum(axis=1)
-        pair_recs = counts.reshape(tiles, p_count, ngrp).sum(axis=2)
-        meta_words = (p_count * ngrp + 3) // 4 * 4
-        words = meta_words + 8 * tile_recs                # u32 words per tile blob
+        words = self.META_WORDS + 8 * tile_recs           # u32 words per tile blob
         tile_off_w = np.concatenate([[0], np.cumsum(words)]).astype(np.int64)
         blob = np.zeros(int(tile_off_w[-1]), dtype=np.uint32)
-        rec_off = np.cumsum(counts, axis=1) - counts       # offset within the tile's records
-        meta = (rec_off.astype(np.uint32) << np.uint32(8)) | counts.astype(np.uint32)
-        meta_idx = tile_off_w[:-1, None] + np.arange(p_count * ngrp)[None, :]
-        blob[meta_idx.ravel()] = meta.ravel()
-        rec_tile = rtpg // (p_count * ngrp)
+        starts = np.cumsum(counts, axis=1) - counts
+        meta_idx = tile_off_w[:-1, None] + np.arange(ngrp)[None, :]
+        blob[meta_idx.ravel()] = starts.astype(np.uint32).ravel()
+        blob[tile_off_w[:-1] + ngrp] = tile_recs.astype(np.uint32)
+        rec_tile = rtg // ngrp
         first_rec = np.concatenate([[0], np.cumsum(tile_recs)])[:-1]
         local = np.arange(nrec) - first_rec[rec_tile]
-        base = tile_off_w[rec_tile] + meta_words + 8 * local
+        base = tile_off_w[rec_tile] + self.META_WORDS + 8 * local
         blob[base] = rs.astype(np.uint32)
         for k in range(self.GROUP):
             blob[base + 4 + k] = weights[:, k].view(np.uint32)
         self.num_rows, self.num_cols, self.num_pairs = num_rows, num_cols, p_count
         self.offsets = offsets
         self.records = nrec
-        self.max_pair_records = int(pair_recs.max()) if pair_recs.size else 0
         self.max_tile_records = int(tile_recs.max()) if tile_recs.size else 0
+        self.max_pair_records = self.max_tile_records
         self.host_blob = blob
         self.host_tile_off = tile_off_w * 4
-        self._rec = (rtpg, rs, weights, mask)
+        self._rec = (rtg, rs, weights, mask)
         self.d_blob = torch.from_numpy(blob.view(np.int32)).to(dev.device()) if blob.size else \
-            torch.zeros(4, dtype=torch.int32, device=dev.device())
+            torch.zeros(16, dtype=torch.int32, device=dev.device())
         self.d_tile_off = dev.as_i64(self.host_tile_off)
 
     @classmethod
@@ -289,10 +285,10 @@ class BandOperator:
 
     def to_csr(self):
         """Decode to (values float32, col_indices int64, row_splits int64)."""
-        rtpg, rs, weights, mask = self._rec
+        rtg, rs, weights, mask = self._rec
         ngrp = self.TILE // self.GROUP
-        t = rtpg // (self.num_pairs * ngrp)
-        g = rtpg % ngrp
+        t = rtg // ngrp
+        g = rtg % ngrp
         rec, c = np.nonzero(mask)
         rows = t[rec] * self.TILE + g[rec] * self.GROUP + c
         cols = rs[rec]

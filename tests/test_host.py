@@ -124,7 +124,7 @@ def test_ell_roundtrip_bit_exact(golden_scene):
         assert_array_equal(splits, ref.row_splits)
         assert_array_equal(vals, ref.values.astype(np.float32))
         # every record's sample index lies inside the operator; padded weights are zero
-        rtpg, rs, weights, mask = ell._rec
+        rtg, rs, weights, mask = ell._rec
         assert np.all(rs < spec.offsets[-1]) and np.all(weights[~mask] == 0)
 
 
@@ -137,7 +137,7 @@ def test_ell_empty_and_keep_all(golden_scene):
     full = _ell(s.truncate_sparse(interp, interp.matrix.size), spec.offsets)
     groups = (grid.num_points + 3) // 4
     assert full.records == groups * spec.offsets[-1]
-    assert full.max_pair_records <= 8 * int(np.max(np.diff(spec.offsets)))
+    assert full.max_tile_records <= 8 * int(spec.offsets[-1])
 
 
 def test_errors_mirror_reference():
