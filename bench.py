@@ -47,11 +47,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU per step (default: config)")
-    ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "si"])
+    ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "conv_h", "si"])
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--variants", default="sspi,slri,lr,conv",
+    ap.add_argument("--variants", default="sspi,slri,lr,conv,conv_h",
                     help="comma list of extra variants measured on the same workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -146,8 +146,10 @@ def fit_operator(wl, variant, args):
             return s.truncate_low_rank(interp, args.rank_r)
         keep = s.resolve_sparsity(args.nnz, wl.grid.num_points, wl.pairs.num_pairs, interp.matrix.size)
         return s.truncate_sparse(interp, keep)
+    if variant == "conv":        # steering generated on chip from the TDOA table
+        return s.steering_operator(wl.tdoa, wl.frame)
     srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 36)
-    if variant == "conv":
+    if variant == "conv_h":      # stored steering matrix (the reference's SrpMatrix, TMA-fed)
         return srp
     return s.truncate_srp_matrix(srp, args.rank_r)
 
@@ -204,7 +206,8 @@ def run_ours(args):
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def make_pipe(variant, op):
-        return MapPipeline(variant, op, wl.frame, wl.pairs, wl.spec, frames=count)
+        return MapPipeline("conv" if variant == "conv_h" else variant, op, wl.frame, wl.pairs, wl.spec,
+                           frames=count)
 
     def timed(fn, steps, warmup, gather):
         for _ in range(warmup):
@@ -253,7 +256,7 @@ def run_ours(args):
     t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush)
     hbm, bf16, peak_src = peaks()
     abytes = algorithmic_bytes(wl, args.variant, count, op)
-    if args.variant == "conv":
+    if args.variant in ("conv", "conv_h"):
         dom_name, dom_ms = "srp_map_tc", t_map
         achieved = conv_flops(wl, count) / (dom_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": bf16,
@@ -302,12 +305,14 @@ def run_ours(args):
                 ms_v, _ = timed(pv.replay, k, 3, False)
                 entry = {"value": total / (ms_v / 1e3), "unit": UNIT, "ms_per_step": ms_v,
                          "gpu_launches_per_step": pipe_launches(pv)}
-                if v == "conv":
+                if v in ("conv", "conv_h"):
                     tf, tm = stage_times(s, wl, v, opv, x_dev, count, flush)
                     entry["tflops_step"] = conv_flops(wl, count) / (ms_v / 1e3) / 1e12
                     entry["tflops_gemm"] = conv_flops(wl, count) / (tm / 1e3) / 1e12
                     entry["kernel_ms"] = {"frontend": tf, "map": tm}
                     entry["precision"] = "tf32 (tcgen05, RNE operands)"
+                    entry["operator"] = ("steering generated on chip" if v == "conv"
+                                         else "stored steering matrix via TMA")
                 if v in ("lr", "slri"):
                     entry["rank"] = args.rank_r
                 pv.run(x_dev)
@@ -368,7 +373,8 @@ def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10):
         front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames)
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
     else:
-        front = lambda: s.gcc_frames(x_dev, wl.frame, wl.pairs, frames, tf32=(variant == "conv"))
+        front = lambda: s.gcc_frames(x_dev, wl.frame, wl.pairs, frames,
+                                     tf32=(variant in ("conv", "conv_h")))
         mapf = s.lr_map if variant == "lr" else s.srp_map_exact
     mid = front()
     mapf(op, mid, argmax=True)
@@ -417,8 +423,9 @@ def oracle_chain(wl, variant, op, x, nf):
     win = O.frame_window(wl.frame.frame_len, wl.frame.window)
     spectra = O.stft_frames(x, wl.frame.frame_len, wl.frame.hop, win, np.arange(nf))
     psi = O.fd_gcc(spectra, wl.pairs.pairs)
-    if variant == "conv":
-        return O.srp_map_exact(op.matrix, psi)
+    if variant in ("conv", "conv_h"):
+        mat = op.matrix if hasattr(op, "matrix") else op.materialize(1 << 36).matrix
+        return O.srp_map_exact(mat, psi)
     if variant == "lr":
         return O.lr_map(op.tall, op.fat, psi)
     xi = O.td_gcc_samples(psi, wl.spec.counts, wl.frame.half_len, "ifft")

@@ -22,7 +22,7 @@ from .frontend import FdGcc, FrameSpec, fd_gcc, frame_window, gcc_frames, num_fr
 from .maps import (decode_keys, evaluate_map, locate, lr_map, map_argmax, si_map, slri_map,
                    sspi_map, srp_map_exact)
 from .operators import (DEFAULT_MATRIX_CAP_BYTES, FixedNnzInterp, InterpMatrix, LowRankInterp,
-                        LowRankSrp, sparse_interp_fixed,
+                        LowRankSrp, SteeringTdoa, sparse_interp_fixed, steering_operator,
                         SparseInterp, SrpMatrix, build_interp_matrix, build_srp_matrix,
                         check_capacity, low_rank_interp_from_svd, low_rank_srp_from_svd,
                         resolve_sparsity, srp_matrix_shape, truncate_low_rank, truncate_sparse,

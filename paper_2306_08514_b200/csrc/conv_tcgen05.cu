@@ -121,11 +121,106 @@ struct __align__(1024) Smem {
   uint32_t tmem_base;
 };
 
-template <int BLOCK_N>
+// On-chip steering operand: A[i][2c] = cos(theta), A[i][2c+1] = -sin(theta) with
+// theta = pi k x[i][p] / K for complex column c = p (K-1) + k - 1 (srp.py:51-62,
+// frontend.py:67-71), x = dt * fs.  Generated per k-block by the four epilogue warps
+// (one row each: a sincospi seed per pair segment, then a complex rotation per bin),
+// rounded to TF32 and written in the 128-byte-swizzled K-major layout TMA would produce.
+struct GenParams {
+  const float* xtab;   // [J][P]
+  int32_t P;
+  int32_t B;           // bins per pair (K - 1)
+  float inv_k;         // 1 / K
+};
+
+// round to nearest TF32 in one instruction (ties away from zero; the phasors never tie in
+// practice, and rounding-to-nearest keeps the product unbiased unlike plain truncation)
+__device__ __forceinline__ uint32_t cvt_tf32(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return u;
+}
+
+// Per-row generator state carried across k-blocks (one thread per operand row).
+struct GenState {
+  int pair;          // pair of the carried rotation (-1: none)
+  int next_k;        // bin whose phasor `seed` holds
+  int since;         // blocks since the last exact seed
+  float2 seed, s1, s2, s4, s8;   // exp(j pi k x / K) at next_k, and step powers
+  float x;
+};
+
+__device__ __forceinline__ void gen_state_init(GenState& g) {
+  g.pair = -1; g.next_k = 0; g.since = 0; g.x = 0.f;
+  g.seed = g.s1 = g.s2 = g.s4 = g.s8 = make_float2(1.f, 0.f);
+}
+
+__device__ __forceinline__ void gen_a_block(float* a_stage, int row, int64_t i, bool valid, int kb,
+                                            const GenParams& gp, GenState& g) {
+  const int total = gp.P * gp.B;
+  const int c0 = kb * 16;
+  float2 e[16];
+  const int p0 = c0 / gp.B, p1 = (c0 + 15) / gp.B;
+  if (valid && p0 == p1 && c0 + 15 < total) {
+    // fast path: 16 consecutive bins of one pair, e_j = seed * step^j (depth-4 product tree)
+    const int k0 = c0 - p0 * gp.B + 1;
+    if (g.pair != p0 || g.next_k != k0 || g.since >= 4) {
+      if (g.pair != p0) {
+        g.pair = p0;
+        g.x = __ldg(gp.xtab + i * gp.P + p0);
+        float sn, cs;
+        sincospif(g.x * gp.inv_k, &sn, &cs);
+        g.s1 = make_float2(cs, sn);
+        g.s2 = cmul(g.s1, g.s1);
+        g.s4 = cmul(g.s2, g.s2);
+        g.s8 = cmul(g.s4, g.s4);
+      }
+      float sn, cs;
+      sincospif((float)k0 * g.x * gp.inv_k, &sn, &cs);   // exact re-seed bounds the drift
+      g.seed = make_float2(cs, sn);
+      g.since = 0;
+    }
+    e[0] = g.seed;
+    e[1] = cmul(e[0], g.s1);
+    e[2] = cmul(e[0], g.s2);
+    e[3] = cmul(e[1], g.s2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[4 + j] = cmul(e[j], g.s4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[8 + j] = cmul(e[j], g.s8);
+    g.seed = cmul(e[8], g.s8);
+    g.next_k = k0 + 16;
+    g.since += 1;
+  } else {
+    // block straddles a pair boundary (or the tail): exact phasor per element
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = c0 + j;
+      e[j] = make_float2(0.f, 0.f);
+      if (valid && c < total) {
+        const int pc = c / gp.B;
+        const int k = c - pc * gp.B + 1;
+        const float x = __ldg(gp.xtab + i * gp.P + pc);
+        float sn, cs;
+        sincospif((float)k * x * gp.inv_k, &sn, &cs);
+        e[j] = make_float2(cs, sn);
+      }
+    }
+    g.pair = -1;
+  }
+  unsigned char* rowp = reinterpret_cast<unsigned char*>(a_stage) + row * 128;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)   // (Re H, -Im H), TF32-rounded, 128-byte swizzle: chunk q -> q ^ (row & 7)
+    *reinterpret_cast<uint4*>(rowp + ((q ^ (row & 7)) << 4)) =
+        make_uint4(cvt_tf32(e[2 * q].x), cvt_tf32(-e[2 * q].y), cvt_tf32(e[2 * q + 1].x),
+                   cvt_tf32(-e[2 * q + 1].y));
+}
+
+template <int BLOCK_N, bool GEN_A>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  int64_t J, int64_t F, int32_t Kd, float* __restrict__ z,
-                 unsigned long long* __restrict__ keys, float alpha) {
+                 unsigned long long* __restrict__ keys, float alpha, const GenParams gp) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   Smem<BLOCK_N>& sm = *reinterpret_cast<Smem<BLOCK_N>*>(
@@ -147,7 +242,7 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.full[s], GEN_A ? 1 + 128 : 1);   // + the 128 generator threads
       mbar_init(&sm.empty[s], 1);
     }
     mbar_init(&sm.tmem_full, 1);
@@ -167,13 +262,13 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 
   if (warp == 0) {
     if (lane == 0) {
-      constexpr uint32_t kBytes = (BLOCK_M + BLOCK_N) * BLOCK_K * sizeof(float);
+      constexpr uint32_t kBytes = ((GEN_A ? 0 : BLOCK_M) + BLOCK_N) * BLOCK_K * sizeof(float);
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % STAGES;
         const uint32_t round = kb / STAGES;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
         mbar_expect_tx(&sm.full[s], kBytes);
-        tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
+        if (!GEN_A) tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
         tma_load_2d(sm.b[s], &map_b, &sm.full[s], kb * BLOCK_K, n_blk * BLOCK_N);
       }
     }
@@ -202,6 +297,20 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int quarter = warp & 3;
+    if (GEN_A) {   // generate the steering operand stage by stage
+      const int row = quarter * 32 + lane;
+      const int64_t gi = (int64_t)m_blk * BLOCK_M + row;
+      GenState g;
+      gen_state_init(g);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t round = kb / STAGES;
+        mbar_wait(&sm.empty[s], (round & 1) ^ 1);
+        gen_a_block(sm.a[s], row, gi, gi < J, kb, gp, g);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+      }
+    }
     mbar_wait(&sm.tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int64_t i = (int64_t)m_blk * BLOCK_M + quarter * 32 + lane;
@@ -275,16 +384,16 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   return SRPGPU_OK;
 }
 
-template <int BLOCK_N>
+template <int BLOCK_N, bool GEN_A>
 static int launch(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, const float* h2, int64_t h2_ld,
-                  int64_t J, float* z, uint64_t* keys, cudaStream_t st) {
+                  int64_t J, float* z, uint64_t* keys, cudaStream_t st, const GenParams& gp) {
   CUtensorMap ma, mb;
-  int s = make_map(&ma, h2, J, Kd, h2_ld, BLOCK_M);
+  int s = make_map(&mb, gcc, F, Kd, gcc_ld, BLOCK_N);
   if (s) return s;
-  s = make_map(&mb, gcc, F, Kd, gcc_ld, BLOCK_N);
-  if (s) return s;
+  if (GEN_A) ma = mb;
+  else if ((s = make_map(&ma, h2, J, Kd, h2_ld, BLOCK_M))) return s;
   const size_t smem = sizeof(Smem<BLOCK_N>) + 1024;
-  auto kern = conv_tf32_kernel<BLOCK_N>;
+  auto kern = conv_tf32_kernel<BLOCK_N, GEN_A>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("srp_map_tc: cannot reserve %zu B shared memory", smem);
     return SRPGPU_ERR_LAUNCH;
@@ -292,7 +401,7 @@ static int launch(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, const
   const int64_t tiles = ((J + BLOCK_M - 1) / BLOCK_M) * ((F + BLOCK_N - 1) / BLOCK_N);
   SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "srp_map_tc: too many tiles");
   kern<<<(unsigned)tiles, kThreads, smem, st>>>(ma, mb, J, F, Kd, z,
-                                                 reinterpret_cast<unsigned long long*>(keys), 2.0f);
+                                                 reinterpret_cast<unsigned long long*>(keys), 2.0f, gp);
   SRPGPU_CHECK_LAUNCH("srp_map_tc");
   return SRPGPU_OK;
 }
@@ -351,7 +460,30 @@ extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_f
   if (num_frames <= 0) return SRPGPU_OK;
   const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
   const int64_t n256 = (num_frames + 255) / 256;
+  const tc::GenParams gp = {};
   if (m_tiles * n256 >= 2 * (int64_t)num_sms())
-    return tc::launch<256>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st);
-  return tc::launch<128>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st);
+    return tc::launch<256, false>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st, gp);
+  return tc::launch<128, false>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st, gp);
+}
+
+extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t num_pairs,
+                                   int32_t half_len, const float* xtab, int64_t num_candidates, float* z,
+                                   uint64_t* keys, srpgpu_stream_t stream) {
+  const int32_t bins = half_len - 1;
+  const int32_t Kd = 2 * num_pairs * bins;
+  SRPGPU_CHECK_ARG(num_pairs >= 1 && bins >= 1 && num_candidates >= 1, SRPGPU_ERR_DIMENSION,
+                   "srp_map_tdoa: empty operator");
+  SRPGPU_CHECK_ARG(gcc_ld >= Kd && gcc_ld % 4 == 0 && ((uintptr_t)gcc & 15) == 0, SRPGPU_ERR_VALUE,
+                   "srp_map_tdoa: gcc rows must cover 2*P*(K-1) floats with a 16-byte pitch");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  if (num_frames <= 0) return SRPGPU_OK;
+  tc::GenParams gp;
+  gp.xtab = xtab; gp.P = num_pairs; gp.B = bins; gp.inv_k = 1.0f / (float)half_len;
+  const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
+  const int64_t n256 = (num_frames + 255) / 256;
+  if (m_tiles * n256 >= 2 * (int64_t)num_sms())
+    return tc::launch<256, true>(gcc, gcc_ld, num_frames, Kd, nullptr, 0, num_candidates, z, keys, st, gp);
+  return tc::launch<128, true>(gcc, gcc_ld, num_frames, Kd, nullptr, 0, num_candidates, z, keys, st, gp);
 }

@@ -465,6 +465,10 @@ def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, ou
                              f"match a {srp.num_pairs} x {srp.num_bins} transform")
     if precision not in ("tf32", "fp32"):
         raise ValueError(f"unknown precision {precision!r}")
+    if not hasattr(srp, "matrix"):           # implicit operator: steering generated on chip
+        if precision != "tf32":
+            raise ValueError("the on-chip steering path is TF32; materialize() the operator for fp32")
+        return _srp_map_tdoa(srp, gcc, argmax, out_map)
     n = srp.num_pairs * srp.num_bins
     h2 = steering_device(srp, tf32=(precision == "tf32"))
     j, ld = h2.shape
@@ -491,6 +495,32 @@ def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, ou
                      dev.stream_ptr())
         nat.call("srpgpu_srp_map_tc", dev.ptr(vp), ld, f, n, dev.ptr(h2), ld, j, dev.ptr(z),
                  dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+def _xtab_device(op) -> torch.Tensor:
+    """x[i][p] = dt_p(i) * fs as float32 (the on-chip steering generator's input)."""
+    return dev.CACHE.get(op, "xtab_f32", lambda: dev.as_f32(
+        np.asarray(op.tdoa.delta_t, dtype=np.float64) * float(op.frame.sample_rate)))
+
+
+def _srp_map_tdoa(op, gcc, argmax: bool, out_map: bool):
+    n = op.num_pairs * op.num_bins
+    ld = _pad4(2 * n)
+    padded = getattr(gcc, "padded", None)
+    if getattr(gcc, "tf32_rounded", False) and padded is not None and padded.shape[1] == ld:
+        vp, batched = padded, gcc.values.dim() == 2
+    else:
+        v, batched = _gcc_matrix(gcc, op.num_pairs, op.num_bins)
+        vp = torch.empty((v.shape[0], ld), dtype=torch.float32, device=v.device)
+        nat.call("srpgpu_round_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, v.shape[0], 2 * n,
+                 dev.stream_ptr())
+    f, j = vp.shape[0], op.num_candidates
+    xt = _xtab_device(op)
+    z = torch.empty((f, j), dtype=torch.float32, device=vp.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    nat.call("srpgpu_srp_map_tdoa", dev.ptr(vp), ld, f, op.num_pairs, op.num_bins + 1, dev.ptr(xt), j,
+             dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 

@@ -339,3 +339,35 @@ def sparse_interp_fixed(tdoa, spec, frame, nnz: int, rows=None) -> FixedNnzInter
         cols[p, :, :k] = np.take_along_axis(sel_c, back, 1) + off[p]
         values[p, :, :k] = np.take_along_axis(sel_v, back, 1)
     return FixedNnzInterp(values=values, cols=cols, kept=kept, num_cols=int(off[-1]))
+
+
+@dataclass(frozen=True)
+class SteeringTdoa:
+    """The conventional operator H[i, pB+k-1] = exp(j w_k dt_p(i)) kept implicit.
+
+    `srp_map_exact` accepts it wherever it accepts an `SrpMatrix` (srp.py:22-62): the
+    GPU generates H on chip from the TDOA table instead of reading it from memory, so
+    grids whose H cannot be stored (BASELINE cfg4: 334611 x 61320 complex) still map.
+    """
+
+    tdoa: object
+    frame: object
+
+    @property
+    def num_pairs(self) -> int:
+        return self.tdoa.num_pairs
+
+    @property
+    def num_bins(self) -> int:
+        return self.frame.num_bins
+
+    @property
+    def num_candidates(self) -> int:
+        return self.tdoa.num_candidates
+
+    def materialize(self, max_bytes: int = DEFAULT_MATRIX_CAP_BYTES) -> SrpMatrix:
+        return build_srp_matrix(self.tdoa, self.frame, max_bytes)
+
+
+def steering_operator(tdoa, frame) -> SteeringTdoa:
+    return SteeringTdoa(tdoa=tdoa, frame=frame)

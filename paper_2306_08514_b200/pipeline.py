@@ -32,6 +32,8 @@ class MapPipeline:
                  out_map: bool = True, precision: str = "tf32", graph: bool = True):
         if variant not in self.VARIANTS:
             raise ValueError(f"unknown map variant {variant!r}")
+        if variant == "conv_h":
+            variant = "conv"
         if variant in ("sspi", "si", "slri") and spec is None:
             raise ValueError(f"{variant} needs a SampleSpec")
         self.variant, self.op, self.frame, self.pairs, self.spec = variant, op, frame, pairs, spec

@@ -309,3 +309,20 @@ def test_pipeline_graph_matches_eager(golden_scene):
     zc, ic = conv.run(torch.from_numpy(x.astype(np.float32)).cuda())
     assert_map_close(zc, g["z_conv"])
     assert_argmax_agrees(ic, g["z_conv"])
+
+
+def test_conventional_map_onchip_steering(golden_scene):
+    """H generated on chip from the TDOA table (no stored operator) matches the reference map."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    op = s.steering_operator(tdoa, frame)
+    F = g["psi"].shape[0]
+    gcc = s.gcc_frames(g["samples"], frame, pairs, range(F), tf32=True)
+    z, idx = s.srp_map_exact(op, gcc, argmax=True)
+    assert_map_close(z, g["z_conv"])
+    assert_argmax_agrees(idx, g["z_conv"])
+    gcc2 = s.FdGcc(torch.from_numpy(g["psi"].astype(np.complex64)).cuda(), pairs.num_pairs,
+                   frame.num_bins, "phat")
+    assert_map_close(s.srp_map_exact(op, gcc2), g["z_conv"])
+    with pytest.raises(ValueError):
+        s.srp_map_exact(op, gcc2, precision="fp32")
