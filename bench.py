@@ -120,6 +120,38 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def extra_peaks():
+    """TF32 tensor / FP32 SIMT peaks measured on this pool by tools/measure_peaks.py."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "measured_peaks_extra.json")) as f:
+            p = json.load(f)
+        return float(p["tf32_tflops"]), float(p["fp32_tflops"]), "measured (profiles/measured_peaks_extra.json)"
+    except (OSError, KeyError, ValueError):
+        return 1100.0 / 2 * 1.38, 74.4, "nominal"
+
+
+def frontend_flops(wl, variant, frames):
+    """FFT + PHAT flops of the fused frontend (5 L log2 L per complex FFT)."""
+    import math
+    L = wl.frame.frame_len
+    m, p = wl.array.num_mics, wl.pairs.num_pairs
+    ffts = (m + 1) // 2 + ((p + 1) // 2 if variant in ("sspi", "si", "slri") else 0)
+    return frames * (ffts * 5 * L * math.log2(L) + 20 * p * wl.frame.num_bins)
+
+
+def map_flops(wl, variant, op, frames):
+    if variant in ("sspi", "si"):
+        kept = getattr(op, "num_kept", None)
+        return 2.0 * frames * (kept if kept is not None else op.matrix.size)
+    if variant == "slri":
+        r = op.tall.shape[1]
+        return 2.0 * frames * r * (wl.spec.total_samples + wl.grid.num_points)
+    if variant == "lr":
+        r = op.tall.shape[1]
+        return frames * (8.0 * r * wl.pairs.num_pairs * wl.frame.num_bins + 4.0 * wl.grid.num_points * r)
+    return conv_flops(wl, frames)
+
+
 def ncu_traffic(workload: str, kernel: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -136,8 +168,19 @@ def build_scene(args, total_frames):
     return workloads.make(args.workload, num_frames=total_frames)
 
 
+DENSE_LAMBDA_CAP = 4 << 30   # above this the dense Lambda (and its SVD / global top-Q) is not built
+
+
 def fit_operator(wl, variant, args):
     import paper_2306_08514_b200 as s
+    dense_bytes = 8 * wl.grid.num_points * wl.spec.total_samples
+    if variant == "sspi" and dense_bytes > DENSE_LAMBDA_CAP:
+        # cfg4: Lambda is 18.7 GB -> fixed nnz per (candidate, pair), built pair by pair
+        nnz = int(round(float(args.nnz[:-2]))) if args.nnz.endswith("jp") else int(args.nnz)
+        return s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, max(1, nnz))
+    if variant in ("si", "slri", "lr") and dense_bytes > DENSE_LAMBDA_CAP:
+        raise ValueError(f"{variant} needs the dense operator / its SVD "
+                         f"({dense_bytes / 1e9:.1f} GB): infeasible at this grid")
     if variant in ("sspi", "si", "slri"):
         interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
         if variant == "si":
@@ -256,11 +299,13 @@ def run_ours(args):
     t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush)
     hbm, bf16, peak_src = peaks()
     abytes = algorithmic_bytes(wl, args.variant, count, op)
+    tf32_peak, fp32_peak, xsrc = extra_peaks()
     if args.variant in ("conv", "conv_h"):
         dom_name, dom_ms = "srp_map_tc", t_map
         achieved = conv_flops(wl, count) / (dom_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": bf16,
-                "unit": "TFLOP/s", "frac": achieved / bf16, "peak_source": f"{peak_src} bf16",
+        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": tf32_peak,
+                "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                "peak_source": f"TF32 cuBLAS {xsrc}", "frac_of_bf16_peak": achieved / bf16,
                 "traffic": ncu_traffic(args.workload, dom_name)}
     else:
         if t_map >= t_front:
@@ -273,6 +318,12 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
+    # the SIMT stages are FP32-issue / L1 bound at these sizes: their FP32 fractions
+    roof["fp32_frac"] = {
+        "frontend": frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak,
+        "map": (map_flops(wl, args.variant, op, count) / (t_map / 1e3) / 1e12 / fp32_peak
+                if args.variant not in ("conv", "conv_h") else None),
+        "fp32_peak_tflops": fp32_peak, "peak_source": f"FP32 SIMT cuBLAS {xsrc}"}
 
     # ---- e2e through the public pipeline API: pinned host samples in, argmax indices out
     out_host = torch.empty(count, dtype=torch.int64).pin_memory()
@@ -335,7 +386,9 @@ def run_ours(args):
                        "candidates": wl.grid.num_points, "pairs": wl.pairs.num_pairs,
                        "frame_len": wl.frame.frame_len, "total_lags": wl.spec.total_samples,
                        "variant": args.variant,
-                       "operator": (args.nnz if args.variant == "sspi" else
+                       "operator": ((args.nnz if not hasattr(op, "kept") else
+                                     f"{int(op.values.shape[2])} nnz per (candidate, pair)")
+                                    if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
                        "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
                        "execution": "CUDA graph per batch"},
@@ -424,12 +477,20 @@ def oracle_chain(wl, variant, op, x, nf):
     spectra = O.stft_frames(x, wl.frame.frame_len, wl.frame.hop, win, np.arange(nf))
     psi = O.fd_gcc(spectra, wl.pairs.pairs)
     if variant in ("conv", "conv_h"):
+        if not hasattr(op, "matrix") and 16 * op.num_candidates * op.num_pairs * op.num_bins > DENSE_LAMBDA_CAP:
+            raise ValueError("dense H infeasible: conventional parity is checked on row blocks in tests")
         mat = op.matrix if hasattr(op, "matrix") else op.materialize(1 << 36).matrix
         return O.srp_map_exact(mat, psi)
     if variant == "lr":
         return O.lr_map(op.tall, op.fat, psi)
     xi = O.td_gcc_samples(psi, wl.spec.counts, wl.frame.half_len, "ifft")
     if variant == "sspi":
+        if hasattr(op, "kept"):   # fixed-nnz blocks (cfg4): gather-sum pair by pair
+            z = np.zeros((xi.shape[0], op.values.shape[1]))
+            for p in range(op.values.shape[0]):
+                k = int(op.kept[p])
+                z += np.einsum("jk,fjk->fj", op.values[p, :, :k], xi[:, op.cols[p, :, :k]])
+            return z
         return O.sspi_map(op.values, op.col_indices, op.row_splits, xi)
     if variant == "slri":
         return O.slri_map(op.tall, op.fat, xi)
