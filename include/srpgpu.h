@@ -160,10 +160,16 @@ int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int3
  * candidate i, pair p, bin k: H = exp(j pi k x[i][p] / K), x = xtab [J][P] f32 = dt * fs
  * (srp.py:51-62).  Same tcgen05 GEMM, TMA streams only the TF32-rounded gcc rows
  * (gcc_ld floats per frame, 16-byte pitch).  The operator for grids whose H does not
- * fit in memory (BASELINE cfg4: 164 GB). */
+ * fit in memory (BASELINE cfg4: 164 GB).  split = 1 selects 3xTF32 (near-fp32 accuracy,
+ * 3 MMAs per k-step): gcc then holds the hi plane [F][gcc_ld] followed by the lo plane
+ * (srpgpu_split_tf32), and the steering residual is generated on chip as well. */
 int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t num_pairs,
-                        int32_t half_len, const float* xtab, int64_t num_candidates, float* z,
-                        uint64_t* keys, srpgpu_stream_t stream);
+                        int32_t half_len, const float* xtab, int64_t num_candidates, int32_t split,
+                        float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* dst = [hi plane rows][lo plane rows]: hi = tf32_rne(src), lo = tf32_rne(src - hi). */
+int srpgpu_split_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,
+                      int64_t cols, srpgpu_stream_t stream);
 
 /* dst[r][c] = tf32_rne(src[r][c]) for c < cols, 0 for cols <= c < ld_dst. */
 int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,

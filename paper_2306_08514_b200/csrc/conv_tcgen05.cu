@@ -2,25 +2,19 @@
 //
 //   z[f][i] = 2 Re( sum_k H[i][k] psi[f][k] )          srp.py:65-71
 //           = 2 * sum_k' A[i][k'] B[f][k']
-//   A = interleaved (Re H, -Im H) rows  [J][2PB]   (fp32 storage, read as TF32)
+//   A = interleaved (Re H, -Im H) rows  [J][2PB]   (TF32 operands)
 //   B = psi viewed as interleaved (re, im) floats [F][2PB]
 //
-// D = A . B^T is a K-major x K-major ("TN") GEMM with M = candidates, N = frames.
-// Warp-specialised CTA (192 threads):
-//   warp 0      TMA producer: cp.async.bulk.tensor 2D tiles of A and B into a
-//               STAGES-deep shared-memory ring (128-byte swizzle), mbarrier
-//               full/empty handshake;
-//   warp 1      TMEM allocator + single-thread MMA issuer:
-//               tcgen05.mma.cta_group::1.kind::tf32, accumulator in TMEM,
-//               tcgen05.commit frees each smem stage and finally signals the
-//               epilogue;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers, x2, coalesced store
-//               of z[f][i] (lanes = consecutive candidates) and the fused
-//               per-frame argmax (packed keys, atomicMax).
-// Tiles are rasterised in groups of GROUP_M candidate tiles so concurrently
-// running CTAs share both A and B k-slices in L2.
+// D = A . B^T is a K-major x K-major ("TN") GEMM with M = candidates (128 per CTA),
+// N = frames (256 per CTA), tcgen05.mma.cta_group::1.kind::tf32 with the accumulator in
+// TMEM.  A is either streamed by TMA from a stored matrix (srpgpu_srp_map_tc, the
+// drop-in SrpMatrix) or generated on chip from the TDOA table (srpgpu_srp_map_tdoa:
+// the steering matrix of a large grid is never stored).  K is accumulated in chunks
+// folded into fp32 registers (see conv_gen_chunked_kernel) because the tensor core's
+// in-pipe accumulation is not IEEE fp32.  Epilogue: coalesced z stores and the fused
+// per-frame argmax (packed keys, atomicMax).  Tiles are rasterised in groups of
+// GROUP_M candidate tiles so concurrently running CTAs share k-slices in L2.
 #include <cuda.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -30,9 +24,7 @@ namespace tc {
 constexpr int BLOCK_M = 128;
 constexpr int BLOCK_K = 32;          // fp32 elements = 128 bytes = one swizzle atom row
 constexpr int UMMA_K = 8;            // tf32: 32 bytes per MMA
-constexpr int STAGES = 4;
 constexpr int GROUP_M = 16;
-constexpr int kThreads = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -111,16 +103,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BLOCK_N>
-struct __align__(1024) Smem {
-  float a[STAGES][BLOCK_M * BLOCK_K];   // 16 KB per stage
-  float b[STAGES][BLOCK_N * BLOCK_K];   // 16 / 32 KB per stage
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint64_t tmem_full;
-  uint32_t tmem_base;
-};
-
 // On-chip steering operand: A[i][2c] = cos(theta), A[i][2c+1] = -sin(theta) with
 // theta = pi k x[i][p] / K for complex column c = p (K-1) + k - 1 (srp.py:51-62,
 // frontend.py:67-71), x = dt * fs.  Generated per k-block by the four epilogue warps
@@ -138,7 +120,7 @@ struct GenParams {
 __device__ __forceinline__ uint32_t cvt_tf32(float x) {
   uint32_t u;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-  return u;
+  return u & 0xFFFFE000u;   // the low 13 bits of the result are not guaranteed to be zero
 }
 
 // Per-row generator state carried across k-blocks (one thread per operand row).
@@ -155,14 +137,55 @@ __device__ __forceinline__ void gen_state_init(GenState& g) {
   g.seed = g.s1 = g.s2 = g.s4 = g.s8 = make_float2(1.f, 0.f);
 }
 
-__device__ __forceinline__ void gen_a_block(float* a_stage, int row, int64_t i, bool valid, int kb,
-                                            const GenParams& gp, GenState& g) {
+// The GEMM kernel (128 candidates x 256 frames per CTA).  The tensor core's in-pipe
+// accumulation is not IEEE fp32 (measured: 3.8e-5 normalized error against an exact
+// evaluation of its own TF32 operands at K = 3600), so K is cut into chunks of CHUNK
+// k-blocks accumulated in two alternating 256-column TMEM tiles (all 512 columns);
+// while the MMA fills one, eight folding warps tcgen05.ld the other and add it into
+// fp32 running sums held in registers.  With SPLIT the three 3xTF32 products go to the
+// same chunk tile.  Roles (10 warps): 0 TMA (psi, and A when GEN = false), 1 TMEM
+// alloc + MMA issue, 2..9 steering generators (two threads per operand row, 8 bins
+// each) and folders: warp w owns TMEM lane quarter w % 4 and column half (w - 2) / 4,
+// 128 running sums per thread.
+constexpr int CHUNK = 16;
+constexpr int kThreadsC = 320;
+
+template <bool SPLIT>
+struct __align__(1024) SmemC {
+  static constexpr int BN = 256;
+  static constexpr int NS = SPLIT ? 2 : 4;
+  static constexpr int NP = SPLIT ? 2 : 1;
+  float a[NS][NP][BLOCK_M * BLOCK_K];
+  float b[NS][NP][BN * BLOCK_K];
+  uint64_t full[NS];
+  uint64_t empty[NS];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+// 8 bins [8 half, 8 half + 8) of k-block kb for one operand row (fast path: product tree
+// from a carried seed; re-seeded exactly every 4 blocks and at pair changes)
+template <bool SPLIT>
+__device__ __forceinline__ void gen_a_half(float* a_stage, float* a_lo, int row, int half, int64_t i,
+                                           bool valid, int kb, const GenParams& gp, GenState& g) {
   const int total = gp.P * gp.B;
-  const int c0 = kb * 16;
-  float2 e[16];
-  const int p0 = c0 / gp.B, p1 = (c0 + 15) / gp.B;
-  if (valid && p0 == p1 && c0 + 15 < total) {
-    // fast path: 16 consecutive bins of one pair, e_j = seed * step^j (depth-4 product tree)
+  const int c0 = kb * 16 + 8 * half;
+  float2 e[8];
+  const int p0 = c0 / gp.B, p1 = (c0 + 7) / gp.B;
+  if (valid && p0 == p1 && c0 + 7 < total) {
     const int k0 = c0 - p0 * gp.B + 1;
     if (g.pair != p0 || g.next_k != k0 || g.since >= 4) {
       if (g.pair != p0) {
@@ -173,10 +196,10 @@ __device__ __forceinline__ void gen_a_block(float* a_stage, int row, int64_t i, 
         g.s1 = make_float2(cs, sn);
         g.s2 = cmul(g.s1, g.s1);
         g.s4 = cmul(g.s2, g.s2);
-        g.s8 = cmul(g.s4, g.s4);
+        g.s8 = cmul(cmul(g.s4, g.s4), cmul(g.s4, g.s4));   // step to the next block: s^16
       }
       float sn, cs;
-      sincospif((float)k0 * g.x * gp.inv_k, &sn, &cs);   // exact re-seed bounds the drift
+      sincospif((float)k0 * g.x * gp.inv_k, &sn, &cs);
       g.seed = make_float2(cs, sn);
       g.since = 0;
     }
@@ -186,15 +209,12 @@ __device__ __forceinline__ void gen_a_block(float* a_stage, int row, int64_t i, 
     e[3] = cmul(e[1], g.s2);
 #pragma unroll
     for (int j = 0; j < 4; ++j) e[4 + j] = cmul(e[j], g.s4);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) e[8 + j] = cmul(e[j], g.s8);
-    g.seed = cmul(e[8], g.s8);
+    g.seed = cmul(e[0], g.s8);
     g.next_k = k0 + 16;
     g.since += 1;
   } else {
-    // block straddles a pair boundary (or the tail): exact phasor per element
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 8; ++j) {
       const int c = c0 + j;
       e[j] = make_float2(0.f, 0.f);
       if (valid && c < total) {
@@ -209,27 +229,36 @@ __device__ __forceinline__ void gen_a_block(float* a_stage, int row, int64_t i, 
     g.pair = -1;
   }
   unsigned char* rowp = reinterpret_cast<unsigned char*>(a_stage) + row * 128;
+  unsigned char* rowl = reinterpret_cast<unsigned char*>(a_lo) + row * 128;
 #pragma unroll
-  for (int q = 0; q < 8; ++q)   // (Re H, -Im H), TF32-rounded, 128-byte swizzle: chunk q -> q ^ (row & 7)
-    *reinterpret_cast<uint4*>(rowp + ((q ^ (row & 7)) << 4)) =
-        make_uint4(cvt_tf32(e[2 * q].x), cvt_tf32(-e[2 * q].y), cvt_tf32(e[2 * q + 1].x),
-                   cvt_tf32(-e[2 * q + 1].y));
+  for (int qq = 0; qq < 4; ++qq) {
+    const int q = 4 * half + qq;
+    const float v0 = e[2 * qq].x, v1 = -e[2 * qq].y, v2 = e[2 * qq + 1].x, v3 = -e[2 * qq + 1].y;
+    const uint4 hi = make_uint4(cvt_tf32(v0), cvt_tf32(v1), cvt_tf32(v2), cvt_tf32(v3));
+    *reinterpret_cast<uint4*>(rowp + ((q ^ (row & 7)) << 4)) = hi;
+    if (SPLIT)
+      *reinterpret_cast<uint4*>(rowl + ((q ^ (row & 7)) << 4)) =
+          make_uint4(cvt_tf32(v0 - __uint_as_float(hi.x)), cvt_tf32(v1 - __uint_as_float(hi.y)),
+                     cvt_tf32(v2 - __uint_as_float(hi.z)), cvt_tf32(v3 - __uint_as_float(hi.w)));
+  }
 }
 
-template <int BLOCK_N, bool GEN_A>
-__global__ void __launch_bounds__(kThreads, 1)
-conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                 int64_t J, int64_t F, int32_t Kd, float* __restrict__ z,
-                 unsigned long long* __restrict__ keys, float alpha, const GenParams gp) {
+// GEN = false: the steering operand is streamed by TMA from a stored matrix instead
+// (map_a), with the same chunked accumulation (the drop-in SrpMatrix path).
+template <bool SPLIT, bool GEN = true>
+__global__ void __launch_bounds__(kThreadsC, 1)
+conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_b2,
+                        const __grid_constant__ CUtensorMap map_a, int64_t J, int64_t F, int32_t Kd,
+                        float* __restrict__ z, unsigned long long* __restrict__ keys, float alpha,
+                        const GenParams gp) {
+  constexpr int BN = 256;
+  using SM = SmemC<SPLIT>;
+  constexpr int NS = SM::NS;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for the 128B-swizzled tiles
-  Smem<BLOCK_N>& sm = *reinterpret_cast<Smem<BLOCK_N>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // grouped rasterisation: GROUP_M m-tiles share each n-tile sweep
   const int m_tiles = (int)((J + BLOCK_M - 1) / BLOCK_M);
-  const int n_tiles = (int)((F + BLOCK_N - 1) / BLOCK_N);
+  const int n_tiles = (int)((F + BN - 1) / BN);
   const int tile = blockIdx.x;
   const int group = tile / (GROUP_M * n_tiles);
   const int first_m = group * GROUP_M;
@@ -237,22 +266,26 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   const int m_blk = first_m + (tile % (GROUP_M * n_tiles)) % gsize;
   const int n_blk = (tile % (GROUP_M * n_tiles)) / gsize;
   const int num_kb = (Kd + BLOCK_K - 1) / BLOCK_K;
+  const int num_chunks = (num_kb + CHUNK - 1) / CHUNK;
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], GEN_A ? 1 + 128 : 1);   // + the 128 generator threads
+    if (SPLIT) prefetch_tmap(&map_b2);
+    if (!GEN) prefetch_tmap(&map_a);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.full[s], GEN ? 1 + 256 : 1);
       mbar_init(&sm.empty[s], 1);
     }
-    mbar_init(&sm.tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.tfull[b], 1);
+      mbar_init(&sm.tempty[b], 8);   // one arrive per folding warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "n"(BLOCK_N < 32 ? 32 : BLOCK_N));
+                     smem_u32(&sm.tmem_base)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -262,74 +295,102 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 
   if (warp == 0) {
     if (lane == 0) {
-      constexpr uint32_t kBytes = ((GEN_A ? 0 : BLOCK_M) + BLOCK_N) * BLOCK_K * sizeof(float);
+      constexpr uint32_t kBytes = (BN * SM::NP + (GEN ? 0 : BLOCK_M)) * BLOCK_K * sizeof(float);
       for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t round = kb / STAGES;
+        const int s = kb % NS;
+        const uint32_t round = kb / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
         mbar_expect_tx(&sm.full[s], kBytes);
-        if (!GEN_A) tma_load_2d(sm.a[s], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
-        tma_load_2d(sm.b[s], &map_b, &sm.full[s], kb * BLOCK_K, n_blk * BLOCK_N);
+        if (!GEN) tma_load_2d(sm.a[s][0], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
+        tma_load_2d(sm.b[s][0], &map_b, &sm.full[s], kb * BLOCK_K, n_blk * BN);
+        if (SPLIT) tma_load_2d(sm.b[s][SM::NP - 1], &map_b2, &sm.full[s], kb * BLOCK_K, n_blk * BN);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // kind::tf32: D f32 (bits 4-5 = 1), A/B tf32 (= 2), both K-major, N>>3, M>>4
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BLOCK_N >> 3) << 17) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BLOCK_M >> 4) << 24);
       for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t round = kb / STAGES;
+        const int chunk = kb / CHUNK, b = chunk & 1;
+        const bool first = (kb % CHUNK) == 0;
+        if (first) {   // the fold warps have drained this chunk tile (first two chunks pass)
+          mbar_wait(&sm.tempty[b], ((chunk >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        const int s = kb % NS;
+        const uint32_t round = kb / NS;
         mbar_wait(&sm.full[s], round & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = smem_desc(sm.a[s]);
-        const uint64_t db = smem_desc(sm.b[s]);
+        const uint64_t da = smem_desc(sm.a[s][0]);
+        const uint64_t db = smem_desc(sm.b[s][0]);
+        const uint64_t da2 = smem_desc(sm.a[s][SM::NP - 1]);
+        const uint64_t db2 = smem_desc(sm.b[s][SM::NP - 1]);
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
 #pragma unroll
         for (int k = 0; k < BLOCK_K / UMMA_K; ++k) {
-          // advance the start address by k * 32 bytes inside the 128-byte swizzle row
-          mma_tf32(tmem, da + (uint64_t)((k * UMMA_K * 4) >> 4), db + (uint64_t)((k * UMMA_K * 4) >> 4),
-                   idesc, (kb | k) != 0);
+          const uint64_t off = (uint64_t)((k * UMMA_K * 4) >> 4);
+          mma_tf32(acc, da + off, db + off, idesc, (first && k == 0) ? 0u : 1u);
+          if (SPLIT) {
+            mma_tf32(acc, da + off, db2 + off, idesc, 1);
+            mma_tf32(acc, da2 + off, db + off, idesc, 1);
+          }
         }
         mma_commit(&sm.empty[s]);
+        if ((kb % CHUNK) == CHUNK - 1 || kb == num_kb - 1) mma_commit(&sm.tfull[b]);
       }
-      mma_commit(&sm.tmem_full);
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
-    const int quarter = warp & 3;
-    if (GEN_A) {   // generate the steering operand stage by stage
-      const int row = quarter * 32 + lane;
-      const int64_t gi = (int64_t)m_blk * BLOCK_M + row;
-      GenState g;
-      gen_state_init(g);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t round = kb / STAGES;
+    const int t = threadIdx.x - 64;            // 0..255
+    const int row = t & 127, half = t >> 7;
+    const int64_t gi = (int64_t)m_blk * BLOCK_M + row;
+    // fold ownership: TMEM lane quarter (warp % 4) x column half ((warp - 2) / 4)
+    const int quarter = warp & 3, chalf = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    float sum[128];
+#pragma unroll
+    for (int c = 0; c < 128; ++c) sum[c] = 0.f;
+    auto fold = [&](int chunk) {
+      const int b = chunk & 1;
+      mbar_wait(&sm.tfull[b], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_base + (uint32_t)(b * BN + chalf * 128 + c0), r);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sum[c0 + c] += __uint_as_float(r[c]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.tempty[b])) : "memory");
+    };
+    GenState g;
+    gen_state_init(g);
+    int folded = 0;
+    for (int kb = 0; kb < num_kb; ++kb) {
+      if (GEN) {
+        const int s = kb % NS;
+        const uint32_t round = kb / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
-        gen_a_block(sm.a[s], row, gi, gi < J, kb, gp, g);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+        gen_a_half<SPLIT>(sm.a[s][0], sm.a[s][SM::NP - 1], row, half, gi, gi < J, kb, gp, g);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
       }
+      if ((kb % CHUNK) == CHUNK - 1 && kb / CHUNK >= 1) fold(folded++);
     }
-    mbar_wait(&sm.tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    while (folded < num_chunks) fold(folded++);
     const int64_t i = (int64_t)m_blk * BLOCK_M + quarter * 32 + lane;
     const bool row_ok = i < J;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BLOCK_N; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, r);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const int64_t f = (int64_t)n_blk * BLOCK_N + c0 + c;
-        if (f >= F) break;
-        const float v = alpha * __uint_as_float(r[c]);
-        if (z && row_ok) z[f * J + i] = v;
-        if (keys) {
-          unsigned long long k = row_ok ? make_key(v, (uint32_t)i) : 0ull;
-          k = warp_key_max(k);
-          if (lane == 0 && k) atomicMax(keys + f, k);
-        }
+    for (int c = 0; c < 128; ++c) {
+      const int64_t f = (int64_t)n_blk * BN + chalf * 128 + c;
+      if (f >= F) break;
+      const float v = alpha * sum[c];
+      if (z && row_ok) z[f * J + i] = v;
+      if (keys) {
+        unsigned long long k = row_ok ? make_key(v, (uint32_t)i) : 0ull;
+        k = warp_key_max(k);
+        if (lane == 0 && k) atomicMax(keys + f, k);
       }
     }
   }
@@ -337,8 +398,7 @@ conv_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(BLOCK_N < 32 ? 32 : BLOCK_N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
 }
 
@@ -370,39 +430,13 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
   cuuint32_t box[2] = {(cuuint32_t)BLOCK_K, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  static const int tma_tf32 = [] {
-    const char* e = getenv("SRPGPU_TMA_TF32");
-    return e && e[0] == '1';
-  }();
-  CUresult r = enc(map, tma_tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("srp_map_tc: cuTensorMapEncodeTiled failed (%d)", (int)r);
     return SRPGPU_ERR_LAUNCH;
   }
-  return SRPGPU_OK;
-}
-
-template <int BLOCK_N, bool GEN_A>
-static int launch(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, const float* h2, int64_t h2_ld,
-                  int64_t J, float* z, uint64_t* keys, cudaStream_t st, const GenParams& gp) {
-  CUtensorMap ma, mb;
-  int s = make_map(&mb, gcc, F, Kd, gcc_ld, BLOCK_N);
-  if (s) return s;
-  if (GEN_A) ma = mb;
-  else if ((s = make_map(&ma, h2, J, Kd, h2_ld, BLOCK_M))) return s;
-  const size_t smem = sizeof(Smem<BLOCK_N>) + 1024;
-  auto kern = conv_tf32_kernel<BLOCK_N, GEN_A>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-    set_error("srp_map_tc: cannot reserve %zu B shared memory", smem);
-    return SRPGPU_ERR_LAUNCH;
-  }
-  const int64_t tiles = ((J + BLOCK_M - 1) / BLOCK_M) * ((F + BLOCK_N - 1) / BLOCK_N);
-  SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "srp_map_tc: too many tiles");
-  kern<<<(unsigned)tiles, kThreads, smem, st>>>(ma, mb, J, F, Kd, z,
-                                                 reinterpret_cast<unsigned long long*>(keys), 2.0f, gp);
-  SRPGPU_CHECK_LAUNCH("srp_map_tc");
   return SRPGPU_OK;
 }
 
@@ -417,6 +451,59 @@ __global__ void round_tf32_kernel(const float* __restrict__ src, int64_t ld_src,
     if (c < cols) v = tf32_rne(__ldg(src + r * ld_src + c));
     dst[r * ld_dst + c] = v;
   }
+}
+
+// hi = tf32_rne(x), lo = tf32_rne(x - hi) into two planes (3xTF32 operands)
+__global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld_src, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t ld_dst, int64_t cols) {
+  const int64_t r = blockIdx.y;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ld_dst;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float h = 0.f, l = 0.f;
+    if (c < cols) {
+      const float v = __ldg(src + r * ld_src + c);
+      h = tf32_rne(v);
+      l = tf32_rne(v - h);
+    }
+    hi[r * ld_dst + c] = h;
+    lo[r * ld_dst + c] = l;
+  }
+}
+
+template <bool SPLIT, bool GEN = true>
+static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, int64_t J, float* z,
+                          uint64_t* keys, cudaStream_t st, const GenParams& gp, const float* h2 = nullptr,
+                          int64_t h2_ld = 0) {
+  CUtensorMap mb, mb2, ma;
+  int s = make_map(&mb, gcc, F, Kd, gcc_ld, 256);
+  if (s) return s;
+  mb2 = mb;
+  ma = mb;
+  if (SPLIT && (s = make_map(&mb2, gcc + F * gcc_ld, F, Kd, gcc_ld, 256))) return s;
+  if (!GEN && (s = make_map(&ma, h2, J, Kd, h2_ld, BLOCK_M))) return s;
+  const size_t smem = sizeof(SmemC<SPLIT>) + 1024;
+  auto kern = conv_gen_chunked_kernel<SPLIT, GEN>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    set_error("srp_map_tdoa: cannot reserve %zu B shared memory", smem);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  const int64_t tiles = ((J + BLOCK_M - 1) / BLOCK_M) * ((F + 255) / 256);
+  SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "srp_map_tdoa: too many tiles");
+  kern<<<(unsigned)tiles, kThreadsC, smem, st>>>(mb, mb2, ma, J, F, Kd, z,
+                                                  reinterpret_cast<unsigned long long*>(keys), 2.0f, gp);
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, kern);
+      set_error("srp_map_tdoa: launch failed: %s (regs %d, max threads %d, static smem %zu, local %zu, "
+                "dynamic smem %zu)", cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock,
+                fa.sharedSizeBytes, fa.localSizeBytes, smem);
+      return SRPGPU_ERR_LAUNCH;
+    }
+    count_launch();
+  }
+  return SRPGPU_OK;
 }
 
 }  // namespace tc
@@ -445,6 +532,20 @@ extern "C" int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, i
   return SRPGPU_OK;
 }
 
+extern "C" int srpgpu_split_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,
+                                 int64_t cols, srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(ld_dst >= cols && ld_src >= cols && rows >= 0, SRPGPU_ERR_DIMENSION,
+                   "split_tf32: bad pitches");
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((ld_dst + 255) / 256, 64), (unsigned)nr);
+    tc::split_tf32_kernel<<<grid, 256, 0, as_stream(stream)>>>(src + r0 * ld_src, ld_src, dst + r0 * ld_dst,
+                                                                dst + (rows + r0) * ld_dst, ld_dst, cols);
+    SRPGPU_CHECK_LAUNCH("split_tf32");
+  }
+  return SRPGPU_OK;
+}
+
 extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
                                  const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,
                                  uint64_t* keys, srpgpu_stream_t stream) {
@@ -461,14 +562,15 @@ extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_f
   const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
   const int64_t n256 = (num_frames + 255) / 256;
   const tc::GenParams gp = {};
-  if (m_tiles * n256 >= 2 * (int64_t)num_sms())
-    return tc::launch<256, false>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st, gp);
-  return tc::launch<128, false>(gcc, gcc_ld, num_frames, Kd, h2, h2_ld, num_candidates, z, keys, st, gp);
+  (void)m_tiles; (void)n256;
+  // chunked TMEM accumulation folded into fp32 registers (see conv_gen_chunked_kernel)
+  return tc::launch_chunked<false, false>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp, h2,
+                                          h2_ld);
 }
 
 extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t num_pairs,
-                                   int32_t half_len, const float* xtab, int64_t num_candidates, float* z,
-                                   uint64_t* keys, srpgpu_stream_t stream) {
+                                   int32_t half_len, const float* xtab, int64_t num_candidates,
+                                   int32_t split, float* z, uint64_t* keys, srpgpu_stream_t stream) {
   const int32_t bins = half_len - 1;
   const int32_t Kd = 2 * num_pairs * bins;
   SRPGPU_CHECK_ARG(num_pairs >= 1 && bins >= 1 && num_candidates >= 1, SRPGPU_ERR_DIMENSION,
@@ -483,7 +585,9 @@ extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num
   gp.xtab = xtab; gp.P = num_pairs; gp.B = bins; gp.inv_k = 1.0f / (float)half_len;
   const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
   const int64_t n256 = (num_frames + 255) / 256;
-  if (m_tiles * n256 >= 2 * (int64_t)num_sms())
-    return tc::launch<256, true>(gcc, gcc_ld, num_frames, Kd, nullptr, 0, num_candidates, z, keys, st, gp);
-  return tc::launch<128, true>(gcc, gcc_ld, num_frames, Kd, nullptr, 0, num_candidates, z, keys, st, gp);
+  (void)m_tiles; (void)n256;
+  // chunked TMEM accumulation folded into fp32 registers (bounded in-pipe accumulation)
+  if (split)   // 3xTF32: gcc holds the hi plane [F][gcc_ld] followed by the lo plane
+    return tc::launch_chunked<true>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp);
+  return tc::launch_chunked<false>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp);
 }

@@ -291,9 +291,12 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
     SRPGPU_CHECK_LAUNCH("sspi_map(rows)");
     return SRPGPU_OK;
   }
+  // whole tiles up to 160 KB stay resident (one bulk copy, reused by every frame tile); larger
+  // tiles are streamed in 40 KB record chunks so that 3+ CTAs stay resident per SM
   const int64_t cap = kRecBudget / (int64_t)sizeof(BandRec);
   (void)max_pair_records;
-  prm.rec_cap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(cap, max_tile_records));
+  prm.rec_cap = (int32_t)std::max<int64_t>(
+      1, max_tile_records <= cap ? max_tile_records : (40 * 1024) / (int64_t)sizeof(BandRec));
   const size_t smem = (size_t)kTileF * kWarps * 8 + (size_t)kTileF * (kTileI + 1) * 4 +
                       (size_t)prm.rec_cap * sizeof(BandRec);
   if (cudaFuncSetAttribute(sspi_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=

@@ -463,12 +463,14 @@ def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, ou
     if (gcc.num_pairs, gcc.num_bins) != (srp.num_pairs, srp.num_bins):
         raise DimensionError(f"cross-spectra for {gcc.num_pairs} pairs x {gcc.num_bins} bins do not "
                              f"match a {srp.num_pairs} x {srp.num_bins} transform")
-    if precision not in ("tf32", "fp32"):
+    if precision not in ("tf32", "fp32", "tf32x3"):
         raise ValueError(f"unknown precision {precision!r}")
+    if precision == "tf32x3" and hasattr(srp, "matrix"):
+        raise ValueError("3xTF32 is provided by the on-chip steering operator (steering_operator)")
     if not hasattr(srp, "matrix"):           # implicit operator: steering generated on chip
-        if precision != "tf32":
-            raise ValueError("the on-chip steering path is TF32; materialize() the operator for fp32")
-        return _srp_map_tdoa(srp, gcc, argmax, out_map)
+        if precision == "fp32":
+            raise ValueError("the on-chip steering path is TF32 / 3xTF32; materialize() it for fp32")
+        return _srp_map_tdoa(srp, gcc, argmax, out_map, split=(precision == "tf32x3"))
     n = srp.num_pairs * srp.num_bins
     h2 = steering_device(srp, tf32=(precision == "tf32"))
     j, ld = h2.shape
@@ -504,23 +506,35 @@ def _xtab_device(op) -> torch.Tensor:
         np.asarray(op.tdoa.delta_t, dtype=np.float64) * float(op.frame.sample_rate)))
 
 
-def _srp_map_tdoa(op, gcc, argmax: bool, out_map: bool):
+def _srp_map_tdoa(op, gcc, argmax: bool, out_map: bool, split: bool = False):
     n = op.num_pairs * op.num_bins
     ld = _pad4(2 * n)
     padded = getattr(gcc, "padded", None)
-    if getattr(gcc, "tf32_rounded", False) and padded is not None and padded.shape[1] == ld:
+    if split:                              # hi / lo TF32 planes of psi
+        if getattr(gcc, "tf32_rounded", False):
+            raise ValueError("tf32x3 needs unrounded cross-spectra (gcc_frames(..., tf32=False))")
+        if getattr(gcc, "split_planes", None) is not None:
+            vp, batched = gcc.split_planes, gcc.values.dim() == 2
+            f = vp.shape[0] // 2
+        else:
+            v, batched = _gcc_matrix(gcc, op.num_pairs, op.num_bins)
+            f = v.shape[0]
+            vp = torch.empty((2 * f, ld), dtype=torch.float32, device=v.device)
+            nat.call("srpgpu_split_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, f, 2 * n, dev.stream_ptr())
+    elif getattr(gcc, "tf32_rounded", False) and padded is not None and padded.shape[1] == ld:
         vp, batched = padded, gcc.values.dim() == 2
+        f = vp.shape[0]
     else:
         v, batched = _gcc_matrix(gcc, op.num_pairs, op.num_bins)
-        vp = torch.empty((v.shape[0], ld), dtype=torch.float32, device=v.device)
-        nat.call("srpgpu_round_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, v.shape[0], 2 * n,
-                 dev.stream_ptr())
-    f, j = vp.shape[0], op.num_candidates
+        f = v.shape[0]
+        vp = torch.empty((f, ld), dtype=torch.float32, device=v.device)
+        nat.call("srpgpu_round_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, f, 2 * n, dev.stream_ptr())
+    j = op.num_candidates
     xt = _xtab_device(op)
     z = torch.empty((f, j), dtype=torch.float32, device=vp.device) if out_map else None
     keys = _new_keys(f, argmax)
     nat.call("srpgpu_srp_map_tdoa", dev.ptr(vp), ld, f, op.num_pairs, op.num_bins + 1, dev.ptr(xt), j,
-             dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+             1 if split else 0, dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 

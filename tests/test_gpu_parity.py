@@ -324,5 +324,9 @@ def test_conventional_map_onchip_steering(golden_scene):
     gcc2 = s.FdGcc(torch.from_numpy(g["psi"].astype(np.complex64)).cuda(), pairs.num_pairs,
                    frame.num_bins, "phat")
     assert_map_close(s.srp_map_exact(op, gcc2), g["z_conv"])
+    err = assert_map_close(s.srp_map_exact(op, gcc2, precision="tf32x3"), g["z_conv"])
+    assert err.max() < 1e-5                      # split precision: fp32 class
     with pytest.raises(ValueError):
         s.srp_map_exact(op, gcc2, precision="fp32")
+    with pytest.raises(ValueError):
+        s.srp_map_exact(op, gcc, precision="tf32x3")   # pre-rounded psi cannot be split

@@ -140,11 +140,16 @@ def test_cfg3_conventional_tf32(cfg3):
 
 
 def test_cfg4_conventional_onchip_steering():
-    """cfg4's H (164 GB as fp32) is never stored: generated on chip; oracle on a row block."""
+    """cfg4's H (164 GB as fp32) is never stored: generated on chip; oracle on a row block.
+
+    3xTF32 (split-precision tensor-core GEMM) meets the 1e-4 bound; plain TF32 is
+    allowed at cfg4 by BASELINE.json "with error reported" and is only bounded loosely.
+    """
     wl = workloads.make("cfg4", num_frames=8)
     x = torch.from_numpy(wl.samples).cuda()
-    gcc = s.gcc_frames(x, wl.frame, wl.pairs, tf32=True)
-    z, idx = s.srp_map_exact(s.steering_operator(wl.tdoa, wl.frame), gcc, argmax=True)
+    op = s.steering_operator(wl.tdoa, wl.frame)
+    z, idx = s.srp_map_exact(op, s.gcc_frames(x, wl.frame, wl.pairs), precision="tf32x3", argmax=True)
+    z_tf32 = s.srp_map_exact(op, s.gcc_frames(x, wl.frame, wl.pairs, tf32=True))
     psi_ref = oracle_psi(wl, 2)
     # oracle rows: a 1/97 subsample plus each frame's peak neighbourhood, so that the
     # normalization max|z_ref| is the map's true maximum (the north-star metric)
@@ -157,6 +162,9 @@ def test_cfg4_conventional_onchip_steering():
     got = z[:2, rows].float().cpu().numpy()
     err = O.normalized_max_error(got, z_ref)
     assert err.max() <= TOL
+    err_tf32 = O.normalized_max_error(z_tf32[:2, rows].float().cpu().numpy(), z_ref)
+    print(f"cfg4 conventional: 3xTF32 error {err.max():.2e}, TF32 error {err_tf32.max():.2e}")
+    assert err_tf32.max() <= 2e-3
     # the peak itself: the GPU argmax is (one of) the oracle's maxima over the checked rows
     for f in range(2):
         j = int(np.searchsorted(rows, peaks[f]))
