@@ -397,7 +397,11 @@ int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const c
   if (disabled) return 1;
   // a warp per frame while there are fewer frames than resident warps (latency-bound),
   // two warps per frame for large batches (throughput-bound)
-  const bool small = wp.F <= (int64_t)num_sms() * 8;
+  static const int force = [] {
+    const char* e = getenv("SRPGPU_WPF");
+    return e ? atoi(e) : 0;
+  }();
+  const bool small = force ? force == 1 : wp.F <= (int64_t)num_sms() * 8;
   if (out == W_OUT_GCC) return small ? wf::by_len<W_OUT_GCC, 1>(wp, st, what) : wf::by_len<W_OUT_GCC, 2>(wp, st, what);
   if (out == W_OUT_XI) return small ? wf::by_len<W_OUT_XI, 1>(wp, st, what) : wf::by_len<W_OUT_XI, 2>(wp, st, what);
   return 1;

@@ -85,3 +85,76 @@ class MapPipeline:
                 samples = torch.from_numpy(np.ascontiguousarray(samples, dtype=np.float32))
             self.input.copy_(samples, non_blocking=True)
         return self.replay()
+
+
+class MapStream:
+    """Streamed batches: host samples in, per-frame argmax out, copies overlapped.
+
+    The batched counterpart of the reference's per-frame `cmd_map` loop
+    (cli.py:241-258).  `depth` MapPipeline slots (each its own input buffer,
+    graph and outputs) rotate; batch n's host->device copy runs on a copy
+    stream while batch n-1's chain runs on the compute stream, and the per-frame
+    argmax of each batch is read back into pinned host memory.  `after_batch`
+    (e.g. an NCCL gather of argmax keys) is enqueued on the compute stream after
+    each chain.
+    """
+
+    def __init__(self, variant: str, op, frame, pairs, spec=None, frames: int = 1, depth: int = 2,
+                 after_batch=None, **kw):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.slots = [MapPipeline(variant, op, frame, pairs, spec, frames=frames, **kw)
+                      for _ in range(depth)]
+        self.copy_stream = torch.cuda.Stream()
+        self.compute_stream = torch.cuda.Stream()
+        self.after_batch = after_batch
+        self.frames = int(frames)
+        self._out = [torch.empty(self.frames, dtype=torch.int64).pin_memory() for _ in range(depth)]
+        self._free = [torch.cuda.Event() for _ in range(depth)]     # slot's chain has consumed its input
+        self._done = [torch.cuda.Event() for _ in range(depth)]     # slot's argmax is on the host
+        self._used = [False] * depth
+        self._count = 0
+
+    @property
+    def input_shape(self):
+        return tuple(self.slots[0].input.shape)
+
+    def submit(self, samples) -> int:
+        """Enqueue one batch of (M, n) samples (pinned host tensor for async copies)."""
+        k = self._count % len(self.slots)
+        slot = self.slots[k]
+        if isinstance(samples, np.ndarray):
+            samples = torch.from_numpy(np.ascontiguousarray(samples, dtype=np.float32))
+        if tuple(samples.shape) != self.input_shape:
+            raise ValueError(f"batch shape {tuple(samples.shape)} != {self.input_shape}")
+        if self._used[k]:
+            self._done[k].synchronize()    # the host may still be reading this slot's output
+        cur = torch.cuda.current_stream()
+        self.copy_stream.wait_stream(cur)
+        with torch.cuda.stream(self.copy_stream):
+            if self._used[k]:
+                self.copy_stream.wait_event(self._free[k])
+            slot.input.copy_(samples, non_blocking=True)
+        self.compute_stream.wait_stream(self.copy_stream)
+        with torch.cuda.stream(self.compute_stream):
+            z, idx = slot.replay()
+            self._free[k].record()
+            if self.after_batch is not None:
+                self.after_batch(idx)
+            self._out[k].copy_(idx, non_blocking=True)
+            self._done[k].record()
+        self._used[k] = True
+        self._count += 1
+        return self._count - 1
+
+    def result(self, ticket: int) -> np.ndarray:
+        """Per-frame argmax of batch `ticket` (waits for it; valid until the slot is reused)."""
+        if ticket < self._count - len(self.slots) or ticket >= self._count:
+            raise ValueError(f"batch {ticket} is no longer (or not yet) held")
+        k = ticket % len(self.slots)
+        self._done[k].synchronize()
+        return self._out[k].numpy().copy()
+
+    def join(self):
+        """Make the caller's current stream wait for every submitted batch."""
+        torch.cuda.current_stream().wait_stream(self.compute_stream)

@@ -311,6 +311,40 @@ def test_pipeline_graph_matches_eager(golden_scene):
     assert_argmax_agrees(ic, g["z_conv"])
 
 
+def test_map_stream_matches_pipeline(golden_scene):
+    """Streamed batches (overlapped copies, rotating slots) give the pipeline's argmax."""
+    from paper_2306_08514_b200.pipeline import MapPipeline, MapStream
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = 4
+    n = (F - 1) * frame.hop + frame.frame_len
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    total = g["samples"].shape[1]
+    starts = [0, frame.hop, 2 * frame.hop, 5 * frame.hop, frame.hop]
+    starts = [st for st in starts if st + n <= total]
+    batches = [torch.from_numpy(np.ascontiguousarray(g["samples"][:, st:st + n], dtype=np.float32))
+               .pin_memory() for st in starts]
+    ref = MapPipeline("sspi", sp, frame, pairs, spec, frames=F)
+    want = [ref.run(b)[1].cpu().numpy() for b in batches]
+    stream = MapStream("sspi", sp, frame, pairs, spec, frames=F, depth=2)
+    got = []
+    for t, b in enumerate(batches):
+        assert stream.submit(b) == t
+        if t > 0:
+            got.append(stream.result(t - 1))      # previous batch, while batch t is in flight
+    got.append(stream.result(len(batches) - 1))
+    for t in range(len(batches)):
+        assert np.array_equal(got[t], want[t])
+    with pytest.raises(ValueError):
+        stream.submit(batches[0][:, :-1])
+    with pytest.raises(ValueError):
+        stream.result(len(batches))               # not submitted yet
+    for t in range(2):                            # rotate both slots past batch 0
+        stream.submit(batches[0])
+    with pytest.raises(ValueError):
+        stream.result(0)                          # slot already reused
+
+
 def test_conventional_map_onchip_steering(golden_scene):
     """H generated on chip from the TDOA table (no stored operator) matches the reference map."""
     _, g = golden_scene

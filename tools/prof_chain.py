@@ -29,7 +29,12 @@ def main():
     wl = workloads.make(a.workload, num_frames=frames)
     x = torch.from_numpy(wl.samples).cuda()
     rng = range(frames)
-    if a.variant in ("sspi", "slri", "si"):
+    if a.variant == "sspi" and a.workload == "cfg4":     # dense Lambda infeasible: fixed nnz per (i, p)
+        op = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
+        for _ in range(a.reps):
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng)
+            z, idx = s.sspi_map(op, xi, argmax=True)
+    elif a.variant in ("sspi", "slri", "si"):
         interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
         if a.variant == "sspi":
             op = s.truncate_sparse(interp, s.resolve_sparsity(a.nnz, wl.grid.num_points,
@@ -42,12 +47,17 @@ def main():
         for _ in range(a.reps):
             xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng)
             z, idx = fn(op, xi, argmax=True)
-    else:
-        srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 36)
-        op = srp if a.variant == "conv" else s.truncate_srp_matrix(srp, a.rank)
+    elif a.variant == "conv":          # on-chip steering (bench variant "conv")
+        op = s.steering_operator(wl.tdoa, wl.frame)
         for _ in range(a.reps):
-            g = s.gcc_frames(x, wl.frame, wl.pairs, rng, tf32=(a.variant == "conv"))
-            z, idx = (s.srp_map_exact if a.variant == "conv" else s.lr_map)(op, g, argmax=True)
+            g = s.gcc_frames(x, wl.frame, wl.pairs, rng, tf32=True)
+            z, idx = s.srp_map_exact(op, g, argmax=True)
+    else:                              # stored operator: conv_h (SrpMatrix) or lr
+        srp = s.build_srp_matrix(wl.tdoa, wl.frame, max_bytes=1 << 36)
+        op = srp if a.variant == "conv_h" else s.truncate_srp_matrix(srp, a.rank)
+        for _ in range(a.reps):
+            g = s.gcc_frames(x, wl.frame, wl.pairs, rng, tf32=(a.variant == "conv_h"))
+            z, idx = (s.srp_map_exact if a.variant == "conv_h" else s.lr_map)(op, g, argmax=True)
     torch.cuda.synchronize()
     print("ok", a.workload, a.variant, frames, int(idx[0]))
 
