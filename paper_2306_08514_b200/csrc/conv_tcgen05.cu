@@ -15,6 +15,7 @@
 // per-frame argmax (packed keys, atomicMax).  Tiles are rasterised in groups of
 // GROUP_M candidate tiles so concurrently running CTAs share k-slices in L2.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -113,28 +114,44 @@ struct GenParams {
   int32_t P;
   int32_t B;           // bins per pair (K - 1)
   float inv_k;         // 1 / K
+  int32_t dbg;         // DIAGNOSTIC (temporary): 1 skip generation, 2 skip B loads
 };
 
-// round to nearest TF32 in one instruction (ties away from zero; the phasors never tie in
-// practice, and rounding-to-nearest keeps the product unbiased unlike plain truncation)
+// Round a finite fp32 value to nearest TF32, ties away from zero (= cvt.rna.tf32.f32,
+// which sm_100a emulates in ~5 instructions): add half a TF32 ulp to the magnitude bits
+// (sign-magnitude format: the carry rounds |x| up and propagates into the exponent) and
+// clear the 13 dropped bits.  The phasors are bounded by 1, so no overflow to inf.
+// Rounding to nearest keeps the product unbiased, unlike the tensor core's truncation.
 __device__ __forceinline__ uint32_t cvt_tf32(float x) {
-  uint32_t u;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-  return u & 0xFFFFE000u;   // the low 13 bits of the result are not guaranteed to be zero
+  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
 }
 
-// Per-row generator state carried across k-blocks (one thread per operand row).
+// the same rounding for an MMA operand only: kind::tf32 ignores the low 13 bits, so the
+// mask is not needed (one instruction)
+__device__ __forceinline__ uint32_t cvt_tf32_op(float x) { return __float_as_uint(x) + 0x1000u; }
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+// Per-thread generator state carried across k-blocks: the (pair, bin) position of the
+// thread's first bin in the current block is advanced incrementally (no integer
+// division in the loop), and the phasor rotation of the current pair is carried.
 struct GenState {
-  int pair;          // pair of the carried rotation (-1: none)
-  int next_k;        // bin whose phasor `seed` holds
+  int p;             // pair of the first bin of this thread's 8 in the current k-block
+  int k;             // its bin (1-based, <= B)
+  int seeded_p;      // pair of the carried rotation (-1: none)
   int since;         // blocks since the last exact seed
-  float2 seed, s1, s2, s4, s8;   // exp(j pi k x / K) at next_k, and step powers
+  float2 seed, s1, s2, s4, s16;  // exp(j pi k x / K) at bin k of pair p, and step powers
   float x;
 };
 
-__device__ __forceinline__ void gen_state_init(GenState& g) {
-  g.pair = -1; g.next_k = 0; g.since = 0; g.x = 0.f;
-  g.seed = g.s1 = g.s2 = g.s4 = g.s8 = make_float2(1.f, 0.f);
+__device__ __forceinline__ void gen_state_init(GenState& g, int c0, int B) {
+  g.p = c0 / B;
+  g.k = c0 - g.p * B + 1;
+  g.seeded_p = -1; g.since = 0; g.x = 0.f;
+  g.seed = g.s1 = g.s2 = g.s4 = g.s16 = make_float2(1.f, 0.f);
 }
 
 // The GEMM kernel (128 candidates x 256 frames per CTA).  The tensor core's in-pipe
@@ -143,12 +160,23 @@ __device__ __forceinline__ void gen_state_init(GenState& g) {
 // k-blocks accumulated in two alternating 256-column TMEM tiles (all 512 columns);
 // while the MMA fills one, eight folding warps tcgen05.ld the other and add it into
 // fp32 running sums held in registers.  With SPLIT the three 3xTF32 products go to the
-// same chunk tile.  Roles (10 warps): 0 TMA (psi, and A when GEN = false), 1 TMEM
-// alloc + MMA issue, 2..9 steering generators (two threads per operand row, 8 bins
-// each) and folders: warp w owns TMEM lane quarter w % 4 and column half (w - 2) / 4,
-// 128 running sums per thread.
+// same chunk tile.  Roles (20 warps): warpgroup 0 = control (warp 0 TMA of psi, and
+// of A when GEN = false; warp 1 TMEM alloc + MMA issue), shrunk to kCtlRegs registers;
+// warps 4..19 = steering generators (four threads per operand row, 4 bins each) and
+// folders: warp w owns TMEM lane quarter w % 4 and column quarter (w - 4) / 4, 64
+// running sums per thread, grown to kWorkerRegs registers.  Sixteen worker warps hide
+// the generator's per-block latency (it is a serial wait/generate/fence/arrive chain
+// per warp) far better than eight warps holding 128 sums each.
 constexpr int CHUNK = 16;
-constexpr int kThreadsC = 320;
+constexpr int kCtl = 4;                            // control warpgroup: 0 TMA, 1 MMA, 2-3 idle
+constexpr int kWorkers = 16;                       // generator + fold warps (4 warpgroups)
+constexpr int kThreadsC = 32 * (kCtl + kWorkers);
+// setmaxnreg redistributes the CTA's own pool (launch: 640 threads x 96 registers):
+// 4 warps x 32 + 16 warps x 112 = 61440 registers exactly (inc blocks if over)
+constexpr int kCtlRegs = 32, kWorkerRegs = 112;
+static_assert(32 * (kCtl * kCtlRegs + kWorkers * kWorkerRegs) <= kThreadsC * 96, "register pool");
+constexpr int kNB = 16 * BLOCK_M / (32 * kWorkers); // bins per generator thread per k-block
+constexpr int kFoldCols = 256 / (kWorkers / 4);     // accumulator columns per fold thread
 
 template <bool SPLIT>
 struct __align__(1024) SmemC {
@@ -176,71 +204,84 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
-// 8 bins [8 half, 8 half + 8) of k-block kb for one operand row (fast path: product tree
-// from a carried seed; re-seeded exactly every 4 blocks and at pair changes)
+// NB bins [NB part, NB part + NB) of the current k-block for one operand row.  The row
+// holds the conjugate phasors exp(-j pi k x / K) as (re, im) = (cos, -sin) pairs.  Fast
+// path: product tree from a carried seed, re-seeded exactly every kReseed blocks and at
+// pair changes; a block straddling a pair boundary (or past the last pair) takes the
+// compact per-bin path.  Advances g.
+constexpr int kReseed = 8;
+
 template <bool SPLIT>
-__device__ __forceinline__ void gen_a_half(float* a_stage, float* a_lo, int row, int half, int64_t i,
-                                           bool valid, int kb, const GenParams& gp, GenState& g) {
-  const int total = gp.P * gp.B;
-  const int c0 = kb * 16 + 8 * half;
-  float2 e[8];
-  const int p0 = c0 / gp.B, p1 = (c0 + 7) / gp.B;
-  if (valid && p0 == p1 && c0 + 7 < total) {
-    const int k0 = c0 - p0 * gp.B + 1;
-    if (g.pair != p0 || g.next_k != k0 || g.since >= 4) {
-      if (g.pair != p0) {
-        g.pair = p0;
-        g.x = __ldg(gp.xtab + i * gp.P + p0);
+__device__ __forceinline__ void store4(uint32_t hi_addr, uint32_t lo_addr, float v0, float v1, float v2, float v3) {
+  if (SPLIT) {
+    const uint32_t h0 = cvt_tf32(v0), h1 = cvt_tf32(v1), h2 = cvt_tf32(v2), h3 = cvt_tf32(v3);
+    sts128(hi_addr, h0, h1, h2, h3);
+    sts128(lo_addr, cvt_tf32_op(v0 - __uint_as_float(h0)), cvt_tf32_op(v1 - __uint_as_float(h1)),
+           cvt_tf32_op(v2 - __uint_as_float(h2)), cvt_tf32_op(v3 - __uint_as_float(h3)));
+  } else {
+    sts128(hi_addr, cvt_tf32_op(v0), cvt_tf32_op(v1), cvt_tf32_op(v2), cvt_tf32_op(v3));
+  }
+}
+
+template <bool SPLIT, int NB>
+__device__ __forceinline__ void gen_a_part(uint32_t a_stage, uint32_t a_lo, int row, int part, int64_t i,
+                                           bool valid, const GenParams& gp, GenState& g) {
+  static_assert(NB == 4 || NB == 8, "bins per thread");
+  const uint32_t rowp = a_stage + row * 128, rowl = a_lo + row * 128;
+  if (valid && g.p < gp.P && g.k + NB - 1 <= gp.B) {
+    if (g.seeded_p != g.p || g.since >= kReseed) {
+      if (g.seeded_p != g.p) {
+        g.seeded_p = g.p;
+        g.x = __ldg(gp.xtab + i * gp.P + g.p);
         float sn, cs;
         sincospif(g.x * gp.inv_k, &sn, &cs);
-        g.s1 = make_float2(cs, sn);
+        g.s1 = make_float2(cs, -sn);
         g.s2 = cmul(g.s1, g.s1);
         g.s4 = cmul(g.s2, g.s2);
-        g.s8 = cmul(cmul(g.s4, g.s4), cmul(g.s4, g.s4));   // step to the next block: s^16
+        const float2 s8 = cmul(g.s4, g.s4);
+        g.s16 = cmul(s8, s8);                          // step to the next block
       }
       float sn, cs;
-      sincospif((float)k0 * g.x * gp.inv_k, &sn, &cs);
-      g.seed = make_float2(cs, sn);
+      sincospif((float)g.k * g.x * gp.inv_k, &sn, &cs);
+      g.seed = make_float2(cs, -sn);
       g.since = 0;
     }
+    float2 e[NB];
     e[0] = g.seed;
     e[1] = cmul(e[0], g.s1);
     e[2] = cmul(e[0], g.s2);
     e[3] = cmul(e[1], g.s2);
+    if (NB == 8) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) e[4 + j] = cmul(e[j], g.s4);
-    g.seed = cmul(e[0], g.s8);
-    g.next_k = k0 + 16;
-    g.since += 1;
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = c0 + j;
-      e[j] = make_float2(0.f, 0.f);
-      if (valid && c < total) {
-        const int pc = c / gp.B;
-        const int k = c - pc * gp.B + 1;
-        const float x = __ldg(gp.xtab + i * gp.P + pc);
-        float sn, cs;
-        sincospif((float)k * x * gp.inv_k, &sn, &cs);
-        e[j] = make_float2(cs, sn);
-      }
+      for (int j = 0; j < 4; ++j) e[4 + j] = cmul(e[j], g.s4);
     }
-    g.pair = -1;
-  }
-  unsigned char* rowp = reinterpret_cast<unsigned char*>(a_stage) + row * 128;
-  unsigned char* rowl = reinterpret_cast<unsigned char*>(a_lo) + row * 128;
+    g.seed = cmul(e[0], g.s16);
+    g.since += 1;
 #pragma unroll
-  for (int qq = 0; qq < 4; ++qq) {
-    const int q = 4 * half + qq;
-    const float v0 = e[2 * qq].x, v1 = -e[2 * qq].y, v2 = e[2 * qq + 1].x, v3 = -e[2 * qq + 1].y;
-    const uint4 hi = make_uint4(cvt_tf32(v0), cvt_tf32(v1), cvt_tf32(v2), cvt_tf32(v3));
-    *reinterpret_cast<uint4*>(rowp + ((q ^ (row & 7)) << 4)) = hi;
-    if (SPLIT)
-      *reinterpret_cast<uint4*>(rowl + ((q ^ (row & 7)) << 4)) =
-          make_uint4(cvt_tf32(v0 - __uint_as_float(hi.x)), cvt_tf32(v1 - __uint_as_float(hi.y)),
-                     cvt_tf32(v2 - __uint_as_float(hi.z)), cvt_tf32(v3 - __uint_as_float(hi.w)));
+    for (int qq = 0; qq < NB / 2; ++qq) {
+      const uint32_t off = (uint32_t)((((NB / 2) * part + qq) ^ (row & 7)) << 4);
+      store4<SPLIT>(rowp + off, rowl + off, e[2 * qq].x, e[2 * qq].y, e[2 * qq + 1].x, e[2 * qq + 1].y);
+    }
+  } else {
+    int pp = g.p, kk = g.k;
+#pragma unroll 1
+    for (int j = 0; j < NB; j += 2) {
+      float v[4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float sn = 0.f, cs = 0.f;
+        if (valid && pp < gp.P) sincospif((float)kk * __ldg(gp.xtab + i * gp.P + pp) * gp.inv_k, &sn, &cs);
+        v[2 * h] = cs;
+        v[2 * h + 1] = -sn;
+        if (++kk > gp.B) { kk = 1; ++pp; }
+      }
+      const uint32_t off = (uint32_t)((((NB / 2) * part + j / 2) ^ (row & 7)) << 4);
+      store4<SPLIT>(rowp + off, rowl + off, v[0], v[1], v[2], v[3]);
+    }
+    g.seeded_p = -1;
   }
+  g.k += 16;
+  while (g.k > gp.B) { g.k -= gp.B; ++g.p; }
 }
 
 // GEN = false: the steering operand is streamed by TMA from a stored matrix instead
@@ -273,12 +314,12 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
     if (SPLIT) prefetch_tmap(&map_b2);
     if (!GEN) prefetch_tmap(&map_a);
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&sm.full[s], GEN ? 1 + 256 : 1);
+      mbar_init(&sm.full[s], GEN ? 1 + kWorkers : 1);   // TMA + one arrive per generator warp
       mbar_init(&sm.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.tfull[b], 1);
-      mbar_init(&sm.tempty[b], 8);   // one arrive per folding warp
+      mbar_init(&sm.tempty[b], kWorkers);   // one arrive per folding warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -293,13 +334,26 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
+  // each role runs to its own exit (no code is shared after the register split):
+  // tcgen05 fence + named barrier over the whole CTA, then warp 1 frees TMEM
+  auto end_sync = [] {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();                                   // reconverge before the aligned barrier
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreadsC) : "memory");
+  };
+  if (warp < kCtl) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
+    if (warp == 0) {
     if (lane == 0) {
       constexpr uint32_t kBytes = (BN * SM::NP + (GEN ? 0 : BLOCK_M)) * BLOCK_K * sizeof(float);
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % NS;
         const uint32_t round = kb / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
+        if (GEN && (gp.dbg & 2)) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+          continue;
+        }
         mbar_expect_tx(&sm.full[s], kBytes);
         if (!GEN) tma_load_2d(sm.a[s][0], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
         tma_load_2d(sm.b[s][0], &map_b, &sm.full[s], kb * BLOCK_K, n_blk * BN);
@@ -339,24 +393,33 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
         if ((kb % CHUNK) == CHUNK - 1 || kb == num_kb - 1) mma_commit(&sm.tfull[b]);
       }
     }
-  } else {
-    const int t = threadIdx.x - 64;            // 0..255
-    const int row = t & 127, half = t >> 7;
+    }
+    end_sync();
+    if (warp == 1) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWorkerRegs));
+  {
+    const int t = threadIdx.x - 32 * kCtl;     // 0 .. 32 kWorkers - 1
+    const int row = t & (BLOCK_M - 1), part = t / BLOCK_M;
     const int64_t gi = (int64_t)m_blk * BLOCK_M + row;
-    // fold ownership: TMEM lane quarter (warp % 4) x column half ((warp - 2) / 4)
-    const int quarter = warp & 3, chalf = (warp - 2) >> 2;
+    // fold ownership: TMEM lane quarter (warp % 4) x column slice ((warp - 2) / 4)
+    const int quarter = warp & 3, cslice = (warp - kCtl) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    float sum[128];
+    float sum[kFoldCols];
 #pragma unroll
-    for (int c = 0; c < 128; ++c) sum[c] = 0.f;
+    for (int c = 0; c < kFoldCols; ++c) sum[c] = 0.f;
     auto fold = [&](int chunk) {
       const int b = chunk & 1;
       mbar_wait(&sm.tfull[b], (chunk >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 0; c0 < kFoldCols; c0 += 32) {
         uint32_t r[32];
-        tmem_ld32(lane_base + (uint32_t)(b * BN + chalf * 128 + c0), r);
+        tmem_ld32(lane_base + (uint32_t)(b * BN + cslice * kFoldCols + c0), r);
 #pragma unroll
         for (int c = 0; c < 32; ++c) sum[c0 + c] += __uint_as_float(r[c]);
       }
@@ -365,25 +428,40 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.tempty[b])) : "memory");
     };
     GenState g;
-    gen_state_init(g);
+    gen_state_init(g, kNB * part, gp.B > 0 ? gp.B : 1);
     int folded = 0;
-    for (int kb = 0; kb < num_kb; ++kb) {
+    // two k-blocks per synchronisation round: the generator is latency-bound per round
+    // (wait, generate, fence, arrive), so pairing blocks halves the rounds
+    static_assert(CHUNK % 2 == 0 && SM::NS % 2 == 0, "k-block pairs must not straddle chunks/rings");
+    for (int kb = 0; kb < num_kb; kb += 2) {
+      const bool two = kb + 1 < num_kb;
       if (GEN) {
         const int s = kb % NS;
         const uint32_t round = kb / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
-        gen_a_half<SPLIT>(sm.a[s][0], sm.a[s][SM::NP - 1], row, half, gi, gi < J, kb, gp, g);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+        if (two) mbar_wait(&sm.empty[s + 1], (round & 1) ^ 1);
+        if (!(gp.dbg & 1)) {
+#pragma unroll 1
+          for (int u = 0; u < (two ? 2 : 1); ++u)
+            gen_a_part<SPLIT, kNB>(smem_u32(sm.a[s + u][0]), smem_u32(sm.a[s + u][SM::NP - 1]), row, part, gi,
+                                   gi < J, gp, g);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // own writes -> async proxy
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+          if (two)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s + 1])) : "memory");
+        }
       }
-      if ((kb % CHUNK) == CHUNK - 1 && kb / CHUNK >= 1) fold(folded++);
+      if (two && ((kb + 1) % CHUNK) == CHUNK - 1 && (kb + 1) / CHUNK >= 1) fold(folded++);
     }
     while (folded < num_chunks) fold(folded++);
     const int64_t i = (int64_t)m_blk * BLOCK_M + quarter * 32 + lane;
     const bool row_ok = i < J;
 #pragma unroll
-    for (int c = 0; c < 128; ++c) {
-      const int64_t f = (int64_t)n_blk * BN + chalf * 128 + c;
+    for (int c = 0; c < kFoldCols; ++c) {
+      const int64_t f = (int64_t)n_blk * BN + cslice * kFoldCols + c;
       if (f >= F) break;
       const float v = alpha * sum[c];
       if (z && row_ok) z[f * J + i] = v;
@@ -394,12 +472,7 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
-  }
+  end_sync();
 }
 
 // ---- host: TMA descriptors through the driver entry point (no -lcuda) ----
@@ -583,6 +656,7 @@ extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num
   if (num_frames <= 0) return SRPGPU_OK;
   tc::GenParams gp;
   gp.xtab = xtab; gp.P = num_pairs; gp.B = bins; gp.inv_k = 1.0f / (float)half_len;
+  { const char* e = getenv("SRPGPU_CONV_DBG"); gp.dbg = e ? atoi(e) : 0; }
   const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
   const int64_t n256 = (num_frames + 255) / 256;
   (void)m_tiles; (void)n256;
