@@ -40,6 +40,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -224,11 +234,10 @@ __device__ __forceinline__ void store4(uint32_t hi_addr, uint32_t lo_addr, float
 }
 
 template <bool SPLIT, int NB>
-__device__ __forceinline__ void gen_a_part(uint32_t a_stage, uint32_t a_lo, int row, int part, int64_t i,
-                                           bool valid, const GenParams& gp, GenState& g) {
+__device__ __forceinline__ void gen_a_part(uint32_t rowp, uint32_t rowl, const uint32_t (&off)[NB / 2], int qbase,
+                                           int rx, int64_t i, const GenParams& gp, GenState& g) {
   static_assert(NB == 4 || NB == 8, "bins per thread");
-  const uint32_t rowp = a_stage + row * 128, rowl = a_lo + row * 128;
-  if (valid && g.p < gp.P && g.k + NB - 1 <= gp.B) {
+  if (g.p < gp.P && g.k + NB - 1 <= gp.B) {
     if (g.seeded_p != g.p || g.since >= kReseed) {
       if (g.seeded_p != g.p) {
         g.seeded_p = g.p;
@@ -258,10 +267,8 @@ __device__ __forceinline__ void gen_a_part(uint32_t a_stage, uint32_t a_lo, int 
     g.seed = cmul(e[0], g.s16);
     g.since += 1;
 #pragma unroll
-    for (int qq = 0; qq < NB / 2; ++qq) {
-      const uint32_t off = (uint32_t)((((NB / 2) * part + qq) ^ (row & 7)) << 4);
-      store4<SPLIT>(rowp + off, rowl + off, e[2 * qq].x, e[2 * qq].y, e[2 * qq + 1].x, e[2 * qq + 1].y);
-    }
+    for (int qq = 0; qq < NB / 2; ++qq)
+      store4<SPLIT>(rowp + off[qq], rowl + off[qq], e[2 * qq].x, e[2 * qq].y, e[2 * qq + 1].x, e[2 * qq + 1].y);
   } else {
     int pp = g.p, kk = g.k;
 #pragma unroll 1
@@ -270,18 +277,18 @@ __device__ __forceinline__ void gen_a_part(uint32_t a_stage, uint32_t a_lo, int 
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float sn = 0.f, cs = 0.f;
-        if (valid && pp < gp.P) sincospif((float)kk * __ldg(gp.xtab + i * gp.P + pp) * gp.inv_k, &sn, &cs);
+        if (pp < gp.P) sincospif((float)kk * __ldg(gp.xtab + i * gp.P + pp) * gp.inv_k, &sn, &cs);
         v[2 * h] = cs;
         v[2 * h + 1] = -sn;
         if (++kk > gp.B) { kk = 1; ++pp; }
       }
-      const uint32_t off = (uint32_t)((((NB / 2) * part + j / 2) ^ (row & 7)) << 4);
-      store4<SPLIT>(rowp + off, rowl + off, v[0], v[1], v[2], v[3]);
+      const uint32_t o = (uint32_t)(((qbase + j / 2) ^ rx) << 4);
+      store4<SPLIT>(rowp + o, rowl + o, v[0], v[1], v[2], v[3]);
     }
     g.seeded_p = -1;
   }
-  g.k += 16;
-  while (g.k > gp.B) { g.k -= gp.B; ++g.p; }
+  g.k += 16;                                            // B >= 16 (checked on the host)
+  if (g.k > gp.B) { g.k -= gp.B; ++g.p; }
 }
 
 // GEN = false: the steering operand is streamed by TMA from a stored matrix instead
@@ -301,11 +308,15 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
   const int m_tiles = (int)((J + BLOCK_M - 1) / BLOCK_M);
   const int n_tiles = (int)((F + BN - 1) / BN);
   const int tile = blockIdx.x;
-  const int group = tile / (GROUP_M * n_tiles);
-  const int first_m = group * GROUP_M;
-  const int gsize = min(m_tiles - first_m, GROUP_M);
-  const int m_blk = first_m + (tile % (GROUP_M * n_tiles)) % gsize;
-  const int n_blk = (tile % (GROUP_M * n_tiles)) / gsize;
+  // raster: with a stored operator, groups of GROUP_M candidate tiles sweep the frame
+  // tiles (both operands reused from L2); with on-chip steering only psi is read, so all
+  // candidate tiles of one frame tile run together and psi is read from HBM once
+  const int gm = GEN ? m_tiles : GROUP_M;
+  const int group = tile / (gm * n_tiles);
+  const int first_m = group * gm;
+  const int gsize = min(m_tiles - first_m, gm);
+  const int m_blk = first_m + (tile % (gm * n_tiles)) % gsize;
+  const int n_blk = (tile % (gm * n_tiles)) / gsize;
   const int num_kb = (Kd + BLOCK_K - 1) / BLOCK_K;
   const int num_chunks = (num_kb + CHUNK - 1) / CHUNK;
 
@@ -429,6 +440,13 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
     };
     GenState g;
     gen_state_init(g, kNB * part, gp.B > 0 ? gp.B : 1);
+    const int64_t gi_c = gi < J ? gi : J - 1;          // rows past J: any finite values (discarded)
+    constexpr uint32_t kPlane = BLOCK_M * BLOCK_K * sizeof(float), kStage = SM::NP * kPlane;
+    const uint32_t a_row = smem_u32(&sm.a[0][0][0]) + row * 128;
+    const uint32_t full0 = smem_u32(&sm.full[0]), empty0 = smem_u32(&sm.empty[0]);
+    uint32_t off[kNB / 2];
+#pragma unroll
+    for (int qq = 0; qq < kNB / 2; ++qq) off[qq] = (uint32_t)((((kNB / 2) * part + qq) ^ (row & 7)) << 4);
     int folded = 0;
     // two k-blocks per synchronisation round: the generator is latency-bound per round
     // (wait, generate, fence, arrive), so pairing blocks halves the rounds
@@ -437,21 +455,21 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
       const bool two = kb + 1 < num_kb;
       if (GEN) {
         const int s = kb % NS;
-        const uint32_t round = kb / NS;
-        mbar_wait(&sm.empty[s], (round & 1) ^ 1);
-        if (two) mbar_wait(&sm.empty[s + 1], (round & 1) ^ 1);
+        const uint32_t par = ((kb / NS) & 1) ^ 1;
+        mbar_wait_addr(empty0 + 8 * s, par);
+        if (two) mbar_wait_addr(empty0 + 8 * (s + 1), par);
         if (!(gp.dbg & 1)) {
-#pragma unroll 1
-          for (int u = 0; u < (two ? 2 : 1); ++u)
-            gen_a_part<SPLIT, kNB>(smem_u32(sm.a[s + u][0]), smem_u32(sm.a[s + u][SM::NP - 1]), row, part, gi,
-                                   gi < J, gp, g);
+          const uint32_t st0 = a_row + s * kStage;
+          gen_a_part<SPLIT, kNB>(st0, st0 + (SM::NP - 1) * kPlane, off, (kNB / 2) * part, row & 7, gi_c, gp, g);
+          if (two)
+            gen_a_part<SPLIT, kNB>(st0 + kStage, st0 + kStage + (SM::NP - 1) * kPlane, off, (kNB / 2) * part,
+                                   row & 7, gi_c, gp, g);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // own writes -> async proxy
         __syncwarp();
         if (lane == 0) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
-          if (two)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s + 1])) : "memory");
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * s) : "memory");
+          if (two) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * (s + 1)) : "memory");
         }
       }
       if (two && ((kb + 1) % CHUNK) == CHUNK - 1 && (kb + 1) / CHUNK >= 1) fold(folded++);
@@ -648,6 +666,7 @@ extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num
   const int32_t Kd = 2 * num_pairs * bins;
   SRPGPU_CHECK_ARG(num_pairs >= 1 && bins >= 1 && num_candidates >= 1, SRPGPU_ERR_DIMENSION,
                    "srp_map_tdoa: empty operator");
+  SRPGPU_CHECK_ARG(bins >= 16, SRPGPU_ERR_UNSUPPORTED, "srp_map_tdoa: frames shorter than 34 samples");
   SRPGPU_CHECK_ARG(gcc_ld >= Kd && gcc_ld % 4 == 0 && ((uintptr_t)gcc & 15) == 0, SRPGPU_ERR_VALUE,
                    "srp_map_tdoa: gcc rows must cover 2*P*(K-1) floats with a 16-byte pitch");
   cudaStream_t st = as_stream(stream);
