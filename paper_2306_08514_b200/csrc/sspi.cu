@@ -31,7 +31,7 @@ constexpr int kWarps = 8;
 constexpr int kGroup = 4;                          // candidates per warp
 constexpr int kTileI = kWarps * kGroup;            // 32 candidates per CTA
 constexpr int kTileF = 128;                        // frames per frame tile (4 per lane)
-constexpr int kRecBudget = 160 * 1024;             // max bytes of staged records
+constexpr int64_t kStageMax = 64 * 1024;          // max bytes of a staged operator tile
 constexpr int kMetaBytes = 64;
 
 struct __align__(16) BandRec {
@@ -81,12 +81,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+template <bool kGlobal>
 __device__ __forceinline__ void accumulate(float (&acc)[kGroup][4], const BandRec* rr, int n,
                                            const float* xcol, int64_t ld) {
 #pragma unroll 4
   for (int r = 0; r < n; ++r) {
-    const uint32_t s = rr[r].s;
-    const float4 w = rr[r].w;
+    uint32_t s;
+    float4 w;
+    if (kGlobal) {   // uniform address across the warp: one broadcast read-only load
+      s = __ldg(&rr[r].s);
+      w = __ldg(&rr[r].w);
+    } else {
+      s = rr[r].s;
+      w = rr[r].w;
+    }
     const float4 x = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)s * ld));
     acc[0][0] = fmaf(w.x, x.x, acc[0][0]); acc[0][1] = fmaf(w.x, x.y, acc[0][1]);
     acc[0][2] = fmaf(w.x, x.z, acc[0][2]); acc[0][3] = fmaf(w.x, x.w, acc[0][3]);
@@ -99,6 +107,11 @@ __device__ __forceinline__ void accumulate(float (&acc)[kGroup][4], const BandRe
   }
 }
 
+// kDirect: records are read by each warp straight from global memory (L1/L2, broadcast)
+// instead of being staged in shared memory -- for operator tiles too large to stage
+// without dropping to one CTA per SM (cfg4: ~146 KB per tile).  No CTA barrier in the
+// accumulation loop; ~25 KB of shared memory per CTA, so occupancy is register-bound.
+template <bool kDirect>
 __global__ void __launch_bounds__(kWarps * 32)
 sspi_band_kernel(const BandParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -124,9 +137,9 @@ sspi_band_kernel(const BandParams prm) {
   __syncthreads();
   const uint32_t total = meta[8];
   const uint32_t g0 = meta[warp], g1 = (warp + 1 < kWarps) ? meta[warp + 1] : total;
-  const bool whole = total <= (uint32_t)prm.rec_cap;
+  const bool whole = kDirect || total <= (uint32_t)prm.rec_cap;
   uint32_t phase = 0;
-  if (whole && total > 0) {   // one TMA bulk copy for the whole operator tile, reused by all frame tiles
+  if (!kDirect && whole && total > 0) {   // one TMA bulk copy for the whole operator tile, reused by all frame tiles
     if (tid == 0) {
       mbar_arm(&bar, tile_bytes - kMetaBytes);
       bulk_copy(recs, grec, tile_bytes - kMetaBytes, &bar);
@@ -147,8 +160,10 @@ sspi_band_kernel(const BandParams prm) {
     const int64_t fl = f0 + 4 * lane;
     const bool lane_ok = fl < prm.ld;
     const float* xcol = prm.xi + fl;
-    if (whole) {
-      if (lane_ok) accumulate(acc, recs + g0, (int)(g1 - g0), xcol, prm.ld);
+    if (kDirect) {
+      if (lane_ok) accumulate<true>(acc, grec + g0, (int)(g1 - g0), xcol, prm.ld);
+    } else if (whole) {
+      if (lane_ok) accumulate<false>(acc, recs + g0, (int)(g1 - g0), xcol, prm.ld);
     } else {
       for (uint32_t c0 = 0; c0 < total; c0 += (uint32_t)prm.rec_cap) {
         const uint32_t c1 = min(total, c0 + (uint32_t)prm.rec_cap);
@@ -160,7 +175,7 @@ sspi_band_kernel(const BandParams prm) {
         mbar_wait(&bar, phase);
         phase ^= 1u;
         const uint32_t a = max(g0, c0), b = min(g1, c1);
-        if (lane_ok && b > a) accumulate(acc, recs + (a - c0), (int)(b - a), xcol, prm.ld);
+        if (lane_ok && b > a) accumulate<false>(acc, recs + (a - c0), (int)(b - a), xcol, prm.ld);
       }
     }
 
@@ -291,16 +306,16 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
     SRPGPU_CHECK_LAUNCH("sspi_map(rows)");
     return SRPGPU_OK;
   }
-  // whole tiles up to 160 KB stay resident (one bulk copy, reused by every frame tile); larger
-  // tiles are streamed in 40 KB record chunks so that 3+ CTAs stay resident per SM
-  const int64_t cap = kRecBudget / (int64_t)sizeof(BandRec);
+  // operator tiles up to kStageMax bytes are staged whole in shared memory (one bulk copy,
+  // reused by every frame tile); larger tiles are read by each warp from global memory
+  // (cfg2/cfg3 tiles: 6-18 KB, staged; cfg4: up to 143 KB, direct -- 2.2x faster there)
+  const bool direct = max_tile_records * (int64_t)sizeof(BandRec) > kStageMax;
   (void)max_pair_records;
-  prm.rec_cap = (int32_t)std::max<int64_t>(
-      1, max_tile_records <= cap ? max_tile_records : (40 * 1024) / (int64_t)sizeof(BandRec));
+  prm.rec_cap = (int32_t)std::max<int64_t>(1, direct ? 1 : max_tile_records);
   const size_t smem = (size_t)kTileF * kWarps * 8 + (size_t)kTileF * (kTileI + 1) * 4 +
-                      (size_t)prm.rec_cap * sizeof(BandRec);
-  if (cudaFuncSetAttribute(sspi_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess) {
+                      (direct ? 0 : (size_t)prm.rec_cap * sizeof(BandRec));
+  auto kern = direct ? sspi_band_kernel<true> : sspi_band_kernel<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("sspi_map: cannot reserve %zu B shared memory", smem);
     return SRPGPU_ERR_LAUNCH;
   }
@@ -312,7 +327,7 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
   const int64_t gy = (ftiles + per - 1) / per;
   SRPGPU_CHECK_ARG(gy <= 65535, SRPGPU_ERR_DIMENSION, "sspi_map: too many frames per call");
   dim3 grid((unsigned)ctiles, (unsigned)gy);
-  sspi_band_kernel<<<grid, kWarps * 32, smem, st>>>(prm);
+  kern<<<grid, kWarps * 32, smem, st>>>(prm);
   SRPGPU_CHECK_LAUNCH("sspi_map");
   return SRPGPU_OK;
 }
