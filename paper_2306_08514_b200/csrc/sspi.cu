@@ -81,6 +81,47 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Direct variant: records read from global memory, software-pipelined one group of 4
+// ahead so that only the xi load latency is exposed (records do not depend on data).
+__device__ __forceinline__ void accumulate_direct(float (&acc)[kGroup][4], const BandRec* rr, int n,
+                                                  const float* xcol, int64_t ld) {
+  constexpr int U = 4;
+  uint32_t s[U];
+  float4 w[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    s[u] = u < n ? __ldg(&rr[u].s) : 0u;
+    w[u] = u < n ? __ldg(&rr[u].w) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int r = 0; r < n; r += U) {
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)   // padding slots read row 0 with zero weights
+      x[u] = __ldg(reinterpret_cast<const float4*>(xcol + (int64_t)s[u] * ld));
+    uint32_t sn[U];
+    float4 wn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = r + U + u;
+      sn[u] = q < n ? __ldg(&rr[q].s) : 0u;
+      wn[u] = q < n ? __ldg(&rr[q].w) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[0][0] = fmaf(w[u].x, x[u].x, acc[0][0]); acc[0][1] = fmaf(w[u].x, x[u].y, acc[0][1]);
+      acc[0][2] = fmaf(w[u].x, x[u].z, acc[0][2]); acc[0][3] = fmaf(w[u].x, x[u].w, acc[0][3]);
+      acc[1][0] = fmaf(w[u].y, x[u].x, acc[1][0]); acc[1][1] = fmaf(w[u].y, x[u].y, acc[1][1]);
+      acc[1][2] = fmaf(w[u].y, x[u].z, acc[1][2]); acc[1][3] = fmaf(w[u].y, x[u].w, acc[1][3]);
+      acc[2][0] = fmaf(w[u].z, x[u].x, acc[2][0]); acc[2][1] = fmaf(w[u].z, x[u].y, acc[2][1]);
+      acc[2][2] = fmaf(w[u].z, x[u].z, acc[2][2]); acc[2][3] = fmaf(w[u].z, x[u].w, acc[2][3]);
+      acc[3][0] = fmaf(w[u].w, x[u].x, acc[3][0]); acc[3][1] = fmaf(w[u].w, x[u].y, acc[3][1]);
+      acc[3][2] = fmaf(w[u].w, x[u].z, acc[3][2]); acc[3][3] = fmaf(w[u].w, x[u].w, acc[3][3]);
+      s[u] = sn[u];
+      w[u] = wn[u];
+    }
+  }
+}
+
 template <bool kGlobal>
 __device__ __forceinline__ void accumulate(float (&acc)[kGroup][4], const BandRec* rr, int n,
                                            const float* xcol, int64_t ld) {
@@ -161,7 +202,7 @@ sspi_band_kernel(const BandParams prm) {
     const bool lane_ok = fl < prm.ld;
     const float* xcol = prm.xi + fl;
     if (kDirect) {
-      if (lane_ok) accumulate<true>(acc, grec + g0, (int)(g1 - g0), xcol, prm.ld);
+      if (lane_ok) accumulate_direct(acc, grec + g0, (int)(g1 - g0), xcol, prm.ld);
     } else if (whole) {
       if (lane_ok) accumulate<false>(acc, recs + g0, (int)(g1 - g0), xcol, prm.ld);
     } else {
@@ -183,6 +224,30 @@ sspi_band_kernel(const BandParams prm) {
     const int64_t ib = i0 + warp * kGroup;
     const int nvalid = (int)(prm.J - ib < kGroup ? (prm.J - ib > 0 ? prm.J - ib : 0) : kGroup);
     const bool aligned = (prm.J % 4 == 0);
+    if (kDirect) {   // warps finish independently: no CTA barrier, one atomic per (lane, frame)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int64_t f = fl + t;
+        if (f >= prm.F || nvalid == 0) continue;
+        float best = acc[0][t];
+        int bi = 0;
+#pragma unroll
+        for (int c = 1; c < kGroup; ++c)
+          if (c < nvalid && acc[c][t] > best) { best = acc[c][t]; bi = c; }
+        if (prm.z) {
+          float* zr = prm.z + f * prm.J + ib;
+          if (aligned && nvalid == kGroup) {
+            __stcs(reinterpret_cast<float4*>(zr), make_float4(acc[0][t], acc[1][t], acc[2][t], acc[3][t]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < kGroup; ++c)
+              if (c < nvalid) __stcs(zr + c, acc[c][t]);
+          }
+        }
+        if (prm.keys) atomicMax(prm.keys + f, make_key(best, (uint32_t)(ib + bi)));
+      }
+      continue;
+    }
     const bool vec = prm.z && nvalid == kGroup && aligned;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -312,8 +377,8 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
   const bool direct = max_tile_records * (int64_t)sizeof(BandRec) > kStageMax;
   (void)max_pair_records;
   prm.rec_cap = (int32_t)std::max<int64_t>(1, direct ? 1 : max_tile_records);
-  const size_t smem = (size_t)kTileF * kWarps * 8 + (size_t)kTileF * (kTileI + 1) * 4 +
-                      (direct ? 0 : (size_t)prm.rec_cap * sizeof(BandRec));
+  const size_t smem = direct ? 0 : (size_t)kTileF * kWarps * 8 + (size_t)kTileF * (kTileI + 1) * 4 +
+                                     (size_t)prm.rec_cap * sizeof(BandRec);
   auto kern = direct ? sspi_band_kernel<true> : sspi_band_kernel<false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("sspi_map: cannot reserve %zu B shared memory", smem);
