@@ -12,7 +12,7 @@ ties to the lowest candidate index), and `out_map=False` to skip writing z
 (argmax-only output).
 
 Operators are converted to device layouts once per operator object
-(`_device.CACHE`): the SSPI operator becomes a pair-major ELL array, low-rank
+(`_device.CACHE`): the SSPI operator becomes a tiled-band record array, low-rank
 factors are cast to float32 (complex factors folded into real ones), and the
 steering matrix is stored as interleaved (Re H, -Im H) rows for the
 tensor-core GEMM.
@@ -105,106 +105,6 @@ def _sample_offsets(samples, num_cols: int) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- SSPI / SI
-
-class EllOperator:
-    """Pair-major ELL image of a CSR interpolation operator (device + host index).
-
-    For pair p: width W_p = max_i (entries of row i inside pair p's column block);
-    entry (i, w) at ell_off[p] + i*W_p + w, packed (float32 value bits, absolute
-    column).  `counts[p, i]` (host) records the real entries so the ELL decodes
-    back to the reference CSR exactly (padding entries have value 0).
-    """
-
-    def __init__(self, values, cols, splits, num_cols: int, offsets: np.ndarray):
-        values = np.asarray(values, dtype=np.float64)
-        cols = np.asarray(cols, dtype=np.int64)
-        splits = np.asarray(splits, dtype=np.int64)
-        j = splits.shape[0] - 1
-        p_count = offsets.shape[0] - 1
-        rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
-        pair = np.searchsorted(offsets, cols, side="right") - 1
-        counts = np.zeros((p_count, j), dtype=np.int64)
-        np.add.at(counts, (pair, rows), 1)
-        widths = counts.max(axis=1) if j else np.zeros(p_count, np.int64)
-        widths = np.maximum(widths, 0)
-        j_pad = (j + 31) // 32 * 32          # rows padded for the 32-candidate TMA tiles
-        ell_off = np.concatenate([[0], np.cumsum(widths * j_pad)]).astype(np.int64)
-        # rank of each entry inside its (pair, row) group; CSR order is (row, col)
-        order = np.lexsort((cols, rows, pair))
-        grp = pair[order] * j + rows[order]
-        start = np.r_[0, np.flatnonzero(np.diff(grp)) + 1]
-        rank = np.empty(order.size, dtype=np.int64)
-        if order.size:
-            first = np.repeat(start, np.diff(np.r_[start, order.size]))
-            rank[order] = np.arange(order.size) - first
-        packed = np.zeros((int(ell_off[-1]), 2), dtype=np.uint32)
-        for p in range(p_count):   # padding: value 0, column = first column of the block
-            packed[ell_off[p]:ell_off[p + 1], 1] = offsets[p]
-        slot = ell_off[pair] + rows * widths[pair] + rank
-        packed[slot, 0] = values.astype(np.float32).view(np.uint32)
-        packed[slot, 1] = cols.astype(np.uint32)
-        self.num_rows, self.num_cols, self.num_pairs, self.rows_padded = j, num_cols, p_count, j_pad
-        self.offsets = offsets
-        self.widths = widths
-        self.counts = counts
-        self.ell_off = ell_off
-        self.host_packed = packed
-        self.max_block = int(np.max(np.diff(offsets))) if p_count else 0
-        self.d_packed = torch.from_numpy(packed.reshape(-1).view(np.int32)).to(dev.device()) \
-            if packed.size else torch.zeros(2, dtype=torch.int32, device=dev.device())
-        self.d_offsets = dev.as_i32(offsets)
-        self.d_widths = dev.as_i32(widths)
-        self.d_ell_off = dev.as_i64(ell_off)
-
-    def to_csr(self):
-        """Decode back to (values float32, col_indices int64, row_splits int64)."""
-        vals, cols, per_row = [], [], np.zeros(self.num_rows, dtype=np.int64)
-        entries = []
-        for p in range(self.num_pairs):
-            w = int(self.widths[p])
-            if w == 0:
-                continue
-            blk = self.host_packed[self.ell_off[p]:self.ell_off[p + 1]].reshape(self.rows_padded, w, 2)
-            mask = np.arange(w)[None, :] < self.counts[p][:, None]
-            r, k = np.nonzero(mask)
-            entries.append((r, blk[r, k, 1].astype(np.int64), blk[r, k, 0]))
-        if entries:
-            r = np.concatenate([e[0] for e in entries])
-            c = np.concatenate([e[1] for e in entries])
-            v = np.concatenate([e[2] for e in entries])
-            order = np.lexsort((c, r))
-            r, c, v = r[order], c[order], v[order]
-            per_row = np.bincount(r, minlength=self.num_rows)
-            vals, cols = v.view(np.float32), c
-        else:
-            vals, cols = np.zeros(0, np.float32), np.zeros(0, np.int64)
-        splits = np.concatenate([[0], np.cumsum(per_row)]).astype(np.int64)
-        return vals, cols, splits
-
-
-    @classmethod
-    def from_fixed(cls, fx, offsets: np.ndarray) -> "EllOperator":
-        """ELL image of a FixedNnzInterp without going through a CSR (cfg4-size operators)."""
-        self = cls.__new__(cls)
-        p_count, j, k = fx.values.shape
-        j_pad = (j + 31) // 32 * 32
-        packed = np.zeros((p_count, j_pad, k, 2), dtype=np.uint32)
-        packed[:, :, :, 1] = np.asarray(offsets[:-1], dtype=np.uint32)[:, None, None]
-        packed[:, :j, :, 0] = fx.values.astype(np.float32).view(np.uint32)
-        packed[:, :j, :, 1] = fx.cols.astype(np.uint32)
-        self.num_rows, self.num_cols, self.num_pairs, self.rows_padded = j, int(fx.num_cols), p_count, j_pad
-        self.offsets = offsets
-        self.widths = np.full(p_count, k, dtype=np.int64)
-        self.counts = np.repeat(np.asarray(fx.kept, dtype=np.int64)[:, None], j, axis=1)
-        self.ell_off = np.arange(p_count + 1, dtype=np.int64) * j_pad * k
-        self.host_packed = packed.reshape(-1, 2)
-        self.max_block = int(np.max(np.diff(offsets))) if p_count else 0
-        self.d_packed = torch.from_numpy(self.host_packed.reshape(-1).view(np.int32)).to(dev.device())
-        self.d_offsets = dev.as_i32(offsets)
-        self.d_widths = dev.as_i32(self.widths)
-        self.d_ell_off = dev.as_i64(self.ell_off)
-        return self
-
 
 class BandOperator:
     """Tiled band image of a sparse interpolation operator (what the SSPI kernel reads).
@@ -351,7 +251,7 @@ def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True):
 def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
     """Dense sampling+interpolation map z = Lambda xi (interpolation.py:129-136).
 
-    Runs the SSPI kernel on the keep-all ELL, so sspi_map(keep=all) == si_map
+    Runs the SSPI kernel on the keep-all band image, so sspi_map(keep=all) == si_map
     bit for bit, as in the reference (interpolation.py:112-126).
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])

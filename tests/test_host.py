@@ -1,8 +1,8 @@
-"""Host-side logic of the product (no GPU): geometry, operator fits, ELL layout.
+"""Host-side logic of the product (no GPU): geometry, operator fits, band layout.
 
 Operator fitting stays on the host and is uploaded once; these tests pin it
 bit-exactly to reference-generated golden vectors (sparse structure, TDOA,
-lag counts) and check the pair-major ELL encoding decodes back to the
+lag counts) and check the tiled-band operator encoding decodes back to the
 reference CSR exactly.
 """
 
@@ -99,7 +99,7 @@ def test_fixed_nnz_fit_keeps_nearest_lags(golden_scene):
         assert_array_equal(sp1.col_indices, glob.col_indices)
 
 
-def _ell(sp, off):
+def _band(sp, off):
     # the operator image needs a device for its upload; build the host image on CPU tensors
     from paper_2306_08514_b200 import maps
     import torch
@@ -113,28 +113,28 @@ def _ell(sp, off):
         maps.dev.device = orig
 
 
-def test_ell_roundtrip_bit_exact(golden_scene):
+def test_band_roundtrip_bit_exact(golden_scene):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     for tag in keep_tags(g):
         ref = sparse_from_golden(g, tag)
-        ell = _ell(ref, spec.offsets)
-        vals, cols, splits = ell.to_csr()
+        band = _band(ref, spec.offsets)
+        vals, cols, splits = band.to_csr()
         assert_array_equal(cols, ref.col_indices)
         assert_array_equal(splits, ref.row_splits)
         assert_array_equal(vals, ref.values.astype(np.float32))
         # every record's sample index lies inside the operator; padded weights are zero
-        rtg, rs, weights, mask = ell._rec
+        rtg, rs, weights, mask = band._rec
         assert np.all(rs < spec.offsets[-1]) and np.all(weights[~mask] == 0)
 
 
-def test_ell_empty_and_keep_all(golden_scene):
+def test_band_empty_and_keep_all(golden_scene):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     interp = s.build_interp_matrix(tdoa, spec, frame)
-    empty = _ell(s.truncate_sparse(interp, 0), spec.offsets)
+    empty = _band(s.truncate_sparse(interp, 0), spec.offsets)
     assert empty.records == 0
-    full = _ell(s.truncate_sparse(interp, interp.matrix.size), spec.offsets)
+    full = _band(s.truncate_sparse(interp, interp.matrix.size), spec.offsets)
     groups = (grid.num_points + 3) // 4
     assert full.records == groups * spec.offsets[-1]
     assert full.max_tile_records <= 8 * int(spec.offsets[-1])
@@ -194,7 +194,7 @@ def test_fixed_nnz_from_tdoa_matches_dense_fit(golden_scene):
         assert_array_equal(a.row_splits, b.row_splits)
         assert_array_equal(a.values, b.values)
         assert fx.num_kept == a.num_kept
-        vals, cols, splits = _ell(fx, spec.offsets).to_csr()
+        vals, cols, splits = _band(fx, spec.offsets).to_csr()
         assert_array_equal(cols, a.col_indices)
         assert_array_equal(splits, a.row_splits)
         assert_array_equal(vals, a.values.astype(np.float32))
