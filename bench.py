@@ -427,8 +427,9 @@ def run_ours(args):
             "gpu_launches_per_step": launches_per_step,
             "clocks": clocks.summary(), "parity": parity, "variants": variants,
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()                 # rank 0's parity / CPU legs finish before teardown
         dist.destroy_process_group()
 
 

@@ -29,7 +29,10 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
   __shared__ __align__(16) float As[kGK][kGI + 4];
   __shared__ __align__(16) float Bs[kGK][kGF + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t i0 = (int64_t)blockIdx.x * kGI, f0 = (int64_t)blockIdx.y * kGF;
+  // frame tiles run fastest: co-resident CTAs then cover many frames, so their per-frame
+  // key atomics spread over many addresses (candidate-fastest order had ~1000 CTAs
+  // hammering the same 64 keys); both operands are small and stay L2-resident
+  const int64_t f0 = (int64_t)blockIdx.x * kGF, i0 = (int64_t)blockIdx.y * kGI;
   float acc[4][4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
@@ -156,7 +159,6 @@ int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out
             int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
             const char* what, bool b_trans = false, float* split_ws = nullptr) {
   if (I <= 0 || F <= 0) return SRPGPU_OK;
-  SRPGPU_CHECK_ARG(F <= 65535ll * kGF, SRPGPU_ERR_DIMENSION, "%s: too many frames", what);
   const int64_t ctas = ((I + kGI - 1) / kGI) * ((F + kGF - 1) / kGF);
   int64_t split = 1;
   if (split_ws && !keys && ldo == I && ctas < 2 * num_sms())
@@ -164,7 +166,8 @@ int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out
                                                     K / 256}));
   const int64_t chunk = ((K + split - 1) / split + kGK - 1) / kGK * kGK;
   split = (K + chunk - 1) / chunk;
-  dim3 grid((unsigned)((I + kGI - 1) / kGI), (unsigned)((F + kGF - 1) / kGF), (unsigned)split);
+  SRPGPU_CHECK_ARG((I + kGI - 1) / kGI <= 65535, SRPGPU_ERR_DIMENSION, "%s: too many candidates", what);
+  dim3 grid((unsigned)((F + kGF - 1) / kGF), (unsigned)((I + kGI - 1) / kGI), (unsigned)split);
   float* dst = split > 1 ? split_ws : out;
   const float a = split > 1 ? 1.0f : alpha;
   if (b_trans)
