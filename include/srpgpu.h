@@ -171,6 +171,14 @@ int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, in
 int srpgpu_split_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,
                       int64_t cols, srpgpu_stream_t stream);
 
+/* Steering operand from the reference's complex128 matrix (srp.py:51-62; the "conv"
+ * payload of an SRPM cache, cache.py:1-19 / cli.py:137-140): src = interleaved
+ * (re, im) float64 rows of pitch ld_src complex elements; dst[r][2c] = f32(Re),
+ * dst[r][2c+1] = -f32(Im), TF32-rounded (RNE) when tf32 != 0.  Pad columns of dst
+ * are not written. */
+int srpgpu_c128_to_steering(const void* src, int64_t ld_src, int64_t rows, int64_t cols, float* dst,
+                            int64_t ld_dst, int32_t tf32, srpgpu_stream_t stream);
+
 /* dst[r][c] = tf32_rne(src[r][c]) for c < cols, 0 for cols <= c < ld_dst. */
 int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,
                       int64_t cols, srpgpu_stream_t stream);

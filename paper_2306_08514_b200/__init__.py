@@ -13,11 +13,14 @@ run on hand-written sm_100a kernels (libsrpgpu.so, C-ABI in include/srpgpu.h):
 Each accepts a leading frame axis and returns device tensors.  Host-side
 geometry and operator fitting (float64 NumPy, uploaded once) mirror the
 reference builders.  Fused chains: `gcc_frames` (samples -> cross-spectra) and
-`frames_to_samples` (samples -> TD-GCC samples).  There is no CPU fallback.
+`frames_to_samples` (samples -> TD-GCC samples).  Operator caches in the
+reference's SRPM format load straight into device layouts (`load_operator`).
+There is no CPU fallback.
 """
 
-from .errors import (CapacityError, ConfigError, DimensionError, InvalidGeometryError,
-                     InvalidGridError, NativeLibraryError, SrpMapError)
+from .errors import (CacheFormatError, CapacityError, ConfigError, DimensionError,
+                     InvalidGeometryError, InvalidGridError, NativeLibraryError, SrpMapError)
+from .cache import CacheBundle, load_cache, load_operator, operator_from_bundle, params_hash, save_cache
 from .frontend import FdGcc, FrameSpec, fd_gcc, frame_window, gcc_frames, num_frames, stft_frame
 from .maps import (decode_keys, evaluate_map, locate, lr_map, map_argmax, si_map, slri_map,
                    sspi_map, srp_map_exact)

@@ -44,6 +44,7 @@ SIGNATURES = {
     "srpgpu_srp_map_tdoa": [_P, _I64, _I64, _I32, _I32, _P, _I64, _I32, _P, _P, _P],
     "srpgpu_split_tf32": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "srpgpu_round_tf32": [_P, _I64, _P, _I64, _I64, _I64, _P],
+    "srpgpu_c128_to_steering": [_P, _I64, _I64, _I64, _P, _I64, _I32, _P],
     "srpgpu_gemm_nt": [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _F32, _P, _P],
     "srpgpu_argmax": [_P, _I64, _I64, _I64, _P, _P],
     "srpgpu_decode_keys": [_P, _I64, _P, _P, _P],

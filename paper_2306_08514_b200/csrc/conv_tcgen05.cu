@@ -544,6 +544,22 @@ __global__ void round_tf32_kernel(const float* __restrict__ src, int64_t ld_src,
   }
 }
 
+// Steering operand straight from the reference's complex128 matrix (srp.py:51-62 /
+// an SRPM cache payload, cache.py:1-19): dst[r][2c] = f32(Re H), dst[r][2c+1] = -f32(Im H),
+// optionally TF32-rounded (RNE) -- bit-identical to the host conversion conj -> complex64
+// -> tf32_rne, so uploads can ship the float64 payload and convert on the GPU.
+__global__ void c128_to_steering_kernel(const double2* __restrict__ src, int64_t ld_src, int64_t rows,
+                                        int64_t cols, float2* __restrict__ dst, int64_t ld_dst2, int tf32) {
+  const int64_t n = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const double2 h = __ldcs(src + r * ld_src + c);
+    float re = __double2float_rn(h.x), im = -__double2float_rn(h.y);
+    if (tf32) { re = tf32_rne(re); im = tf32_rne(im); }
+    dst[r * ld_dst2 + c] = make_float2(re, im);
+  }
+}
+
 // hi = tf32_rne(x), lo = tf32_rne(x - hi) into two planes (3xTF32 operands)
 __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld_src, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t ld_dst, int64_t cols) {
@@ -604,6 +620,21 @@ int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
 }  // namespace srpgpu
 
 using namespace srpgpu;
+
+extern "C" int srpgpu_c128_to_steering(const void* src, int64_t ld_src, int64_t rows, int64_t cols, float* dst,
+                                       int64_t ld_dst, int32_t tf32, srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rows >= 0 && cols >= 0 && ld_src >= cols && ld_dst >= 2 * cols && ld_dst % 2 == 0,
+                   SRPGPU_ERR_DIMENSION, "c128_to_steering: bad pitches");
+  SRPGPU_CHECK_ARG(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 7) == 0, SRPGPU_ERR_VALUE,
+                   "c128_to_steering: misaligned operands");
+  if (rows == 0 || cols == 0) return SRPGPU_OK;
+  const int64_t n = rows * cols;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 16 * (int64_t)num_sms());
+  tc::c128_to_steering_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const double2*>(src), ld_src, rows, cols, reinterpret_cast<float2*>(dst), ld_dst / 2, tf32);
+  SRPGPU_CHECK_LAUNCH("c128_to_steering");
+  return SRPGPU_OK;
+}
 
 extern "C" int srpgpu_round_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst,
                                  int64_t rows, int64_t cols, srpgpu_stream_t stream) {

@@ -336,19 +336,22 @@ def _tf32_rne_host(a: np.ndarray) -> np.ndarray:
 def steering_device(srp, tf32: bool = True) -> torch.Tensor:
     """(J, ld) float32: interleaved (Re H, -Im H) per bin, row pitch padded to 16 B.
 
-    tf32=True stores the TF32-rounded (RNE) operand of the tensor-core map.
+    tf32=True stores the TF32-rounded (RNE) operand of the tensor-core map.  The
+    complex128 matrix (in memory, or memory-mapped from an SRPM cache) is shipped in
+    row blocks as float64 and converted on the GPU (srpgpu_c128_to_steering), which
+    is bit-identical to conj -> complex64 -> tf32_rne on the host.
     """
     def build():
         h = np.asarray(srp.matrix)
         j, n = h.shape
         ld = _pad4(2 * n)
         out = torch.zeros((j, ld), dtype=torch.float32, device=dev.device())
-        step = max(1, (64 << 20) // max(1, 8 * n))       # upload in row blocks (bounded host RAM)
+        step = max(1, (256 << 20) // max(1, 16 * n))      # 256 MB host blocks
         for r0 in range(0, j, step):
-            blk = np.conj(h[r0:r0 + step]).astype(np.complex64).view(np.float32)
-            if tf32:
-                blk = _tf32_rne_host(blk)
-            out[r0:r0 + blk.shape[0], :2 * n] = torch.from_numpy(blk).to(out.device)
+            blk = np.array(h[r0:r0 + step], dtype=np.complex128, order="C", copy=True)  # memmap -> RAM block
+            src = torch.from_numpy(blk.view(np.float64)).to(out.device)
+            nat.call("srpgpu_c128_to_steering", dev.ptr(src), n, blk.shape[0], n, dev.ptr(out[r0]), ld,
+                     1 if tf32 else 0, dev.stream_ptr())
         return out
     return dev.CACHE.get(srp, "h2_tf32" if tf32 else "h2_f32", build)
 
