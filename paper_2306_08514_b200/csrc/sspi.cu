@@ -5,14 +5,16 @@
 // the reference (interpolation.py:112-126).
 //
 // Operator layout: "tiled band" (built once on the host from the reference CSR).
-// Candidates are cut into tiles of 32 and each tile into 8 groups of 4.  For every
-// (tile, group, pair) the union of the lags kept by the group's 4 candidates becomes a
-// run of records {u32 sample index, 3 x pad, f32 weight[4]} (weight 0 where a candidate
-// does not keep that lag).  A tile's blob is contiguous and group-major:
-//     meta[16] : u32 start record of groups 0..7, meta[8] = record total (64 bytes)
-//     records  : group 0 (pairs ascending, then sample index), group 1, ...
-// so each warp walks one flat record range and one TMA bulk copy stages the tile
-// (record-range chunks when it exceeds the shared-memory budget).
+// Candidates are cut into groups of 4 consecutive rows, placed 8 to a tile (in index
+// order by default; any permutation of the groups is allowed -- BandOperator in maps.py).
+// For every (group, pair) the union of the lags kept by the group's 4 candidates
+// becomes a run of records {u32 sample index, 3 x pad, f32 weight[4]} (weight 0
+// where a candidate does not keep that lag).  A tile's blob is contiguous:
+//     meta[32] : u32 start record of slots 0..7, meta[8] = record total,
+//                meta[16 + g] = first candidate of slot g, meta[24 + g] = its count
+//     records  : slot 0 (pairs ascending, then sample index), slot 1, ...
+// so each warp walks one flat record range, and one TMA bulk copy stages the tile
+// (or, for large tiles, warps read their records from global memory).
 //
 // Samples are lag-major xi[s][f] (row pitch ld, frames contiguous).  CTA = 32
 // candidates x (n x 128) frames: the operator tile is staged once, then the CTA
@@ -32,7 +34,7 @@ constexpr int kGroup = 4;                          // candidates per warp
 constexpr int kTileI = kWarps * kGroup;            // 32 candidates per CTA
 constexpr int kTileF = 128;                        // frames per frame tile (4 per lane)
 constexpr int64_t kStageMax = 64 * 1024;          // max bytes of a staged operator tile
-constexpr int kMetaBytes = 64;
+constexpr int kMetaBytes = 128;
 
 struct __align__(16) BandRec {
   uint32_t s, pad0, pad1, pad2;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 sspi_band_kernel(const BandParams prm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t meta[16];
+  __shared__ uint32_t meta[32];
   unsigned long long* kred = reinterpret_cast<unsigned long long*>(smem_raw);        // [TF][8]
   float* zs = reinterpret_cast<float*>(smem_raw + (size_t)kTileF * kWarps * 8);      // [TF][TI+1]
   BandRec* recs = reinterpret_cast<BandRec*>(smem_raw + (size_t)kTileF * kWarps * 8 +
@@ -165,7 +167,6 @@ sspi_band_kernel(const BandParams prm) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tile = blockIdx.x;
-  const int64_t i0 = tile * kTileI;
   const unsigned char* tb = prm.blob + prm.tile_off[tile];
   const uint32_t tile_bytes = (uint32_t)(prm.tile_off[tile + 1] - prm.tile_off[tile]);
   const BandRec* grec = reinterpret_cast<const BandRec*>(tb + kMetaBytes);
@@ -174,7 +175,7 @@ sspi_band_kernel(const BandParams prm) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < 16) meta[tid] = reinterpret_cast<const uint32_t*>(tb)[tid];
+  if (tid < 32) meta[tid] = reinterpret_cast<const uint32_t*>(tb)[tid];
   __syncthreads();
   const uint32_t total = meta[8];
   const uint32_t g0 = meta[warp], g1 = (warp + 1 < kWarps) ? meta[warp + 1] : total;
@@ -221,8 +222,8 @@ sspi_band_kernel(const BandParams prm) {
     }
 
     // ---- outputs: z from registers, per-frame argmax keys
-    const int64_t ib = i0 + warp * kGroup;
-    const int nvalid = (int)(prm.J - ib < kGroup ? (prm.J - ib > 0 ? prm.J - ib : 0) : kGroup);
+    const int64_t ib = meta[16 + warp];                 // the slot's group: first candidate, count
+    const int nvalid = (int)meta[24 + warp];
     const bool aligned = (prm.J % 4 == 0);
     if (kDirect) {   // warps finish independently: no CTA barrier, one atomic per (lane, frame)
 #pragma unroll
@@ -272,11 +273,13 @@ sspi_band_kernel(const BandParams prm) {
     }
     __syncthreads();
     if (prm.z && !aligned) {   // unaligned rows: transpose through shared memory, coalesced rows
-      const int ti_valid = (int)(prm.J - i0 < kTileI ? prm.J - i0 : kTileI);
+      const int slot = lane >> 2, c = lane & 3;          // column lane = slot * 4 + c
+      const bool live = c < (int)meta[24 + slot];
+      const int64_t col = (int64_t)meta[16 + slot] + c;
       for (int row = warp; row < kTileF; row += kWarps) {
         const int64_t fg = f0 + row;
         if (fg >= prm.F) break;
-        if (lane < ti_valid) prm.z[fg * prm.J + i0 + lane] = zs[row * (kTileI + 1) + lane];
+        if (live) prm.z[fg * prm.J + col] = zs[row * (kTileI + 1) + lane];
       }
     }
     if (prm.keys && tid < kTileF) {
@@ -296,23 +299,29 @@ sspi_band_kernel(const BandParams prm) {
 // (candidate, frame) walking its group's records in the tile kernel's order, so
 // both kernels give bit-identical maps.
 __global__ void sspi_band_rows_kernel(const BandParams prm) {
-  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // operator position
   const int64_t f = blockIdx.y;
-  const bool live = gi < prm.J;
+  const int64_t tile = t / kTileI;
+  const int g = (int)((t % kTileI) / kGroup), c = (int)(t % kGroup);
+  const int64_t tiles = (prm.J + kTileI - 1) / kTileI;
+  bool live = tile < tiles;
+  int64_t gi = 0;
   float acc = 0.f;
   if (live) {
-    const int64_t tile = gi / kTileI;
-    const int g = (int)((gi % kTileI) / kGroup), c = (int)(gi % kGroup);
     const unsigned char* tb = prm.blob + prm.tile_off[tile];
     const uint32_t* meta = reinterpret_cast<const uint32_t*>(tb);
-    const BandRec* grec = reinterpret_cast<const BandRec*>(tb + kMetaBytes);
-    const uint32_t r1 = (g + 1 < kWarps) ? meta[g + 1] : meta[8];
-    for (uint32_t r = meta[g]; r < r1; ++r) {
-      const float4 w = grec[r].w;
-      const float wc = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
-      acc = fmaf(wc, __ldg(prm.xi + (int64_t)grec[r].s * prm.ld + f), acc);
+    live = c < (int)meta[24 + g];
+    gi = (int64_t)meta[16 + g] + c;
+    if (live) {
+      const BandRec* grec = reinterpret_cast<const BandRec*>(tb + kMetaBytes);
+      const uint32_t r1 = (g + 1 < kWarps) ? meta[g + 1] : meta[8];
+      for (uint32_t r = meta[g]; r < r1; ++r) {
+        const float4 w = grec[r].w;
+        const float wc = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
+        acc = fmaf(wc, __ldg(prm.xi + (int64_t)grec[r].s * prm.ld + f), acc);
+      }
+      if (prm.z) prm.z[f * prm.J + gi] = acc;
     }
-    if (prm.z) prm.z[f * prm.J + gi] = acc;
   }
   if (prm.keys) {
     unsigned long long key = live ? make_key(acc, (uint32_t)gi) : 0ull;
@@ -366,7 +375,8 @@ extern "C" int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t
     }
   }
   if (num_frames < 32) {
-    dim3 grid((unsigned)((num_candidates + 255) / 256), (unsigned)num_frames);
+    const int64_t slots = (num_candidates + kTileI - 1) / kTileI * kTileI;
+    dim3 grid((unsigned)((slots + 255) / 256), (unsigned)num_frames);
     sspi_band_rows_kernel<<<grid, 256, 0, st>>>(prm);
     SRPGPU_CHECK_LAUNCH("sspi_map(rows)");
     return SRPGPU_OK;

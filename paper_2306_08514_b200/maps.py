@@ -109,33 +109,47 @@ def _sample_offsets(samples, num_cols: int) -> np.ndarray:
 class BandOperator:
     """Tiled band image of a sparse interpolation operator (what the SSPI kernel reads).
 
-    Candidates are cut into tiles of 32 and groups of 4.  For each (tile, group, pair)
-    the union of the sample indices kept by the group's candidates becomes records
-    {u32 sample index, 3 pad, f32 weight[4]}.  Tile blob = meta[16] u32 (start record
-    of groups 0..7, then the record total; 64 bytes) + records, group-major (then pair,
-    then ascending sample index); `tile_off` holds the blob byte offsets.  `mask`
-    (host) marks the (record, candidate) slots that are real kept entries, so the
-    image decodes back to the reference CSR exactly (`to_csr`).
+    Candidates are cut into groups of 4 consecutive rows; groups are placed 8 to a
+    tile.  For each (group, pair) the union of the sample indices kept by the group's
+    candidates becomes records {u32 sample index, 3 pad, f32 weight[4]}.  Tile blob =
+    meta[32] u32 (start record of slots 0..7, the record total, 7 spare; first
+    candidate of slots 0..7; candidates in slots 0..7; 128 bytes) + records,
+    slot-major (then pair, then ascending sample index); `tile_off` holds the blob
+    byte offsets.
+
+    Groups are placed in index order unless `placement` (a permutation of the
+    groups) says otherwise; a candidate's accumulation order does not depend on its
+    placement, so the maps are bit-identical either way.  (Lag-space locality
+    orderings were measured at cfg3/cfg4 and gave no gain, so none is applied.)
+    `mask` (host) marks the (record, candidate) slots that are real kept entries, so
+    the image decodes back to the reference CSR exactly (`to_csr`).
     """
 
-    TILE, GROUP, META_WORDS = 32, 4, 16
+    TILE, GROUP, META_WORDS = 32, 4, 32
 
-    def __init__(self, rows, cols, vals, num_rows: int, num_cols: int, offsets: np.ndarray):
+    def __init__(self, rows, cols, vals, num_rows: int, num_cols: int, offsets: np.ndarray,
+                 placement=None):
         rows = np.asarray(rows, dtype=np.int64)
         cols = np.asarray(cols, dtype=np.int64)
         vals = np.asarray(vals, dtype=np.float64)
         p_count = offsets.shape[0] - 1
         ngrp = self.TILE // self.GROUP
-        tiles = max(1, (num_rows + self.TILE - 1) // self.TILE)
+        groups = max(1, (num_rows + self.GROUP - 1) // self.GROUP)
+        tiles = (groups + ngrp - 1) // ngrp
         pair = np.searchsorted(offsets, cols, side="right") - 1
-        t = rows // self.TILE
-        g = (rows % self.TILE) // self.GROUP
+        grp = rows // self.GROUP
         c = rows % self.GROUP
-        key = ((t * ngrp + g) * p_count + pair) * num_cols + cols
+        order = np.arange(groups, dtype=np.int64) if placement is None else \
+            np.asarray(placement, dtype=np.int64)
+        if order.shape != (groups,) or not np.array_equal(np.sort(order), np.arange(groups)):
+            raise ValueError("placement must be a permutation of the candidate groups")
+        slot_of = np.empty(groups, dtype=np.int64)
+        slot_of[order] = np.arange(groups, dtype=np.int64)        # group -> tile * 8 + slot
+        key = (slot_of[grp] * p_count + pair) * num_cols + cols
         uniq, inv = np.unique(key, return_inverse=True)
         nrec = uniq.shape[0]
         rs = uniq % num_cols
-        rtg = uniq // num_cols // p_count                 # t * 8 + g
+        rtg = uniq // num_cols // p_count                 # tile * 8 + slot
         weights = np.zeros((nrec, self.GROUP), dtype=np.float32)
         mask = np.zeros((nrec, self.GROUP), dtype=bool)
         weights[inv, c] = vals.astype(np.float32)
@@ -149,6 +163,12 @@ class BandOperator:
         meta_idx = tile_off_w[:-1, None] + np.arange(ngrp)[None, :]
         blob[meta_idx.ravel()] = starts.astype(np.uint32).ravel()
         blob[tile_off_w[:-1] + ngrp] = tile_recs.astype(np.uint32)
+        placed = np.full(tiles * ngrp, -1, dtype=np.int64)
+        placed[:groups] = order                           # slot -> group (-1: empty slot)
+        first = np.where(placed >= 0, placed * self.GROUP, 0)
+        ncand = np.where(placed >= 0, np.clip(num_rows - placed * self.GROUP, 0, self.GROUP), 0)
+        blob[(meta_idx + 16).ravel()] = first.astype(np.uint32)
+        blob[(meta_idx + 24).ravel()] = ncand.astype(np.uint32)
         rec_tile = rtg // ngrp
         first_rec = np.concatenate([[0], np.cumsum(tile_recs)])[:-1]
         local = np.arange(nrec) - first_rec[rec_tile]
@@ -159,11 +179,13 @@ class BandOperator:
         self.num_rows, self.num_cols, self.num_pairs = num_rows, num_cols, p_count
         self.offsets = offsets
         self.records = nrec
+        self.tiles = tiles
         self.max_tile_records = int(tile_recs.max()) if tile_recs.size else 0
         self.max_pair_records = self.max_tile_records
         self.host_blob = blob
         self.host_tile_off = tile_off_w * 4
-        self._rec = (rtg, rs, weights, mask)
+        self.group_order = order
+        self._rec = (placed[rtg], rs, weights, mask)
         self.d_blob = torch.from_numpy(blob.view(np.int32)).to(dev.device()) if blob.size else \
             torch.zeros(16, dtype=torch.int32, device=dev.device())
         self.d_tile_off = dev.as_i64(self.host_tile_off)
@@ -185,12 +207,9 @@ class BandOperator:
 
     def to_csr(self):
         """Decode to (values float32, col_indices int64, row_splits int64)."""
-        rtg, rs, weights, mask = self._rec
-        ngrp = self.TILE // self.GROUP
-        t = rtg // ngrp
-        g = rtg % ngrp
+        grp, rs, weights, mask = self._rec
         rec, c = np.nonzero(mask)
-        rows = t[rec] * self.TILE + g[rec] * self.GROUP + c
+        rows = grp[rec] * self.GROUP + c
         cols = rs[rec]
         vals = weights[rec, c]
         order = np.lexsort((cols, rows))

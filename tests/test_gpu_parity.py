@@ -311,6 +311,28 @@ def test_pipeline_graph_matches_eager(golden_scene):
     assert_argmax_agrees(ic, g["z_conv"])
 
 
+def test_band_group_placement_bit_identical(golden_scene):
+    """Placing candidate groups in another order leaves every map bit-identical
+    (tile kernel and the small-batch rows kernel both read the slot meta)."""
+    from paper_2306_08514_b200 import maps
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    j = sp.row_splits.shape[0] - 1
+    rows = np.repeat(np.arange(j), np.diff(sp.row_splits))
+    groups = (j + 3) // 4
+    for nf in (g["psi"].shape[0], 40):
+        n = (nf - 1) * frame.hop + frame.frame_len
+        x = np.tile(g["samples"], (1, n // g["samples"].shape[1] + 1))[:, :n]
+        xi = s.frames_to_samples(x, frame, pairs, spec, range(nf))
+        out = []
+        for placement in (None, np.arange(groups)[::-1].copy()):
+            op = maps.BandOperator(rows, sp.col_indices, sp.values, j, int(sp.num_cols),
+                                   spec.offsets, placement=placement)
+            out.append(maps._band_map(op, xi, True, True))
+        assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
 def test_map_stream_matches_pipeline(golden_scene):
     """Streamed batches (overlapped copies, rotating slots) give the pipeline's argmax."""
     from paper_2306_08514_b200.pipeline import MapPipeline, MapStream

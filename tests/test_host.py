@@ -99,7 +99,7 @@ def test_fixed_nnz_fit_keeps_nearest_lags(golden_scene):
         assert_array_equal(sp1.col_indices, glob.col_indices)
 
 
-def _band(sp, off):
+def _band(sp, off, placement=None):
     # the operator image needs a device for its upload; build the host image on CPU tensors
     from paper_2306_08514_b200 import maps
     import torch
@@ -107,18 +107,40 @@ def _band(sp, off):
     maps.dev.device = lambda: torch.device("cpu")
     try:
         if np.ndim(getattr(sp, "cols", np.zeros(1))) == 3:
-            return maps.BandOperator.from_fixed(sp, off)
-        return maps.BandOperator.from_csr(sp.values, sp.col_indices, sp.row_splits, int(sp.num_cols), off)
+            fx = sp
+            keep = np.arange(fx.values.shape[2])[None, :] < np.asarray(fx.kept)[:, None]
+            sel = np.broadcast_to(keep[:, None, :], fx.values.shape)
+            rows = np.broadcast_to(np.arange(fx.values.shape[1])[None, :, None], fx.values.shape)[sel]
+            return maps.BandOperator(rows, fx.cols[sel].astype(np.int64), fx.values[sel], fx.values.shape[1],
+                                     int(fx.num_cols), off, placement=placement)
+        j = sp.row_splits.shape[0] - 1
+        rows = np.repeat(np.arange(j), np.diff(sp.row_splits))
+        return maps.BandOperator(rows, sp.col_indices, sp.values, j, int(sp.num_cols), off, placement=placement)
     finally:
         maps.dev.device = orig
 
 
-def test_band_roundtrip_bit_exact(golden_scene):
+@pytest.mark.parametrize("permuted", [False, True])
+def test_band_roundtrip_bit_exact(golden_scene, permuted):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     for tag in keep_tags(g):
         ref = sparse_from_golden(g, tag)
-        band = _band(ref, spec.offsets)
+        groups = (grid.num_points + 3) // 4
+        band = _band(ref, spec.offsets, np.arange(groups)[::-1].copy() if permuted else None)
+        if permuted:   # meta bases/counts describe each slot
+            assert np.array_equal(np.sort(band.group_order), np.arange(groups))
+            meta = band.host_blob.reshape(-1)
+            for t in range(band.tiles):
+                w0 = band.host_tile_off[t] // 4
+                for slot in range(8):
+                    gidx = t * 8 + slot
+                    if gidx < groups:
+                        grp = band.group_order[gidx]
+                        assert meta[w0 + 16 + slot] == 4 * grp
+                        assert meta[w0 + 24 + slot] == min(4, grid.num_points - 4 * grp)
+                    else:
+                        assert meta[w0 + 24 + slot] == 0
         vals, cols, splits = band.to_csr()
         assert_array_equal(cols, ref.col_indices)
         assert_array_equal(splits, ref.row_splits)
