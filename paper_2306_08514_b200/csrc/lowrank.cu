@@ -108,6 +108,150 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
   }
 }
 
+// Rank-space -> candidate product with a small inner dimension (SLRI: K = R,
+// interpolation.py:178-185; LR: K = 2R, lowrank.py:51-57):
+//     out[f][i] = alpha * sum_k A[i][k] B[f][k],   K <= KB,
+// which is output-bound (K FMAs per 4-byte map element), K <= 16 here.  CTA = 64 frames x a run of
+// 128-candidate tiles: the frames' B rows stay in shared memory, the next A tile is
+// prefetched into registers while the current one is multiplied, z is written with
+// coalesced 16-byte streaming stores, and the per-frame argmax is carried in
+// registers across the run (one key atomic per frame per CTA).  Thread (tx, ty) owns
+// frames 4ty..4ty+3 and candidates 4tx..4tx+3, 64+4tx..64+4tx+3 of each tile.  The k
+// order of every sum is 0..K-1, as in gemm_nt.
+constexpr int kOF = 64, kOI = 128;
+
+template <int KB>
+__global__ void __launch_bounds__(256)
+lowrank_out_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                   float* __restrict__ out, int64_t ldo, int64_t I, int64_t F, int K, int tiles_per_cta,
+                   float alpha, unsigned long long* __restrict__ keys) {
+  __shared__ __align__(16) float Bs[KB][kOF];
+  __shared__ __align__(16) float As[2][KB][kOI];
+  constexpr int kPer = KB * kOI / 256;            // A elements per thread per tile
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t f0 = (int64_t)blockIdx.x * kOF;
+  const int64_t tile0 = (int64_t)blockIdx.y * tiles_per_cta;
+  const int64_t ntiles = (I + kOI - 1) / kOI;
+  const int nt = (int)(ntiles - tile0 < tiles_per_cta ? ntiles - tile0 : tiles_per_cta);
+  for (int e = tid; e < KB * kOF; e += 256) {   // alpha folded into the rank-space operand
+    const int f = e / KB, k = e % KB;
+    Bs[k][f] = (k < K && f0 + f < F) ? alpha * __ldg(B + (f0 + f) * ldb + k) : 0.f;
+  }
+  float areg[kPer];
+  auto load_a = [&](int t) {
+    const int64_t i0 = (tile0 + t) * kOI;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int e = tid + j * 256, i = e / KB, k = e % KB;
+      areg[j] = (k < K && i0 + i < I) ? __ldg(A + (i0 + i) * lda + k) : 0.f;
+    }
+  };
+  auto store_a = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int e = tid + j * 256;
+      As[buf][e % KB][e / KB] = areg[j];
+    }
+  };
+  // running first maximum per frame over this thread's candidates (ascending index)
+  float bval[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  uint32_t bidx[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  const bool vec = (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (nt > 0) {
+    load_a(0);
+    store_a(0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nt; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nt) load_a(t + 1);
+    float acc[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc[u][v] = 0.f;
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][ty * 4]);
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][tx * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + tx * 4]);
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[u][v] = fmaf(bv[u], av[v], acc[u][v]);
+    }
+    const int64_t i0 = (tile0 + t) * kOI;
+    const uint32_t c0 = (uint32_t)i0 + tx * 4;              // candidates c0..c0+3, c0+64..c0+67
+    const bool full = i0 + kOI <= I && vec;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t f = f0 + ty * 4 + u;
+      if (f >= F) continue;
+      float* row = out + f * ldo;
+      if (full) {
+        if (out) {
+          __stcs(reinterpret_cast<float4*>(row + c0), make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]));
+          __stcs(reinterpret_cast<float4*>(row + c0 + 64), make_float4(acc[u][4], acc[u][5], acc[u][6], acc[u][7]));
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint32_t c = c0 + (v & 3) + (v >> 2) * 64;
+          if (acc[u][v] > bval[u]) { bval[u] = acc[u][v]; bidx[u] = c; }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint32_t c = c0 + (v & 3) + (v >> 2) * 64;
+          if ((int64_t)c < I) {
+            if (out) __stcs(row + c, acc[u][v]);
+            if (acc[u][v] > bval[u] || bidx[u] == 0xFFFFFFFFu) { bval[u] = acc[u][v]; bidx[u] = c; }
+          }
+        }
+      }
+    }
+    if (t + 1 < nt) store_a(buf ^ 1);
+    __syncthreads();
+  }
+  if (keys) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      unsigned long long k = bidx[u] != 0xFFFFFFFFu ? make_key(bval[u], bidx[u]) : 0ull;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) k = key_max(k, __shfl_xor_sync(0xffffffffu, k, o));
+      const int64_t f = f0 + ty * 4 + u;
+      if (tx == 0 && f < F && k) atomicMax(keys + f, k);
+    }
+  }
+}
+
+// Dispatch for the small-K candidate product; falls back to gemm_nt beyond K = 16.
+int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
+            int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
+            const char* what, bool b_trans, float* split_ws);
+
+static int lowrank_out(const float* A, int64_t lda, const float* B, int64_t ldb, float* out, int64_t ldo,
+                       int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
+                       const char* what) {
+  if (I <= 0 || F <= 0) return SRPGPU_OK;
+  // K = 32 (LR at R = 16) needs 119 registers here (2 CTAs/SM) and measured slower than
+  // gemm_nt, so only K <= 16 takes this kernel
+  if (K > 16) return gemm_nt(A, lda, B, ldb, out, ldo, I, F, K, alpha, keys, st, what, false, nullptr);
+  const int64_t ftiles = (F + kOF - 1) / kOF, itiles = (I + kOI - 1) / kOI;
+  // enough CTAs for ~4 waves of 148 SMs x 3 resident, each sweeping a run of candidate tiles
+  const int64_t want = 12 * (int64_t)num_sms();
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(itiles, (want + ftiles - 1) / ftiles));
+  const int64_t per = (itiles + chunks - 1) / chunks;
+  chunks = (itiles + per - 1) / per;
+  SRPGPU_CHECK_ARG(chunks <= 65535, SRPGPU_ERR_DIMENSION, "%s: too many candidates", what);
+  dim3 grid((unsigned)ftiles, (unsigned)chunks);
+  auto* kp = reinterpret_cast<unsigned long long*>(keys);
+  lowrank_out_kernel<16><<<grid, 256, 0, st>>>(A, lda, B, ldb, out, ldo, I, F, (int)K, (int)per, alpha, kp);
+  SRPGPU_CHECK_LAUNCH(what);
+  return SRPGPU_OK;
+}
+
 // out[f][i] = sum_z part[z][f][i] in a fixed order (deterministic split-K)
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t nz, int64_t n,
                                      float* __restrict__ out) {
@@ -223,8 +367,8 @@ extern "C" int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t
               num_frames, total_samples, 1.0f, nullptr, st, "slri_map(fat)", samples_ld != 0,
               work + num_frames * (int64_t)rank);
   if (s) return s;
-  return gemm_nt(tall, rank, work, rank, z, num_candidates, num_candidates, num_frames, rank, 1.0f,
-                 keys, st, "slri_map(tall)");
+  return lowrank_out(tall, rank, work, rank, z, num_candidates, num_candidates, num_frames, rank, 1.0f,
+                     keys, st, "slri_map(tall)");
 }
 
 extern "C" int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_len,
@@ -241,8 +385,8 @@ extern "C" int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_l
               work + num_frames * (int64_t)(2 * rank));
   if (s) return s;
   // z = [2 Re tall, -2 Im tall] . work
-  return gemm_nt(tall2, 2 * rank, work, 2 * rank, z, num_candidates, num_candidates, num_frames,
-                 2 * rank, 1.0f, keys, st, "lr_map(tall)");
+  return lowrank_out(tall2, 2 * rank, work, 2 * rank, z, num_candidates, num_candidates, num_frames,
+                     2 * rank, 1.0f, keys, st, "lr_map(tall)");
 }
 
 extern "C" int srpgpu_srp_map_simt(const float* gcc, int64_t num_frames, int32_t gcc_len,
