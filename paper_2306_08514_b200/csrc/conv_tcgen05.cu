@@ -15,7 +15,6 @@
 // per-frame argmax (packed keys, atomicMax).  Tiles are rasterised in groups of
 // GROUP_M candidate tiles so concurrently running CTAs share k-slices in L2.
 #include <cuda.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -124,7 +123,6 @@ struct GenParams {
   int32_t P;
   int32_t B;           // bins per pair (K - 1)
   float inv_k;         // 1 / K
-  int32_t dbg;         // DIAGNOSTIC (temporary): 1 skip generation, 2 skip B loads
 };
 
 // Round a finite fp32 value to nearest TF32, ties away from zero (= cvt.rna.tf32.f32,
@@ -361,10 +359,6 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
         const int s = kb % NS;
         const uint32_t round = kb / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
-        if (GEN && (gp.dbg & 2)) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
-          continue;
-        }
         mbar_expect_tx(&sm.full[s], kBytes);
         if (!GEN) tma_load_2d(sm.a[s][0], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
         tma_load_2d(sm.b[s][0], &map_b, &sm.full[s], kb * BLOCK_K, n_blk * BN);
@@ -458,13 +452,11 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
         const uint32_t par = ((kb / NS) & 1) ^ 1;
         mbar_wait_addr(empty0 + 8 * s, par);
         if (two) mbar_wait_addr(empty0 + 8 * (s + 1), par);
-        if (!(gp.dbg & 1)) {
-          const uint32_t st0 = a_row + s * kStage;
-          gen_a_part<SPLIT, kNB>(st0, st0 + (SM::NP - 1) * kPlane, off, (kNB / 2) * part, row & 7, gi_c, gp, g);
-          if (two)
-            gen_a_part<SPLIT, kNB>(st0 + kStage, st0 + kStage + (SM::NP - 1) * kPlane, off, (kNB / 2) * part,
-                                   row & 7, gi_c, gp, g);
-        }
+        const uint32_t st0 = a_row + s * kStage;
+        gen_a_part<SPLIT, kNB>(st0, st0 + (SM::NP - 1) * kPlane, off, (kNB / 2) * part, row & 7, gi_c, gp, g);
+        if (two)
+          gen_a_part<SPLIT, kNB>(st0 + kStage, st0 + kStage + (SM::NP - 1) * kPlane, off, (kNB / 2) * part,
+                                 row & 7, gi_c, gp, g);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // own writes -> async proxy
         __syncwarp();
         if (lane == 0) {
@@ -706,7 +698,6 @@ extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num
   if (num_frames <= 0) return SRPGPU_OK;
   tc::GenParams gp;
   gp.xtab = xtab; gp.P = num_pairs; gp.B = bins; gp.inv_k = 1.0f / (float)half_len;
-  { const char* e = getenv("SRPGPU_CONV_DBG"); gp.dbg = e ? atoi(e) : 0; }
   const int64_t m_tiles = (num_candidates + tc::BLOCK_M - 1) / tc::BLOCK_M;
   const int64_t n256 = (num_frames + 255) / 256;
   (void)m_tiles; (void)n256;

@@ -12,8 +12,6 @@
 //   * the inverse is pruned: only the 2N_p+1 kept lags (|n| <= N_p) are produced,
 //     i.e. outputs k1 in {0, LP-1} of the second step when N_p < 32.
 //   * frame energy for the PHAT floor by warp shuffles.
-#include <stdlib.h>
-
 #include "frontend_warp.cuh"
 
 namespace srpgpu {
@@ -390,18 +388,9 @@ static int by_len(const WarpParams& wp, cudaStream_t st, const char* what) {
 // Returns 0 on launch, 1 if the shape is not covered (caller uses the block kernel),
 // a negative status on error.
 int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what) {
-  static const int disabled = [] {
-    const char* e = getenv("SRPGPU_FRONTEND");
-    return e && e[0] == 'b';
-  }();
-  if (disabled) return 1;
   // a warp per frame while there are fewer frames than resident warps (latency-bound),
   // two warps per frame for large batches (throughput-bound)
-  static const int force = [] {
-    const char* e = getenv("SRPGPU_WPF");
-    return e ? atoi(e) : 0;
-  }();
-  const bool small = force ? force == 1 : wp.F <= (int64_t)num_sms() * 8;
+  const bool small = wp.F <= (int64_t)num_sms() * 8;
   if (out == W_OUT_GCC) return small ? wf::by_len<W_OUT_GCC, 1>(wp, st, what) : wf::by_len<W_OUT_GCC, 2>(wp, st, what);
   if (out == W_OUT_XI) return small ? wf::by_len<W_OUT_XI, 1>(wp, st, what) : wf::by_len<W_OUT_XI, 2>(wp, st, what);
   return 1;
