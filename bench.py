@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "conv_h", "si"])
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
+    ap.add_argument("--engine", default="auto", choices=["auto", "tc", "band"],
+                    help="SSPI / SI map engine (maps.interp_engine)")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--variants", default="sspi,slri,lr,conv,conv_h",
                     help="comma list of extra variants measured on the same workload")
@@ -197,16 +199,21 @@ def fit_operator(wl, variant, args):
     return s.truncate_srp_matrix(srp, args.rank_r)
 
 
-def algorithmic_bytes(wl, variant, frames, op):
+def algorithmic_bytes(wl, variant, frames, op, engine="auto"):
     """Per-launch algorithmic bytes of the dominant kernels."""
     m, hop = wl.array.num_mics, wl.frame.hop
     p, b, j = wl.pairs.num_pairs, wl.frame.num_bins, wl.grid.num_points
     s_tot = wl.spec.total_samples
     out = {"frontend": frames * (4 * m * hop + (4 * s_tot if variant in ("sspi", "slri", "si") else 8 * p * b))}
     if variant in ("sspi", "si"):
-        nnz_stored = getattr(op, "num_kept", None)
-        nnz_stored = nnz_stored if nnz_stored is not None else j * s_tot
-        out["map"] = frames * (4 * s_tot + 4 * j) + 8 * nnz_stored
+        from paper_2306_08514_b200 import maps
+        if maps.uses_tc(variant, op, engine):   # dense bf16 hi/lo planes: 4 B per sample slot
+            c8 = (s_tot + 7) // 8 * 8
+            out["map"] = frames * (4 * c8 + 4 * j) + 4 * j * c8
+        else:
+            nnz_stored = getattr(op, "num_kept", None)
+            nnz_stored = nnz_stored if nnz_stored is not None else j * s_tot
+            out["map"] = frames * (4 * s_tot + 4 * j) + 8 * nnz_stored
     elif variant == "slri":
         r = op.tall.shape[1]
         out["map"] = frames * (4 * s_tot + 4 * j) + 4 * (j * r + r * s_tot)
@@ -250,7 +257,7 @@ def run_ours(args):
 
     def make_pipe(variant, op):
         return MapPipeline("conv" if variant == "conv_h" else variant, op, wl.frame, wl.pairs, wl.spec,
-                           frames=count)
+                           frames=count, engine=args.engine)
 
     def timed(fn, steps, warmup, gather):
         for _ in range(warmup):
@@ -296,9 +303,9 @@ def run_ours(args):
     launches_per_step = pipe_launches(pipe)
 
     # ---- per-kernel times for the roofline: each stage captured alone, CUDA events
-    t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush)
+    t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush, engine=args.engine)
     hbm, bf16, peak_src = peaks()
-    abytes = algorithmic_bytes(wl, args.variant, count, op)
+    abytes = algorithmic_bytes(wl, args.variant, count, op, args.engine)
     tf32_peak, fp32_peak, xsrc = extra_peaks()
     if args.variant in ("conv", "conv_h"):
         dom_name, dom_ms = ("srp_map_tdoa" if args.variant == "conv" else "srp_map_tc"), t_map
@@ -318,6 +325,13 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
+    from paper_2306_08514_b200 import maps as _maps
+    if _maps.uses_tc(args.variant, op, args.engine):
+        # tensor-core interpolation engine: 3 bf16 MMA passes over the dense operator
+        c8 = (wl.spec.total_samples + 7) // 8 * 8
+        tflops = 3 * 2.0 * wl.grid.num_points * c8 * count / (t_map / 1e3) / 1e12
+        roof["map_engine"] = {"engine": "tcgen05 kind::f16, bf16 hi/lo x3 (dense operator)",
+                              "tensor_tflops": tflops, "frac_of_bf16_peak": tflops / bf16}
     # the SIMT stages are FP32-issue / L1 bound at these sizes: their FP32 fractions
     roof["fp32_frac"] = {
         "frontend": frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak,
@@ -332,7 +346,7 @@ def run_ours(args):
     e2e_steps = max(5, args.steps // 2)
     gather = (lambda i: D.gather_frame_keys(i, total)) if world > 1 else None
     stream = MapStream("conv" if args.variant == "conv_h" else args.variant, op, wl.frame, wl.pairs,
-                       wl.spec, frames=count, depth=2, after_batch=gather)
+                       wl.spec, frames=count, depth=2, after_batch=gather, engine=args.engine)
 
     def e2e_run(n):
         tickets = []
@@ -419,6 +433,8 @@ def run_ours(args):
                                      f"{int(op.values.shape[2])} nnz per (candidate, pair)")
                                     if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
+                       "map_engine": (("tensor cores (dense bf16x3)" if _maps.uses_tc(args.variant, op, args.engine)
+                                       else "FP32 tiled band") if args.variant in ("sspi", "si") else None),
                        "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
                        "execution": "CUDA graph per batch"},
             "candidates_per_s": value * wl.grid.num_points,
@@ -448,13 +464,18 @@ def pipe_launches(pipe) -> int:
     return nat.launch_count() - before
 
 
-def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10):
+def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto"):
     """Median device time of the frontend kernel and of the map kernel(s), each in its own graph."""
     import torch
     frames = range(0, count)
     if variant in ("sspi", "si", "slri"):
-        front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames)
+        from paper_2306_08514_b200 import maps
+        tc = maps.uses_tc(variant, op, engine)  # the pipeline's frontend also writes the bf16 planes
+        front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames, planes=tc)
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
+        if variant != "slri":
+            mapf0 = mapf
+            mapf = lambda o, m, argmax: mapf0(o, m, argmax=argmax, engine="tc" if tc else "band")
     else:
         front = lambda: s.gcc_frames(x_dev, wl.frame, wl.pairs, frames,
                                      tf32=(variant in ("conv", "conv_h")))
@@ -534,8 +555,8 @@ def cpu_baseline(wl, variant, op, seconds):
     x_all = wl.samples.astype(np.float64)
     done, t0 = 0, time.perf_counter()
     total_frames = wl.num_frames
-    while time.perf_counter() - t0 < seconds and done < total_frames:
-        f0 = done
+    while time.perf_counter() - t0 < seconds:
+        f0 = done % total_frames                  # cycle the workload's frames until the budget
         n = min(nf_chunk, total_frames - f0)
         seg = x_all[:, f0 * wl.frame.hop:(f0 + n - 1) * wl.frame.hop + wl.frame.frame_len]
         z = oracle_chain(wl, variant, op, seg, n)

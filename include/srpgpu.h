@@ -98,6 +98,18 @@ int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t
                              int32_t total_samples, float* samples_out, int64_t samples_ld,
                              srpgpu_stream_t stream);
 
+/* frames_to_samples plus the bf16 hi/lo planes [2][F][cols8] of the samples (the
+ * tensor-core interpolation map's operand, see srpgpu_interp_map_tc), written by the
+ * same kernel; cols8 >= total_samples, a multiple of 8. */
+int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels, int64_t num_samples,
+                                    int64_t ld_samples, const float* window, int32_t frame_len,
+                                    int32_t hop, int64_t first_frame, int64_t num_frames,
+                                    const int32_t* pairs, int32_t num_pairs, int32_t weighting,
+                                    int32_t floor_mode, double floor_value, const int32_t* counts,
+                                    const int32_t* offsets, int32_t total_samples, float* samples_out,
+                                    int64_t samples_ld, void* planes, int32_t cols8,
+                                    srpgpu_stream_t stream);
+
 /* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
 int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
                               int32_t half_len, const int32_t* pairs, int32_t num_pairs,
@@ -120,6 +132,22 @@ int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t num_frames
                     int32_t total_samples, int32_t num_pairs, const int64_t* tile_offsets,
                     const void* blob, int64_t num_candidates, int64_t max_pair_records,
                     int64_t max_tile_records, float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* Tensor-core engine for the same maps (si_map :129-136 / sspi_map :188-195) when the
+ * operator is stored dense (dropped entries = 0).  Operands are bf16 hi/lo plane pairs
+ * [2][rows][cols8] (x = hi + lo; cols8 = S rounded up to 8, zero beyond S) made by
+ * srpgpu_split_bf16; z ~= Lh.xh + Lh.xl + Ll.xh in fp32 (tcgen05 kind::f16).
+ * samples_planes: [2][F][cols8]; op_planes: [2][J][cols8]; z [F][J] and keys [F] are
+ * each optional (NULL).  Both plane buffers 16-byte aligned. */
+int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const void* op_planes,
+                         int64_t num_candidates, int32_t cols8, float* z, uint64_t* keys,
+                         srpgpu_stream_t stream);
+
+/* f32 [rows][cols] (row pitch ld_src; or lag-major src[c * ld_src + r] if lag_major)
+ * -> bf16 planes dst[0][r][c] = bf16_rne(x), dst[1][r][c] = bf16_rne(x - hi), pitch
+ * cols8 (multiple of 8, zero-filled in [cols, cols8)). */
+int srpgpu_split_bf16(const float* src, int64_t ld_src, int32_t lag_major, int64_t rows, int32_t cols,
+                      void* dst, int32_t cols8, srpgpu_stream_t stream);
 
 /* frame-major [rows][ld_src] -> lag-major [cols][ld_dst] (zero-filled pad columns). */
 int srpgpu_transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,

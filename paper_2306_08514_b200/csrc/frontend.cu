@@ -41,6 +41,9 @@ struct FrontendParams {
   int64_t gcc_ld;             // complex elements per frame row of gcc_out (>= P*(K-1))
   int64_t xi_ld;              // 0: xi_out is frame-major [F][S]; > 0: lag-major [S][xi_ld]
   int32_t round_tf32;         // round gcc_out to TF32 (RNE) for the tensor-core map
+  uint16_t* xi_planes;        // optional bf16 hi/lo planes [2][F][cols8] (warp path only)
+  int32_t cols8;
+  int32_t* warp_used;         // set to 1 when the warp-per-frame kernel ran
 };
 
 constexpr int kFrontThreads = 256;
@@ -298,7 +301,9 @@ static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* 
     wp.counts = prm.counts; wp.offsets = prm.offsets; wp.S = prm.S;
     wp.gcc_out = prm.gcc_out; wp.gcc_ld = prm.gcc_ld; wp.round_tf32 = prm.round_tf32;
     wp.xi_out = prm.xi_out; wp.xi_ld = prm.xi_ld;
+    wp.xi_planes = prm.xi_planes; wp.cols8 = prm.cols8;
     const int r = frontend_warp_launch(wp, OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI, stream, what);
+    if (r == 0 && prm.warp_used) *prm.warp_used = 1;
     if (r <= 0) return r;
   }
   const int need = (OUT == OUT_XI) ? (prm.P + 1) / 2 : (IN == IN_SAMPLES ? (prm.M + 1) / 2 : 0);
@@ -461,6 +466,38 @@ extern "C" int srpgpu_frames_to_samples(const float* samples, int32_t num_channe
                    "frames_to_samples: lag-major pitch smaller than the frame count");
   if ((st = check_frames(prm, num_samples, "frames_to_samples"))) return st;
   return launch_frontend<IN_SAMPLES, OUT_XI>(prm, as_stream(stream), "frames_to_samples");
+}
+
+extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels,
+                                               int64_t num_samples, int64_t ld_samples, const float* window,
+                                               int32_t frame_len, int32_t hop, int64_t first_frame,
+                                               int64_t num_frames, const int32_t* pairs, int32_t num_pairs,
+                                               int32_t weighting, int32_t floor_mode, double floor_value,
+                                               const int32_t* counts, const int32_t* offsets,
+                                               int32_t total_samples, float* samples_out, int64_t samples_ld,
+                                               void* planes, int32_t cols8, srpgpu_stream_t stream) {
+  FrontendParams prm = {};
+  int st = fill_common(prm, frame_len, "frames_to_samples");
+  if (st) return st;
+  SRPGPU_CHECK_ARG(weighting == 0 || weighting == 1, SRPGPU_ERR_VALUE, "frames_to_samples: unknown weighting");
+  SRPGPU_CHECK_ARG(planes != nullptr && cols8 >= total_samples && cols8 % 8 == 0 && ((uintptr_t)planes & 15) == 0,
+                   SRPGPU_ERR_VALUE, "frames_to_samples: bf16 planes need cols8 >= S, a multiple of 8, 16-byte aligned");
+  prm.samples = samples; prm.ld_samples = ld_samples; prm.window = window;
+  prm.M = num_channels; prm.hop = hop; prm.first_frame = first_frame; prm.F = num_frames;
+  prm.pairs = pairs; prm.P = num_pairs; prm.weighting = weighting; prm.floor_mode = floor_mode;
+  prm.floor_value = (float)floor_value; prm.counts = counts; prm.offsets = offsets;
+  prm.S = total_samples; prm.xi_out = samples_out; prm.xi_ld = samples_ld;
+  prm.xi_planes = reinterpret_cast<uint16_t*>(planes); prm.cols8 = cols8;
+  int32_t warp_used = 0;
+  prm.warp_used = &warp_used;
+  SRPGPU_CHECK_ARG(samples_ld == 0 || samples_ld >= num_frames, SRPGPU_ERR_DIMENSION,
+                   "frames_to_samples: lag-major pitch smaller than the frame count");
+  if ((st = check_frames(prm, num_samples, "frames_to_samples"))) return st;
+  if ((st = launch_frontend<IN_SAMPLES, OUT_XI>(prm, as_stream(stream), "frames_to_samples"))) return st;
+  if (warp_used || num_frames == 0) return SRPGPU_OK;
+  // block-kernel frame lengths: split the f32 samples afterwards
+  return srpgpu_split_bf16(samples_out, samples_ld ? samples_ld : total_samples, samples_ld ? 1 : 0, num_frames,
+                           total_samples, planes, cols8, stream);
 }
 
 extern "C" int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames,

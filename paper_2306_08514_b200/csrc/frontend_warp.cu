@@ -12,6 +12,8 @@
 //   * the inverse is pruned: only the 2N_p+1 kept lags (|n| <= N_p) are produced,
 //     i.e. outputs k1 in {0, LP-1} of the second step when N_p < 32.
 //   * frame energy for the PHAT floor by warp shuffles.
+#include <cuda_bf16.h>
+
 #include "frontend_warp.cuh"
 
 namespace srpgpu {
@@ -140,6 +142,18 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
     raw.y *= inv;
   }
   return raw;
+}
+
+// one xi sample: the f32 output and, when requested, its bf16 hi/lo planes
+__device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int col, float v) {
+  dst[col * sst] = v;
+  if (prm.xi_planes) {
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+    __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes) + f * prm.cols8 + col;
+    pl[0] = hi;
+    pl[prm.F * prm.cols8] = lo;
+  }
 }
 
 constexpr int kWarps = 4;   // per CTA
@@ -328,22 +342,29 @@ frontend_warp_kernel(const WarpParams prm) {
                 const int n = 32 * brev<LP>(i) + k2;
                 const float2 x = v[r * LP + i];
                 const int da = (n <= Na) ? n : ((L - n <= Na) ? 2 * Na + 1 - (L - n) : -1);
-                if (da >= 0) dst[(oa + da) * sst] = x.x;
+                if (da >= 0) put_xi(prm, dst, sst, f, oa + da, x.x);
                 const int db = (n <= Nb) ? n : ((L - n <= Nb) ? 2 * Nb + 1 - (L - n) : -1);
-                if (db >= 0) dst[(ob + db) * sst] = -x.y;
+                if (db >= 0) put_xi(prm, dst, sst, f, ob + db, -x.y);
               }
             } else {
               const float2 x0 = v[r * LP + 0];   // n = k2
               const float2 x1 = v[r * LP + 1];   // n = L - 32 + k2, distance d = 32 - k2
               const int d = 32 - k2;
-              if (k2 <= Na) dst[(oa + k2) * sst] = x0.x;
-              if (d <= Na) dst[(oa + 2 * Na + 1 - d) * sst] = x1.x;
-              if (k2 <= Nb) dst[(ob + k2) * sst] = -x0.y;
-              if (d <= Nb) dst[(ob + 2 * Nb + 1 - d) * sst] = -x1.y;
+              if (k2 <= Na) put_xi(prm, dst, sst, f, oa + k2, x0.x);
+              if (d <= Na) put_xi(prm, dst, sst, f, oa + 2 * Na + 1 - d, x1.x);
+              if (k2 <= Nb) put_xi(prm, dst, sst, f, ob + k2, -x0.y);
+              if (d <= Nb) put_xi(prm, dst, sst, f, ob + 2 * Nb + 1 - d, -x1.y);
             }
           }
         }
         __syncwarp();
+      }
+      if (prm.xi_planes && mi == 0) {                // zero the planes' pad columns [S, cols8)
+        uint16_t* pl = prm.xi_planes + f * prm.cols8;
+        for (int c = prm.S + lane; c < prm.cols8; c += 32) {
+          pl[c] = 0;
+          pl[prm.F * prm.cols8 + c] = 0;
+        }
       }
     }
     frame_sync<kWpf>(fg);                            // spectra free for the next frame

@@ -24,6 +24,10 @@ struct WarpParams {
   int32_t round_tf32;
   float* xi_out;
   int64_t xi_ld;   // 0: frame-major [F][S]; > 0: lag-major [S][xi_ld]
+  // optional bf16 hi/lo planes [2][F][cols8] of xi for the tensor-core interpolation map
+  // (interp_tc.cu): hi = bf16_rne(x), lo = bf16_rne(x - hi), zero in [S, cols8)
+  uint16_t* xi_planes;
+  int32_t cols8;
 };
 
 // 0: launched; 1: shape not covered (use the block kernel); < 0: error status.

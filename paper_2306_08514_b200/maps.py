@@ -260,21 +260,143 @@ def _check_cols(samples, num_cols: int) -> None:
                              f"{num_cols} columns")
 
 
-def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True):
-    """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195)."""
-    _check_cols(samples, int(sp.num_cols))         # reference DimensionError check first
-    op = band_from_sparse(sp, _sample_offsets(samples, int(sp.num_cols)))
+# ----------------------------------------------------------------- SSPI / SI on tensor cores
+
+ENGINES = ("auto", "tc", "band")
+TC_MAX_COLS = 2048          # dense rows beyond this many samples: the band engine
+TC_DENSITY = 12             # tensor cores while cols8 <= TC_DENSITY * kept entries per row
+
+
+def _cols8(n: int) -> int:
+    return (int(n) + 7) // 8 * 8
+
+
+class DenseInterpOperator:
+    """Dense bf16 hi/lo planes [2][J][cols8] of an interpolation operator (tensor-core engine).
+
+    The sparse fit's dropped entries are zeros, so the dense product equals the sparse
+    one (interpolation.py:121-126); operands are split x = bf16(x) + bf16(x - bf16(x)).
+    """
+
+    def __init__(self, mat32: np.ndarray):
+        j, s = mat32.shape
+        self.num_rows, self.num_cols, self.cols8 = j, s, _cols8(s)
+        src = torch.from_numpy(np.ascontiguousarray(mat32, dtype=np.float32)).to(dev.device())
+        self.planes = torch.empty((2, j, self.cols8), dtype=torch.bfloat16, device=src.device)
+        nat.call("srpgpu_split_bf16", dev.ptr(src), s, 0, j, s, dev.ptr(self.planes), self.cols8,
+                 dev.stream_ptr())
+
+
+def dense_from_sparse(sp) -> DenseInterpOperator:
+    def build():
+        splits = np.asarray(sp.row_splits, dtype=np.int64)
+        j, s = splits.shape[0] - 1, int(sp.num_cols)
+        mat = np.zeros((j, s), dtype=np.float32)
+        rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
+        mat[rows, np.asarray(sp.col_indices, dtype=np.int64)] = np.asarray(sp.values).astype(np.float32)
+        return DenseInterpOperator(mat)
+    return dev.CACHE.get(sp, "dense_bf16x2", build)
+
+
+def dense_from_matrix(interp) -> DenseInterpOperator:
+    return dev.CACHE.get(interp, "dense_bf16x2",
+                         lambda: DenseInterpOperator(np.asarray(interp.matrix).astype(np.float32)))
+
+
+def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto") -> str:
+    """'tc' (dense operator on the tensor cores) or 'band' (tiled-band SpMM on FP32)."""
+    if engine not in ENGINES:
+        raise ValueError(f"unknown engine {engine!r}")
+    if engine != "auto":
+        return engine
+    c8 = _cols8(num_cols)
+    return "tc" if c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0) else "band"
+
+
+def sample_planes(samples, num_cols: int):
+    """(bf16 planes [2][F][cols8], frames, batched) of any samples input.
+
+    Kernel-produced TdGccSamples may already carry the planes (`bf16_planes`).
+    """
+    planes = getattr(samples, "bf16_planes", None)
+    if planes is not None and planes.shape[2] == _cols8(num_cols):
+        vals = samples.values
+        batched = vals.dim() == 2
+        return planes, (vals.shape[0] if batched else 1), batched
+    c8 = _cols8(num_cols)
+    buf = getattr(samples, "lag_major", None)
+    if buf is not None and buf.shape[0] == num_cols:
+        vals = samples.values
+        batched = vals.dim() == 2
+        f = vals.shape[0] if batched else 1
+        planes = torch.empty((2, f, c8), dtype=torch.bfloat16, device=buf.device)
+        nat.call("srpgpu_split_bf16", dev.ptr(buf), buf.shape[1], 1, f, num_cols, dev.ptr(planes), c8,
+                 dev.stream_ptr())
+        return planes, f, batched
+    x, batched = _sample_matrix(samples, num_cols)
+    f = x.shape[0]
+    planes = torch.empty((2, f, c8), dtype=torch.bfloat16, device=x.device)
+    nat.call("srpgpu_split_bf16", dev.ptr(x), num_cols, 0, f, num_cols, dev.ptr(planes), c8, dev.stream_ptr())
+    return planes, f, batched
+
+
+def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
+    planes, f, batched = sample_planes(samples, op.num_cols)
+    z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    if op.num_rows == 0:
+        return _finish(z, keys, batched, argmax)
+    nat.call("srpgpu_interp_map_tc", dev.ptr(planes), f, dev.ptr(op.planes), op.num_rows, op.cols8,
+             dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+def uses_tc(variant: str, op, engine: str = "auto") -> bool:
+    """Whether sspi_map / si_map on this operator take the tensor-core engine."""
+    if variant == "si":
+        n = int(np.asarray(op.matrix).shape[1])
+        return interp_engine(n, n, engine) == "tc"
+    if variant == "sspi":
+        if hasattr(op, "kept") and np.ndim(getattr(op, "cols", None)) == 3:
+            return False
+        return interp_engine(int(op.num_cols), _kept_per_row(op), engine) == "tc"
+    return False
+
+
+def _kept_per_row(sp) -> float:
+    if hasattr(sp, "row_splits"):
+        j = max(1, np.asarray(sp.row_splits).shape[0] - 1)
+        return float(np.asarray(sp.values).shape[0]) / j
+    return float(np.sum(np.asarray(sp.kept)))            # fixed-nnz: k per (row, pair)
+
+
+def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
+    """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195).
+
+    engine "tc": the operator densified into bf16 hi/lo planes on the tensor cores
+    (3 MMA passes, ~1e-6 normalized error); "band": the tiled-band FP32 SpMM; "auto"
+    picks "tc" for short sample vectors relative to the kept entries per row.
+    """
+    num_cols = int(sp.num_cols)
+    _check_cols(samples, num_cols)                 # reference DimensionError check first
+    fixed = hasattr(sp, "kept") and np.ndim(getattr(sp, "cols", None)) == 3
+    eng = "band" if fixed else interp_engine(num_cols, _kept_per_row(sp), engine)
+    if eng == "tc":
+        return _tc_map(dense_from_sparse(sp), samples, argmax, out_map)
+    op = band_from_sparse(sp, _sample_offsets(samples, num_cols))
     return _band_map(op, samples, argmax, out_map)
 
 
-def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True):
+def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
     """Dense sampling+interpolation map z = Lambda xi (interpolation.py:129-136).
 
-    Runs the SSPI kernel on the keep-all band image, so sspi_map(keep=all) == si_map
-    bit for bit, as in the reference (interpolation.py:112-126).
+    Runs the same engine and operator image as sspi_map on the keep-all fit, so
+    sspi_map(keep=all) == si_map bit for bit, as in the reference (interpolation.py:112-126).
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
     _check_cols(samples, num_cols)
+    if interp_engine(num_cols, num_cols, engine) == "tc":
+        return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
         offsets = np.array([0, num_cols], dtype=np.int64)

@@ -29,7 +29,8 @@ class MapPipeline:
 
     def __init__(self, variant: str, op, frame, pairs, spec=None, frames: int = 1,
                  num_channels: int | None = None, weighting: str = "phat", floor=None,
-                 out_map: bool = True, precision: str = "tf32", graph: bool = True):
+                 out_map: bool = True, precision: str = "tf32", graph: bool = True,
+                 engine: str = "auto"):
         if variant not in self.VARIANTS:
             raise ValueError(f"unknown map variant {variant!r}")
         if variant == "conv_h":
@@ -39,6 +40,7 @@ class MapPipeline:
         self.variant, self.op, self.frame, self.pairs, self.spec = variant, op, frame, pairs, spec
         self.frames = int(frames)
         self.weighting, self.floor, self.out_map, self.precision = weighting, floor, out_map, precision
+        self.engine = engine              # sspi / si: "auto" | "tc" | "band" (maps.interp_engine)
         m = num_channels or pairs.num_mics
         n = (self.frames - 1) * frame.hop + frame.frame_len
         self.input = torch.zeros((m, n), dtype=torch.float32, device=device())
@@ -56,10 +58,13 @@ class MapPipeline:
         rng = range(0, self.frames)
         v = self.variant
         if v in ("sspi", "si", "slri"):
+            tc = maps.uses_tc(v, self.op, self.engine)
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
-                                            self.weighting, self.floor)
-            fn = {"sspi": maps.sspi_map, "si": maps.si_map, "slri": maps.slri_map}[v]
-            return fn(self.op, xi, argmax=True, out_map=self.out_map)
+                                            self.weighting, self.floor, planes=tc)
+            if v == "slri":
+                return maps.slri_map(self.op, xi, argmax=True, out_map=self.out_map)
+            fn = maps.sspi_map if v == "sspi" else maps.si_map
+            return fn(self.op, xi, argmax=True, out_map=self.out_map, engine="tc" if tc else "band")
         gcc = fe.gcc_frames(self.input, self.frame, self.pairs, rng, self.weighting, self.floor,
                             tf32=(v == "conv" and self.precision == "tf32"))
         if v == "lr":

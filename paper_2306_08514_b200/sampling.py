@@ -85,6 +85,8 @@ class TdGccSamples:
     values: torch.Tensor
     spec: object
     lag_major: object = field(default=None, repr=False, compare=False)
+    # bf16 hi/lo planes [2][F][cols8] for the tensor-core interpolation map (optional)
+    bf16_planes: object = field(default=None, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -113,8 +115,8 @@ def _new_samples(frames: int, s_total: int, dev_):
     return buf, ld, buf[:, :frames].t()
 
 
-def _wrap(view, buf, spec, batched: bool) -> "TdGccSamples":
-    return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf)
+def _wrap(view, buf, spec, batched: bool, planes=None) -> "TdGccSamples":
+    return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf, bf16_planes=planes)
 
 
 def _check_gcc(gcc, spec) -> None:
@@ -141,10 +143,12 @@ def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
 
 
 def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
-                      floor=None) -> TdGccSamples:
+                      floor=None, planes: bool = False) -> TdGccSamples:
     """Fused stft_frame -> fd_gcc -> td_gcc_samples for a range of frames.
 
-    Neither the spectra nor the cross-spectra touch HBM; one kernel launch.
+    Neither the spectra nor the cross-spectra touch HBM; one kernel launch.  With
+    `planes` the same kernel also writes the bf16 hi/lo planes the tensor-core
+    interpolation map reads (`bf16_planes`).
     """
     x = _signal(samples)
     if x.shape[0] != pairs.num_mics:
@@ -157,11 +161,16 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
     counts, offsets = _spec_device(spec)
     s_total = int(spec_offsets(spec)[-1])
     buf, ld, view = _new_samples(count, s_total, x.device)
-    nat.call("srpgpu_frames_to_samples", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
-             dev.ptr(_window_device(frame)), frame.frame_len, frame.hop, first, count,
-             dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
-             dev.ptr(offsets), s_total, dev.ptr(buf), ld, dev.stream_ptr())
-    return _wrap(view, buf, spec, batched)
+    args = (dev.ptr(x), x.shape[0], x.shape[1], x.shape[1], dev.ptr(_window_device(frame)), frame.frame_len,
+            frame.hop, first, count, dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval,
+            dev.ptr(counts), dev.ptr(offsets), s_total, dev.ptr(buf), ld)
+    if not planes:
+        nat.call("srpgpu_frames_to_samples", *args, dev.stream_ptr())
+        return _wrap(view, buf, spec, batched)
+    cols8 = (s_total + 7) // 8 * 8
+    pl = torch.empty((2, count, cols8), dtype=torch.bfloat16, device=x.device)
+    nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, dev.stream_ptr())
+    return _wrap(view, buf, spec, batched, pl)
 
 
 def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:

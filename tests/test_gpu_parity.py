@@ -102,24 +102,45 @@ def test_fused_frames_to_samples(golden_scene):
 
 # ------------------------------------------------------------------ maps
 
-def test_sspi_and_si_maps(golden_scene):
+@pytest.mark.parametrize("engine", ["tc", "band"])
+def test_sspi_and_si_maps(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     xi = s.TdGccSamples(torch.from_numpy(g["xi_ifft"].astype(np.float32)).cuda(), spec)
     for tag in keep_tags(g):
         sp = sparse_from_golden(g, tag)
-        z, idx = s.sspi_map(sp, xi, argmax=True)
+        z, idx = s.sspi_map(sp, xi, argmax=True, engine=engine)
         ref = g[f"z_sspi_{tag}"]
         if np.abs(ref).max() == 0:
             assert np.all(np_(z) == 0)
             continue
         assert_map_close(z, ref)
         assert_argmax_agrees(idx, ref)
+        zo, io = s.sspi_map(sp, xi, argmax=True, out_map=False, engine=engine)
+        assert zo is None and torch.equal(io, idx)         # argmax-only output
     interp = s.InterpMatrix(g["interp"], spec)
-    z_si = s.si_map(interp, xi)
+    z_si = s.si_map(interp, xi, engine=engine)
     assert_map_close(z_si, g["z_si"])
-    z_all = s.sspi_map(sparse_from_golden(g, "all"), xi)
+    z_all = s.sspi_map(sparse_from_golden(g, "all"), xi, engine=engine)
     assert torch.equal(z_all, z_si)                        # bitwise, as in the reference
+
+
+def test_sspi_engines_agree_on_frame_batches(golden_scene):
+    """Tensor-core engine: a frame's map does not depend on its batch or tile position,
+    matches the band engine within the parity bar, and covers F / J tails of the tiles."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    x = np.tile(g["xi_ifft"].astype(np.float32), (70, 1))[:300]   # 3 frame tiles, ragged
+    xt = s.TdGccSamples(torch.from_numpy(x).cuda(), spec)
+    zt, it = s.sspi_map(sp, xt, argmax=True, engine="tc")
+    zb, ib = s.sspi_map(sp, xt, argmax=True, engine="band")
+    z1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tc")
+    assert torch.equal(zt[7], z1)
+    ref = O.sspi_map(sp.values, sp.col_indices, sp.row_splits, x.astype(np.float64))
+    assert_map_close(zt, ref)
+    assert_map_close(zb, ref)
+    assert_argmax_agrees(it, ref)
 
 
 def test_sspi_tile_and_row_kernels_agree(golden_scene):
