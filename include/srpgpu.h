@@ -161,6 +161,22 @@ int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t num_frames
                     int64_t num_candidates, float* work, float* z, uint64_t* keys,
                     srpgpu_stream_t stream);
 
+/* slri_map with the candidate product on the tensor cores: work [F][R] = fat . xi
+ * (fp32, work holds 17 * F * R floats as for srpgpu_slri_map), split into bf16 planes
+ * work_planes [2][F][cols8], then z = tall . work^T by srpgpu_interp_map_tc against
+ * tall_planes [2][J][cols8] (srpgpu_split_bf16 of tall; cols8 >= R, multiple of 8). */
+int srpgpu_slri_map_tc(const float* samples, int64_t samples_ld, int64_t num_frames,
+                       int32_t total_samples, const float* fat, const void* tall_planes, int32_t rank,
+                       int32_t cols8, int64_t num_candidates, float* work, void* work_planes, float* z,
+                       uint64_t* keys, srpgpu_stream_t stream);
+
+/* lr_map with the candidate product on the tensor cores; tall2_planes = planes of
+ * [2 Re tall, -2 Im tall] ([2][J][cols8], cols8 >= 2R); work 17 * F * 2R floats,
+ * work_planes [2][F][cols8]. */
+int srpgpu_lr_map_tc(const float* gcc, int64_t num_frames, int32_t gcc_len, const float* fat2,
+                     const void* tall2_planes, int32_t rank, int32_t cols8, int64_t num_candidates,
+                     float* work, void* work_planes, float* z, uint64_t* keys, srpgpu_stream_t stream);
+
 /* lr_map (lowrank.py:51-57): z = 2 Re(tall (fat psi)).  Complex factors folded
  * into real ones once on the host: fat2 [2R][2PB] with rows r: (Re fat, -Im fat)
  * and R+r: (Im fat, Re fat) interleaved per bin; tall2 [J][2R] = (2 Re tall | -2 Im tall).

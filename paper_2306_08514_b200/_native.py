@@ -42,6 +42,8 @@ SIGNATURES = {
     "srpgpu_interp_map_tc": [_P, _I64, _P, _I64, _I32, _P, _P, _P],
     "srpgpu_split_bf16": [_P, _I64, _I32, _I64, _I32, _P, _I32, _P],
     "srpgpu_slri_map": [_P, _I64, _I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
+    "srpgpu_slri_map_tc": [_P, _I64, _I64, _I32, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P],
+    "srpgpu_lr_map_tc": [_P, _I64, _I32, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "srpgpu_lr_map": [_P, _I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_srp_map_simt": [_P, _I64, _I32, _P, _I64, _P, _P, _P],
     "srpgpu_srp_map_tc": [_P, _I64, _I64, _I32, _P, _I64, _I64, _P, _P, _P],

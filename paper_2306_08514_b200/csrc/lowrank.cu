@@ -371,6 +371,44 @@ extern "C" int srpgpu_slri_map(const float* samples, int64_t samples_ld, int64_t
                      keys, st, "slri_map(tall)");
 }
 
+// The rank-R candidate products on the tensor cores: the factor product work[F][R]
+// (fp32 SIMT, as above) is split into bf16 hi/lo planes and z = tall . work^T runs on
+// the dense-operand tcgen05 kernel of interp_tc.cu (K = R: the product is bound by the
+// z write, not by the MMA).  tall_planes: [2][J][cols8] (srpgpu_split_bf16 of tall).
+extern "C" int srpgpu_slri_map_tc(const float* samples, int64_t samples_ld, int64_t num_frames,
+                                  int32_t total_samples, const float* fat, const void* tall_planes,
+                                  int32_t rank, int32_t cols8, int64_t num_candidates, float* work,
+                                  void* work_planes, float* z, uint64_t* keys, srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rank >= 1 && cols8 >= rank && cols8 % 8 == 0, SRPGPU_ERR_VALUE,
+                   "slri_map_tc: rank must be >= 1 and cols8 >= rank, a multiple of 8");
+  cudaStream_t st = as_stream(stream);
+  if (num_frames <= 0) return srpgpu_interp_map_tc(work_planes, 0, tall_planes, num_candidates, cols8, z, keys, stream);
+  int s = gemm_nt(fat, total_samples, samples, samples_ld ? samples_ld : total_samples, work, rank, rank,
+                  num_frames, total_samples, 1.0f, nullptr, st, "slri_map(fat)", samples_ld != 0,
+                  work + num_frames * (int64_t)rank);
+  if (s) return s;
+  if ((s = srpgpu_split_bf16(work, rank, 0, num_frames, rank, work_planes, cols8, stream))) return s;
+  return srpgpu_interp_map_tc(work_planes, num_frames, tall_planes, num_candidates, cols8, z, keys, stream);
+}
+
+// lr_map with the output product on the tensor cores; tall2_planes = split of
+// [2 Re tall, -2 Im tall] ([2][J][cols8], cols8 >= 2R).
+extern "C" int srpgpu_lr_map_tc(const float* gcc, int64_t num_frames, int32_t gcc_len, const float* fat2,
+                                const void* tall2_planes, int32_t rank, int32_t cols8, int64_t num_candidates,
+                                float* work, void* work_planes, float* z, uint64_t* keys,
+                                srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rank >= 1 && cols8 >= 2 * rank && cols8 % 8 == 0, SRPGPU_ERR_VALUE,
+                   "lr_map_tc: rank must be >= 1 and cols8 >= 2 rank, a multiple of 8");
+  cudaStream_t st = as_stream(stream);
+  if (num_frames <= 0) return srpgpu_interp_map_tc(work_planes, 0, tall2_planes, num_candidates, cols8, z, keys, stream);
+  int s = gemm_nt(fat2, 2 * (int64_t)gcc_len, gcc, 2 * (int64_t)gcc_len, work, 2 * rank, 2 * rank, num_frames,
+                  2 * (int64_t)gcc_len, 1.0f, nullptr, st, "lr_map(fat)", false,
+                  work + num_frames * (int64_t)(2 * rank));
+  if (s) return s;
+  if ((s = srpgpu_split_bf16(work, 2 * rank, 0, num_frames, 2 * rank, work_planes, cols8, stream))) return s;
+  return srpgpu_interp_map_tc(work_planes, num_frames, tall2_planes, num_candidates, cols8, z, keys, stream);
+}
+
 extern "C" int srpgpu_lr_map(const float* gcc, int64_t num_frames, int32_t gcc_len,
                              const float* fat2, const float* tall2, int32_t rank,
                              int64_t num_candidates, float* work, float* z, uint64_t* keys,

@@ -79,6 +79,18 @@ __device__ __forceinline__ uint64_t smem_desc(const void* p) {
   return d;
 }
 
+// K-major operand tile with a 64-byte swizzle: rows of 64 B, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t smem_desc_sw64(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
+  return d;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -127,7 +139,8 @@ inline EncodeTiledFn encode_fn() {
 // swizzle, box = box_cols x box_rows (box_cols * elem_bytes <= 128); out-of-range
 // elements of a load are zero-filled, of a store clipped.
 inline int make_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, int elem_bytes, const void* base, int64_t rows,
-                       int64_t cols, int64_t ld, int box_cols, int box_rows, const char* what) {
+                       int64_t cols, int64_t ld, int box_cols, int box_rows, const char* what,
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) {
     set_error("%s: cuTensorMapEncodeTiled unavailable", what);
@@ -138,7 +151,7 @@ inline int make_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, int elem_byt
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("%s: cuTensorMapEncodeTiled failed (%d)", what, (int)r);
     return SRPGPU_ERR_LAUNCH;

@@ -412,8 +412,24 @@ def _slri_device(lr):
     return dev.CACHE.get(lr, "slri_f32", build)
 
 
-def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True):
-    """Low-rank interpolation map z = tall (fat xi) (interpolation.py:178-185)."""
+def _planes_of(mat32: np.ndarray) -> DenseInterpOperator:
+    return DenseInterpOperator(mat32)
+
+
+def _lowrank_engine(engine: str) -> str:
+    """'tc': the rank-R candidate product on the tensor cores (z-write bound); 'simt': fp32."""
+    if engine not in ("auto", "tc", "simt"):
+        raise ValueError(f"unknown engine {engine!r}")
+    return "simt" if engine == "simt" else "tc"
+
+
+def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
+    """Low-rank interpolation map z = tall (fat xi) (interpolation.py:178-185).
+
+    The factor product fat.xi runs in fp32; engine "tc" (default) evaluates the
+    candidate product tall.(fat xi) on the tensor cores with bf16 hi/lo operands
+    (~1e-6 normalized error), "simt" in fp32 SIMT.
+    """
     fat = np.asarray(lr.fat)
     buf, f, batched = _lag_major(samples, fat.shape[1])
     d_fat, d_tall = _slri_device(lr)
@@ -421,6 +437,14 @@ def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True):
     work = torch.empty((17, f, r), dtype=torch.float32, device=buf.device)   # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
+    if _lowrank_engine(engine) == "tc":
+        tp = dev.CACHE.get(lr, "slri_tall_bf16x2",
+                           lambda: _planes_of(np.asarray(lr.tall, dtype=np.float64).astype(np.float32)))
+        wp = torch.empty((2, f, tp.cols8), dtype=torch.bfloat16, device=buf.device)
+        nat.call("srpgpu_slri_map_tc", dev.ptr(buf), buf.shape[1], f, fat.shape[1], dev.ptr(d_fat),
+                 dev.ptr(tp.planes), r, tp.cols8, j, dev.ptr(work), dev.ptr(wp), dev.ptr(z), dev.ptr(keys),
+                 dev.stream_ptr())
+        return _finish(z, keys, batched, argmax)
     nat.call("srpgpu_slri_map", dev.ptr(buf), buf.shape[1], f, fat.shape[1], dev.ptr(d_fat),
              dev.ptr(d_tall), r, j, dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
@@ -439,8 +463,12 @@ def _lr_device(lr):
     return dev.CACHE.get(lr, "lr_f32", build)
 
 
-def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True):
-    """Low-rank SRP map z = 2 Re(tall (fat psi)) (lowrank.py:51-57)."""
+def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
+    """Low-rank SRP map z = 2 Re(tall (fat psi)) (lowrank.py:51-57).
+
+    engine as for slri_map: "tc" (default) runs the candidate product on the tensor
+    cores, "simt" in fp32.
+    """
     fat = np.asarray(lr.fat)
     vals = gcc if isinstance(gcc, (torch.Tensor, np.ndarray)) else gcc.values
     v = dev.as_c64(vals)
@@ -454,6 +482,12 @@ def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True):
     work = torch.empty((17, f, 2 * r), dtype=torch.float32, device=v.device)  # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
     keys = _new_keys(f, argmax)
+    if _lowrank_engine(engine) == "tc":
+        tp = dev.CACHE.get(lr, "lr_tall2_bf16x2", lambda: _planes_of(d_tall2.cpu().numpy()))
+        wp = torch.empty((2, f, tp.cols8), dtype=torch.bfloat16, device=v.device)
+        nat.call("srpgpu_lr_map_tc", dev.ptr(v), f, fat.shape[1], dev.ptr(d_fat2), dev.ptr(tp.planes), r,
+                 tp.cols8, j, dev.ptr(work), dev.ptr(wp), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+        return _finish(z, keys, batched, argmax)
     nat.call("srpgpu_lr_map", dev.ptr(v), f, fat.shape[1], dev.ptr(d_fat2), dev.ptr(d_tall2), r, j,
              dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)

@@ -165,27 +165,29 @@ def test_sspi_empty_operator_and_dimension_error(golden_scene):
         s.sspi_map(sp0, torch.ones(spec.total_samples + 1, device="cuda"))
 
 
-def test_slri_map(golden_scene):
+@pytest.mark.parametrize("engine", ["tc", "simt"])
+def test_slri_map(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     xi = torch.from_numpy(g["xi_ifft"].astype(np.float32)).cuda()
     for r in g["ranks"]:
         lr = s.LowRankInterp(g[f"slri_{r}_tall"], g[f"slri_{r}_fat"], np.zeros(r))
-        z, idx = s.slri_map(lr, xi, argmax=True)
+        z, idx = s.slri_map(lr, xi, argmax=True, engine=engine)
         assert_map_close(z, g[f"z_slri_{r}"])
         assert_argmax_agrees(idx, g[f"z_slri_{r}"])
     with pytest.raises(s.DimensionError):
         s.slri_map(lr, torch.zeros(3, device="cuda"))
 
 
-def test_lr_map(golden_scene):
+@pytest.mark.parametrize("engine", ["tc", "simt"])
+def test_lr_map(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
     psi = torch.from_numpy(g["psi"].astype(np.complex64)).cuda()
     for r in g["ranks"]:
         lr = s.LowRankSrp(g[f"lr_{r}_tall"], g[f"lr_{r}_fat"], np.zeros(r))
         gcc = s.FdGcc(psi, pairs.num_pairs, frame.num_bins, "phat")
-        z, idx = s.lr_map(lr, gcc, argmax=True)
+        z, idx = s.lr_map(lr, gcc, argmax=True, engine=engine)
         assert_map_close(z, g[f"z_lr_{r}"])
         assert_argmax_agrees(idx, g[f"z_lr_{r}"])
 

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nnz", default="2jp")
     ap.add_argument("--rank", type=int, default=16)
+    ap.add_argument("--engine", default="auto", help="sspi / si / slri / lr map engine")
     a = ap.parse_args()
     frames = a.frames or {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000}.get(a.workload, 1000)
     wl = workloads.make(a.workload, num_frames=frames)
@@ -43,10 +44,12 @@ def main():
             op = s.truncate_low_rank(interp, a.rank)
         else:
             op = interp
+        from paper_2306_08514_b200 import maps
         fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
+        planes = maps.uses_tc(a.variant, op, a.engine)
         for _ in range(a.reps):
-            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng)
-            z, idx = fn(op, xi, argmax=True)
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=planes)
+            z, idx = fn(op, xi, argmax=True, engine=a.engine)
     elif a.variant == "conv":          # on-chip steering (bench variant "conv")
         op = s.steering_operator(wl.tdoa, wl.frame)
         for _ in range(a.reps):
@@ -57,7 +60,8 @@ def main():
         op = srp if a.variant == "conv_h" else s.truncate_srp_matrix(srp, a.rank)
         for _ in range(a.reps):
             g = s.gcc_frames(x, wl.frame, wl.pairs, rng, tf32=(a.variant == "conv_h"))
-            z, idx = (s.srp_map_exact if a.variant == "conv_h" else s.lr_map)(op, g, argmax=True)
+            z, idx = (s.srp_map_exact(op, g, argmax=True) if a.variant == "conv_h"
+                      else s.lr_map(op, g, argmax=True, engine=a.engine))
     torch.cuda.synchronize()
     print("ok", a.workload, a.variant, frames, int(idx[0]))
 
