@@ -154,12 +154,13 @@ def map_flops(wl, variant, op, frames):
     return conv_flops(wl, frames)
 
 
-def ncu_traffic(workload: str, kernel: str):
+def ncu_traffic(workload: str, variant: str, kernel: str):
+    """Per-launch DRAM bytes of `kernel` from one `ncu --set full` capture (profiles/traffic.json)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(workload, {}).get(kernel)
-    except (OSError, ValueError):
+            return json.load(f).get(workload, {}).get(variant, {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -207,7 +208,7 @@ def algorithmic_bytes(wl, variant, frames, op, engine="auto"):
     out = {"frontend": frames * (4 * m * hop + (4 * s_tot if variant in ("sspi", "slri", "si") else 8 * p * b))}
     if variant in ("sspi", "si"):
         from paper_2306_08514_b200 import maps
-        if maps.uses_tc(variant, op, engine):   # dense bf16 hi/lo planes: 4 B per sample slot
+        if maps.uses_tc(variant, op, engine, frames):   # dense bf16 hi/lo planes: 4 B per sample slot
             c8 = (s_tot + 7) // 8 * 8
             out["map"] = frames * (4 * c8 + 4 * j) + 4 * j * c8
         else:
@@ -313,7 +314,7 @@ def run_ours(args):
         roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": tf32_peak,
                 "unit": "TFLOP/s", "frac": achieved / tf32_peak,
                 "peak_source": f"TF32 cuBLAS {xsrc}", "frac_of_bf16_peak": achieved / bf16,
-                "traffic": ncu_traffic(args.workload, dom_name)}
+                "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
     else:
         if t_map >= t_front:
             dom_name, dom_ms, dom_bytes = f"{args.variant}_map", t_map, abytes["map"]
@@ -323,10 +324,10 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dom_bytes,
-                "traffic": ncu_traffic(args.workload, dom_name)}
+                "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
     from paper_2306_08514_b200 import maps as _maps
-    if _maps.uses_tc(args.variant, op, args.engine):
+    if _maps.uses_tc(args.variant, op, args.engine, count):
         # tensor-core interpolation engine: 3 bf16 MMA passes over the dense operator
         c8 = (wl.spec.total_samples + 7) // 8 * 8
         tflops = 3 * 2.0 * wl.grid.num_points * c8 * count / (t_map / 1e3) / 1e12
@@ -433,7 +434,8 @@ def run_ours(args):
                                      f"{int(op.values.shape[2])} nnz per (candidate, pair)")
                                     if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
-                       "map_engine": (("tensor cores (dense bf16x3)" if _maps.uses_tc(args.variant, op, args.engine)
+                       "map_engine": (("tensor cores (dense bf16x3)" if _maps.uses_tc(args.variant, op, args.engine,
+                                                                                      count)
                                        else "FP32 tiled band") if args.variant in ("sspi", "si") else None),
                        "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
                        "execution": "CUDA graph per batch"},
@@ -470,7 +472,7 @@ def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto")
     frames = range(0, count)
     if variant in ("sspi", "si", "slri"):
         from paper_2306_08514_b200 import maps
-        tc = maps.uses_tc(variant, op, engine)  # the pipeline's frontend also writes the bf16 planes
+        tc = maps.uses_tc(variant, op, engine, count)  # the pipeline's frontend also writes the planes
         front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames, planes=tc)
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
         if variant != "slri":

@@ -303,12 +303,17 @@ def dense_from_matrix(interp) -> DenseInterpOperator:
                          lambda: DenseInterpOperator(np.asarray(interp.matrix).astype(np.float32)))
 
 
-def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto") -> str:
+TC_MIN_FRAMES = 0           # batches below this take the band engine (set from the cfg5 batch sweep)
+
+
+def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None) -> str:
     """'tc' (dense operator on the tensor cores) or 'band' (tiled-band SpMM on FP32)."""
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}")
     if engine != "auto":
         return engine
+    if frames is not None and frames < TC_MIN_FRAMES:
+        return "band"
     c8 = _cols8(num_cols)
     return "tc" if c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0) else "band"
 
@@ -351,16 +356,23 @@ def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
     return _finish(z, keys, batched, argmax)
 
 
-def uses_tc(variant: str, op, engine: str = "auto") -> bool:
-    """Whether sspi_map / si_map on this operator take the tensor-core engine."""
+def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -> bool:
+    """Whether sspi_map / si_map on this operator (and batch size) take the tensor-core engine."""
     if variant == "si":
         n = int(np.asarray(op.matrix).shape[1])
-        return interp_engine(n, n, engine) == "tc"
+        return interp_engine(n, n, engine, frames) == "tc"
     if variant == "sspi":
         if hasattr(op, "kept") and np.ndim(getattr(op, "cols", None)) == 3:
             return False
-        return interp_engine(int(op.num_cols), _kept_per_row(op), engine) == "tc"
+        return interp_engine(int(op.num_cols), _kept_per_row(op), engine, frames) == "tc"
     return False
+
+
+def _num_frames(samples) -> int:
+    plain = isinstance(samples, (torch.Tensor, np.ndarray, list, tuple))
+    vals = samples if plain else samples.values
+    shape = tuple(vals.shape) if hasattr(vals, "shape") else np.shape(vals)
+    return int(shape[0]) if len(shape) == 2 else 1
 
 
 def _kept_per_row(sp) -> float:
@@ -380,7 +392,7 @@ def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True, engine:
     num_cols = int(sp.num_cols)
     _check_cols(samples, num_cols)                 # reference DimensionError check first
     fixed = hasattr(sp, "kept") and np.ndim(getattr(sp, "cols", None)) == 3
-    eng = "band" if fixed else interp_engine(num_cols, _kept_per_row(sp), engine)
+    eng = "band" if fixed else interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples))
     if eng == "tc":
         return _tc_map(dense_from_sparse(sp), samples, argmax, out_map)
     op = band_from_sparse(sp, _sample_offsets(samples, num_cols))
@@ -395,7 +407,7 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engin
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
     _check_cols(samples, num_cols)
-    if interp_engine(num_cols, num_cols, engine) == "tc":
+    if interp_engine(num_cols, num_cols, engine, _num_frames(samples)) == "tc":
         return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
@@ -416,11 +428,20 @@ def _planes_of(mat32: np.ndarray) -> DenseInterpOperator:
     return DenseInterpOperator(mat32)
 
 
-def _lowrank_engine(engine: str) -> str:
-    """'tc': the rank-R candidate product on the tensor cores (z-write bound); 'simt': fp32."""
+LOWRANK_TC_MIN_OUTPUTS = 1 << 24   # frames x candidates from which the tensor-core product wins
+
+
+def _lowrank_engine(engine: str, outputs: int) -> str:
+    """'tc': the rank-R candidate product on the tensor cores (z-write bound); 'simt': fp32.
+
+    "auto" takes the tensor cores for large maps (cfg3: SLRI 0.88 -> 0.72 ms per 10^4
+    frames) and fp32 SIMT for small ones (cfg2: 70 vs 81 us, launch-latency bound).
+    """
     if engine not in ("auto", "tc", "simt"):
         raise ValueError(f"unknown engine {engine!r}")
-    return "simt" if engine == "simt" else "tc"
+    if engine == "auto":
+        return "tc" if outputs >= LOWRANK_TC_MIN_OUTPUTS else "simt"
+    return engine
 
 
 def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
@@ -437,7 +458,7 @@ def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True, engine:
     work = torch.empty((17, f, r), dtype=torch.float32, device=buf.device)   # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=buf.device) if out_map else None
     keys = _new_keys(f, argmax)
-    if _lowrank_engine(engine) == "tc":
+    if _lowrank_engine(engine, f * j) == "tc":
         tp = dev.CACHE.get(lr, "slri_tall_bf16x2",
                            lambda: _planes_of(np.asarray(lr.tall, dtype=np.float64).astype(np.float32)))
         wp = torch.empty((2, f, tp.cols8), dtype=torch.bfloat16, device=buf.device)
@@ -482,7 +503,7 @@ def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True, engine: str =
     work = torch.empty((17, f, 2 * r), dtype=torch.float32, device=v.device)  # + split-K partials
     z = torch.empty((f, j), dtype=torch.float32, device=v.device) if out_map else None
     keys = _new_keys(f, argmax)
-    if _lowrank_engine(engine) == "tc":
+    if _lowrank_engine(engine, f * j) == "tc":
         tp = dev.CACHE.get(lr, "lr_tall2_bf16x2", lambda: _planes_of(d_tall2.cpu().numpy()))
         wp = torch.empty((2, f, tp.cols8), dtype=torch.bfloat16, device=v.device)
         nat.call("srpgpu_lr_map_tc", dev.ptr(v), f, fat.shape[1], dev.ptr(d_fat2), dev.ptr(tp.planes), r,

@@ -58,7 +58,7 @@ class MapPipeline:
         rng = range(0, self.frames)
         v = self.variant
         if v in ("sspi", "si", "slri"):
-            tc = maps.uses_tc(v, self.op, self.engine)
+            tc = maps.uses_tc(v, self.op, self.engine, self.frames)
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
                                             self.weighting, self.floor, planes=tc)
             if v == "slri":

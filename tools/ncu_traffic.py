@@ -2,10 +2,11 @@
 
     python tools/ncu_traffic.py cfg2:sspi:profiles/r1_full_cfg2_sspi_raw.csv ... > profiles/traffic.json
 
-Each argument is workload:variant:csv.  Kernels are keyed the way bench.py names the
-dominant kernel (`frontend`, `<variant>_map`, `srp_map_tc` for the stored-operator
-tensor-core map, `srp_map_tdoa` for the on-chip-steering one); the value is
-dram__bytes_read.sum + dram__bytes_write.sum averaged over that kernel's launches.
+Each argument is workload:variant:csv.  Output: {workload: {variant: {kernel: bytes}}}
+with kernels keyed the way bench.py names the dominant kernel (`frontend`,
+`<variant>_map`, `srp_map_tc` for the stored-operator tensor-core map, `srp_map_tdoa`
+for the on-chip-steering one; `<variant>_factor` for the low-rank factor product); the
+value is dram__bytes_read.sum + dram__bytes_write.sum averaged over that kernel's launches.
 """
 
 import csv
@@ -21,10 +22,12 @@ def key_of(name: str, variant: str):
     if "conv_gen_chunked_kernel" in name:
         targs = name.split("conv_gen_chunked_kernel<", 1)[1].split(">", 1)[0].replace(" ", "")
         return "srp_map_tdoa" if targs.endswith(("true", "1")) else "srp_map_tc"   # <SPLIT, GEN>
-    if "sspi" in name:
-        return "sspi_map"
-    if "gemm_nt" in name or "splitk" in name:
+    if "sspi" in name or "interp_tc" in name:
         return f"{variant}_map"
+    if "lowrank_out" in name:
+        return f"{variant}_map"
+    if "gemm_nt" in name or "splitk" in name or "split_bf16" in name:
+        return f"{variant}_factor"
     return None
 
 
@@ -45,7 +48,7 @@ def main(args):
                  + float(r[iw].replace(",", "")) * UNITS.get(units[iw], 1))
             acc.setdefault(k, []).append(b)
         for k, v in acc.items():
-            out.setdefault(workload, {})[k] = sum(v) / len(v)
+            out.setdefault(workload, {}).setdefault(variant, {})[k] = sum(v) / len(v)
         out.setdefault("_sources", {})[f"{workload}:{variant}"] = path
     json.dump(out, sys.stdout, indent=1, sort_keys=True)
     print()

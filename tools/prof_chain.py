@@ -46,7 +46,7 @@ def main():
             op = interp
         from paper_2306_08514_b200 import maps
         fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
-        planes = maps.uses_tc(a.variant, op, a.engine)
+        planes = maps.uses_tc(a.variant, op, a.engine, frames)
         for _ in range(a.reps):
             xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=planes)
             z, idx = fn(op, xi, argmax=True, engine=a.engine)

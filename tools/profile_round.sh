@@ -8,7 +8,7 @@ mkdir -p $out
 full() {   # name workload variant kernel-regex frames
   local name=$1 wl=$2 var=$3 rx=$4 fr=$5
   timeout 600 python tools/prof_chain.py --workload $wl --variant $var --frames $fr --reps 2 || return 1
-  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$rx" -s 2 -c 2 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$rx" -s ${6:-2} -c ${7:-2} \
     -o $out/${tag}_full_${name} -f python tools/prof_chain.py --workload $wl --variant $var --frames $fr --reps 2 \
     > $out/${tag}_full_${name}.log 2>&1
   ncu -i $out/${tag}_full_${name}.ncu-rep --page raw --csv > $out/${tag}_full_${name}_raw.csv
@@ -20,8 +20,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   > $out/${tag}_launches_ncu.log 2>&1
 echo "launches rc=$?"
 full cfg2_sspi cfg2 sspi "frontend|sspi" 1000
-full cfg3_sspi cfg3 sspi "frontend|sspi" 10000
-full cfg3_slri cfg3 slri "frontend|gemm|splitk" 10000
+full cfg3_sspi cfg3 sspi "frontend|sspi|interp_tc" 10000
+full cfg3_slri cfg3 slri "frontend|gemm|splitk|interp_tc|split_bf16" 10000 5 5
 full cfg3_conv cfg3 conv "frontend|conv_gen" 10000
 full cfg3_conv_h cfg3 conv_h "frontend|conv_gen" 10000
 full cfg4_sspi cfg4 sspi "frontend|sspi" 10000
