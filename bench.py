@@ -303,6 +303,7 @@ def run_ours(args):
     # kernels per step: counted when the graph was captured (replays do not pass the host counter)
     launches_per_step = pipe_launches(pipe)
 
+    from paper_2306_08514_b200 import maps as _maps
     # ---- per-kernel times for the roofline: each stage captured alone, CUDA events
     t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush, engine=args.engine)
     hbm, bf16, peak_src = peaks()
@@ -326,7 +327,6 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
-    from paper_2306_08514_b200 import maps as _maps
     if _maps.uses_tc(args.variant, op, args.engine, count):
         # tensor-core interpolation engine: 3 bf16 MMA passes over the dense operator
         c8 = (wl.spec.total_samples + 7) // 8 * 8
@@ -337,7 +337,8 @@ def run_ours(args):
     roof["fp32_frac"] = {
         "frontend": frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak,
         "map": (map_flops(wl, args.variant, op, count) / (t_map / 1e3) / 1e12 / fp32_peak
-                if args.variant not in ("conv", "conv_h") else None),
+                if args.variant not in ("conv", "conv_h") and not _maps.uses_tc(args.variant, op, args.engine, count)
+                else None),
         "fp32_peak_tflops": fp32_peak, "peak_source": f"FP32 SIMT cuBLAS {xsrc}"}
 
     # ---- e2e through the public streaming API: pinned host samples in, argmax indices out.

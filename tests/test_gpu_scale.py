@@ -112,16 +112,17 @@ def cfg3():
     return wl, x, psi_ref, xi_ref
 
 
-def test_cfg3_full_grid(cfg3):
+@pytest.mark.parametrize("engine", ["tc", "band"])
+def test_cfg3_full_grid(cfg3, engine):
     wl, x, psi_ref, xi_ref = cfg3
     assert wl.grid.num_points == 32760 and wl.pairs.num_pairs == 28
-    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec)
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, planes=(engine == "tc"))
     interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame)
     sp = s.truncate_sparse(interp, 2 * wl.grid.num_points * wl.pairs.num_pairs)
-    z, idx = s.sspi_map(sp, xi, argmax=True)
+    z, idx = s.sspi_map(sp, xi, argmax=True, engine=engine)
     check(z, O.sspi_map(sp.values, sp.col_indices, sp.row_splits, xi_ref), idx)
     lr = s.truncate_low_rank(interp, 16)
-    z, idx = s.slri_map(lr, xi, argmax=True)
+    z, idx = s.slri_map(lr, xi, argmax=True, engine="tc" if engine == "tc" else "simt")
     check(z, O.slri_map(lr.tall, lr.fat, xi_ref), idx)
     # pole rows (polar 180 deg, 360 azimuths) are exact duplicates -> identical map values
     zz = z[:, -360:]
