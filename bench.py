@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "conv_h", "si"])
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
-    ap.add_argument("--engine", default="auto", choices=["auto", "tc", "band"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "tc", "tile", "band"],
                     help="SSPI / SI map engine (maps.interp_engine)")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--variants", default="sspi,slri,lr,conv,conv_h",
@@ -208,9 +208,13 @@ def algorithmic_bytes(wl, variant, frames, op, engine="auto"):
     out = {"frontend": frames * (4 * m * hop + (4 * s_tot if variant in ("sspi", "slri", "si") else 8 * p * b))}
     if variant in ("sspi", "si"):
         from paper_2306_08514_b200 import maps
-        if maps.uses_tc(variant, op, engine, frames):   # dense bf16 hi/lo planes: 4 B per sample slot
-            c8 = (s_tot + 7) // 8 * 8
+        eng = maps.map_engine(variant, op, engine, frames)
+        c8 = (s_tot + 7) // 8 * 8
+        if eng == "tc":                                 # dense bf16 hi/lo planes: 4 B per sample slot
             out["map"] = frames * (4 * c8 + 4 * j) + 4 * j * c8
+        elif eng == "tile":                             # gathered windows: the tile slabs once
+            t = maps.tile_from_sparse(op, maps.spec_offsets(wl.spec))
+            out["map"] = frames * (4 * c8 + 4 * j) + 4 * t.num_slabs * 128 * 64
         else:
             nnz_stored = getattr(op, "num_kept", None)
             nnz_stored = nnz_stored if nnz_stored is not None else j * s_tot
@@ -327,17 +331,24 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
     roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
-    if _maps.uses_tc(args.variant, op, args.engine, count):
+    eng = _maps.map_engine(args.variant, op, args.engine, count)
+    if eng == "tc":
         # tensor-core interpolation engine: 3 bf16 MMA passes over the dense operator
         c8 = (wl.spec.total_samples + 7) // 8 * 8
         tflops = 3 * 2.0 * wl.grid.num_points * c8 * count / (t_map / 1e3) / 1e12
         roof["map_engine"] = {"engine": "tcgen05 kind::f16, bf16 hi/lo x3 (dense operator)",
                               "tensor_tflops": tflops, "frac_of_bf16_peak": tflops / bf16}
+    elif eng == "tile":
+        t = _maps.tile_from_sparse(op, _maps.spec_offsets(wl.spec))
+        tflops = 3 * 2.0 * t.num_slabs * 128 * 64 * count / (t_map / 1e3) / 1e12
+        roof["map_engine"] = {"engine": "tcgen05 kind::f16, bf16 hi/lo x3 (per-tile gathered lag windows)",
+                              "tiles": t.num_tiles, "mean_k": t.mean_k, "tensor_tflops": tflops,
+                              "frac_of_bf16_peak": tflops / bf16}
     # the SIMT stages are FP32-issue / L1 bound at these sizes: their FP32 fractions
     roof["fp32_frac"] = {
         "frontend": frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak,
         "map": (map_flops(wl, args.variant, op, count) / (t_map / 1e3) / 1e12 / fp32_peak
-                if args.variant not in ("conv", "conv_h") and not _maps.uses_tc(args.variant, op, args.engine, count)
+                if args.variant not in ("conv", "conv_h") and eng not in ("tc", "tile")
                 else None),
         "fp32_peak_tflops": fp32_peak, "peak_source": f"FP32 SIMT cuBLAS {xsrc}"}
 
@@ -435,9 +446,9 @@ def run_ours(args):
                                      f"{int(op.values.shape[2])} nnz per (candidate, pair)")
                                     if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
-                       "map_engine": (("tensor cores (dense bf16x3)" if _maps.uses_tc(args.variant, op, args.engine,
-                                                                                      count)
-                                       else "FP32 tiled band") if args.variant in ("sspi", "si") else None),
+                       "map_engine": {"tc": "tensor cores (dense bf16x3)",
+                                      "tile": "tensor cores (gathered lag windows, bf16x3)",
+                                      "band": "FP32 tiled band"}.get(eng),
                        "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
                        "execution": "CUDA graph per batch"},
             "candidates_per_s": value * wl.grid.num_points,
@@ -473,12 +484,13 @@ def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto")
     frames = range(0, count)
     if variant in ("sspi", "si", "slri"):
         from paper_2306_08514_b200 import maps
-        tc = maps.uses_tc(variant, op, engine, count)  # the pipeline's frontend also writes the planes
-        front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames, planes=tc)
+        eng = maps.map_engine(variant, op, engine, count)   # the pipeline's frontend also writes the planes
+        front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames,
+                                            planes=eng in ("tc", "tile"), natural=eng == "tile")
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
         if variant != "slri":
             mapf0 = mapf
-            mapf = lambda o, m, argmax: mapf0(o, m, argmax=argmax, engine="tc" if tc else "band")
+            mapf = lambda o, m, argmax: mapf0(o, m, argmax=argmax, engine=eng)
     else:
         front = lambda: s.gcc_frames(x_dev, wl.frame, wl.pairs, frames,
                                      tf32=(variant in ("conv", "conv_h")))

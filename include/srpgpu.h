@@ -99,16 +99,20 @@ int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t
                              srpgpu_stream_t stream);
 
 /* frames_to_samples plus the bf16 hi/lo planes [2][F][cols8] of the samples (the
- * tensor-core interpolation map's operand, see srpgpu_interp_map_tc), written by the
- * same kernel; cols8 >= total_samples, a multiple of 8. */
+ * tensor-core interpolation maps' operand), written by the same kernel; cols8 >=
+ * total_samples, a multiple of 8.  planes_ld > 0: lag-major planes [2][cols8][planes_ld]
+ * instead (planes_ld >= F, a multiple of 8; needs lag-major samples, samples_ld > 0).
+ * natural != 0: sample index in natural lag order -N_p..N_p per pair
+ * (srpgpu_interp_map_gather_tc); natural_src [S] int32 maps each natural index to its
+ * storage index (used when a non-warp kernel produced the samples). */
 int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels, int64_t num_samples,
                                     int64_t ld_samples, const float* window, int32_t frame_len,
                                     int32_t hop, int64_t first_frame, int64_t num_frames,
                                     const int32_t* pairs, int32_t num_pairs, int32_t weighting,
                                     int32_t floor_mode, double floor_value, const int32_t* counts,
                                     const int32_t* offsets, int32_t total_samples, float* samples_out,
-                                    int64_t samples_ld, void* planes, int32_t cols8,
-                                    srpgpu_stream_t stream);
+                                    int64_t samples_ld, void* planes, int32_t cols8, int64_t planes_ld,
+                                    int32_t natural, const int32_t* natural_src, srpgpu_stream_t stream);
 
 /* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
 int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
@@ -142,6 +146,35 @@ int srpgpu_sspi_map(const float* samples, int64_t samples_ld, int64_t num_frames
 int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const void* op_planes,
                          int64_t num_candidates, int32_t cols8, float* z, uint64_t* keys,
                          srpgpu_stream_t stream);
+
+/* sspi_map / si_map on the tensor cores for long sample vectors: per-tile gathered lag
+ * windows (host layout: paper_2306_08514_b200/tiles.py).  samples_planes: lag-major
+ * bf16 planes [2][round8(num_cols)][planes_ld] in natural lag order (planes_ld >= F,
+ * multiple of 8); slab_planes [2][num_slabs * 128][64] bf16 (tile operator slabs); group_col
+ * [num_slabs * 8] first natural sample index of each 8-lag group; tile_slab /
+ * tile_nkb [num_tiles] first slab and slab count of each
+ * tile; tile_rows [num_tiles][128] candidate index of each tile row (ascending, -1 pad);
+ * unit_bounds [num_ctas + 1] contiguous work-unit ranges, one persistent CTA each.
+ * z [F][J] and keys [F] optional; a map is written in tile order into z_tiles
+ * [F][num_tiles * 128] (full 32-byte sectors) and gathered back to grid order by
+ * tile_pos [J] (= tile * 128 + row of each candidate). */
+int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, int32_t num_cols,
+                                int64_t planes_ld,
+                                const void* slab_planes, int64_t num_slabs, const int32_t* group_col,
+                                const int32_t* tile_slab, const int32_t* tile_nkb, const int32_t* tile_rows,
+                                int32_t num_tiles, int64_t num_candidates, const int32_t* unit_bounds,
+                                int32_t num_ctas, const int32_t* tile_pos, float* z_tiles, float* z,
+                                uint64_t* keys, srpgpu_stream_t stream);
+
+/* row-wise bf16 hi/lo split: dst[p][r][c] for r < rows, c < cols (pitch ld_dst, plane
+ * stride rows_dst * ld_dst) from src[row_src[r]][c] (row_src NULL: identity). */
+int srpgpu_split_bf16_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols, const int32_t* row_src,
+                           void* dst, int64_t ld_dst, int64_t rows_dst, srpgpu_stream_t stream);
+
+/* srpgpu_split_bf16 with a column source map: dst column c takes source column
+ * col_src[c] (NULL: identity). */
+int srpgpu_split_bf16_cols(const float* src, int64_t ld_src, int32_t lag_major, int64_t rows, int32_t cols,
+                           const int32_t* col_src, void* dst, int32_t cols8, srpgpu_stream_t stream);
 
 /* f32 [rows][cols] (row pitch ld_src; or lag-major src[c * ld_src + r] if lag_major)
  * -> bf16 planes dst[0][r][c] = bf16_rne(x), dst[1][r][c] = bf16_rne(x - hi), pitch

@@ -144,15 +144,25 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
   return raw;
 }
 
-// one xi sample: the f32 output and, when requested, its bf16 hi/lo planes
-__device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int col, float v) {
-  dst[col * sst] = v;
+// one xi sample (storage index d of a pair block at offset o with N lags a side): the
+// f32 output and, when requested, its bf16 hi/lo planes (storage or natural lag order)
+__device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int o, int N, int d,
+                                       float v) {
+  dst[(o + d) * sst] = v;
   if (prm.xi_planes) {
+    const int col = o + (prm.xi_natural ? (d <= N ? N + d : d - N - 1) : d);
     const __nv_bfloat16 hi = __float2bfloat16_rn(v);
     const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-    __nv_bfloat16* pl = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes) + f * prm.cols8 + col;
-    pl[0] = hi;
-    pl[prm.F * prm.cols8] = lo;
+    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes);
+    if (prm.planes_ld) {                      // lag-major [2][cols8][planes_ld]
+      __nv_bfloat16* pl = base + (int64_t)col * prm.planes_ld + f;
+      pl[0] = hi;
+      pl[(int64_t)prm.cols8 * prm.planes_ld] = lo;
+    } else {
+      __nv_bfloat16* pl = base + f * prm.cols8 + col;
+      pl[0] = hi;
+      pl[prm.F * prm.cols8] = lo;
+    }
   }
 }
 
@@ -342,24 +352,24 @@ frontend_warp_kernel(const WarpParams prm) {
                 const int n = 32 * brev<LP>(i) + k2;
                 const float2 x = v[r * LP + i];
                 const int da = (n <= Na) ? n : ((L - n <= Na) ? 2 * Na + 1 - (L - n) : -1);
-                if (da >= 0) put_xi(prm, dst, sst, f, oa + da, x.x);
+                if (da >= 0) put_xi(prm, dst, sst, f, oa, Na, da, x.x);
                 const int db = (n <= Nb) ? n : ((L - n <= Nb) ? 2 * Nb + 1 - (L - n) : -1);
-                if (db >= 0) put_xi(prm, dst, sst, f, ob + db, -x.y);
+                if (db >= 0) put_xi(prm, dst, sst, f, ob, Nb, db, -x.y);
               }
             } else {
               const float2 x0 = v[r * LP + 0];   // n = k2
               const float2 x1 = v[r * LP + 1];   // n = L - 32 + k2, distance d = 32 - k2
               const int d = 32 - k2;
-              if (k2 <= Na) put_xi(prm, dst, sst, f, oa + k2, x0.x);
-              if (d <= Na) put_xi(prm, dst, sst, f, oa + 2 * Na + 1 - d, x1.x);
-              if (k2 <= Nb) put_xi(prm, dst, sst, f, ob + k2, -x0.y);
-              if (d <= Nb) put_xi(prm, dst, sst, f, ob + 2 * Nb + 1 - d, -x1.y);
+              if (k2 <= Na) put_xi(prm, dst, sst, f, oa, Na, k2, x0.x);
+              if (d <= Na) put_xi(prm, dst, sst, f, oa, Na, 2 * Na + 1 - d, x1.x);
+              if (k2 <= Nb) put_xi(prm, dst, sst, f, ob, Nb, k2, -x0.y);
+              if (d <= Nb) put_xi(prm, dst, sst, f, ob, Nb, 2 * Nb + 1 - d, -x1.y);
             }
           }
         }
         __syncwarp();
       }
-      if (prm.xi_planes && mi == 0) {                // zero the planes' pad columns [S, cols8)
+      if (prm.xi_planes && !prm.planes_ld && mi == 0) {   // zero the planes' pad columns [S, cols8)
         uint16_t* pl = prm.xi_planes + f * prm.cols8;
         for (int c = prm.S + lane; c < prm.cols8; c += 32) {
           pl[c] = 0;

@@ -28,6 +28,8 @@ struct WarpParams {
   // (interp_tc.cu): hi = bf16_rne(x), lo = bf16_rne(x - hi), zero in [S, cols8)
   uint16_t* xi_planes;
   int32_t cols8;
+  int32_t xi_natural;   // planes in natural lag order -N_p..N_p per pair (gathered-window engine)
+  int64_t planes_ld;    // 0: planes frame-major [2][F][cols8]; > 0: lag-major [2][cols8][planes_ld]
 };
 
 // 0: launched; 1: shape not covered (use the block kernel); < 0: error status.

@@ -1,0 +1,353 @@
+// SSPI / SI on the tensor cores for long sample vectors (BASELINE cfg4: S = 7028 lags):
+// per-tile gathered lag windows (layout built on the host by tiles.py).
+//
+//   z[f][j] = sum_s Lambda[j][s] xi[f][s]      interpolation.py:121-126, 188-195
+//
+// Candidates come in tiles of 128 that are compact in TDOA space; a tile's operator is
+// dense over K = its candidates' kept lag windows (pair by pair, rounded up to groups of
+// 8 lags), stored as 64-wide slabs [slab][128][64] (bf16 hi / lo planes).  The matching
+// samples are gathered from lag-major, natural-lag-order xi planes [S][F8] (frames
+// contiguous): a group is 8 lag rows, loaded as four 128-byte-swizzled TMA boxes of
+// 64 frames x 8 lags, so no operand is ever materialised per tile.  (A frame-major
+// gather would need one 16-byte box per (frame, group) row: measured 6x slower.)
+//
+// D = A . B^T with A = slab (M = 128 candidates = TMEM lanes, K-major, 128-byte swizzle)
+// and B = gathered xi (N = 256 frames = TMEM columns, MN-major, 128-byte swizzle: 1 KB
+// atoms of 64 frames x 8 lags, 1 KB apart along N (LBO) and 4 KB apart along K (SBO)).
+// Three kind::f16 MMAs per 16-lag step (bf16 hi/lo split, as interp_tc.cu).  Persistent CTAs take balanced contiguous ranges of work units
+// (frame-tile group, tile, frame tile): a tile's slabs are reused from L2 across the
+// group's frame tiles and the group's xi columns stay L2-resident.
+// Roles: warp 0 TMA producer (lanes 0-15 one plane x group each), warp 1 TMEM allocator
+// + MMA issuer, warps 2-9 epilogue
+// (lane quarter warp % 4 = 32 candidates, half of the eight 32-frame chunks each):
+// z rows stored straight from registers, per-frame argmax by a butterfly max across
+// the lanes plus a ballot for the lowest winning candidate (tile rows are ascending).
+#include <cuda_bf16.h>
+
+#include "tc_common.cuh"
+
+namespace srpgpu {
+namespace gtc {
+
+using namespace tc;
+
+constexpr int GM = 128;   // candidates per tile
+constexpr int GN = 256;   // frames per unit
+constexpr int GK = 64;    // lags per slab (k-block)
+constexpr int GG = 8;     // lags per gathered group (8 rows of the lag-major samples)
+constexpr int GA = 64;    // frames per MN atom (128 bytes)
+constexpr int NG = GK / GG;
+constexpr int UK = 16;    // kind::f16 MMA K
+constexpr int NS = 2;     // operand stages (96 KB each)
+constexpr int kEpi = 8;
+constexpr int kThreads = 32 * (2 + kEpi);
+constexpr int FG = 4;     // frame tiles per unit group (must match tiles.TileLayout.unit_bounds)
+constexpr int kMaxSlabs = 256;                    // slabs per tile (K <= 16384 lags)
+constexpr int kMaxGroups = kMaxSlabs * NG;
+
+struct __align__(1024) Smem {
+  uint16_t a[NS][2][GM * GK];          // slab hi / lo (16 KB each, 128-byte swizzle)
+  uint16_t b[NS][2][NG][GN * GG];      // gathered xi hi / lo: 8 groups x 4 atoms [8 lags][64 frames]
+  int32_t rows[2][kMaxGroups];         // the current / next unit's group rows (producer only)
+  uint64_t full[NS], empty[NS], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// MN-major operand, 128-byte swizzle: 1 KB atoms (8 K rows x 64 MN elements);
+// LBO = distance between MN-adjacent atoms, SBO = between K-adjacent 8-row groups
+__device__ __forceinline__ uint64_t desc_mn128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(1024 >> 4) << 16;             // LBO: next 64 frames
+  d |= (uint64_t)((GN * GG * 2) >> 4) << 32;    // SBO: next 8-lag group (4 KB)
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+struct Unit {
+  int t, n;
+};
+
+__device__ __forceinline__ bool decode(int u, int T, int n_tiles, Unit& out) {
+  const int per = T * FG;
+  const int g = u / per, rem = u - g * per;
+  out.t = rem / FG;
+  out.n = g * FG + (rem - out.t * FG);
+  return out.n < n_tiles;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                 const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int64_t F,
+                 int64_t J, int32_t T, const int32_t* __restrict__ group_col, const int32_t* __restrict__ tile_slab,
+                 const int32_t* __restrict__ tile_nkb, const int32_t* __restrict__ tile_rows,
+                 const int32_t* __restrict__ bounds, float* __restrict__ zt, unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)((F + GN - 1) / GN);
+  const int u_begin = bounds[blockIdx.x], u_end = bounds[blockIdx.x + 1];
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ma_hi);
+    prefetch_tmap(&ma_lo);
+    prefetch_tmap(&mb_hi);
+    prefetch_tmap(&mb_lo);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.tfull[b], 1);
+      mbar_init(&sm.tempty[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // the unit's group rows are staged in shared memory (one coalesced load per unit,
+    // prefetched a unit ahead) so the per-k-block loop has no dependent global load;
+    // lane 0 waits and arms the stage; lanes 0-15 then each load one (plane, group):
+    // four 64-frame atoms of its 8 lag rows; lanes 16-17 load the slab planes
+    constexpr uint32_t kBytes = 2u * (GM * GK + GN * GK) * sizeof(uint16_t);
+    const int plane = (lane >> 3) & 1, grp = lane & 7;
+    auto next_unit = [&](int u, Unit& w) {
+      while (u < u_end && !decode(u, T, n_tiles, w)) ++u;
+      return u;
+    };
+    auto stage_rows = [&](int buf, const Unit& w) {
+      const int s0 = __ldg(tile_slab + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int i = lane; i < nk * NG; i += 32) sm.rows[buf][i] = __ldg(group_col + s0 * NG + i);
+    };
+    uint32_t g = 0;
+    int buf = 0;
+    Unit w;
+    int u = next_unit(u_begin, w);
+    if (u < u_end) stage_rows(0, w);
+    while (u < u_end) {
+      Unit wn;
+      const int un = next_unit(u + 1, wn);
+      if (un < u_end) stage_rows(buf ^ 1, wn);          // prefetch the next unit's rows
+      __syncwarp();
+      const int s0 = __ldg(tile_slab + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int slab = s0 + kb;
+        const int row = sm.rows[buf][kb * NG + grp];
+        const int s = g % NS;
+        if (lane == 0) {
+          mbar_wait(&sm.empty[s], ((g / NS) & 1) ^ 1);
+          mbar_expect_tx(&sm.full[s], kBytes);
+        }
+        __syncwarp();
+        if (lane < 16) {
+          const CUtensorMap* mb = plane ? &mb_lo : &mb_hi;
+#pragma unroll
+          for (int a = 0; a < GN / GA; ++a)
+            tma_load_2d(sm.b[s][plane][grp] + a * GA * GG, mb, &sm.full[s], w.n * GN + a * GA, row);
+        } else if (lane < 18) {
+          tma_load_2d(sm.a[s][lane - 16], lane == 16 ? &ma_hi : &ma_lo, &sm.full[s], 0, slab * GM);
+        }
+      }
+      __syncwarp();
+      buf ^= 1;
+      u = un;
+      w = wn;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // D f32, A/B bf16, A K-major, B MN-major (bit 16), N = 256, M = 128
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(GN >> 3) << 17) |
+                                 ((uint32_t)(GM >> 4) << 24);
+      uint32_t g = 0, it = 0;
+      for (int u = u_begin; u < u_end; ++u) {
+        Unit w;
+        if (!decode(u, T, n_tiles, w)) continue;
+        const int nk = __ldg(tile_nkb + w.t);
+        const uint32_t acc = it & 1;
+        mbar_wait(&sm.tempty[acc], ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * GN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % NS;
+          mbar_wait(&sm.full[s], (g / NS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t ah = smem_desc(sm.a[s][0]), al = smem_desc(sm.a[s][1]);
+#pragma unroll
+          for (int k = 0; k < GK / UK; ++k) {
+            const uint64_t aoff = (uint64_t)((k * UK * 2) >> 4);
+            const uint64_t bh = desc_mn128(sm.b[s][0][2 * k]), bl = desc_mn128(sm.b[s][1][2 * k]);
+            mma_bf16(d, ah + aoff, bh, idesc, (kb | k) != 0);
+            mma_bf16(d, ah + aoff, bl, idesc, 1u);
+            mma_bf16(d, al + aoff, bh, idesc, 1u);
+          }
+          mma_commit(&sm.empty[s]);
+        }
+        mma_commit(&sm.tfull[acc]);
+        ++it;
+      }
+    }
+  } else {
+    const int q = warp & 3;                          // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;                // which 4 of the 8 column chunks
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    uint32_t it = 0;
+    for (int u = u_begin; u < u_end; ++u) {
+      Unit w;
+      if (!decode(u, T, n_tiles, w)) continue;
+      const uint32_t acc = it & 1;
+      const int jrow = __ldg(tile_rows + (int64_t)w.t * GM + q * 32 + lane);   // -1: padding row
+      mbar_wait(&sm.tfull[acc], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool any = __any_sync(0xffffffffu, jrow >= 0);
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c = half * 4 + cc;
+        uint32_t r[32];
+        tmem_ld32(lane_base + acc * GN + c * 32, r);
+        const int64_t f0 = (int64_t)w.n * GN + c * 32;
+        if (f0 >= F || !any) continue;               // warp-uniform (after the aligned load)
+        if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
+          const int64_t ldt = (int64_t)T * GM;
+          float* zc = zt + f0 * ldt + (int64_t)w.t * GM + q * 32 + lane;
+          if (f0 + 32 <= F) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) __stcg(zc + t * ldt, __uint_as_float(r[t]));
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (f0 + t < F) __stcg(zc + t * ldt, __uint_as_float(r[t]));
+          }
+        }
+        if (keys) {
+          uint32_t ob[32], v[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) v[t] = ob[t] = jrow >= 0 ? ordered_bits(__uint_as_float(r[t])) : 0u;
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int t = 0; t < o; ++t) {
+              const uint32_t send = up ? v[t] : v[t + o];
+              const uint32_t keep = up ? v[t + o] : v[t];
+              v[t] = max(keep, __shfl_xor_sync(0xffffffffu, send, o));
+            }
+          }
+          // lane t holds frame f0 + t's maximum in v[0]; the lowest lane (= lowest candidate) wins
+          uint32_t win = 0;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const uint32_t vt = __shfl_sync(0xffffffffu, v[0], t);
+            const uint32_t m = __ballot_sync(0xffffffffu, ob[t] == vt);
+            if (lane == t) win = (uint32_t)(__ffs(m) - 1);
+          }
+          const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
+          if (f0 + lane < F && v[0] != 0u)
+            atomicMax(keys + f0 + lane,
+                      ((unsigned long long)v[0] << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[acc]);
+      ++it;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
+// tile order -> grid order: z[f][j] = zt[f][pos[j]] (coalesced writes; the reads follow
+// the tiles' ascending rows, mostly short contiguous runs)
+__global__ void untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
+                              int64_t F, float* __restrict__ z) {
+  for (int64_t f = blockIdx.y; f < F; f += gridDim.y) {
+    const float* src = zt + f * ldt;
+    float* dst = z + f * J;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x)
+      __stcs(dst + j, __ldcs(src + __ldg(pos + j)));
+  }
+}
+
+}  // namespace gtc
+
+int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
+
+}  // namespace srpgpu
+
+using namespace srpgpu;
+
+extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, int32_t num_cols,
+                                           int64_t planes_ld,
+                                           const void* slab_planes, int64_t num_slabs, const int32_t* group_col,
+                                           const int32_t* tile_slab, const int32_t* tile_nkb,
+                                           const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
+                                           const int32_t* unit_bounds, int32_t num_ctas, const int32_t* tile_pos,
+                                           float* z_tiles, float* z, uint64_t* keys, srpgpu_stream_t stream) {
+  using namespace gtc;
+  SRPGPU_CHECK_ARG(num_frames >= 0 && num_cols >= 1 && planes_ld >= num_frames && planes_ld % 8 == 0 &&
+                       num_slabs >= 0 && num_tiles >= 0 && num_candidates >= 1 && num_ctas >= 0,
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_tc: bad shape");
+  SRPGPU_CHECK_ARG(((uintptr_t)samples_planes & 15) == 0 && ((uintptr_t)slab_planes & 15) == 0 &&
+                       ((uintptr_t)group_col & 15) == 0,
+                   SRPGPU_ERR_VALUE, "interp_map_gather_tc: operands must be 16-byte aligned");
+  SRPGPU_CHECK_ARG(num_frames < (1ll << 31) && num_candidates < (1ll << 31) && num_slabs * GM < (1ll << 31),
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_tc: too large");
+  SRPGPU_CHECK_ARG(!z || (z_tiles && tile_pos), SRPGPU_ERR_VALUE,
+                   "interp_map_gather_tc: a map needs the tile-order scratch [F][num_tiles * 128] and tile_pos");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  if (num_frames == 0 || num_tiles == 0 || num_ctas == 0) return SRPGPU_OK;
+  const auto* xs = reinterpret_cast<const uint16_t*>(samples_planes);
+  const auto* xo = reinterpret_cast<const uint16_t*>(slab_planes);
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const int64_t arows = num_slabs * GM;
+  if ((s = make_map_2d(&ma_hi, bf, 2, xo, arows, GK, GK, GK, GM, "interp_map_gather_tc")) ||
+      (s = make_map_2d(&ma_lo, bf, 2, xo + arows * GK, arows, GK, GK, GK, GM, "interp_map_gather_tc")) ||
+      (s = make_map_2d(&mb_hi, bf, 2, xs, num_cols, num_frames, planes_ld, GA, GG, "interp_map_gather_tc")) ||
+      (s = make_map_2d(&mb_lo, bf, 2, xs + (int64_t)((num_cols + 7) / 8 * 8) * planes_ld, num_cols, num_frames,
+                       planes_ld, GA, GG, "interp_map_gather_tc")))   // planes hold round8(S) rows each
+    return s;
+  const size_t smem = sizeof(Smem) + 1024;
+  if (cudaFuncSetAttribute(gather_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    set_error("interp_map_gather_tc: cannot reserve %zu B shared memory", smem);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  gather_tc_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nkb, tile_rows,
+      unit_bounds, z ? z_tiles : nullptr, reinterpret_cast<unsigned long long*>(keys));
+  SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
+  if (z) {
+    dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
+              (unsigned)std::min<int64_t>(num_frames, 65535));
+    untile_kernel<<<grid, 256, 0, st>>>(z_tiles, (int64_t)num_tiles * GM, tile_pos, num_candidates, num_frames, z);
+    SRPGPU_CHECK_LAUNCH("interp_map_gather_tc(untile)");
+  }
+  return SRPGPU_OK;
+}

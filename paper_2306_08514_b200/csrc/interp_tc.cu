@@ -232,20 +232,23 @@ interp_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 // else src[r * ld + c].  32 x 32 tiles through shared memory (coalesced both ways).
 template <bool LAG_MAJOR>
 __global__ void split_bf16_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int32_t cols,
-                                  __nv_bfloat16* __restrict__ dst, int32_t cols8) {
+                                  const int32_t* __restrict__ col_src, __nv_bfloat16* __restrict__ dst,
+                                  int32_t cols8, int64_t r_base) {
   __shared__ float t[32][33];
-  const int64_t r0 = (int64_t)blockIdx.y * 32;
+  const int64_t r0 = r_base + (int64_t)blockIdx.y * 32;
   const int c0 = blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
   for (int k = ty; k < 32; k += 8) {
     if (LAG_MAJOR) {   // t[c][r] = src[(c0 + k) * ld + r0 + tx]
       const int c = c0 + k;
       const int64_t r = r0 + tx;
-      t[k][tx] = (c < cols && r < rows) ? __ldg(src + (int64_t)c * ld + r) : 0.f;
+      const int cs = (c < cols && col_src) ? __ldg(col_src + c) : c;
+      t[k][tx] = (c < cols && r < rows) ? __ldg(src + (int64_t)cs * ld + r) : 0.f;
     } else {           // t[c][r] with r = r0 + k, c = c0 + tx
       const int c = c0 + tx;
       const int64_t r = r0 + k;
-      t[tx][k] = (c < cols && r < rows) ? __ldg(src + r * ld + c) : 0.f;
+      const int cs = (c < cols && col_src) ? __ldg(col_src + c) : c;
+      t[tx][k] = (c < cols && r < rows) ? __ldg(src + r * ld + cs) : 0.f;
     }
   }
   __syncthreads();
@@ -263,6 +266,21 @@ __global__ void split_bf16_kernel(const float* __restrict__ src, int64_t ld, int
   }
 }
 
+// row-wise split: dst[p][r][c] = split(src[row_src[r]][c]) (lag-major samples -> lag-major
+// planes, rows optionally permuted), rows [S], cols = frames
+__global__ void split_rows_kernel(const float* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
+                                  const int32_t* __restrict__ row_src, __nv_bfloat16* __restrict__ dst,
+                                  int64_t ld_dst, int64_t plane) {
+  const int64_t r = blockIdx.y;
+  const int64_t rs = row_src ? __ldg(row_src + r) : r;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+    const float x = __ldg(src + rs * ld_src + c);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    dst[r * ld_dst + c] = hi;
+    dst[plane + r * ld_dst + c] = __float2bfloat16_rn(x - __bfloat162float(hi));
+  }
+}
+
 }  // namespace itc
 
 int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
@@ -271,24 +289,50 @@ int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
 
 using namespace srpgpu;
 
-extern "C" int srpgpu_split_bf16(const float* src, int64_t ld_src, int32_t lag_major, int64_t rows, int32_t cols,
-                                 void* dst, int32_t cols8, srpgpu_stream_t stream) {
+extern "C" int srpgpu_split_bf16_cols(const float* src, int64_t ld_src, int32_t lag_major, int64_t rows, int32_t cols,
+                                      const int32_t* col_src, void* dst, int32_t cols8, srpgpu_stream_t stream) {
   SRPGPU_CHECK_ARG(rows >= 0 && cols >= 0 && cols8 >= cols && cols8 % 8 == 0, SRPGPU_ERR_DIMENSION,
                    "split_bf16: bad shape (rows %lld, cols %d, cols8 %d)", (long long)rows, cols, cols8);
   SRPGPU_CHECK_ARG(lag_major ? ld_src >= rows : ld_src >= cols, SRPGPU_ERR_DIMENSION, "split_bf16: bad pitch");
   SRPGPU_CHECK_ARG(((uintptr_t)dst & 15) == 0, SRPGPU_ERR_VALUE, "split_bf16: destination must be 16-byte aligned");
   if (rows == 0 || cols8 == 0) return SRPGPU_OK;
   const int64_t yb = (rows + 31) / 32;
-  SRPGPU_CHECK_ARG(yb <= 65535, SRPGPU_ERR_DIMENSION, "split_bf16: more than %d rows", 65535 * 32);
   cudaStream_t st = as_stream(stream);
   auto* d = reinterpret_cast<__nv_bfloat16*>(dst);
-  dim3 grid((unsigned)((cols8 + 31) / 32), (unsigned)yb), block(32, 8);
-  if (lag_major)
-    itc::split_bf16_kernel<true><<<grid, block, 0, st>>>(src, ld_src, rows, cols, d, cols8);
-  else
-    itc::split_bf16_kernel<false><<<grid, block, 0, st>>>(src, ld_src, rows, cols, d, cols8);
-  SRPGPU_CHECK_LAUNCH("split_bf16");
+  for (int64_t y0 = 0; y0 < yb; y0 += 65535) {   // grid.y limit: launch in row chunks
+    dim3 grid((unsigned)((cols8 + 31) / 32), (unsigned)std::min<int64_t>(65535, yb - y0)), block(32, 8);
+    if (lag_major)
+      itc::split_bf16_kernel<true><<<grid, block, 0, st>>>(src, ld_src, rows, cols, col_src, d, cols8, y0 * 32);
+    else
+      itc::split_bf16_kernel<false><<<grid, block, 0, st>>>(src, ld_src, rows, cols, col_src, d, cols8, y0 * 32);
+    SRPGPU_CHECK_LAUNCH("split_bf16");
+  }
   return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_split_bf16_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                      const int32_t* row_src, void* dst, int64_t ld_dst, int64_t rows_dst,
+                                      srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rows >= 0 && cols >= 0 && ld_src >= cols && ld_dst >= cols && rows_dst >= rows, SRPGPU_ERR_DIMENSION,
+                   "split_bf16_rows: bad shape");
+  SRPGPU_CHECK_ARG(((uintptr_t)dst & 15) == 0, SRPGPU_ERR_VALUE, "split_bf16_rows: destination must be 16-byte aligned");
+  if (rows == 0 || cols == 0) return SRPGPU_OK;
+  cudaStream_t st = as_stream(stream);
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((cols + 255) / 256, 64), (unsigned)nr);
+    itc::split_rows_kernel<<<grid, 256, 0, st>>>(row_src ? src : src + r0 * ld_src, ld_src, nr, cols,
+                                                 row_src ? row_src + r0 : nullptr,
+                                                 reinterpret_cast<__nv_bfloat16*>(dst) + r0 * ld_dst, ld_dst,
+                                                 rows_dst * ld_dst);
+    SRPGPU_CHECK_LAUNCH("split_bf16_rows");
+  }
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_split_bf16(const float* src, int64_t ld_src, int32_t lag_major, int64_t rows, int32_t cols,
+                                 void* dst, int32_t cols8, srpgpu_stream_t stream) {
+  return srpgpu_split_bf16_cols(src, ld_src, lag_major, rows, cols, nullptr, dst, cols8, stream);
 }
 
 extern "C" int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const void* op_planes,

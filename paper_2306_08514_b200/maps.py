@@ -25,6 +25,7 @@ import torch
 
 from . import _device as dev
 from . import _native as nat
+from . import tiles
 from .errors import DimensionError
 from .sampling import TdGccSamples, spec_offsets
 
@@ -262,9 +263,10 @@ def _check_cols(samples, num_cols: int) -> None:
 
 # ----------------------------------------------------------------- SSPI / SI on tensor cores
 
-ENGINES = ("auto", "tc", "band")
-TC_MAX_COLS = 2048          # dense rows beyond this many samples: the band engine
-TC_DENSITY = 12             # tensor cores while cols8 <= TC_DENSITY * kept entries per row
+ENGINES = ("auto", "tc", "tile", "band")
+TC_MAX_COLS = 2048          # dense rows beyond this many samples: gathered windows ("tile") or band
+TC_DENSITY = 12             # dense tensor cores while cols8 <= TC_DENSITY * kept entries per row
+TILE_DENSITY = 4            # gathered windows while the kept entries per row are sparse
 
 
 def _cols8(n: int) -> int:
@@ -289,11 +291,22 @@ class DenseInterpOperator:
 
 def dense_from_sparse(sp) -> DenseInterpOperator:
     def build():
-        splits = np.asarray(sp.row_splits, dtype=np.int64)
-        j, s = splits.shape[0] - 1, int(sp.num_cols)
+        s = int(sp.num_cols)
+        if np.ndim(sp.values) == 3:          # FixedNnzInterp: (P, J, k) blocks
+            p_count, j, k = sp.values.shape
+            keep = np.broadcast_to((np.arange(k)[None, :] < np.asarray(sp.kept)[:, None])[:, None, :],
+                                   sp.values.shape)
+            rows = np.broadcast_to(np.arange(j, dtype=np.int64)[None, :, None], sp.values.shape)[keep]
+            cols = np.asarray(sp.cols)[keep].astype(np.int64)
+            vals = np.asarray(sp.values)[keep]
+        else:
+            splits = np.asarray(sp.row_splits, dtype=np.int64)
+            j = splits.shape[0] - 1
+            rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
+            cols = np.asarray(sp.col_indices, dtype=np.int64)
+            vals = np.asarray(sp.values)
         mat = np.zeros((j, s), dtype=np.float32)
-        rows = np.repeat(np.arange(j, dtype=np.int64), np.diff(splits))
-        mat[rows, np.asarray(sp.col_indices, dtype=np.int64)] = np.asarray(sp.values).astype(np.float32)
+        mat[rows, cols] = vals.astype(np.float32)
         return DenseInterpOperator(mat)
     return dev.CACHE.get(sp, "dense_bf16x2", build)
 
@@ -306,8 +319,10 @@ def dense_from_matrix(interp) -> DenseInterpOperator:
 TC_MIN_FRAMES = 0           # batches below this take the band engine (set from the cfg5 batch sweep)
 
 
-def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None) -> str:
-    """'tc' (dense operator on the tensor cores) or 'band' (tiled-band SpMM on FP32)."""
+def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None,
+                  pairs: bool = True) -> str:
+    """'tc' (dense operator on the tensor cores), 'tile' (per-tile gathered lag windows on
+    the tensor cores, for long sample vectors) or 'band' (tiled-band SpMM on FP32)."""
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}")
     if engine != "auto":
@@ -315,20 +330,98 @@ def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", fram
     if frames is not None and frames < TC_MIN_FRAMES:
         return "band"
     c8 = _cols8(num_cols)
-    return "tc" if c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0) else "band"
+    if c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0):
+        return "tc"
+    if c8 > TC_MAX_COLS and kept_per_row * TILE_DENSITY < c8 and pairs:
+        return "tile"
+    return "band"
 
 
-def sample_planes(samples, num_cols: int):
-    """(bf16 planes [2][F][cols8], frames, batched) of any samples input.
+class TileOperator:
+    """Device image of the gathered-window operator (tiles.TileLayout) for engine "tile"."""
 
-    Kernel-produced TdGccSamples may already carry the planes (`bf16_planes`).
+    MAX_SLABS = 256             # per tile (interp_gather_tc.cu kMaxSlabs)
+
+    def __init__(self, sp, offsets, num_rows: int):
+        lay = tiles.TileLayout(sp, offsets, num_rows)
+        if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_SLABS:
+            raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} slabs (> {self.MAX_SLABS}): "
+                             "use engine 'band'")
+        d = dev.device()
+        self.num_rows, self.num_cols, self.cols8 = int(num_rows), int(lay.num_cols), _cols8(lay.num_cols)
+        self.num_tiles, self.num_slabs, self.mean_k = lay.num_tiles, lay.num_slabs, lay.mean_k
+        self.planes = torch.empty((2, max(1, lay.num_slabs) * tiles.TILE, tiles.SLAB), dtype=torch.bfloat16,
+                                  device=d)
+        if lay.num_slabs:
+            src = torch.from_numpy(lay.slabs.reshape(-1, tiles.SLAB)).to(d)
+            nat.call("srpgpu_split_bf16", dev.ptr(src), tiles.SLAB, 0, src.shape[0], tiles.SLAB,
+                     dev.ptr(self.planes), tiles.SLAB, dev.stream_ptr())
+            del src
+        self.group_col = dev.as_i32(lay.group_col if lay.group_col.size else np.zeros(8, np.int32))
+        self.tile_slab = dev.as_i32(lay.tile_slab)
+        self.tile_nkb = dev.as_i32(lay.tile_nkb)
+        self.tile_rows = dev.as_i32(lay.tile_rows)
+        self.tile_pos = dev.as_i32(lay.tile_pos)
+        self._layout = lay
+        lay.slabs = None                      # host copy no longer needed
+        self._bounds = {}
+
+    def bounds(self, frames: int):
+        hit = self._bounds.get(frames)
+        if hit is None:
+            ctas = torch.cuda.get_device_properties(dev.device()).multi_processor_count
+            hit = dev.as_i32(self._layout.unit_bounds(frames, ctas))
+            self._bounds[frames] = hit
+        return hit
+
+
+def tile_from_sparse(sp, offsets: np.ndarray) -> TileOperator:
+    num_rows = int(sp.values.shape[1]) if np.ndim(sp.values) == 3 else int(np.asarray(sp.row_splits).shape[0] - 1)
+    return dev.CACHE.get(sp, ("tile_bf16x2", tuple(int(o) for o in offsets)),
+                         lambda: TileOperator(sp, offsets, num_rows))
+
+
+def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
+    planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets)
+    z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
+    zt = torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device) if out_map else None
+    keys = _new_keys(f, argmax)
+    b = op.bounds(f)
+    nat.call("srpgpu_interp_map_gather_tc", dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes),
+             op.num_slabs,
+             dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
+             op.num_tiles, op.num_rows, dev.ptr(b), b.shape[0] - 1, dev.ptr(op.tile_pos), dev.ptr(zt), dev.ptr(z),
+             dev.ptr(keys), dev.stream_ptr())
+    return _finish(z, keys, batched, argmax)
+
+
+def sample_planes(samples, num_cols: int, natural=None):
+    """(bf16 planes, frames, batched) of any samples input.
+
+    natural None: frame-major planes [2][F][cols8] in storage column order (dense engine);
+    natural = the pair offsets: lag-major planes [2][cols8][F8] in natural lag order
+    (gathered-window engine).  Kernel-produced TdGccSamples may already carry them.
     """
+    want_nat = natural is not None
     planes = getattr(samples, "bf16_planes", None)
-    if planes is not None and planes.shape[2] == _cols8(num_cols):
+    c8 = _cols8(num_cols)
+    if planes is not None and bool(getattr(samples, "planes_natural", False)) == want_nat and \
+            planes.shape[1 if want_nat else 2] == c8:
         vals = samples.values
         batched = vals.dim() == 2
         return planes, (vals.shape[0] if batched else 1), batched
-    c8 = _cols8(num_cols)
+    src = None
+    if want_nat:
+        key = ("natural_src_i32", tuple(int(o) for o in natural))
+        src = _NAT_SRC.get(key)
+        if src is None:
+            src = _NAT_SRC.setdefault(key, dev.as_i32(tiles.natural_columns(np.asarray(natural))))
+        buf, f, batched = _lag_major(samples, num_cols)
+        f8 = (f + 7) // 8 * 8
+        planes = torch.empty((2, c8, f8), dtype=torch.bfloat16, device=buf.device)
+        nat.call("srpgpu_split_bf16_rows", dev.ptr(buf), buf.shape[1], num_cols, f, dev.ptr(src), dev.ptr(planes),
+                 f8, c8, dev.stream_ptr())
+        return planes, f, batched
     buf = getattr(samples, "lag_major", None)
     if buf is not None and buf.shape[0] == num_cols:
         vals = samples.values
@@ -345,6 +438,9 @@ def sample_planes(samples, num_cols: int):
     return planes, f, batched
 
 
+_NAT_SRC: dict = {}
+
+
 def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
     planes, f, batched = sample_planes(samples, op.num_cols)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
@@ -356,16 +452,20 @@ def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
     return _finish(z, keys, batched, argmax)
 
 
-def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -> bool:
-    """Whether sspi_map / si_map on this operator (and batch size) take the tensor-core engine."""
+def map_engine(variant: str, op, engine: str = "auto", frames: int | None = None):
+    """Engine sspi_map / si_map take on this operator and batch size ("tc" | "tile" |
+    "band"; None for the other variants)."""
     if variant == "si":
         n = int(np.asarray(op.matrix).shape[1])
-        return interp_engine(n, n, engine, frames) == "tc"
+        return interp_engine(n, n, engine, frames)
     if variant == "sspi":
-        if hasattr(op, "kept") and np.ndim(getattr(op, "cols", None)) == 3:
-            return False
-        return interp_engine(int(op.num_cols), _kept_per_row(op), engine, frames) == "tc"
-    return False
+        return interp_engine(int(op.num_cols), _kept_per_row(op), engine, frames)
+    return None
+
+
+def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -> bool:
+    """Whether sspi_map / si_map on this operator (and batch size) run on the tensor cores."""
+    return map_engine(variant, op, engine, frames) in ("tc", "tile")
 
 
 def _num_frames(samples) -> int:
@@ -386,16 +486,19 @@ def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True, engine:
     """Sparse interpolation map z_i = sum_{e in row i} v_e xi[c_e] (interpolation.py:188-195).
 
     engine "tc": the operator densified into bf16 hi/lo planes on the tensor cores
-    (3 MMA passes, ~1e-6 normalized error); "band": the tiled-band FP32 SpMM; "auto"
-    picks "tc" for short sample vectors relative to the kept entries per row.
+    (3 MMA passes, ~1e-6 normalized error); "tile": the same arithmetic over per-tile
+    gathered lag windows (long sample vectors, BASELINE cfg4); "band": the tiled-band
+    FP32 SpMM; "auto" picks by sample-vector length and sparsity.
     """
     num_cols = int(sp.num_cols)
     _check_cols(samples, num_cols)                 # reference DimensionError check first
-    fixed = hasattr(sp, "kept") and np.ndim(getattr(sp, "cols", None)) == 3
-    eng = "band" if fixed else interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples))
+    offsets = _sample_offsets(samples, num_cols)
+    eng = interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples), offsets.shape[0] > 2)
     if eng == "tc":
         return _tc_map(dense_from_sparse(sp), samples, argmax, out_map)
-    op = band_from_sparse(sp, _sample_offsets(samples, num_cols))
+    if eng == "tile":
+        return _tile_map(tile_from_sparse(sp, offsets), samples, offsets, argmax, out_map)
+    op = band_from_sparse(sp, offsets)
     return _band_map(op, samples, argmax, out_map)
 
 
@@ -407,6 +510,8 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engin
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
     _check_cols(samples, num_cols)
+    if engine == "tile":
+        raise ValueError("si_map keeps every entry: use engine 'tc' or 'band'")
     if interp_engine(num_cols, num_cols, engine, _num_frames(samples)) == "tc":
         return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
     offsets = spec_offsets(interp.spec)

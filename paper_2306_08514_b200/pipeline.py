@@ -58,13 +58,14 @@ class MapPipeline:
         rng = range(0, self.frames)
         v = self.variant
         if v in ("sspi", "si", "slri"):
-            tc = maps.uses_tc(v, self.op, self.engine, self.frames)
+            eng = maps.map_engine(v, self.op, self.engine, self.frames)
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
-                                            self.weighting, self.floor, planes=tc)
+                                            self.weighting, self.floor, planes=eng in ("tc", "tile"),
+                                            natural=eng == "tile")
             if v == "slri":
                 return maps.slri_map(self.op, xi, argmax=True, out_map=self.out_map)
             fn = maps.sspi_map if v == "sspi" else maps.si_map
-            return fn(self.op, xi, argmax=True, out_map=self.out_map, engine="tc" if tc else "band")
+            return fn(self.op, xi, argmax=True, out_map=self.out_map, engine=eng)
         gcc = fe.gcc_frames(self.input, self.frame, self.pairs, rng, self.weighting, self.floor,
                             tf32=(v == "conv" and self.precision == "tf32"))
         if v == "lr":

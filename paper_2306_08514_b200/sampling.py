@@ -21,6 +21,7 @@ import torch
 from . import _device as dev
 from . import _native as nat
 from .errors import ConfigError, DimensionError
+from .tiles import natural_columns as natural_source
 from .frontend import (FdGcc, _check_range, _floor_args, _frame_range, _pairs_device, _signal,
                        _window_device, num_frames)
 
@@ -85,8 +86,11 @@ class TdGccSamples:
     values: torch.Tensor
     spec: object
     lag_major: object = field(default=None, repr=False, compare=False)
-    # bf16 hi/lo planes [2][F][cols8] for the tensor-core interpolation map (optional)
+    # bf16 hi/lo planes for the tensor-core interpolation maps (optional): frame-major
+    # [2][F][cols8] in storage order, or (planes_natural) lag-major [2][cols8][F8] with the
+    # samples in natural lag order per pair
     bf16_planes: object = field(default=None, repr=False, compare=False)
+    planes_natural: bool = field(default=False, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -108,6 +112,10 @@ def pad4(n: int) -> int:
     return (int(n) + 3) // 4 * 4
 
 
+def pad8(n: int) -> int:
+    return (int(n) + 7) // 8 * 8
+
+
 def _new_samples(frames: int, s_total: int, dev_):
     """Lag-major output buffer (S, ld) and its (F, S) view."""
     ld = pad4(max(frames, 1))
@@ -115,8 +123,13 @@ def _new_samples(frames: int, s_total: int, dev_):
     return buf, ld, buf[:, :frames].t()
 
 
-def _wrap(view, buf, spec, batched: bool, planes=None) -> "TdGccSamples":
-    return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf, bf16_planes=planes)
+def _wrap(view, buf, spec, batched: bool, planes=None, natural: bool = False) -> "TdGccSamples":
+    return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf, bf16_planes=planes,
+                        planes_natural=natural)
+
+
+def natural_source_device(spec):
+    return dev.CACHE.get(spec, "natural_src_i32", lambda: dev.as_i32(natural_source(spec_offsets(spec))))
 
 
 def _check_gcc(gcc, spec) -> None:
@@ -143,12 +156,13 @@ def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
 
 
 def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
-                      floor=None, planes: bool = False) -> TdGccSamples:
+                      floor=None, planes: bool = False, natural: bool = False) -> TdGccSamples:
     """Fused stft_frame -> fd_gcc -> td_gcc_samples for a range of frames.
 
     Neither the spectra nor the cross-spectra touch HBM; one kernel launch.  With
     `planes` the same kernel also writes the bf16 hi/lo planes the tensor-core
-    interpolation map reads (`bf16_planes`).
+    interpolation maps read (`bf16_planes`; natural lag order per pair with `natural`,
+    the layout of the gathered-window engine).
     """
     x = _signal(samples)
     if x.shape[0] != pairs.num_mics:
@@ -168,9 +182,17 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
         nat.call("srpgpu_frames_to_samples", *args, dev.stream_ptr())
         return _wrap(view, buf, spec, batched)
     cols8 = (s_total + 7) // 8 * 8
-    pl = torch.empty((2, count, cols8), dtype=torch.bfloat16, device=x.device)
-    nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, dev.stream_ptr())
-    return _wrap(view, buf, spec, batched, pl)
+    src = natural_source_device(spec) if natural else None
+    if natural:     # lag-major natural-order planes [2][cols8][F8] (gathered-window engine)
+        f8 = pad8(count)
+        pl = torch.empty((2, cols8, f8), dtype=torch.bfloat16, device=x.device)
+        planes_ld = f8
+    else:           # frame-major planes [2][F][cols8] (dense tensor-core engine)
+        pl = torch.empty((2, count, cols8), dtype=torch.bfloat16, device=x.device)
+        planes_ld = 0
+    nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, planes_ld, 1 if natural else 0,
+             dev.ptr(src), dev.stream_ptr())
+    return _wrap(view, buf, spec, batched, pl, natural)
 
 
 def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:

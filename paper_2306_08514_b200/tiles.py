@@ -1,0 +1,203 @@
+"""Gathered-window operator layout for the tensor-core SSPI engine on long sample vectors.
+
+When the sample vector is long (BASELINE cfg4: S = 7028 lags over 120 pairs) the dense
+operator rows of `interp_tc` would cost S MACs per candidate against ~240 kept entries.
+Here the candidates are cut into tiles of 128 that are compact in TDOA space
+(recursive bisection along the pair with the widest spread), and each tile only sees
+the union of its candidates' kept lag windows, pair by pair, rounded up to groups of
+8 consecutive lags:
+
+    K(tile) = sum_p 8 * ceil(w_p / 8),   w_p = width of the tile's window of pair p
+
+(cfg4: 1074 on average, against S = 7028).  The tile's operator is stored dense over
+that K as 64-wide slabs (`[slab][128 rows][64]`, zero where a candidate does not keep
+the lag), and the kernel gathers each 8-lag group as 8 rows of the lag-major samples.
+The samples live in *natural* lag order per pair (-N_p .. N_p), so a window is a
+contiguous run of lag rows.
+
+Everything here is host-side layout (the same entries as the reference's sparse
+operator, interpolation.py:68-90 / 155-175, just placed differently).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+TILE, GROUP, SLAB = 128, 8, 64
+
+
+def natural_columns(offsets: np.ndarray) -> np.ndarray:
+    """perm[c_nat] = storage column: natural order -N..N per pair from 0..N, -N..-1."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    out = np.empty(int(offsets[-1]), dtype=np.int64)
+    for p in range(offsets.shape[0] - 1):
+        o, w = int(offsets[p]), int(offsets[p + 1] - offsets[p])
+        n = (w - 1) // 2
+        lags = np.arange(-n, n + 1)
+        out[o:o + w] = o + np.where(lags >= 0, lags, w + lags)
+    return out
+
+
+def to_natural(cols: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+    """Storage column -> natural column (same pair block)."""
+    offsets = np.asarray(offsets, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    pair = np.searchsorted(offsets, cols, side="right") - 1
+    base = offsets[pair]
+    n = (offsets[pair + 1] - base - 1) // 2
+    d = cols - base
+    return base + np.where(d <= n, n + d, d - n - 1)
+
+
+def _entries(sp, offsets):
+    """(rows, pairs, natural cols, values f32) of every kept entry of a sparse operator."""
+    if hasattr(sp, "kept") and np.ndim(getattr(sp, "cols", None)) == 3:    # FixedNnzInterp
+        p_count, j, k = sp.values.shape
+        keep = np.arange(k)[None, :] < np.asarray(sp.kept)[:, None]
+        sel = np.broadcast_to(keep[:, None, :], sp.values.shape)
+        rows = np.broadcast_to(np.arange(j, dtype=np.int64)[None, :, None], sp.values.shape)[sel]
+        cols = np.asarray(sp.cols)[sel].astype(np.int64)
+        vals = np.asarray(sp.values)[sel].astype(np.float32)
+    else:
+        splits = np.asarray(sp.row_splits, dtype=np.int64)
+        rows = np.repeat(np.arange(splits.shape[0] - 1, dtype=np.int64), np.diff(splits))
+        cols = np.asarray(sp.col_indices, dtype=np.int64)
+        vals = np.asarray(sp.values).astype(np.float32)
+    pairs = np.searchsorted(np.asarray(offsets, dtype=np.int64), cols, side="right") - 1
+    return rows, pairs, to_natural(cols, offsets), vals
+
+
+def bisect_tiles(feat: np.ndarray, tile: int = TILE, weight=None) -> list:
+    """Recursive bisection of the rows of `feat` (n, D) into groups of total weight <=
+    `tile` (weight: rows per item, default 1), splitting along the widest coordinate at
+    a multiple of `tile` near the (weighted) median."""
+    w = np.ones(feat.shape[0], dtype=np.int64) if weight is None else np.asarray(weight, dtype=np.int64)
+    out, stack = [], [np.arange(feat.shape[0], dtype=np.int64)]
+    while stack:
+        idx = stack.pop()
+        total = int(w[idx].sum())
+        if total <= tile or idx.shape[0] == 1:
+            out.append(np.sort(idx))
+            continue
+        sub = feat[idx]
+        p = int(np.argmax(sub.max(axis=0) - sub.min(axis=0)))
+        order = idx[np.argsort(sub[:, p], kind="stable")]
+        target = tile * max(1, int(round(total / (2 * tile)))) if total > 2 * tile else total // 2
+        cum = np.cumsum(w[order])
+        n1 = int(np.clip(np.searchsorted(cum, target, side="right"), 1, idx.shape[0] - 1))
+        stack.append(order[n1:])
+        stack.append(order[:n1])
+    return out
+
+
+class TileLayout:
+    """Host image of the gathered-window operator (see the module docstring).
+
+    slabs      (num_slabs, 128, 64) float32 operator values
+    group_col  (num_slabs * 8,) int32: first natural sample index (lag row) of each 8-lag group
+    tile_slab  (T,) int32 first slab of each tile; tile_nkb (T,) slabs per tile
+    tile_rows  (T, 128) int32 candidate of each tile row (ascending; -1 = padding)
+    tile_pos   (J,) int32 position t * 128 + row of each candidate (the kernel writes the map
+               in this tile order, fully coalesced; a gather pass restores grid order)
+    """
+
+    def __init__(self, sp, offsets, num_rows: int):
+        offsets = np.asarray(offsets, dtype=np.int64)
+        p_count = offsets.shape[0] - 1
+        rows, pairs, ncol, vals = _entries(sp, offsets)
+        self.num_rows, self.num_cols, self.num_pairs = int(num_rows), int(offsets[-1]), p_count
+        # per (candidate, pair): window of kept natural columns -> bisection features
+        key = rows * p_count + pairs
+        lo_ip = np.full(num_rows * p_count, np.iinfo(np.int64).max)
+        hi_ip = np.full(num_rows * p_count, -1)
+        np.minimum.at(lo_ip, key, ncol)
+        np.maximum.at(hi_ip, key, ncol)
+        empty = hi_ip < 0
+        feat = ((lo_ip + hi_ip) * 0.5).astype(np.float32).reshape(num_rows, p_count)
+        if empty.any():
+            centre = ((offsets[:-1] + offsets[1:] - 1) * 0.5).astype(np.float32)
+            feat = np.where(empty.reshape(num_rows, p_count), centre[None, :], feat)
+        tiles = bisect_tiles(feat) if num_rows else []
+        t_count = len(tiles)
+        tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
+        tile_of = np.zeros(num_rows, dtype=np.int64)
+        row_of = np.zeros(num_rows, dtype=np.int64)
+        for t, idx in enumerate(tiles):
+            tile_rows[t, :idx.shape[0]] = idx
+            tile_of[idx] = t
+            row_of[idx] = np.arange(idx.shape[0])
+        # per (tile, pair) window over the tile's candidates
+        lo_tp = np.full(t_count * p_count, np.iinfo(np.int64).max)
+        hi_tp = np.full(t_count * p_count, -1)
+        ip = np.arange(num_rows * p_count)
+        tp = tile_of[ip // p_count] * p_count + ip % p_count
+        ok = ~empty
+        np.minimum.at(lo_tp, tp[ok], lo_ip[ok])
+        np.maximum.at(hi_tp, tp[ok], hi_ip[ok])
+        width = np.where(hi_tp >= 0, hi_tp - lo_tp + 1, 0).reshape(t_count, p_count)
+        ngroups = (width + GROUP - 1) // GROUP                           # (T, P)
+        gstart = np.zeros_like(ngroups)
+        gstart[:, 1:] = np.cumsum(ngroups, axis=1)[:, :-1]                # group index of pair p
+        tile_groups = ngroups.sum(axis=1)
+        tile_nkb = np.maximum(1, (tile_groups * GROUP + SLAB - 1) // SLAB)
+        tile_slab = np.zeros(t_count, dtype=np.int64)
+        if t_count:
+            tile_slab[1:] = np.cumsum(tile_nkb)[:-1]
+        num_slabs = int(tile_nkb.sum()) if t_count else 0
+        group_col = np.zeros(num_slabs * (SLAB // GROUP), dtype=np.int64)
+        lo2 = lo_tp.reshape(t_count, p_count)
+        for t in range(t_count):
+            g0 = tile_slab[t] * (SLAB // GROUP)
+            starts = [lo2[t, p] + GROUP * np.arange(ngroups[t, p]) for p in range(p_count) if ngroups[t, p]]
+            if starts:
+                s = np.concatenate(starts)
+                group_col[g0:g0 + s.shape[0]] = s
+        # scatter the entries into the slabs
+        t_e = tile_of[rows]
+        kpos = gstart[t_e, pairs] * GROUP + (ncol - lo2[t_e, pairs])
+        slab = tile_slab[t_e] + kpos // SLAB
+        self.slabs = np.zeros((num_slabs, TILE, SLAB), dtype=np.float32)
+        self.slabs[slab, row_of[rows], kpos % SLAB] = vals
+        self.group_col = group_col.astype(np.int32)
+        self.tile_slab = tile_slab.astype(np.int32)
+        self.tile_nkb = tile_nkb.astype(np.int32)
+        self.tile_rows = tile_rows
+        self.tile_pos = (tile_of * TILE + row_of).astype(np.int32)
+        self.num_tiles = t_count
+        self.num_slabs = num_slabs
+        self.mean_k = float(tile_nkb.mean() * SLAB) if t_count else 0.0
+
+    def unit_bounds(self, frames: int, ctas: int, group: int = 4) -> np.ndarray:
+        """Balanced contiguous ranges of work units per CTA.
+
+        Units run frame-tile-group major (`group` frame tiles of 256), then tile, then the
+        frame tile inside the group, so a tile's slabs are reused from L2 across the
+        group and the group's xi columns stay L2-resident.  Work = slabs (+1 for the
+        epilogue); units past the last frame tile are empty.
+        """
+        n_tiles = (frames + 255) // 256
+        n_groups = (n_tiles + group - 1) // group
+        u = np.arange(n_groups * self.num_tiles * group)
+        n = (u // (self.num_tiles * group)) * group + u % group
+        t = (u % (self.num_tiles * group)) // group
+        work = np.where(n < n_tiles, self.tile_nkb[t].astype(np.int64) + 1, 0)
+        cum = np.concatenate([[0], np.cumsum(work)])
+        targets = np.linspace(0, cum[-1], ctas + 1)
+        bounds = np.searchsorted(cum, targets, side="left")
+        bounds[0], bounds[-1] = 0, u.shape[0]
+        return np.maximum.accumulate(bounds).astype(np.int32)
+
+    def emulate(self, xi_nat: np.ndarray) -> np.ndarray:
+        """float64 reference of the gathered product (test helper): z (F, J)."""
+        f = xi_nat.shape[0]
+        z = np.zeros((f, self.num_rows))
+        pad = np.concatenate([xi_nat, np.zeros((f, SLAB + GROUP))], axis=1)
+        for t in range(self.num_tiles):
+            s0, nk = int(self.tile_slab[t]), int(self.tile_nkb[t])
+            cols = self.group_col[s0 * 8:(s0 + nk) * 8][:, None] + np.arange(GROUP)[None, :]
+            a = self.slabs[s0:s0 + nk].transpose(1, 0, 2).reshape(TILE, nk * SLAB).astype(np.float64)
+            x = pad[:, cols.ravel()]                                     # (F, nk*64)
+            r = self.tile_rows[t]
+            ok = r >= 0
+            z[:, r[ok]] = (x @ a.T)[:, ok]
+        return z

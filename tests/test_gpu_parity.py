@@ -13,6 +13,7 @@ import torch
 import paper_2306_08514_b200 as s
 from oracle import srp_oracle as O
 from conftest import keep_tags, load_golden, scene_objects, sparse_from_golden
+from paper_2306_08514_b200.sampling import spec_offsets
 
 pytestmark = pytest.mark.gpu
 
@@ -102,7 +103,7 @@ def test_fused_frames_to_samples(golden_scene):
 
 # ------------------------------------------------------------------ maps
 
-@pytest.mark.parametrize("engine", ["tc", "band"])
+@pytest.mark.parametrize("engine", ["tc", "tile", "band"])
 def test_sspi_and_si_maps(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
@@ -118,6 +119,8 @@ def test_sspi_and_si_maps(golden_scene, engine):
         assert_argmax_agrees(idx, ref)
         zo, io = s.sspi_map(sp, xi, argmax=True, out_map=False, engine=engine)
         assert zo is None and torch.equal(io, idx)         # argmax-only output
+    if engine == "tile":                                   # keep-all SI is not a gathered-window case
+        return
     interp = s.InterpMatrix(g["interp"], spec)
     z_si = s.si_map(interp, xi, engine=engine)
     assert_map_close(z_si, g["z_si"])
@@ -135,12 +138,36 @@ def test_sspi_engines_agree_on_frame_batches(golden_scene):
     xt = s.TdGccSamples(torch.from_numpy(x).cuda(), spec)
     zt, it = s.sspi_map(sp, xt, argmax=True, engine="tc")
     zb, ib = s.sspi_map(sp, xt, argmax=True, engine="band")
+    zg, ig = s.sspi_map(sp, xt, argmax=True, engine="tile")
     z1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tc")
     assert torch.equal(zt[7], z1)
+    g1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tile")
+    assert torch.equal(zg[7], g1)
     ref = O.sspi_map(sp.values, sp.col_indices, sp.row_splits, x.astype(np.float64))
     assert_map_close(zt, ref)
     assert_map_close(zb, ref)
+    assert_map_close(zg, ref)
     assert_argmax_agrees(it, ref)
+    assert_argmax_agrees(ig, ref)
+
+
+def test_natural_planes_from_frontend(golden_scene):
+    """The frontend's natural-lag-order bf16 planes equal the permuted split of its f32 samples."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    for natural in (False, True):
+        xi = s.frames_to_samples(x, frame, pairs, spec, planes=True, natural=natural)
+        plain = s.TdGccSamples(xi.values.clone(), spec)
+        off = spec_offsets(spec) if natural else None
+        ref, _, _ = s.maps.sample_planes(plain, spec.total_samples, natural=off)
+        assert xi.planes_natural == natural
+        if natural:                                         # lag-major: compare the valid frame columns
+            f = xi.values.shape[0]
+            assert torch.equal(xi.bf16_planes[:, :spec.total_samples, :f].view(torch.int16),
+                               ref[:, :spec.total_samples, :f].view(torch.int16))
+        else:
+            assert torch.equal(xi.bf16_planes.view(torch.int16), ref.view(torch.int16))
 
 
 def test_sspi_tile_and_row_kernels_agree(golden_scene):

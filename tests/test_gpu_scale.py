@@ -172,13 +172,20 @@ def test_cfg4_conventional_onchip_steering():
         assert z_ref[f, j] >= z_ref[f].max() * (1 - 2 * TOL)
 
 
-def test_cfg4_full_grid_sspi():
+@pytest.fixture(scope="module")
+def cfg4_fit():
     wl = workloads.make("cfg4", num_frames=64)
+    return wl, s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
+
+
+@pytest.mark.parametrize("engine", ["tile", "band"])
+def test_cfg4_full_grid_sspi(cfg4_fit, engine):
+    wl, fx = cfg4_fit
     assert wl.grid.num_points == 334611 and wl.pairs.num_pairs == 120
     x = torch.from_numpy(wl.samples).cuda()
-    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec)
-    fx = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
-    z, idx = s.sspi_map(fx, xi, argmax=True)
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, planes=(engine == "tile"),
+                             natural=(engine == "tile"))
+    z, idx = s.sspi_map(fx, xi, argmax=True, engine=engine)
     nf = 4
     xi_ref = O.td_gcc_samples(oracle_psi(wl, nf), wl.spec.counts, wl.frame.half_len)
     z_ref = np.zeros((nf, wl.grid.num_points))

@@ -31,10 +31,13 @@ def main():
     x = torch.from_numpy(wl.samples).cuda()
     rng = range(frames)
     if a.variant == "sspi" and a.workload == "cfg4":     # dense Lambda infeasible: fixed nnz per (i, p)
+        from paper_2306_08514_b200 import maps
         op = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
+        eng = maps.map_engine("sspi", op, a.engine, frames)
         for _ in range(a.reps):
-            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng)
-            z, idx = s.sspi_map(op, xi, argmax=True)
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=eng in ("tc", "tile"),
+                                     natural=eng == "tile")
+            z, idx = s.sspi_map(op, xi, argmax=True, engine=eng)
     elif a.variant in ("sspi", "slri", "si"):
         interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
         if a.variant == "sspi":
@@ -46,9 +49,10 @@ def main():
             op = interp
         from paper_2306_08514_b200 import maps
         fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
-        planes = maps.uses_tc(a.variant, op, a.engine, frames)
+        eng = maps.map_engine(a.variant, op, a.engine, frames)
         for _ in range(a.reps):
-            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=planes)
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=eng in ("tc", "tile"),
+                                     natural=eng == "tile")
             z, idx = fn(op, xi, argmax=True, engine=a.engine)
     elif a.variant == "conv":          # on-chip steering (bench variant "conv")
         op = s.steering_operator(wl.tdoa, wl.frame)

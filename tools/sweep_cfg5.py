@@ -129,7 +129,7 @@ def main():
         fit_s = time.perf_counter() - t0
         pipe = pipe_for("sspi", sp, f_main)
         ms = graph_ms(pipe, 10)
-        eng = "tc" if maps.uses_tc("sspi", sp, "auto", f_main) else "band"
+        eng = maps.map_engine("sspi", sp, "auto", f_main)
         row = {"sweep": "nnz", "nnz_per_cand_pair": q, "kept": int(sp.values.shape[0]), "frames": f_main,
                "ms_per_batch": ms, "maps_per_s": f_main / (ms / 1e3), "engine": eng,
                "host_fit_s": fit_s, **errors("sspi", sp, pipe)}
@@ -150,12 +150,12 @@ def main():
         for fb in batches:
             if fb > wl.num_frames:
                 continue
-            for eng in ("tc", "band", "auto"):
+            for eng in ("tc", "tile", "band", "auto"):
                 pipe = pipe_for("sspi", sp, fb, eng)
                 ms = graph_ms(pipe, 10 if fb >= 1024 else 30)
                 row = {"sweep": "batch", "frames": fb, "ms_per_batch": ms, "maps_per_s": fb / (ms / 1e3),
                        "z_write_GBps": fb * j * 4 / (ms / 1e3) / 1e9, "engine": eng,
-                       "auto_picks": "tc" if maps.uses_tc("sspi", sp, "auto", fb) else "band"}
+                       "auto_picks": maps.map_engine("sspi", sp, "auto", fb)}
                 print(json.dumps(row), flush=True)
                 del pipe
                 torch.cuda.empty_cache()
