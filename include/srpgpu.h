@@ -150,14 +150,15 @@ int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const v
 /* sspi_map / si_map on the tensor cores for long sample vectors: per-tile gathered lag
  * windows (host layout: paper_2306_08514_b200/tiles.py).  samples_planes: lag-major
  * bf16 planes [2][round8(num_cols)][planes_ld] in natural lag order (planes_ld >= F,
- * multiple of 8); slab_planes [2][num_slabs * 128][64] bf16 (tile operator slabs); group_col
- * [num_slabs * 8] first natural sample index of each 8-lag group; tile_slab /
- * tile_nkb [num_tiles] first slab and slab count of each
- * tile; tile_rows [num_tiles][128] candidate index of each tile row (ascending, -1 pad);
+ * multiple of 8); slab_planes [2][num_slabs * 128][64] bf16 (tile operator slabs: 64-lag
+ * block b of a tile, half h -> slab 2b + h); group_col [num_blocks * 8] first natural
+ * sample index of each 8-lag group; tile_slab / tile_nkb [num_tiles] first 64-lag block
+ * and block count of each tile (<= 128); tile_rows [num_tiles][256] candidate index of
+ * each tile row (ascending, -1 pad; rows 0-127 half 0);
  * unit_bounds [num_ctas + 1] contiguous work-unit ranges, one persistent CTA each.
  * z [F][J] and keys [F] optional; a map is written in tile order into z_tiles
- * [F][num_tiles * 128] (full 32-byte sectors) and gathered back to grid order by
- * tile_pos [J] (= tile * 128 + row of each candidate). */
+ * [F][num_tiles * 256] (full 32-byte sectors) and gathered back to grid order by
+ * tile_pos [J] (= tile * 256 + row of each candidate). */
 int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, int32_t num_cols,
                                 int64_t planes_ld,
                                 const void* slab_planes, int64_t num_slabs, const int32_t* group_col,

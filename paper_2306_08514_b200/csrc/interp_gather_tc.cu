@@ -3,25 +3,29 @@
 //
 //   z[f][j] = sum_s Lambda[j][s] xi[f][s]      interpolation.py:121-126, 188-195
 //
-// Candidates come in tiles of 128 that are compact in TDOA space; a tile's operator is
+// Candidates come in tiles of 256 that are compact in TDOA space; a tile's operator is
 // dense over K = its candidates' kept lag windows (pair by pair, rounded up to groups of
-// 8 lags), stored as 64-wide slabs [slab][128][64] (bf16 hi / lo planes).  The matching
-// samples are gathered from lag-major, natural-lag-order xi planes [S][F8] (frames
-// contiguous): a group is 8 lag rows, loaded as four 128-byte-swizzled TMA boxes of
-// 64 frames x 8 lags, so no operand is ever materialised per tile.  (A frame-major
-// gather would need one 16-byte box per (frame, group) row: measured 6x slower.)
+// 8 lags), stored in 64-lag blocks of two 128-row slabs (bf16 hi / lo planes).  The
+// matching samples are gathered from lag-major, natural-lag-order xi planes [S][F8]
+// (frames contiguous): a group is 8 lag rows, loaded as four 128-byte-swizzled TMA boxes
+// of 64 frames x 8 lags.  Each gathered sample stage feeds both 128-row halves of the
+// tile (two MMAs per step), which halves the gather TMA traffic per flop: with 128-row
+// tiles the kernel was bound by the TMA box rate (measured: a quarter of the boxes for
+// the same MMA work ran 2x faster).  A frame-major gather would need one 16-byte box per
+// (frame, group) row: 6x slower again.
 //
-// D = A . B^T with A = slab (M = 128 candidates = TMEM lanes, K-major, 128-byte swizzle)
-// and B = gathered xi (N = 256 frames = TMEM columns, MN-major, 128-byte swizzle: 1 KB
-// atoms of 64 frames x 8 lags, 1 KB apart along N (LBO) and 4 KB apart along K (SBO)).
-// Three kind::f16 MMAs per 16-lag step (bf16 hi/lo split, as interp_tc.cu).  Persistent CTAs take balanced contiguous ranges of work units
-// (frame-tile group, tile, frame tile): a tile's slabs are reused from L2 across the
-// group's frame tiles and the group's xi columns stay L2-resident.
-// Roles: warp 0 TMA producer (lanes 0-15 one plane x group each), warp 1 TMEM allocator
-// + MMA issuer, warps 2-9 epilogue
-// (lane quarter warp % 4 = 32 candidates, half of the eight 32-frame chunks each):
-// z rows stored straight from registers, per-frame argmax by a butterfly max across
-// the lanes plus a ballot for the lowest winning candidate (tile rows are ascending).
+// D_h = A_h . B^T per half h: A_h = slab (M = 128 candidates = TMEM lanes, K-major,
+// 64-byte swizzle, 32-lag k-blocks), B = gathered xi (N = 256 frames = TMEM columns,
+// MN-major, 128-byte swizzle: 1 KB atoms of 64 frames x 8 lags, 1 KB apart along N (LBO)
+// and 4 KB apart along K (SBO)).  Three kind::f16 MMAs per 16-lag step (bf16 hi/lo split,
+// as interp_tc.cu); the two halves fill the 512 TMEM columns.  Persistent CTAs take
+// balanced contiguous ranges of work units (frame-tile group, tile, frame tile).
+// Roles: warp 0 TMA producer (lanes 0-7 one plane x group each, 8-11 the slabs), warp 1
+// TMEM allocator + MMA issuer, warps 2-9 epilogue (lane quarter warp % 4 of one half):
+// the map goes out in tile order, 128 contiguous bytes per warp store (a gather pass
+// restores grid order: scattered 4-byte stores made the L2 read-modify-write each
+// sector), and the per-frame argmax is a butterfly max across the lanes plus a ballot
+// for the lowest winning candidate (tile rows are ascending).
 #include <cuda_bf16.h>
 
 #include "tc_common.cuh"
@@ -31,25 +35,27 @@ namespace gtc {
 
 using namespace tc;
 
-constexpr int GM = 128;   // candidates per tile
+constexpr int GM = 128;   // candidates per tile half (TMEM lanes)
+constexpr int GT = 256;   // candidates per tile (two halves)
 constexpr int GN = 256;   // frames per unit
-constexpr int GK = 64;    // lags per slab (k-block)
+constexpr int GB = 64;    // lags per operator block (slab width)
+constexpr int GK = 32;    // lags per pipeline stage
 constexpr int GG = 8;     // lags per gathered group (8 rows of the lag-major samples)
 constexpr int GA = 64;    // frames per MN atom (128 bytes)
-constexpr int NG = GK / GG;
+constexpr int NG = GK / GG;          // groups per stage
 constexpr int UK = 16;    // kind::f16 MMA K
-constexpr int NS = 2;     // operand stages (96 KB each)
+constexpr int NS = 3;     // operand stages (64 KB each)
 constexpr int kEpi = 8;
 constexpr int kThreads = 32 * (2 + kEpi);
 constexpr int FG = 4;     // frame tiles per unit group (must match tiles.TileLayout.unit_bounds)
-constexpr int kMaxSlabs = 256;                    // slabs per tile (K <= 16384 lags)
-constexpr int kMaxGroups = kMaxSlabs * NG;
+constexpr int kMaxBlocks = 128;                   // 64-lag blocks per tile (K <= 8192 lags)
+constexpr int kMaxGroups = kMaxBlocks * (GB / GG);
 
 struct __align__(1024) Smem {
-  uint16_t a[NS][2][GM * GK];          // slab hi / lo (16 KB each, 128-byte swizzle)
-  uint16_t b[NS][2][NG][GN * GG];      // gathered xi hi / lo: 8 groups x 4 atoms [8 lags][64 frames]
+  uint16_t a[NS][2][2][GM * GK];       // [half][plane] slab columns (8 KB each, 64-byte swizzle)
+  uint16_t b[NS][2][NG][GN * GG];      // [plane][group] 4 atoms [8 lags][64 frames] (4 KB each)
   int32_t rows[2][kMaxGroups];         // the current / next unit's group rows (producer only)
-  uint64_t full[NS], empty[NS], tfull[2], tempty[2];
+  uint64_t full[NS], empty[NS], tfull, tempty;
   uint32_t tmem_base;
 };
 
@@ -89,7 +95,7 @@ __device__ __forceinline__ bool decode(int u, int T, int n_tiles, Unit& out) {
 __global__ void __launch_bounds__(kThreads, 1)
 gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                  const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int64_t F,
-                 int64_t J, int32_t T, const int32_t* __restrict__ group_col, const int32_t* __restrict__ tile_slab,
+                 int64_t J, int32_t T, const int32_t* __restrict__ group_col, const int32_t* __restrict__ tile_blk,
                  const int32_t* __restrict__ tile_nkb, const int32_t* __restrict__ tile_rows,
                  const int32_t* __restrict__ bounds, float* __restrict__ zt, unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -107,10 +113,8 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.tfull[b], 1);
-      mbar_init(&sm.tempty[b], kEpi);
-    }
+    mbar_init(&sm.tfull, 1);
+    mbar_init(&sm.tempty, kEpi);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -126,18 +130,20 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 
   if (warp == 0) {
     // the unit's group rows are staged in shared memory (one coalesced load per unit,
-    // prefetched a unit ahead) so the per-k-block loop has no dependent global load;
-    // lane 0 waits and arms the stage; lanes 0-15 then each load one (plane, group):
-    // four 64-frame atoms of its 8 lag rows; lanes 16-17 load the slab planes
-    constexpr uint32_t kBytes = 2u * (GM * GK + GN * GK) * sizeof(uint16_t);
-    const int plane = (lane >> 3) & 1, grp = lane & 7;
+    // prefetched a unit ahead) so the per-stage loop has no dependent global load;
+    // lane 0 waits and arms the stage; lanes 0-7 then each load one (plane, group):
+    // four 64-frame atoms of its 8 lag rows; lanes 8-11 load the (half, plane) slabs
+    constexpr uint32_t kBytes = 2u * (2 * GM * GK + GN * GK) * sizeof(uint16_t);
+    const int plane = (lane >> 2) & 1, grp = lane & 3;
+    const int ah = ((lane - 8) >> 1) & 1, ap = (lane - 8) & 1;
+    const uint64_t keep = policy_evict_last();   // a tile's slabs are re-read for FG frame tiles
     auto next_unit = [&](int u, Unit& w) {
       while (u < u_end && !decode(u, T, n_tiles, w)) ++u;
       return u;
     };
     auto stage_rows = [&](int buf, const Unit& w) {
-      const int s0 = __ldg(tile_slab + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int i = lane; i < nk * NG; i += 32) sm.rows[buf][i] = __ldg(group_col + s0 * NG + i);
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int i = lane; i < nk * (GB / GG); i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
     };
     uint32_t g = 0;
     int buf = 0;
@@ -149,23 +155,23 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       const int un = next_unit(u + 1, wn);
       if (un < u_end) stage_rows(buf ^ 1, wn);          // prefetch the next unit's rows
       __syncwarp();
-      const int s0 = __ldg(tile_slab + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int kb = 0; kb < nk; ++kb, ++g) {
-        const int slab = s0 + kb;
-        const int row = sm.rows[buf][kb * NG + grp];
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int kq = 0; kq < 2 * nk; ++kq, ++g) {       // 32-lag stages: half a block each
+        const int blk = b0 + (kq >> 1), sub = kq & 1;
+        const int row = sm.rows[buf][kq * NG + grp];
         const int s = g % NS;
         if (lane == 0) {
           mbar_wait(&sm.empty[s], ((g / NS) & 1) ^ 1);
           mbar_expect_tx(&sm.full[s], kBytes);
         }
         __syncwarp();
-        if (lane < 16) {
+        if (lane < 8) {
           const CUtensorMap* mb = plane ? &mb_lo : &mb_hi;
 #pragma unroll
           for (int a = 0; a < GN / GA; ++a)
             tma_load_2d(sm.b[s][plane][grp] + a * GA * GG, mb, &sm.full[s], w.n * GN + a * GA, row);
-        } else if (lane < 18) {
-          tma_load_2d(sm.a[s][lane - 16], lane == 16 ? &ma_hi : &ma_lo, &sm.full[s], 0, slab * GM);
+        } else if (lane < 12) {
+          tma_load_2d_hint(sm.a[s][ah][ap], ap ? &ma_lo : &ma_hi, &sm.full[s], sub * GK, (2 * blk + ah) * GM, keep);
         }
       }
       __syncwarp();
@@ -183,65 +189,66 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
         Unit w;
         if (!decode(u, T, n_tiles, w)) continue;
         const int nk = __ldg(tile_nkb + w.t);
-        const uint32_t acc = it & 1;
-        mbar_wait(&sm.tempty[acc], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&sm.tempty, (it & 1) ^ 1);            // the previous unit's maps are drained
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + acc * GN;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        for (int kq = 0; kq < 2 * nk; ++kq, ++g) {
           const int s = g % NS;
           mbar_wait(&sm.full[s], (g / NS) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t ah = smem_desc(sm.a[s][0]), al = smem_desc(sm.a[s][1]);
 #pragma unroll
           for (int k = 0; k < GK / UK; ++k) {
             const uint64_t aoff = (uint64_t)((k * UK * 2) >> 4);
             const uint64_t bh = desc_mn128(sm.b[s][0][2 * k]), bl = desc_mn128(sm.b[s][1][2 * k]);
-            mma_bf16(d, ah + aoff, bh, idesc, (kb | k) != 0);
-            mma_bf16(d, ah + aoff, bl, idesc, 1u);
-            mma_bf16(d, al + aoff, bh, idesc, 1u);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t d = tmem + h * GN;
+              const uint64_t a_h = smem_desc_sw64(sm.a[s][h][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][h][1]) + aoff;
+              mma_bf16(d, a_h, bh, idesc, (kq | k) != 0);
+              mma_bf16(d, a_h, bl, idesc, 1u);
+              mma_bf16(d, a_l, bh, idesc, 1u);
+            }
           }
           mma_commit(&sm.empty[s]);
         }
-        mma_commit(&sm.tfull[acc]);
+        mma_commit(&sm.tfull);
         ++it;
       }
     }
   } else {
     const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;                // which 4 of the 8 column chunks
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int half = (warp - 2) >> 2;                // which tile half (TMEM columns half * 256)
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
+    const int64_t ldt = (int64_t)T * GT;
     uint32_t it = 0;
     for (int u = u_begin; u < u_end; ++u) {
       Unit w;
       if (!decode(u, T, n_tiles, w)) continue;
-      const uint32_t acc = it & 1;
-      const int jrow = __ldg(tile_rows + (int64_t)w.t * GM + q * 32 + lane);   // -1: padding row
-      mbar_wait(&sm.tfull[acc], (it >> 1) & 1);
+      const int r = half * GM + q * 32 + lane;         // tile row
+      const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);   // -1: padding row
+      mbar_wait(&sm.tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const bool any = __any_sync(0xffffffffu, jrow >= 0);
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c = half * 4 + cc;
-        uint32_t r[32];
-        tmem_ld32(lane_base + acc * GN + c * 32, r);
+      for (int c = 0; c < GN / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(lane_base + c * 32, rr);
         const int64_t f0 = (int64_t)w.n * GN + c * 32;
         if (f0 >= F || !any) continue;               // warp-uniform (after the aligned load)
         if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
-          const int64_t ldt = (int64_t)T * GM;
-          float* zc = zt + f0 * ldt + (int64_t)w.t * GM + q * 32 + lane;
+          float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
           if (f0 + 32 <= F) {
 #pragma unroll
-            for (int t = 0; t < 32; ++t) __stcg(zc + t * ldt, __uint_as_float(r[t]));
+            for (int t = 0; t < 32; ++t) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
           } else {
 #pragma unroll
             for (int t = 0; t < 32; ++t)
-              if (f0 + t < F) __stcg(zc + t * ldt, __uint_as_float(r[t]));
+              if (f0 + t < F) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
           }
         }
         if (keys) {
           uint32_t ob[32], v[32];
 #pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] = ob[t] = jrow >= 0 ? ordered_bits(__uint_as_float(r[t])) : 0u;
+          for (int t = 0; t < 32; ++t) v[t] = ob[t] = jrow >= 0 ? ordered_bits(__uint_as_float(rr[t])) : 0u;
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) {
             const bool up = (lane & o) != 0;
@@ -268,7 +275,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty[acc]);
+      if (lane == 0) mbar_arrive(&sm.tempty);
       ++it;
     }
   }
@@ -284,11 +291,22 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 // the tiles' ascending rows, mostly short contiguous runs)
 __global__ void untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
                               int64_t F, float* __restrict__ z) {
+  constexpr int U = 4;   // independent gathers in flight per thread
   for (int64_t f = blockIdx.y; f < F; f += gridDim.y) {
     const float* src = zt + f * ldt;
     float* dst = z + f * J;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x)
-      __stcs(dst + j, __ldcs(src + __ldg(pos + j)));
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < J; j0 += U * step) {
+      int32_t p[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) p[u] = j0 + u * step < J ? __ldg(pos + j0 + u * step) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(src + p[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j0 + u * step < J) __stcs(dst + j0 + u * step, v[u]);
+    }
   }
 }
 
@@ -327,8 +345,9 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int64_t arows = num_slabs * GM;
-  if ((s = make_map_2d(&ma_hi, bf, 2, xo, arows, GK, GK, GK, GM, "interp_map_gather_tc")) ||
-      (s = make_map_2d(&ma_lo, bf, 2, xo + arows * GK, arows, GK, GK, GK, GM, "interp_map_gather_tc")) ||
+  const CUtensorMapSwizzle sw64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  if ((s = make_map_2d(&ma_hi, bf, 2, xo, arows, GB, GB, GK, GM, "interp_map_gather_tc", sw64)) ||
+      (s = make_map_2d(&ma_lo, bf, 2, xo + arows * GB, arows, GB, GB, GK, GM, "interp_map_gather_tc", sw64)) ||
       (s = make_map_2d(&mb_hi, bf, 2, xs, num_cols, num_frames, planes_ld, GA, GG, "interp_map_gather_tc")) ||
       (s = make_map_2d(&mb_lo, bf, 2, xs + (int64_t)((num_cols + 7) / 8 * 8) * planes_ld, num_cols, num_frames,
                        planes_ld, GA, GG, "interp_map_gather_tc")))   // planes hold round8(S) rows each
@@ -346,7 +365,7 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
   if (z) {
     dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
               (unsigned)std::min<int64_t>(num_frames, 65535));
-    untile_kernel<<<grid, 256, 0, st>>>(z_tiles, (int64_t)num_tiles * GM, tile_pos, num_candidates, num_frames, z);
+    untile_kernel<<<grid, 256, 0, st>>>(z_tiles, (int64_t)num_tiles * GT, tile_pos, num_candidates, num_frames, z);
     SRPGPU_CHECK_LAUNCH("interp_map_gather_tc(untile)");
   }
   return SRPGPU_OK;

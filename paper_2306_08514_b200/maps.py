@@ -340,17 +340,17 @@ def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", fram
 class TileOperator:
     """Device image of the gathered-window operator (tiles.TileLayout) for engine "tile"."""
 
-    MAX_SLABS = 256             # per tile (interp_gather_tc.cu kMaxSlabs)
+    MAX_BLOCKS = 128            # 64-lag operator blocks per tile (interp_gather_tc.cu kMaxBlocks)
 
     def __init__(self, sp, offsets, num_rows: int):
         lay = tiles.TileLayout(sp, offsets, num_rows)
-        if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_SLABS:
-            raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} slabs (> {self.MAX_SLABS}): "
-                             "use engine 'band'")
+        if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
+            raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
+                             f"(> {self.MAX_BLOCKS}): use engine 'band'")
         d = dev.device()
         self.num_rows, self.num_cols, self.cols8 = int(num_rows), int(lay.num_cols), _cols8(lay.num_cols)
         self.num_tiles, self.num_slabs, self.mean_k = lay.num_tiles, lay.num_slabs, lay.mean_k
-        self.planes = torch.empty((2, max(1, lay.num_slabs) * tiles.TILE, tiles.SLAB), dtype=torch.bfloat16,
+        self.planes = torch.empty((2, max(1, lay.num_slabs) * tiles.HALF, tiles.SLAB), dtype=torch.bfloat16,
                                   device=d)
         if lay.num_slabs:
             src = torch.from_numpy(lay.slabs.reshape(-1, tiles.SLAB)).to(d)

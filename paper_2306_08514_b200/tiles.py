@@ -2,16 +2,17 @@
 
 When the sample vector is long (BASELINE cfg4: S = 7028 lags over 120 pairs) the dense
 operator rows of `interp_tc` would cost S MACs per candidate against ~240 kept entries.
-Here the candidates are cut into tiles of 128 that are compact in TDOA space
-(recursive bisection along the pair with the widest spread), and each tile only sees
-the union of its candidates' kept lag windows, pair by pair, rounded up to groups of
-8 consecutive lags:
+Here the candidates are cut into tiles of 256 (two MMA halves of 128 rows that share
+every gathered sample tile) that are compact in TDOA space (recursive bisection along
+the pair with the widest spread), and each tile only sees the union of its candidates'
+kept lag windows, pair by pair, rounded up to groups of 8 consecutive lags:
 
     K(tile) = sum_p 8 * ceil(w_p / 8),   w_p = width of the tile's window of pair p
 
-(cfg4: 1074 on average, against S = 7028).  The tile's operator is stored dense over
-that K as 64-wide slabs (`[slab][128 rows][64]`, zero where a candidate does not keep
-the lag), and the kernel gathers each 8-lag group as 8 rows of the lag-major samples.
+(cfg4: 1182 on average for 256-candidate tiles, 1074 for 128; against S = 7028).  The
+tile's operator is stored dense over that K in 64-lag blocks, each block as two slabs
+(`[2 * block + half][128 rows][64]`, zero where a candidate does not keep the lag), and
+the kernel gathers each 8-lag group as 8 rows of the lag-major samples.
 The samples live in *natural* lag order per pair (-N_p .. N_p), so a window is a
 contiguous run of lag rows.
 
@@ -23,7 +24,7 @@ from __future__ import annotations
 
 import numpy as np
 
-TILE, GROUP, SLAB = 128, 8, 64
+TILE, HALF, GROUP, SLAB = 256, 128, 8, 64
 
 
 def natural_columns(offsets: np.ndarray) -> np.ndarray:
@@ -93,11 +94,12 @@ def bisect_tiles(feat: np.ndarray, tile: int = TILE, weight=None) -> list:
 class TileLayout:
     """Host image of the gathered-window operator (see the module docstring).
 
-    slabs      (num_slabs, 128, 64) float32 operator values
-    group_col  (num_slabs * 8,) int32: first natural sample index (lag row) of each 8-lag group
-    tile_slab  (T,) int32 first slab of each tile; tile_nkb (T,) slabs per tile
-    tile_rows  (T, 128) int32 candidate of each tile row (ascending; -1 = padding)
-    tile_pos   (J,) int32 position t * 128 + row of each candidate (the kernel writes the map
+    slabs      (2 * num_blocks, 128, 64) float32 operator values: block b, half h -> 2b + h
+    group_col  (num_blocks * 8,) int32: first natural sample index (lag row) of each 8-lag group
+    tile_slab  (T,) int32 first 64-lag block of each tile; tile_nkb (T,) blocks per tile
+    tile_rows  (T, 256) int32 candidate of each tile row (ascending; -1 = padding);
+               rows 0-127 are half 0, 128-255 half 1
+    tile_pos   (J,) int32 position t * 256 + row of each candidate (the kernel writes the map
                in this tile order, fully coalesced; a gather pass restores grid order)
     """
 
@@ -143,8 +145,8 @@ class TileLayout:
         tile_slab = np.zeros(t_count, dtype=np.int64)
         if t_count:
             tile_slab[1:] = np.cumsum(tile_nkb)[:-1]
-        num_slabs = int(tile_nkb.sum()) if t_count else 0
-        group_col = np.zeros(num_slabs * (SLAB // GROUP), dtype=np.int64)
+        num_blocks = int(tile_nkb.sum()) if t_count else 0
+        group_col = np.zeros(num_blocks * (SLAB // GROUP), dtype=np.int64)
         lo2 = lo_tp.reshape(t_count, p_count)
         for t in range(t_count):
             g0 = tile_slab[t] * (SLAB // GROUP)
@@ -155,16 +157,18 @@ class TileLayout:
         # scatter the entries into the slabs
         t_e = tile_of[rows]
         kpos = gstart[t_e, pairs] * GROUP + (ncol - lo2[t_e, pairs])
-        slab = tile_slab[t_e] + kpos // SLAB
-        self.slabs = np.zeros((num_slabs, TILE, SLAB), dtype=np.float32)
-        self.slabs[slab, row_of[rows], kpos % SLAB] = vals
+        r_e = row_of[rows]
+        slab = 2 * (tile_slab[t_e] + kpos // SLAB) + r_e // HALF
+        self.slabs = np.zeros((2 * num_blocks, HALF, SLAB), dtype=np.float32)
+        self.slabs[slab, r_e % HALF, kpos % SLAB] = vals
         self.group_col = group_col.astype(np.int32)
         self.tile_slab = tile_slab.astype(np.int32)
         self.tile_nkb = tile_nkb.astype(np.int32)
         self.tile_rows = tile_rows
         self.tile_pos = (tile_of * TILE + row_of).astype(np.int32)
         self.num_tiles = t_count
-        self.num_slabs = num_slabs
+        self.num_blocks = num_blocks
+        self.num_slabs = 2 * num_blocks
         self.mean_k = float(tile_nkb.mean() * SLAB) if t_count else 0.0
 
     def unit_bounds(self, frames: int, ctas: int, group: int = 4) -> np.ndarray:
@@ -180,7 +184,7 @@ class TileLayout:
         u = np.arange(n_groups * self.num_tiles * group)
         n = (u // (self.num_tiles * group)) * group + u % group
         t = (u % (self.num_tiles * group)) // group
-        work = np.where(n < n_tiles, self.tile_nkb[t].astype(np.int64) + 1, 0)
+        work = np.where(n < n_tiles, 2 * self.tile_nkb[t].astype(np.int64) + 2, 0)
         cum = np.concatenate([[0], np.cumsum(work)])
         targets = np.linspace(0, cum[-1], ctas + 1)
         bounds = np.searchsorted(cum, targets, side="left")
@@ -193,11 +197,12 @@ class TileLayout:
         z = np.zeros((f, self.num_rows))
         pad = np.concatenate([xi_nat, np.zeros((f, SLAB + GROUP))], axis=1)
         for t in range(self.num_tiles):
-            s0, nk = int(self.tile_slab[t]), int(self.tile_nkb[t])
-            cols = self.group_col[s0 * 8:(s0 + nk) * 8][:, None] + np.arange(GROUP)[None, :]
-            a = self.slabs[s0:s0 + nk].transpose(1, 0, 2).reshape(TILE, nk * SLAB).astype(np.float64)
+            b0, nk = int(self.tile_slab[t]), int(self.tile_nkb[t])
+            cols = self.group_col[b0 * 8:(b0 + nk) * 8][:, None] + np.arange(GROUP)[None, :]
             x = pad[:, cols.ravel()]                                     # (F, nk*64)
-            r = self.tile_rows[t]
-            ok = r >= 0
-            z[:, r[ok]] = (x @ a.T)[:, ok]
+            for h in range(2):
+                a = self.slabs[2 * b0 + h:2 * (b0 + nk):2].transpose(1, 0, 2).reshape(HALF, nk * SLAB)
+                r = self.tile_rows[t, h * HALF:(h + 1) * HALF]
+                ok = r >= 0
+                z[:, r[ok]] = (x @ a.astype(np.float64).T)[:, ok]
         return z
