@@ -46,6 +46,11 @@ int srpgpu_abi_version(void);
 /* number of kernels launched through this library since load */
 uint64_t srpgpu_launch_count(void);
 int srpgpu_device_sync(void);
+/* Frontend kernel used by srpgpu_gcc_frames / srpgpu_frames_to_samples*: 0 = by batch
+ * size (default), 1 = warp per frame, 2 = a warp per channel / pair task, 3 = the
+ * generic block kernel.  All four compute the same values (within fp32 rounding);
+ * the choice only changes speed.  Process-wide tuning knob, read at launch. */
+int srpgpu_set_frontend_kernel(int32_t which);
 
 /* ---- frontend (srpmap/frontend.py) --------------------------------------- */
 

@@ -26,6 +26,7 @@ SIGNATURES = {
     "srpgpu_abi_version": [],
     "srpgpu_launch_count": [],
     "srpgpu_device_sync": [],
+    "srpgpu_set_frontend_kernel": [_I32],
     "srpgpu_stft": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _P, _P],
     "srpgpu_fd_gcc": [_P, _I64, _I32, _I32, _P, _I32, _I32, _I32, _F64, _P, _P],
     "srpgpu_gcc_frames": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _I32, _I32, _I32,

@@ -2,12 +2,13 @@
 #include <atomic>
 #include <string.h>
 
-#include "common.cuh"
+#include "frontend_warp.cuh"
 
 namespace srpgpu {
 
 static thread_local char g_err[512] = "";
 static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<int> g_frontend_kernel{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -17,6 +18,8 @@ void set_error(const char* fmt, ...) {
 }
 
 void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+int frontend_kernel_choice() { return g_frontend_kernel.load(std::memory_order_relaxed); }
 
 }  // namespace srpgpu
 
@@ -34,5 +37,14 @@ extern "C" int srpgpu_device_sync(void) {
     srpgpu::set_error("device sync: %s", cudaGetErrorString(e));
     return SRPGPU_ERR_LAUNCH;
   }
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_set_frontend_kernel(int32_t which) {
+  if (which < 0 || which > 3) {
+    srpgpu::set_error("frontend kernel choice %d not in 0..3", which);
+    return SRPGPU_ERR_VALUE;
+  }
+  srpgpu::g_frontend_kernel.store(which, std::memory_order_relaxed);
   return SRPGPU_OK;
 }

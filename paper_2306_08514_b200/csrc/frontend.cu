@@ -291,6 +291,9 @@ static size_t frontend_smem(int in, int out, int L, int K, int M, int P, int nbu
   return (b + 15) & ~(size_t)15;
 }
 
+// batches up to this many frames per SM take the task-per-warp kernel (frontend_lane.cu)
+constexpr int64_t kLaneMaxFrames = 16;
+
 template <int IN, int OUT>
 static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* what) {
   if (IN == IN_SAMPLES && OUT != OUT_SPECTRA && prm.F > 0) {
@@ -305,7 +308,12 @@ static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* 
     wp.xi_out = prm.xi_out; wp.xi_ld = prm.xi_ld;
     wp.xi_planes = prm.xi_planes; wp.cols8 = prm.cols8; wp.xi_natural = prm.xi_natural;
     wp.planes_ld = prm.planes_ld;
-    const int r = frontend_warp_launch(wp, OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI, stream, what);
+    const int wout = OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI;
+    const int choice = frontend_kernel_choice();
+    int r = 1;
+    if (choice == 2 || (choice == 0 && prm.F <= kLaneMaxFrames * (int64_t)num_sms()))
+      r = frontend_lane_launch(wp, wout, stream, what);
+    if (r == 1 && choice != 3) r = frontend_warp_launch(wp, wout, stream, what);
     if (r == 0 && prm.warp_used) *prm.warp_used = 1;
     if (r <= 0) return r;
   }

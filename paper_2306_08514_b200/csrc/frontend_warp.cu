@@ -144,28 +144,6 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
   return raw;
 }
 
-// one xi sample (storage index d of a pair block at offset o with N lags a side): the
-// f32 output and, when requested, its bf16 hi/lo planes (storage or natural lag order)
-__device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int o, int N, int d,
-                                       float v) {
-  dst[(o + d) * sst] = v;
-  if (prm.xi_planes) {
-    const int col = o + (prm.xi_natural ? (d <= N ? N + d : d - N - 1) : d);
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes);
-    if (prm.planes_ld) {                      // lag-major [2][cols8][planes_ld]
-      __nv_bfloat16* pl = base + (int64_t)col * prm.planes_ld + f;
-      pl[0] = hi;
-      pl[(int64_t)prm.cols8 * prm.planes_ld] = lo;
-    } else {
-      __nv_bfloat16* pl = base + f * prm.cols8 + col;
-      pl[0] = hi;
-      pl[prm.F * prm.cols8] = lo;
-    }
-  }
-}
-
 constexpr int kWarps = 4;   // per CTA
 
 // named barrier of the kWpf warps sharing one frame (kWpf == 1: the warp itself)

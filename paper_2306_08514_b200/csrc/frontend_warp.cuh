@@ -1,5 +1,7 @@
 // Parameters of the warp-per-frame frontend (frontend_warp.cu), shared with frontend.cu.
 #pragma once
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace srpgpu {
@@ -32,7 +34,35 @@ struct WarpParams {
   int64_t planes_ld;    // 0: planes frame-major [2][F][cols8]; > 0: lag-major [2][cols8][planes_ld]
 };
 
+// one xi sample (storage index d of a pair block at offset o with N lags a side): the
+// f32 output and, when requested, its bf16 hi/lo planes (storage or natural lag order)
+__device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int o, int N, int d,
+                                       float v) {
+  dst[(o + d) * sst] = v;
+  if (prm.xi_planes) {
+    const int col = o + (prm.xi_natural ? (d <= N ? N + d : d - N - 1) : d);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes);
+    if (prm.planes_ld) {                      // lag-major [2][cols8][planes_ld]
+      __nv_bfloat16* pl = base + (int64_t)col * prm.planes_ld + f;
+      pl[0] = hi;
+      pl[(int64_t)prm.cols8 * prm.planes_ld] = lo;
+    } else {
+      __nv_bfloat16* pl = base + f * prm.cols8 + col;
+      pl[0] = hi;
+      pl[prm.F * prm.cols8] = lo;
+    }
+  }
+}
+
 // 0: launched; 1: shape not covered (use the block kernel); < 0: error status.
 int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what);
+
+// Task-per-warp frontend (frontend_lane.cu): same contract as frontend_warp_launch.
+int frontend_lane_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what);
+
+// Frontend kernel choice: 0 auto (by batch size), 1 warp-per-frame, 2 task-per-warp, 3 block.
+int frontend_kernel_choice();
 
 }  // namespace srpgpu

@@ -228,3 +228,29 @@ def gcc_frames(samples, spec, pairs, frames=None, weighting: str = "phat", floor
     padded = torch.view_as_real(buf).reshape(count, 2 * ld) if tf32 else None
     return FdGcc(values=out if batched else out[0], num_pairs=p, num_bins=bins, weighting=weighting,
                  tf32_rounded=tf32, padded=padded)
+
+
+FRONTEND_KERNELS = {"auto": 0, "warp": 1, "task": 2, "block": 3}
+
+
+class frontend_kernel:
+    """Context manager selecting the frontend kernel (`srpgpu_set_frontend_kernel`).
+
+    "auto" (default) picks by batch size; "warp" = a warp per frame
+    (frontend_warp.cu), "task" = a warp per channel / pair task (frontend_lane.cu),
+    "block" = the generic block kernel (frontend.cu).  All compute the same values;
+    this is a tuning and testing knob.  Kernels captured in a CUDA graph keep the
+    choice they were captured with.
+    """
+
+    def __init__(self, which: str):
+        if which not in FRONTEND_KERNELS:
+            raise ValueError(f"unknown frontend kernel {which!r}")
+        self.which = which
+
+    def __enter__(self):
+        nat.call("srpgpu_set_frontend_kernel", FRONTEND_KERNELS[self.which])
+        return self
+
+    def __exit__(self, *exc):
+        nat.call("srpgpu_set_frontend_kernel", 0)

@@ -101,6 +101,39 @@ def test_fused_frames_to_samples(golden_scene):
     assert err2.max() < 2e-5
 
 
+@pytest.mark.parametrize("kernel", ["warp", "task", "block"])
+def test_frontend_kernels_agree(golden_scene, kernel):
+    """Every frontend kernel (warp per frame, warp per task, block) meets the golden
+    vectors on every output layout: psi, frame-major / lag-major xi, bf16 planes."""
+    from paper_2306_08514_b200.frontend import frontend_kernel
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    with frontend_kernel(kernel):
+        psi = np_(s.gcc_frames(x, frame, pairs, range(F)).values)
+        raw = np_(s.gcc_frames(x, frame, pairs, range(F), weighting="none").values)
+        xi = s.frames_to_samples(x, frame, pairs, spec, range(F))
+        xp = s.frames_to_samples(x, frame, pairs, spec, range(F), planes=True)
+        xn = s.frames_to_samples(x, frame, pairs, spec, range(F), planes=True, natural=True)
+        one = s.frames_to_samples(x, frame, pairs, spec, 1)
+    d = np.abs(psi - g["psi"])
+    assert np.quantile(d, 0.999) < 2e-5 and d.max() < 2e-3
+    rel = np.abs(raw - g["psi_none"]) / np.abs(g["psi_none"]).max()
+    assert rel.max() < 2e-6
+    for t in (xi, xp, xn):
+        v = np_(t.values)
+        err = np.abs(v - g["xi_ifft"]).max(axis=1) / np.abs(g["xi_ifft"]).max(axis=1)
+        assert err.max() < 2e-5, f"{kernel}: xi error {err.max():.2e}"
+    assert np.array_equal(np_(one.values), np_(xi.values)[1])
+    ref, _, _ = s.maps.sample_planes(s.TdGccSamples(xp.values.clone(), spec), spec.total_samples)
+    assert torch.equal(xp.bf16_planes.view(torch.int16), ref.view(torch.int16))
+    refn, _, _ = s.maps.sample_planes(s.TdGccSamples(xn.values.clone(), spec), spec.total_samples,
+                                      natural=spec_offsets(spec))
+    S = spec.total_samples
+    assert torch.equal(xn.bf16_planes[:, :S, :F].view(torch.int16), refn[:, :S, :F].view(torch.int16))
+
+
 # ------------------------------------------------------------------ maps
 
 @pytest.mark.parametrize("engine", ["tc", "tile", "band"])
