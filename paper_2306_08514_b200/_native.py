@@ -12,7 +12,8 @@ import threading
 
 from .errors import CapacityError, DimensionError, NativeLibraryError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsrpgpu.so")
+LIB_PATH = os.environ.get("SRPGPU_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                        "libsrpgpu.so")
 
 _P = ctypes.c_void_p
 _I32 = ctypes.c_int32

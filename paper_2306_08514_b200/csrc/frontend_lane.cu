@@ -276,8 +276,12 @@ __device__ __forceinline__ void inverse_pair(const WarpParams& prm, const float2
   }
 }
 
+#ifndef LANE_MINB
+#define LANE_MINB 1
+#endif
+
 template <int Q, int OUT, int WPF>
-__global__ void __launch_bounds__(WPF * 32)
+__global__ void __launch_bounds__(WPF * 32, LANE_MINB)
 frontend_lane_kernel(const WarpParams prm) {
   using G = Geo<Q>;
   constexpr int N = G::N, L = G::L, K = N, B = K - 1, SLOT = G::SLOT;
