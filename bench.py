@@ -37,6 +37,8 @@ sys.path.insert(0, ROOT)
 METRIC = "srp_maps_per_sec"
 UNIT = "maps/s"
 L2_FLUSH_BYTES = 256 << 20
+L2_BYTES = 126 << 20          # B200 L2
+RING_MAX = 256
 
 
 def parse():
@@ -300,10 +302,22 @@ def run_ours(args):
     g_launch0 = _native.launch_count()
     pipe.replay()
     torch.cuda.synchronize()
+    # Ring of pipeline slots (own input buffer, graph and outputs) whose inputs together
+    # exceed twice the L2: consecutive steps read cold inputs, so the K steps are timed as
+    # one region with no flush, and for N > 1 each step's NCCL all-gather of the per-frame
+    # argmax runs asynchronously, overlapped with the next step's chain, inside that region.
+    in_bytes = pipe.input.numel() * 4
+    n_slots = max(2, min(RING_MAX, -(-2 * L2_BYTES // max(1, in_bytes))))
+    slots = [pipe]
+    for _ in range(n_slots - 1):
+        sl = make_pipe(args.variant, op)
+        sl.input.copy_(x_dev)
+        slots.append(sl)
     clocks = ClockSampler(local)
     with clocks:
-        ms_per_step, _ = timed(pipe.replay, args.steps, args.warmup, True)
+        ms_per_step = ring_timed(slots, args.steps, args.warmup, world, dev, total)
     value = total / (ms_per_step / 1e3)
+    del slots[1:]
     # kernels per step: counted when the graph was captured (replays do not pass the host counter)
     launches_per_step = pipe_launches(pipe)
 
@@ -449,7 +463,11 @@ def run_ours(args):
                        "map_engine": {"tc": "tensor cores (dense bf16x3)",
                                       "tile": "tensor cores (gathered lag windows, bf16x3)",
                                       "band": "FP32 tiled band"}.get(eng),
-                       "parallelism": f"frames/{world}", "l2": "flushed between timed steps",
+                       "parallelism": f"frames/{world}",
+                       "l2": (f"inputs larger than L2: a ring of {n_slots} pipeline slots "
+                              f"({n_slots * in_bytes / 2**20:.0f} MiB of inputs), K steps timed as one region"),
+                       "collective": ("NCCL all_gather_into_tensor of the per-frame argmax per step, async, "
+                                      "overlapped with the next step" if world > 1 else None),
                        "execution": "CUDA graph per batch"},
             "candidates_per_s": value * wl.grid.num_points,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e_block,
@@ -476,6 +494,35 @@ def pipe_launches(pipe) -> int:
     p2._chain()                      # eager replay of the same chain counts its kernels
     torch.cuda.synchronize()
     return nat.launch_count() - before
+
+
+def ring_timed(slots, steps, warmup, world, dev, total):
+    """ms per step of `steps` consecutive pipeline replays cycling through `slots`, timed as
+    one CUDA-event region on the compute stream (max over ranks).  For world > 1 every step
+    all-gathers its per-frame argmax over NCCL, asynchronously and overlapped with the next
+    step (distributed.pipelined_steps); the region ends after the last gather."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_08514_b200 import distributed as D
+    fns = [(lambda sl=sl: sl.replay()[1]) for sl in slots]
+    outs = [torch.empty(total, dtype=torch.int64, device=dev) for _ in range(2)] if world > 1 else None
+    D.pipelined_steps(fns, warmup, total, outs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    D.pipelined_steps(fns, steps, total, outs)
+    b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()) / steps
 
 
 def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto"):

@@ -59,6 +59,33 @@ def gather_frame_keys(local_keys: torch.Tensor, total_frames: int, group=None) -
     return torch.cat([o[:c] for o, c in zip(out, counts)])
 
 
+def pipelined_steps(steps, n: int, total_frames: int, outs=None, group=None):
+    """Run n steps of a frame-partitioned pipeline, all-gathering each step's per-frame
+    result (8 bytes per frame, equal frame counts per rank) asynchronously.
+
+    `steps[i % len(steps)]()` enqueues step i and returns its (F_local,) int64 result on
+    the current stream.  Step i's all-gather overlaps step i+1; before step i the stream
+    waits for gather i-2, whose output buffer (a ring of two) and input step slot
+    (`len(steps) >= 2`) are then reused.  Returns the two output buffers; after the call
+    the stream has waited for every gather.  Single process: no collective.
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world > 1 and len(steps) < 2:
+        raise ValueError("pipelined gathers need at least two step slots")
+    works = []
+    for i in range(n):
+        if len(works) >= 2:
+            works[-2].wait()
+        res = steps[i % len(steps)]()
+        if world > 1:
+            if outs is None:
+                outs = [torch.empty(total_frames, dtype=res.dtype, device=res.device) for _ in range(2)]
+            works.append(dist.all_gather_into_tensor(outs[i % 2], res, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return outs
+
+
 def reduce_candidate_keys(local_keys: torch.Tensor, group=None) -> torch.Tensor:
     """All-reduce MAX of per-frame keys of a candidate-partitioned run."""
     vals = keys_to_signed(local_keys.clone())

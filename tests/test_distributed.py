@@ -88,3 +88,51 @@ def test_key_order_matches_argmax_rule():
     i, v = D.decode_host_keys(keys)
     assert i.tolist() == idx.tolist()
     assert v.tolist() == [1.0, 1.0, -2.0, 3.0, 0.0, 0.0]
+
+
+def _pipelined_worker(rank, world, port, frames, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    f0, nf = D.partition(frames * world, world, rank)
+    seen = []
+    slots = [torch.zeros(nf, dtype=torch.int64) for _ in range(3)]
+
+    def step(k):
+        def run():
+            i = len(seen)
+            slots[k].copy_(torch.arange(f0, f0 + nf, dtype=torch.int64) + 1000 * i)   # step i's result
+            seen.append(i)
+            return slots[k]
+        return run
+
+    outs = D.pipelined_steps([step(k) for k in range(3)], steps, frames * world)
+    out[rank] = [o.numpy().copy() for o in outs]
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_pipelined_gathers_two_ranks():
+    """bench.py's N > 1 step loop: each step's per-frame results are all-gathered
+    asynchronously; the two output buffers hold the last two steps of every rank."""
+    frames, steps = 5, 7
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipelined_worker, args=(r, 2, port, frames, steps, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    base = np.arange(2 * frames)
+    for r in range(2):
+        last, prev = out[r][(steps - 1) % 2], out[r][(steps - 2) % 2]
+        np.testing.assert_array_equal(last, base + 1000 * (steps - 1))
+        np.testing.assert_array_equal(prev, base + 1000 * (steps - 2))
+
+
+def test_pipelined_steps_single_process():
+    calls = []
+    outs = D.pipelined_steps([lambda: calls.append(1) or torch.zeros(3, dtype=torch.int64)], 4, 3)
+    assert outs is None and len(calls) == 4
