@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "conv_h", "si"])
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
-    ap.add_argument("--engine", default="auto", choices=["auto", "tc", "tile", "band"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "fused", "tc", "tile", "band"],
                     help="SSPI / SI map engine (maps.interp_engine)")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--variants", default="sspi,slri,lr,conv,conv_h",
@@ -322,12 +322,25 @@ def run_ours(args):
     launches_per_step = pipe_launches(pipe)
 
     from paper_2306_08514_b200 import maps as _maps
+    fused = pipe.uses_fused_chain()
     # ---- per-kernel times for the roofline: each stage captured alone, CUDA events
-    t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush, engine=args.engine)
+    if fused:
+        t_front, t_map = 0.0, fused_time(s, wl, op, x_dev, count, flush)
+    else:
+        t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush, engine=args.engine)
     hbm, bf16, peak_src = peaks()
     abytes = algorithmic_bytes(wl, args.variant, count, op, args.engine)
     tf32_peak, fp32_peak, xsrc = extra_peaks()
-    if args.variant in ("conv", "conv_h"):
+    if fused:
+        sell = _maps.sell_from_sparse(op)
+        fbytes = abytes["frontend"] - count * 4 * wl.spec.total_samples \
+            + count * 4 * wl.grid.num_points + sell.cols.numel() * 6 + sell.chunk_off.numel() * 4
+        achieved = fbytes / (t_map / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "frontend_sspi_kernel (fused chain)", "achieved": achieved,
+                "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": fbytes,
+                "traffic": ncu_traffic(args.workload, args.variant, "fused")}
+    elif args.variant in ("conv", "conv_h"):
         dom_name, dom_ms = ("srp_map_tdoa" if args.variant == "conv" else "srp_map_tc"), t_map
         achieved = conv_flops(wl, count) / (dom_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": tf32_peak,
@@ -344,8 +357,9 @@ def run_ours(args):
                 "frac": achieved / hbm, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
-    roof["kernel_ms"] = {"frontend": t_front, "map": t_map}
-    eng = _maps.map_engine(args.variant, op, args.engine, count)
+    roof["kernel_ms"] = {"fused_chain": t_map} if fused else {"frontend": t_front, "map": t_map}
+    eng = "fused" if fused else _maps.map_engine(args.variant, op, "auto" if args.engine == "fused" else args.engine,
+                                                 count)
     if eng == "tc":
         # tensor-core interpolation engine: 3 bf16 MMA passes over the dense operator
         c8 = (wl.spec.total_samples + 7) // 8 * 8
@@ -360,9 +374,11 @@ def run_ours(args):
                               "frac_of_bf16_peak": tflops / bf16}
     # the SIMT stages are FP32-issue / L1 bound at these sizes: their FP32 fractions
     roof["fp32_frac"] = {
-        "frontend": frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak,
+        "frontend": (None if fused else frontend_flops(wl, args.variant, count) / (t_front / 1e3) / 1e12 / fp32_peak),
+        "fused_chain": ((frontend_flops(wl, args.variant, count) + map_flops(wl, args.variant, op, count))
+                        / (t_map / 1e3) / 1e12 / fp32_peak if fused else None),
         "map": (map_flops(wl, args.variant, op, count) / (t_map / 1e3) / 1e12 / fp32_peak
-                if args.variant not in ("conv", "conv_h") and eng not in ("tc", "tile")
+                if args.variant not in ("conv", "conv_h") and eng not in ("tc", "tile", "fused")
                 else None),
         "fp32_peak_tflops": fp32_peak, "peak_source": f"FP32 SIMT cuBLAS {xsrc}"}
 
@@ -460,7 +476,8 @@ def run_ours(args):
                                      f"{int(op.values.shape[2])} nnz per (candidate, pair)")
                                     if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),
-                       "map_engine": {"tc": "tensor cores (dense bf16x3)",
+                       "map_engine": {"fused": "fused chain: frontend + sliced-ELL SSPI map + argmax in one kernel",
+                                      "tc": "tensor cores (dense bf16x3)",
                                       "tile": "tensor cores (gathered lag windows, bf16x3)",
                                       "band": "FP32 tiled band"}.get(eng),
                        "parallelism": f"frames/{world}",
@@ -523,6 +540,29 @@ def ring_timed(slots, steps, warmup, world, dev, total):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item()) / steps
+
+
+def fused_time(s, wl, op, x_dev, count, flush, reps=10):
+    """Median device time of the fused frames -> SSPI map -> argmax kernel, in its own graph."""
+    import torch
+    from paper_2306_08514_b200 import maps
+    fn = lambda: maps.frames_to_sspi_map(op, x_dev, wl.frame, wl.pairs, wl.spec, range(0, count))
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
 
 
 def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto"):

@@ -119,6 +119,22 @@ int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels, 
                                     int64_t samples_ld, void* planes, int32_t cols8, int64_t planes_ld,
                                     int32_t natural, const int32_t* natural_src, srpgpu_stream_t stream);
 
+/* The whole SSPI chain in one launch (stft_frame + fd_gcc + td_gcc_samples + sspi_map +
+ * locate; frontend.py:89-160, sampling.py:106-134, interpolation.py:188-195, srp.py:74-80):
+ * signal -> z [F][J] (nullable) and the per-frame argmax index [F] int64 / packed key [F]
+ * (each nullable).  The TD-GCC samples never leave shared memory.  The operator is a sliced
+ * ELL image of the SparseInterp CSR: candidates in chunks of 32, chunk c's entries at rows
+ * sell_chunk_off[c] .. sell_chunk_off[c+1]-1 of sell_cols / sell_vals [rows][32] (sample
+ * index uint16, weight f32; padding entries weight 0).  frame_len 256, 512 or 1024;
+ * total_samples <= 65535; SRPGPU_ERR_UNSUPPORTED when the frame does not fit in shared memory. */
+int srpgpu_frames_to_sspi_map(const float* samples, int32_t num_channels, int64_t num_samples,
+                              int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
+                              int64_t first_frame, int64_t num_frames, const int32_t* pairs, int32_t num_pairs,
+                              int32_t weighting, int32_t floor_mode, double floor_value, const int32_t* counts,
+                              const int32_t* offsets, int32_t total_samples, const uint16_t* sell_cols,
+                              const float* sell_vals, const int32_t* sell_chunk_off, int64_t num_candidates,
+                              float* z, int64_t* index, uint64_t* keys, srpgpu_stream_t stream);
+
 /* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
 int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
                               int32_t half_len, const int32_t* pairs, int32_t num_pairs,

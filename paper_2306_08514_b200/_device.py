@@ -26,6 +26,11 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def num_sms() -> int:
+    """SM count of the current device (148 on B200)."""
+    return torch.cuda.get_device_properties(device()).multi_processor_count
+
+
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 

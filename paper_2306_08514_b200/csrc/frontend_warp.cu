@@ -144,6 +144,159 @@ __device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m,
   return raw;
 }
 
+// forward FFTs of one frame (R channel pairs per round, rounds split over the frame's warps)
+// into the shared spectra [M][K+1]; returns this warp's share of sum |Y|^2
+template <int LP, int kWpf>
+__device__ __forceinline__ float forward_frame(const WarpParams& prm, int64_t start, float2* spec, float2* work,
+                                               float2* xp, const float2* twT, int lane, int mi) {
+  using G = Geo<LP>;
+  constexpr int L = G::L, K = G::K, R = G::R, Kp1 = K + 1;
+  const int M = prm.M;
+  const int fi = lane / LP, fl = lane % LP;
+  float energy = 0.f;
+  // ---------------- forward FFTs: R channel pairs per round, rounds split over the warps ----
+  for (int c0 = 2 * R * mi; c0 < M; c0 += 2 * R * kWpf) {
+    const int ca = c0 + 2 * fi, cb = ca + 1;
+    float2 v[32];
+    const float* xa = prm.samples + (int64_t)ca * prm.ld_samples + start;
+    const float* xb = prm.samples + (int64_t)cb * prm.ld_samples + start;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = fl + LP * j;
+      const float w = __ldg(prm.window + n);
+      const float a = (ca < M) ? __ldg(xa + n) * w : 0.f;
+      const float b = (cb < M) ? __ldg(xb + n) * w : 0.f;
+      v[j] = make_float2(a, b);
+    }
+    fft_l<LP, true>(v, xp, twT, fl);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < LP; ++i) xp[32 * brev<LP>(i) + fl + LP * r] = v[r * LP + i];
+    __syncwarp();
+    // unpack the two real spectra: Ya = (Z + conj Z[L-k]) / 2, Yb = (Z - conj Z[L-k]) / 2j
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int qa = c0 + 2 * q, qb = qa + 1;
+      if (qa >= M) break;
+      const float2* zq = work + q * G::XP;
+      for (int k = lane; k < Kp1; k += 32) {
+        const float2 Z = zq[k];
+        const float2 Zc = conjf2(zq[(L - k) & (L - 1)]);
+        const float2 Ya = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y + Zc.y));
+        spec[qa * Kp1 + k] = Ya;
+        energy += Ya.x * Ya.x + Ya.y * Ya.y;
+        if (qb < M) {
+          const float2 Yb = make_float2(0.5f * (Z.y - Zc.y), -0.5f * (Z.x - Zc.x));
+          spec[qb * Kp1 + k] = Yb;
+          energy += Yb.x * Yb.x + Yb.y * Yb.y;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  return energy;
+}
+
+// PHAT cross-spectra + pruned inverse FFTs of one frame's pairs (two pairs per FFT, rounds
+// split over the frame's warps); every kept lag goes to put(offset, N_p, storage index, value)
+template <int LP, int kWpf, class Put>
+__device__ __forceinline__ void inverse_frame(const WarpParams& prm, const float2* spec, float2* work, float2* xp,
+                                              const float2* twT, const int* s_pairs, const int* s_counts,
+                                              const int* s_off, float floor, int lane, int mi, const Put& put) {
+  using G = Geo<LP>;
+  constexpr int L = G::L, K = G::K, R = G::R, Kp1 = K + 1, B = K - 1;
+  const int P = prm.P;
+  const int fi = lane / LP, fl = lane % LP;
+  for (int p0 = 2 * R * mi; p0 < P; p0 += 2 * R * kWpf) {
+    // PHAT cross-spectra of this round's pairs into each FFT's work area: [2][B]
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int pa = p0 + 2 * q, pb = pa + 1;
+      if (pa >= P) break;
+      float2* sq = work + q * G::XP;
+      const int ma = s_pairs[2 * pa], mpa = s_pairs[2 * pa + 1];
+      const int mb = (pb < P) ? s_pairs[2 * pb] : 0, mpb = (pb < P) ? s_pairs[2 * pb + 1] : 0;
+      for (int k = 1 + lane; k < K; k += 32) {
+        sq[k - 1] = cross_phat(spec, Kp1, ma, mpa, k, prm.weighting, floor);
+        sq[B + k - 1] = (pb < P) ? cross_phat(spec, Kp1, mb, mpb, k, prm.weighting, floor)
+                                 : make_float2(0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    const int pa = p0 + 2 * fi, pb = pa + 1;
+    float2 v[32];
+    {
+      const float2* sa = xp;
+      const float2* sb = xp + B;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int k = fl + LP * j;
+        float2 z = make_float2(0.f, 0.f);
+        if (pa < P && k != 0 && k != K) {
+          if (k < K) {
+            const float2 a = sa[k - 1], c = sb[k - 1];
+            z = make_float2(a.x - c.y, a.y + c.x);      // a + j c
+          } else {
+            const float2 a = sa[L - k - 1], c = sb[L - k - 1];
+            z = make_float2(a.x + c.y, -a.y + c.x);     // conj(a) + j conj(c)
+          }
+        }
+        v[j] = conjf2(z);
+      }
+    }
+    __syncwarp();
+    // prune the second FFT step when every kept lag of the warp's pairs has |n| < 32
+    int nmax = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int qa = p0 + 2 * q;
+      if (qa < P) nmax = max(nmax, s_counts[qa]);
+      if (qa + 1 < P) nmax = max(nmax, s_counts[qa + 1]);
+    }
+    const bool full2 = nmax >= 32;
+    if (full2) fft_l<LP, true>(v, xp, twT, fl);
+    else fft_l<LP, false>(v, xp, twT, fl);
+    if (pa < P) {
+      const int Na = s_counts[pa], oa = s_off[pa];
+      const int Nb = (pb < P) ? s_counts[pb] : -1, ob = (pb < P) ? s_off[pb] : 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int k2 = fl + LP * r;
+        if (full2) {
+#pragma unroll
+          for (int i = 0; i < LP; ++i) {
+            const int n = 32 * brev<LP>(i) + k2;
+            const float2 x = v[r * LP + i];
+            const int da = (n <= Na) ? n : ((L - n <= Na) ? 2 * Na + 1 - (L - n) : -1);
+            if (da >= 0) put(oa, Na, da, x.x);
+            const int db = (n <= Nb) ? n : ((L - n <= Nb) ? 2 * Nb + 1 - (L - n) : -1);
+            if (db >= 0) put(ob, Nb, db, -x.y);
+          }
+        } else {
+          const float2 x0 = v[r * LP + 0];   // n = k2
+          const float2 x1 = v[r * LP + 1];   // n = L - 32 + k2, distance d = 32 - k2
+          const int d = 32 - k2;
+          if (k2 <= Na) put(oa, Na, k2, x0.x);
+          if (d <= Na) put(oa, Na, 2 * Na + 1 - d, x1.x);
+          if (k2 <= Nb) put(ob, Nb, k2, -x0.y);
+          if (d <= Nb) put(ob, Nb, 2 * Nb + 1 - d, -x1.y);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// xi sink of the unfused chain: global f32 samples (+ bf16 planes)
+struct GlobalXi {
+  const WarpParams& prm;
+  float* dst;
+  int64_t sst;
+  int64_t f;
+  __device__ __forceinline__ void operator()(int o, int N, int d, float v) const { put_xi(prm, dst, sst, f, o, N, d, v); }
+};
+
 constexpr int kWarps = 4;   // per CTA
 
 // named barrier of the kWpf warps sharing one frame (kWpf == 1: the warp itself)
@@ -200,48 +353,7 @@ frontend_warp_kernel(const WarpParams prm) {
   const int64_t total_groups = (int64_t)gridDim.x * kFpc;
   for (int64_t f = (int64_t)blockIdx.x * kFpc + fg; f < prm.F; f += total_groups) {
     const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
-    float energy = 0.f;
-    // ---------------- forward FFTs: R channel pairs per round, rounds split over the warps ----
-    for (int c0 = 2 * R * mi; c0 < M; c0 += 2 * R * kWpf) {
-      const int ca = c0 + 2 * fi, cb = ca + 1;
-      float2 v[32];
-      const float* xa = prm.samples + (int64_t)ca * prm.ld_samples + start;
-      const float* xb = prm.samples + (int64_t)cb * prm.ld_samples + start;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = fl + LP * j;
-        const float w = __ldg(prm.window + n);
-        const float a = (ca < M) ? __ldg(xa + n) * w : 0.f;
-        const float b = (cb < M) ? __ldg(xb + n) * w : 0.f;
-        v[j] = make_float2(a, b);
-      }
-      fft_l<LP, true>(v, xp, twT, fl);
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int i = 0; i < LP; ++i) xp[32 * brev<LP>(i) + fl + LP * r] = v[r * LP + i];
-      __syncwarp();
-      // unpack the two real spectra: Ya = (Z + conj Z[L-k]) / 2, Yb = (Z - conj Z[L-k]) / 2j
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int qa = c0 + 2 * q, qb = qa + 1;
-        if (qa >= M) break;
-        const float2* zq = work + q * G::XP;
-        for (int k = lane; k < Kp1; k += 32) {
-          const float2 Z = zq[k];
-          const float2 Zc = conjf2(zq[(L - k) & (L - 1)]);
-          const float2 Ya = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y + Zc.y));
-          spec[qa * Kp1 + k] = Ya;
-          energy += Ya.x * Ya.x + Ya.y * Ya.y;
-          if (qb < M) {
-            const float2 Yb = make_float2(0.5f * (Z.y - Zc.y), -0.5f * (Z.x - Zc.x));
-            spec[qb * Kp1 + k] = Yb;
-            energy += Yb.x * Yb.x + Yb.y * Yb.y;
-          }
-        }
-      }
-      __syncwarp();
-    }
+    float energy = forward_frame<LP, kWpf>(prm, start, spec, work, xp, twT, lane, mi);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
     if (lane == 0) s_energy[wid] = energy;
@@ -269,84 +381,8 @@ frontend_warp_kernel(const WarpParams prm) {
     } else {
       float* dst = prm.xi_out + (prm.xi_ld ? f : f * (int64_t)prm.S);
       const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
-      for (int p0 = 2 * R * mi; p0 < P; p0 += 2 * R * kWpf) {
-        // PHAT cross-spectra of this round's pairs into each FFT's work area: [2][B]
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int pa = p0 + 2 * q, pb = pa + 1;
-          if (pa >= P) break;
-          float2* sq = work + q * G::XP;
-          const int ma = s_pairs[2 * pa], mpa = s_pairs[2 * pa + 1];
-          const int mb = (pb < P) ? s_pairs[2 * pb] : 0, mpb = (pb < P) ? s_pairs[2 * pb + 1] : 0;
-          for (int k = 1 + lane; k < K; k += 32) {
-            sq[k - 1] = cross_phat(spec, Kp1, ma, mpa, k, prm.weighting, floor);
-            sq[B + k - 1] = (pb < P) ? cross_phat(spec, Kp1, mb, mpb, k, prm.weighting, floor)
-                                     : make_float2(0.f, 0.f);
-          }
-        }
-        __syncwarp();
-        const int pa = p0 + 2 * fi, pb = pa + 1;
-        float2 v[32];
-        {
-          const float2* sa = xp;
-          const float2* sb = xp + B;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int k = fl + LP * j;
-            float2 z = make_float2(0.f, 0.f);
-            if (pa < P && k != 0 && k != K) {
-              if (k < K) {
-                const float2 a = sa[k - 1], c = sb[k - 1];
-                z = make_float2(a.x - c.y, a.y + c.x);      // a + j c
-              } else {
-                const float2 a = sa[L - k - 1], c = sb[L - k - 1];
-                z = make_float2(a.x + c.y, -a.y + c.x);     // conj(a) + j conj(c)
-              }
-            }
-            v[j] = conjf2(z);
-          }
-        }
-        __syncwarp();
-        // prune the second FFT step when every kept lag of the warp's pairs has |n| < 32
-        int nmax = 0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int qa = p0 + 2 * q;
-          if (qa < P) nmax = max(nmax, s_counts[qa]);
-          if (qa + 1 < P) nmax = max(nmax, s_counts[qa + 1]);
-        }
-        const bool full2 = nmax >= 32;
-        if (full2) fft_l<LP, true>(v, xp, twT, fl);
-        else fft_l<LP, false>(v, xp, twT, fl);
-        if (pa < P) {
-          const int Na = s_counts[pa], oa = s_off[pa];
-          const int Nb = (pb < P) ? s_counts[pb] : -1, ob = (pb < P) ? s_off[pb] : 0;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const int k2 = fl + LP * r;
-            if (full2) {
-#pragma unroll
-              for (int i = 0; i < LP; ++i) {
-                const int n = 32 * brev<LP>(i) + k2;
-                const float2 x = v[r * LP + i];
-                const int da = (n <= Na) ? n : ((L - n <= Na) ? 2 * Na + 1 - (L - n) : -1);
-                if (da >= 0) put_xi(prm, dst, sst, f, oa, Na, da, x.x);
-                const int db = (n <= Nb) ? n : ((L - n <= Nb) ? 2 * Nb + 1 - (L - n) : -1);
-                if (db >= 0) put_xi(prm, dst, sst, f, ob, Nb, db, -x.y);
-              }
-            } else {
-              const float2 x0 = v[r * LP + 0];   // n = k2
-              const float2 x1 = v[r * LP + 1];   // n = L - 32 + k2, distance d = 32 - k2
-              const int d = 32 - k2;
-              if (k2 <= Na) put_xi(prm, dst, sst, f, oa, Na, k2, x0.x);
-              if (d <= Na) put_xi(prm, dst, sst, f, oa, Na, 2 * Na + 1 - d, x1.x);
-              if (k2 <= Nb) put_xi(prm, dst, sst, f, ob, Nb, k2, -x0.y);
-              if (d <= Nb) put_xi(prm, dst, sst, f, ob, Nb, 2 * Nb + 1 - d, -x1.y);
-            }
-          }
-        }
-        __syncwarp();
-      }
+      inverse_frame<LP, kWpf>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, floor, lane, mi,
+                              GlobalXi{prm, dst, sst, f});
       if (prm.xi_planes && !prm.planes_ld && mi == 0) {   // zero the planes' pad columns [S, cols8)
         uint16_t* pl = prm.xi_planes + f * prm.cols8;
         for (int c = prm.S + lane; c < prm.cols8; c += 32) {
@@ -357,6 +393,171 @@ frontend_warp_kernel(const WarpParams prm) {
     }
     frame_sync<kWpf>(fg);                            // spectra free for the next frame
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused chain for latency-scale batches: samples -> spectra -> PHAT ->
+// pruned inverse FFT -> SSPI map -> per-frame argmax in ONE kernel.  A CTA's 4 warps each
+// run one frame's frontend (the warp-per-frame code above) with the TD-GCC samples kept in
+// shared memory as xs[S][4] (frame fastest); then the 4 warps evaluate the sparse map for
+// all 4 frames at once: one float4 shared load per operator entry feeds 4 FMAs.  The
+// operator is a sliced ELL (chunks of 32 candidates, per-chunk width, column-major within a
+// chunk) read coalesced through L1.  z is written once; one CTA owns its frames, so the
+// argmax index is written directly (no key reset, no atomics, no decode launch).
+struct SmemXi {
+  float* xs;
+  int fg;
+  __device__ __forceinline__ void operator()(int o, int, int d, float v) const { xs[(o + d) * 4 + fg] = v; }
+};
+
+constexpr int kMapW = 16;   // operator entries per chunk taken by the unrolled (all loads first) path
+
+template <int LP>
+__global__ void __launch_bounds__(kWarps * 32)
+frontend_sspi_kernel(const WarpParams prm, const SellMap mp) {
+  using G = Geo<LP>;
+  constexpr int L = G::L, K = G::K;
+  constexpr int Kp1 = K + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
+  int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
+  int* s_counts = s_pairs + 2 * prm.P;                                  // [P]
+  int* s_off = s_counts + prm.P;                                        // [P+1]
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
+  const int M = prm.M, P = prm.P, S = prm.S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t frame_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
+  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * frame_bytes);  // [M][K+1]
+  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
+  float* xs = reinterpret_cast<float*>(smem_raw + head + kWarps * frame_bytes);    // [S][4]
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(xs + 4 * (size_t)S);   // [4 warps][4]
+  int* s_choff = reinterpret_cast<int*>(s_keys + 16);                                       // [nch + 1]
+  float2* xp = work + (lane / LP) * G::XP;
+
+  for (int e = threadIdx.x; e < 32 * LP; e += blockDim.x) {
+    const int k2 = e / LP, l = e % LP;
+    float sn, cs;
+    sincospif(2.0f * (float)(k2 * l) / (float)L, &sn, &cs);
+    twT[e] = make_float2(cs, -sn);
+  }
+  for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) s_pairs[i] = prm.pairs[i];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_counts[i] = prm.counts[i];
+  for (int i = threadIdx.x; i <= P; i += blockDim.x) s_off[i] = prm.offsets[i];
+  const int64_t J = mp.J;
+  const int nch = (int)((J + 31) / 32);
+  for (int i = threadIdx.x; i <= nch; i += blockDim.x) s_choff[i] = mp.chunk_off[i];
+  __syncthreads();
+
+  const float4* xs4 = reinterpret_cast<const float4*>(xs);
+  const int64_t groups = (prm.F + 3) / 4;
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    const int64_t f = g * 4 + wid;
+    if (f < prm.F) {
+      const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
+      float energy = forward_frame<LP, 1>(prm, start, spec, work, xp, twT, lane, 0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+      const float floor = (prm.weighting && prm.floor_mode == 0) ? prm.floor_value * energy : prm.floor_value;
+      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, floor, lane, 0, SmemXi{xs, wid});
+    } else {
+      for (int s = lane; s < S; s += 32) xs[s * 4 + wid] = 0.f;
+    }
+    __syncthreads();                                  // xs of the CTA's 4 frames complete
+    unsigned long long best[4] = {0ull, 0ull, 0ull, 0ull};
+    // two chunks per warp at a time, all their entries loaded before any is used (the
+    // operator streams from L2: issue every load of both chunks, then do the FMAs)
+    for (int c = wid; c < nch; c += 2 * kWarps) {
+      const int cb = c + kWarps;
+      const int ea = s_choff[c], na = s_choff[c + 1] - ea;
+      const int eb = cb < nch ? s_choff[cb] : 0, nb = cb < nch ? s_choff[cb + 1] - eb : 0;
+      float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+      if (na <= kMapW && nb <= kMapW) {
+        uint32_t col[2][kMapW];
+        float wv[2][kMapW];
+#pragma unroll
+        for (int t = 0; t < kMapW; ++t) {
+          col[0][t] = t < na ? __ldg(mp.cols + (int64_t)(ea + t) * 32 + lane) : 0u;
+          wv[0][t] = t < na ? __ldg(mp.vals + (int64_t)(ea + t) * 32 + lane) : 0.f;
+          col[1][t] = t < nb ? __ldg(mp.cols + (int64_t)(eb + t) * 32 + lane) : 0u;
+          wv[1][t] = t < nb ? __ldg(mp.vals + (int64_t)(eb + t) * 32 + lane) : 0.f;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int t = 0; t < kMapW; ++t) {
+            const float4 x = xs4[col[h][t]];
+            acc[h].x = fmaf(wv[h][t], x.x, acc[h].x);
+            acc[h].y = fmaf(wv[h][t], x.y, acc[h].y);
+            acc[h].z = fmaf(wv[h][t], x.z, acc[h].z);
+            acc[h].w = fmaf(wv[h][t], x.w, acc[h].w);
+          }
+      } else {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int e0 = h ? eb : ea, n = h ? nb : na;
+#pragma unroll 4
+          for (int e = e0; e < e0 + n; ++e) {
+            const float w = __ldg(mp.vals + (int64_t)e * 32 + lane);
+            const float4 x = xs4[__ldg(mp.cols + (int64_t)e * 32 + lane)];
+            acc[h].x = fmaf(w, x.x, acc[h].x);
+            acc[h].y = fmaf(w, x.y, acc[h].y);
+            acc[h].z = fmaf(w, x.z, acc[h].z);
+            acc[h].w = fmaf(w, x.w, acc[h].w);
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = (int64_t)(h ? cb : c) * 32 + lane;
+        if (i < J) {
+          const float a[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
+#pragma unroll
+          for (int fr = 0; fr < 4; ++fr) {
+            if (mp.z && g * 4 + fr < prm.F) __stcs(mp.z + (g * 4 + fr) * J + i, a[fr]);
+            best[fr] = key_max(best[fr], make_key(a[fr], (uint32_t)i));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int fr = 0; fr < 4; ++fr) best[fr] = warp_key_max(best[fr]);
+    if (lane == 0) {
+#pragma unroll
+      for (int fr = 0; fr < 4; ++fr) s_keys[wid * 4 + fr] = best[fr];
+    }
+    __syncthreads();                                  // xs free; s_keys complete
+    if (wid == 0 && lane < 4 && g * 4 + lane < prm.F) {
+      unsigned long long k = s_keys[lane];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) k = key_max(k, s_keys[w * 4 + lane]);
+      if (mp.keys) mp.keys[g * 4 + lane] = k;
+      if (mp.index) mp.index[g * 4 + lane] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+    }
+  }
+}
+
+template <int LP>
+static int launch_sspi(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what) {
+  using G = Geo<LP>;
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1) * 4) + 15) & ~(size_t)15;
+  const size_t frame_bytes = ((size_t)wp.M * (G::K + 1) + G::WORK) * sizeof(float2);
+  const size_t smem = head + kWarps * frame_bytes + (size_t)wp.S * 16 + 16 * 8 + (size_t)((mp.J + 31) / 32 + 1) * 4;
+  SRPGPU_CHECK_ARG(smem <= 227 * 1024, SRPGPU_ERR_UNSUPPORTED,
+                   "%s: %d channels x %d samples per frame and %d TD-GCC samples need %zu B of shared memory",
+                   what, wp.M, wp.L, wp.S, smem);
+  auto kern = frontend_sspi_kernel<LP>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    set_error("%s: cannot reserve %zu B shared memory", what, smem);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = std::min<int64_t>((wp.F + 3) / 4, (int64_t)num_sms() * per_sm);
+  if (grid <= 0) return SRPGPU_OK;
+  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp, mp);
+  SRPGPU_CHECK_LAUNCH(what);
+  return SRPGPU_OK;
 }
 
 template <int LP, int OUT, int kWpf>
@@ -396,6 +597,17 @@ static int by_len(const WarpParams& wp, cudaStream_t st, const char* what) {
 
 // Returns 0 on launch, 1 if the shape is not covered (caller uses the block kernel),
 // a negative status on error.
+int frontend_sspi_launch(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what) {
+  switch (wp.L) {
+    case 256: return wf::launch_sspi<8>(wp, mp, st, what);
+    case 512: return wf::launch_sspi<16>(wp, mp, st, what);
+    case 1024: return wf::launch_sspi<32>(wp, mp, st, what);
+    default:
+      set_error("%s: the fused chain needs a frame length of 256, 512 or 1024 (got %d)", what, wp.L);
+      return SRPGPU_ERR_UNSUPPORTED;
+  }
+}
+
 int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what) {
   // warps per frame (measured on B200, graph replays): a CTA of 4 warps per frame for
   // tiny batches (cfg1, 100 frames: 25 -> 15 us; the frame's FFT rounds run side by side),

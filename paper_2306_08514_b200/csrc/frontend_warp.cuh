@@ -56,6 +56,20 @@ __device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_
   }
 }
 
+// Sliced-ELL sparse interpolation operator + outputs of the fused frames -> SSPI map chain.
+struct SellMap {
+  const uint16_t* cols;      // [sum_c W_c][32] sample index per entry (chunk c = candidates 32c..32c+31)
+  const float* vals;         // [sum_c W_c][32] weight (0 in padding entries)
+  const int32_t* chunk_off;  // [ceil(J/32) + 1] first entry row of each chunk
+  int64_t J;
+  float* z;                  // [F][J] or null
+  int64_t* index;            // [F] argmax index or null
+  uint64_t* keys;            // [F] packed argmax keys or null
+};
+
+// frontend + SSPI map + argmax in one launch (frame lengths 256 / 512 / 1024).
+int frontend_sspi_launch(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what);
+
 // 0: launched; 1: shape not covered (use the block kernel); < 0: error status.
 int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what);
 

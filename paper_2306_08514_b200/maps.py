@@ -793,3 +793,99 @@ def evaluate_map(kind, op, spec, frame, gcc, path="ifft", **kw):
     if kind == "sspi":
         return sspi_map(op, xi, **kw)
     raise ValueError(f"unknown map kind {kind!r}")
+
+
+# ----------------------------------------------------------------- fused chain (SSPI)
+
+FUSED_MAX_NNZ = 32            # widest sparse row the fused chain takes (its cost grows with nnz)
+FUSED_MAX_FRAMES_PER_SM = 8   # latency-scale batches only (a warp per frame, one wave)
+FUSED_FRAME_LENS = (256, 512, 1024)
+
+
+class SellOperator:
+    """Sliced-ELL device image of a sparse interpolation fit (CSR SparseInterp) for the
+    fused frames -> SSPI map chain: candidates in chunks of 32, chunk c has width W_c = its
+    longest row, entries stored [row][lane] so a warp reads 32 candidates' entry t with one
+    coalesced load.  Padding entries have weight 0 (and sample index 0)."""
+
+    def __init__(self, sp):
+        splits = np.asarray(sp.row_splits, dtype=np.int64)
+        cols = np.asarray(sp.col_indices, dtype=np.int64)
+        vals = np.asarray(sp.values, dtype=np.float64)
+        j = splits.shape[0] - 1
+        nnz = np.diff(splits)
+        nch = (j + 31) // 32
+        width = np.zeros(nch * 32, dtype=np.int64)
+        width[:j] = nnz
+        width = width.reshape(nch, 32).max(axis=1)
+        off = np.zeros(nch + 1, dtype=np.int64)
+        np.cumsum(width, out=off[1:])
+        rows = int(off[-1])
+        c = np.zeros((max(rows, 1), 32), dtype=np.uint16)
+        v = np.zeros((max(rows, 1), 32), dtype=np.float32)
+        cand = np.repeat(np.arange(j, dtype=np.int64), nnz)
+        slot = np.arange(cols.shape[0], dtype=np.int64) - np.repeat(splits[:-1], nnz)
+        c[off[cand // 32] + slot, cand % 32] = cols
+        v[off[cand // 32] + slot, cand % 32] = vals.astype(np.float32)
+        d = dev.device()
+        self.num_rows, self.num_cols = j, int(sp.num_cols)
+        self.max_row_nnz = int(nnz.max()) if j else 0
+        self.padding = rows * 32 / max(1, cols.shape[0])
+        self.cols = torch.from_numpy(c.view(np.int16)).to(d)
+        self.vals = torch.from_numpy(v).to(d)
+        self.chunk_off = torch.from_numpy(off.astype(np.int32)).to(d)
+
+
+def sell_from_sparse(sp) -> SellOperator:
+    return dev.CACHE.get(sp, "sell", lambda: SellOperator(sp))
+
+
+def fused_eligible(sp, frame, spec, frames: int, num_channels: int) -> bool:
+    """Whether frames_to_sspi_map takes this operator / frame shape / batch (the pipeline's
+    choice for latency-scale batches: cfg1 / cfg2)."""
+    if not hasattr(sp, "row_splits") or frame.frame_len not in FUSED_FRAME_LENS:
+        return False
+    s_tot = int(spec_offsets(spec)[-1])
+    if s_tot > 4096 or int(sp.num_cols) != s_tot or frames > FUSED_MAX_FRAMES_PER_SM * dev.num_sms():
+        return False
+    nnz = np.diff(np.asarray(sp.row_splits))
+    if nnz.size == 0 or int(nnz.max()) > FUSED_MAX_NNZ:
+        return False
+    k = frame.frame_len // 2
+    lp = frame.frame_len // 32
+    smem = 4 * ((num_channels * (k + 1) + (32 // lp) * 32 * (lp + 1)) * 8) + 16 * s_tot + 8 * 1024
+    return smem <= 220 * 1024
+
+
+def frames_to_sspi_map(sp, samples, frame, pairs, spec, frames=None, weighting: str = "phat", floor=None,
+                       *, argmax: bool = True, out_map: bool = True):
+    """The SSPI chain in one kernel: stft_frame -> fd_gcc -> td_gcc_samples -> sspi_map ->
+    locate over a range of frames (frontend.py:89-160, sampling.py:106-134,
+    interpolation.py:188-195, srp.py:74-80).  The TD-GCC samples stay in shared memory.
+    Returns z (F, J) (None without out_map) and, with argmax, the per-frame argmax (F,)."""
+    from . import frontend as fe
+    from .sampling import _spec_device
+    x = fe._signal(samples)
+    if x.shape[0] != pairs.num_mics:
+        raise DimensionError(f"expected {pairs.num_mics} channels, got {x.shape[0]}")
+    if spec.num_pairs != pairs.num_pairs or spec.half_len != frame.half_len:
+        raise DimensionError("sample spec does not match the pairs / frame")
+    s_tot = int(spec_offsets(spec)[-1])
+    if int(sp.num_cols) != s_tot:
+        raise DimensionError(f"operator with {int(sp.num_cols)} columns does not match {s_tot} samples")
+    first, count, batched = fe._frame_range(frames, fe.num_frames(frame, x.shape[1]))
+    fe._check_range(frame, first, count, x.shape[1])
+    w, mode, fval = fe._floor_args(weighting, floor)
+    counts, offsets = _spec_device(spec)
+    op = sell_from_sparse(sp)
+    z = torch.empty((count, op.num_rows), dtype=torch.float32, device=x.device) if out_map else None
+    idx = torch.empty(count, dtype=torch.int64, device=x.device) if argmax else None
+    nat.call("srpgpu_frames_to_sspi_map", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
+             dev.ptr(fe._window_device(frame)), frame.frame_len, frame.hop, first, count,
+             dev.ptr(fe._pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts), dev.ptr(offsets),
+             s_tot, dev.ptr(op.cols), dev.ptr(op.vals), dev.ptr(op.chunk_off), op.num_rows, dev.ptr(z),
+             dev.ptr(idx), None, dev.stream_ptr())
+    zz = None if z is None else (z if batched else z[0])
+    if not argmax:
+        return zz
+    return zz, (idx if batched else idx[0])

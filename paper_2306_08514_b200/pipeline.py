@@ -3,6 +3,8 @@
 The per-frame reference loop (cli.py:241-258: stft_frame -> fd_gcc ->
 evaluate_map -> locate) becomes one graph replay per batch of frames:
 
+    sspi (latency-scale batches, small sparse rows): frames_to_sspi_map -- the whole chain,
+                       argmax included, in one kernel
     sspi / si / slri :  frames_to_samples (1 fused kernel) -> map kernel(s) with fused argmax
     lr / conv        :  gcc_frames (1 fused kernel)        -> map kernel(s) with fused argmax
 
@@ -40,7 +42,7 @@ class MapPipeline:
         self.variant, self.op, self.frame, self.pairs, self.spec = variant, op, frame, pairs, spec
         self.frames = int(frames)
         self.weighting, self.floor, self.out_map, self.precision = weighting, floor, out_map, precision
-        self.engine = engine              # sspi / si: "auto" | "tc" | "band" (maps.interp_engine)
+        self.engine = engine              # sspi / si: "auto" | "fused" | "tc" | "tile" | "band"
         m = num_channels or pairs.num_mics
         n = (self.frames - 1) * frame.hop + frame.frame_len
         self.input = torch.zeros((m, n), dtype=torch.float32, device=device())
@@ -57,6 +59,10 @@ class MapPipeline:
     def _chain(self):
         rng = range(0, self.frames)
         v = self.variant
+        if self.uses_fused_chain():
+            # latency-scale batches: the whole chain in one kernel (xi never leaves shared memory)
+            return maps.frames_to_sspi_map(self.op, self.input, self.frame, self.pairs, self.spec, rng,
+                                           self.weighting, self.floor, argmax=True, out_map=self.out_map)
         if v in ("sspi", "si", "slri"):
             eng = maps.map_engine(v, self.op, self.engine, self.frames)
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
@@ -72,6 +78,17 @@ class MapPipeline:
             return maps.lr_map(self.op, gcc, argmax=True, out_map=self.out_map)
         return maps.srp_map_exact(self.op, gcc, precision=self.precision, argmax=True,
                                   out_map=self.out_map)
+
+    def uses_fused_chain(self) -> bool:
+        """sspi on latency-scale batches with short sparse rows: frames_to_sspi_map."""
+        if self.variant != "sspi" or self.engine not in ("auto", "fused"):
+            return False
+        ok = maps.fused_eligible(self.op, self.frame, self.spec, self.frames, self.input.shape[0])
+        if self.engine == "fused":
+            if not ok:
+                raise ValueError("the fused SSPI chain does not take this operator / frame shape / batch")
+            return True
+        return ok and maps.map_engine("sspi", self.op, "auto", self.frames) == "band"
 
     def _run_eager(self):
         return self._chain()

@@ -134,6 +134,51 @@ def test_frontend_kernels_agree(golden_scene, kernel):
     assert torch.equal(xn.bf16_planes[:, :S, :F].view(torch.int16), refn[:, :S, :F].view(torch.int16))
 
 
+def test_fused_sspi_chain(golden_scene):
+    """frames_to_sspi_map (frontend + SSPI map + argmax in one kernel, xi in shared memory)
+    against the reference maps, the unfused chain, argmax-only output and single frames."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, range(F))
+    for tag in keep_tags(g):
+        sp = sparse_from_golden(g, tag)
+        z, idx = s.maps.frames_to_sspi_map(sp, x, frame, pairs, spec, range(F))
+        ref = g[f"z_sspi_{tag}"]
+        zu, iu = s.sspi_map(sp, xi, argmax=True, engine="band")
+        if np.abs(ref).max() == 0:
+            assert np.all(np_(z) == 0)
+            continue
+        assert_map_close(z, ref)
+        assert_argmax_agrees(idx, ref)
+        assert O.normalized_max_error(np_(z), np_(zu)).max() < 1e-5
+        zo, io = s.maps.frames_to_sspi_map(sp, x, frame, pairs, spec, range(F), out_map=False)
+        assert zo is None and torch.equal(io, idx)
+        z1, i1 = s.maps.frames_to_sspi_map(sp, x, frame, pairs, spec, F - 1)
+        assert z1.shape == (grid.num_points,) and torch.equal(z1, z[F - 1]) and int(i1) == int(idx[F - 1])
+    with pytest.raises(s.DimensionError):
+        s.maps.frames_to_sspi_map(sparse_from_golden(g, keep_tags(g)[0]), x[:-1], frame, pairs, spec)
+
+
+def test_fused_sspi_pipeline(golden_scene):
+    """MapPipeline engine 'fused' (one kernel per replay) matches its eager run and the band chain."""
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    tag = [t for t in keep_tags(g) if t != "all"][0]
+    sp = sparse_from_golden(g, tag)
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    pipe = MapPipeline("sspi", sp, frame, pairs, spec, frames=F, engine="fused")
+    assert pipe.uses_fused_chain()
+    z, idx = pipe.run(x)
+    torch.cuda.synchronize()
+    z_b, i_b = MapPipeline("sspi", sp, frame, pairs, spec, frames=F, engine="band").run(x)
+    assert O.normalized_max_error(np_(z), np_(z_b)).max() < 1e-5
+    assert_argmax_agrees(idx, g[f"z_sspi_{tag}"])
+
+
 # ------------------------------------------------------------------ maps
 
 @pytest.mark.parametrize("engine", ["tc", "tile", "band"])
