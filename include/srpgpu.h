@@ -176,7 +176,8 @@ int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const v
  * sample index of each 8-lag group; tile_slab / tile_nkb [num_tiles] first 64-lag block
  * and block count of each tile (<= 128); tile_rows [num_tiles][256] candidate index of
  * each tile row (ascending, -1 pad; rows 0-127 half 0);
- * unit_bounds [num_ctas + 1] contiguous work-unit ranges, one persistent CTA each.
+ * num_ctas persistent CTAs take the work units (group of 8 frame tiles, tile, frame tile)
+ * round-robin (num_ctas = the SM count).
  * z [F][J] and keys [F] optional; a map is written in tile order into z_tiles
  * [F][num_tiles * 256] (full 32-byte sectors) and gathered back to grid order by
  * tile_pos [J] (= tile * 256 + row of each candidate). */
@@ -184,8 +185,8 @@ int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, 
                                 int64_t planes_ld,
                                 const void* slab_planes, int64_t num_slabs, const int32_t* group_col,
                                 const int32_t* tile_slab, const int32_t* tile_nkb, const int32_t* tile_rows,
-                                int32_t num_tiles, int64_t num_candidates, const int32_t* unit_bounds,
-                                int32_t num_ctas, const int32_t* tile_pos, float* z_tiles, float* z,
+                                int32_t num_tiles, int64_t num_candidates, int32_t num_ctas,
+                                const int32_t* tile_pos, float* z_tiles, float* z,
                                 uint64_t* keys, srpgpu_stream_t stream);
 
 /* row-wise bf16 hi/lo split: dst[p][r][c] for r < rows, c < cols (pitch ld_dst, plane

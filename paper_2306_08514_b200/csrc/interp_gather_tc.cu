@@ -18,8 +18,8 @@
 // 64-byte swizzle, 32-lag k-blocks), B = gathered xi (N = 256 frames = TMEM columns,
 // MN-major, 128-byte swizzle: 1 KB atoms of 64 frames x 8 lags, 1 KB apart along N (LBO)
 // and 4 KB apart along K (SBO)).  Three kind::f16 MMAs per 16-lag step (bf16 hi/lo split,
-// as interp_tc.cu); the two halves fill the 512 TMEM columns.  Persistent CTAs take
-// balanced contiguous ranges of work units (frame-tile group, tile, frame tile).
+// as interp_tc.cu); the two halves fill the 512 TMEM columns.  Persistent CTAs take the
+// work units (frame-tile group, tile, frame tile) round-robin.
 // Roles: warp 0 TMA producer (lanes 0-7 one plane x group each, 8-11 the slabs), warp 1
 // TMEM allocator + MMA issuer, warps 2-9 epilogue (lane quarter warp % 4 of one half):
 // the map goes out in tile order, 128 contiguous bytes per warp store (a gather pass
@@ -47,7 +47,7 @@ constexpr int UK = 16;    // kind::f16 MMA K
 constexpr int NS = 3;     // operand stages (64 KB each)
 constexpr int kEpi = 8;
 constexpr int kThreads = 32 * (2 + kEpi);
-constexpr int FG = 4;     // frame tiles per unit group (must match tiles.TileLayout.unit_bounds)
+constexpr int FG = 8;     // frame tiles per unit group
 constexpr int kMaxBlocks = 128;                   // 64-lag blocks per tile (K <= 8192 lags)
 constexpr int kMaxGroups = kMaxBlocks * (GB / GG);
 
@@ -97,12 +97,15 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
                  const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int64_t F,
                  int64_t J, int32_t T, const int32_t* __restrict__ group_col, const int32_t* __restrict__ tile_blk,
                  const int32_t* __restrict__ tile_nkb, const int32_t* __restrict__ tile_rows,
-                 const int32_t* __restrict__ bounds, float* __restrict__ zt, unsigned long long* __restrict__ keys) {
+                 float* __restrict__ zt, unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)((F + GN - 1) / GN);
-  const int u_begin = bounds[blockIdx.x], u_end = bounds[blockIdx.x + 1];
+  // units round-robin over the CTAs: at any moment the grid works on ~gridDim.x consecutive
+  // units of ONE frame-tile group, so that group's xi columns stay L2-resident and each
+  // tile's slabs are fetched from DRAM once per group (the FG CTAs sharing them run together)
+  const int u_total = ((n_tiles + FG - 1) / FG) * T * FG;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&ma_hi);
@@ -138,7 +141,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
     const int ah = ((lane - 8) >> 1) & 1, ap = (lane - 8) & 1;
     const uint64_t keep = policy_evict_last();   // a tile's slabs are re-read for FG frame tiles
     auto next_unit = [&](int u, Unit& w) {
-      while (u < u_end && !decode(u, T, n_tiles, w)) ++u;
+      while (u < u_total && !decode(u, T, n_tiles, w)) u += gridDim.x;
       return u;
     };
     auto stage_rows = [&](int buf, const Unit& w) {
@@ -148,12 +151,12 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
     uint32_t g = 0;
     int buf = 0;
     Unit w;
-    int u = next_unit(u_begin, w);
-    if (u < u_end) stage_rows(0, w);
-    while (u < u_end) {
+    int u = next_unit(blockIdx.x, w);
+    if (u < u_total) stage_rows(0, w);
+    while (u < u_total) {
       Unit wn;
-      const int un = next_unit(u + 1, wn);
-      if (un < u_end) stage_rows(buf ^ 1, wn);          // prefetch the next unit's rows
+      const int un = next_unit(u + gridDim.x, wn);
+      if (un < u_total) stage_rows(buf ^ 1, wn);        // prefetch the next unit's rows
       __syncwarp();
       const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
       for (int kq = 0; kq < 2 * nk; ++kq, ++g) {       // 32-lag stages: half a block each
@@ -185,7 +188,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(GN >> 3) << 17) |
                                  ((uint32_t)(GM >> 4) << 24);
       uint32_t g = 0, it = 0;
-      for (int u = u_begin; u < u_end; ++u) {
+      for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
         Unit w;
         if (!decode(u, T, n_tiles, w)) continue;
         const int nk = __ldg(tile_nkb + w.t);
@@ -220,7 +223,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
     const int64_t ldt = (int64_t)T * GT;
     uint32_t it = 0;
-    for (int u = u_begin; u < u_end; ++u) {
+    for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
       Unit w;
       if (!decode(u, T, n_tiles, w)) continue;
       const int r = half * GM + q * 32 + lane;         // tile row
@@ -323,7 +326,7 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
                                            const void* slab_planes, int64_t num_slabs, const int32_t* group_col,
                                            const int32_t* tile_slab, const int32_t* tile_nkb,
                                            const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
-                                           const int32_t* unit_bounds, int32_t num_ctas, const int32_t* tile_pos,
+                                           int32_t num_ctas, const int32_t* tile_pos,
                                            float* z_tiles, float* z, uint64_t* keys, srpgpu_stream_t stream) {
   using namespace gtc;
   SRPGPU_CHECK_ARG(num_frames >= 0 && num_cols >= 1 && planes_ld >= num_frames && planes_ld % 8 == 0 &&
@@ -360,7 +363,7 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
   }
   gather_tc_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nkb, tile_rows,
-      unit_bounds, z ? z_tiles : nullptr, reinterpret_cast<unsigned long long*>(keys));
+      z ? z_tiles : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
   if (z) {
     dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),

@@ -364,15 +364,6 @@ class TileOperator:
         self.tile_pos = dev.as_i32(lay.tile_pos)
         self._layout = lay
         lay.slabs = None                      # host copy no longer needed
-        self._bounds = {}
-
-    def bounds(self, frames: int):
-        hit = self._bounds.get(frames)
-        if hit is None:
-            ctas = torch.cuda.get_device_properties(dev.device()).multi_processor_count
-            hit = dev.as_i32(self._layout.unit_bounds(frames, ctas))
-            self._bounds[frames] = hit
-        return hit
 
 
 def tile_from_sparse(sp, offsets: np.ndarray) -> TileOperator:
@@ -386,11 +377,10 @@ def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
     zt = torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device) if out_map else None
     keys = _new_keys(f, argmax)
-    b = op.bounds(f)
     nat.call("srpgpu_interp_map_gather_tc", dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes),
              op.num_slabs,
              dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
-             op.num_tiles, op.num_rows, dev.ptr(b), b.shape[0] - 1, dev.ptr(op.tile_pos), dev.ptr(zt), dev.ptr(z),
+             op.num_tiles, op.num_rows, dev.num_sms(), dev.ptr(op.tile_pos), dev.ptr(zt), dev.ptr(z),
              dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 

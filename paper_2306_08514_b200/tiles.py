@@ -171,26 +171,6 @@ class TileLayout:
         self.num_slabs = 2 * num_blocks
         self.mean_k = float(tile_nkb.mean() * SLAB) if t_count else 0.0
 
-    def unit_bounds(self, frames: int, ctas: int, group: int = 4) -> np.ndarray:
-        """Balanced contiguous ranges of work units per CTA.
-
-        Units run frame-tile-group major (`group` frame tiles of 256), then tile, then the
-        frame tile inside the group, so a tile's slabs are reused from L2 across the
-        group and the group's xi columns stay L2-resident.  Work = slabs (+1 for the
-        epilogue); units past the last frame tile are empty.
-        """
-        n_tiles = (frames + 255) // 256
-        n_groups = (n_tiles + group - 1) // group
-        u = np.arange(n_groups * self.num_tiles * group)
-        n = (u // (self.num_tiles * group)) * group + u % group
-        t = (u % (self.num_tiles * group)) // group
-        work = np.where(n < n_tiles, 2 * self.tile_nkb[t].astype(np.int64) + 2, 0)
-        cum = np.concatenate([[0], np.cumsum(work)])
-        targets = np.linspace(0, cum[-1], ctas + 1)
-        bounds = np.searchsorted(cum, targets, side="left")
-        bounds[0], bounds[-1] = 0, u.shape[0]
-        return np.maximum.accumulate(bounds).astype(np.int32)
-
     def emulate(self, xi_nat: np.ndarray) -> np.ndarray:
         """float64 reference of the gathered product (test helper): z (F, J)."""
         f = xi_nat.shape[0]

@@ -427,11 +427,16 @@ def test_pipeline_graph_matches_eager(golden_scene):
     x = g["samples"][:, :(F - 1) * frame.hop + frame.frame_len]
     tag = keep_tags(g)[0]
     sp = sparse_from_golden(g, tag)
-    pipe = MapPipeline("sspi", sp, frame, pairs, spec, frames=F)
-    z, idx = pipe.run(x)
     xi = s.frames_to_samples(x, frame, pairs, spec, range(F))
+    eng = s.maps.map_engine("sspi", sp, "auto", F)
+    pipe = MapPipeline("sspi", sp, frame, pairs, spec, frames=F, engine=eng)   # the unfused chain
+    z, idx = pipe.run(x)
     z2, idx2 = s.sspi_map(sp, xi, argmax=True)
     assert torch.equal(z, z2) and torch.equal(idx, idx2)
+    auto = MapPipeline("sspi", sp, frame, pairs, spec, frames=F)               # fused where eligible
+    za, ia = auto.run(x)
+    assert O.normalized_max_error(np_(za), np_(z2)).max() < 1e-5
+    assert_argmax_agrees(ia, g[f"z_sspi_{tag}"])
     conv = MapPipeline("conv", s.build_srp_matrix(tdoa, frame, max_bytes=1 << 34), frame, pairs,
                        frames=F)
     zc, ic = conv.run(torch.from_numpy(x.astype(np.float32)).cuda())

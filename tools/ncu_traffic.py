@@ -4,7 +4,7 @@
 
 Each argument is workload:variant:csv.  Output: {workload: {variant: {kernel: bytes}}}
 with kernels keyed the way bench.py names the dominant kernel (`frontend`,
-`<variant>_map`, `srp_map_tc` for the stored-operator tensor-core map, `srp_map_tdoa`
+`<variant>_map`, `fused` for the one-kernel SSPI chain, `srp_map_tc` for the stored-operator tensor-core map, `srp_map_tdoa`
 for the on-chip-steering one; `<variant>_factor` for the low-rank factor product); the
 value is dram__bytes_read.sum + dram__bytes_write.sum averaged over that kernel's launches.
 """
@@ -17,6 +17,12 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 
 
 def key_of(name: str, variant: str):
+    if "frontend_sspi" in name:
+        return "fused"
+    if "untile" in name:
+        return f"{variant}_untile"
+    if "gather_tc" in name:
+        return f"{variant}_map"
     if "frontend" in name:
         return "frontend"
     if "conv_gen_chunked_kernel" in name:
