@@ -292,10 +292,12 @@ static size_t frontend_smem(int in, int out, int L, int K, int M, int P, int nbu
 }
 
 // The task-per-warp kernel (frontend_lane.cu) wins on tiny batches (cfg1, 100 frames: 15 vs
-// 17 us) and on many channels / long lag windows (cfg4, M = 16, N_p up to 58: 2.6 vs 10.4 ms
-// per 10^4 frames); the warp-per-frame kernel stays for the 1000-10^4 frame batches of
-// cfg2 / cfg3, where the two measure within noise of each other (tools/bench_frontend.py).
-constexpr int64_t kLaneMaxFrames = 2;   // frames per SM
+// 17 us; cfg3 geometry, 1000 frames: 53 vs 61 us) and on many channels / long lag windows
+// (cfg4, M = 16, N_p up to 58: 2.6 vs 10.4 ms per 10^4 frames); the warp-per-frame kernel
+// wins at cfg2 (1000 frames: 33 vs 39 us) and on large batches (cfg3, 10^4 frames: 0.38 vs
+// 0.43 ms), medians of 5 alternating runs (tools/bench_frontend.py --rounds 5).
+constexpr int64_t kLaneMaxFrames = 2;    // frames per SM (M < 8)
+constexpr int64_t kLaneMaxFrames8 = 12;  // frames per SM (M >= 8)
 constexpr int kLaneMinMics = 12;
 
 template <int IN, int OUT>
@@ -315,7 +317,8 @@ static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* 
     const int wout = OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI;
     const int choice = frontend_kernel_choice();
     int r = 1;
-    if (choice == 2 || (choice == 0 && (prm.F <= kLaneMaxFrames * (int64_t)num_sms() || prm.M >= kLaneMinMics)))
+    const int64_t lane_frames = (prm.M >= 8 ? kLaneMaxFrames8 : kLaneMaxFrames) * (int64_t)num_sms();
+    if (choice == 2 || (choice == 0 && (prm.F <= lane_frames || prm.M >= kLaneMinMics)))
       r = frontend_lane_launch(wp, wout, stream, what);
     if (r == 1 && choice != 3) r = frontend_warp_launch(wp, wout, stream, what);
     if (r == 0 && prm.warp_used) *prm.warp_used = 1;

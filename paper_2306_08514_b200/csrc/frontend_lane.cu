@@ -96,18 +96,6 @@ __device__ __forceinline__ int zpos(int k) {
   return k + (16 / Geo<Q>::E) * (k / (Q * Q));
 }
 
-__device__ __forceinline__ float2 phat(float2 a, float2 b, int weighting, float floor) {
-  float2 raw = cmulc(a, b);
-  if (weighting) {
-    // raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158)
-    const float mag2 = raw.x * raw.x + raw.y * raw.y;
-    const float inv = (mag2 > floor * floor && mag2 > 0.f) ? rsqrtf(mag2) : (floor > 0.f ? 1.0f / floor : 0.f);
-    raw.x *= inv;
-    raw.y *= inv;
-  }
-  return raw;
-}
-
 struct Tables {
   const float2* twA;    // [Q][32]  W_N^{l a}
   const float2* twL;    // [N]      W_L^k
@@ -206,7 +194,7 @@ __device__ __forceinline__ void transpose_reduce(float (&v)[32 * R], int lane) {
 
 // Inverse task: pair p's PHAT cross-spectrum -> its kept TD-GCC lags |n| <= Np.
 template <int Q>
-__device__ __forceinline__ void inverse_pair(const WarpParams& prm, const float2* ya, const float2* yb, float floor,
+__device__ __forceinline__ void inverse_pair(const WarpParams& prm, const float2* ya, const float2* yb, const Phat& ph,
                                              const Tables& t, int lane, int Np, int off, int64_t f, float* dst,
                                              int64_t sst) {
   using G = Geo<Q>;
@@ -216,7 +204,7 @@ __device__ __forceinline__ void inverse_pair(const WarpParams& prm, const float2
 #pragma unroll
   for (int j = 0; j < Q; ++j) {
     const int k = lane + 32 * j;
-    ps[j] = (k == 0) ? make_float2(0.f, 0.f) : phat(ya[k], yb[k], prm.weighting, floor);
+    ps[j] = (k == 0) ? make_float2(0.f, 0.f) : ph(cmulc(ya[k], yb[k]));
   }
   // Psi[N - k]: lane 32 - l, register Q - 1 - j (lane 0: its own register Q - j, Psi[N] = 0)
   const int src = (32 - lane) & 31;
@@ -336,13 +324,14 @@ frontend_lane_kernel(const WarpParams prm) {
       for (int w = 0; w < WPF; ++w) e += s_energy[w];
       floor = prm.floor_value * e;
     }
+    const Phat ph(prm.weighting, floor);
     if (OUT == W_OUT_GCC) {
       float2* dst = prm.gcc_out + f * prm.gcc_ld;
       for (int p = wid; p < P; p += WPF) {
         const float2* ya = spec + (size_t)s_pairs[2 * p] * SLOT;
         const float2* yb = spec + (size_t)s_pairs[2 * p + 1] * SLOT;
         for (int k = 1 + lane; k < K; k += 32) {
-          float2 val = phat(ya[k], yb[k], prm.weighting, floor);
+          float2 val = ph(cmulc(ya[k], yb[k]));
           if (prm.round_tf32) val = make_float2(tf32_rne(val.x), tf32_rne(val.y));
           dst[p * B + k - 1] = val;
         }
@@ -354,7 +343,7 @@ frontend_lane_kernel(const WarpParams prm) {
       const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
       for (int p = wid; p < P; p += WPF)
         inverse_pair<Q>(prm, spec + (size_t)s_pairs[2 * p] * SLOT, spec + (size_t)s_pairs[2 * p + 1] * SLOT,
-                           floor, t, lane, s_counts[p], s_off[p], f, dst, sst);
+                           ph, t, lane, s_counts[p], s_off[p], f, dst, sst);
       if (prm.xi_planes && !prm.planes_ld && wid == 0) {   // zero the planes' pad columns [S, cols8)
         uint16_t* pl = prm.xi_planes + f * prm.cols8;
         for (int c = prm.S + lane; c < prm.cols8; c += 32) {

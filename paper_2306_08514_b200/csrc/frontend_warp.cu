@@ -129,19 +129,10 @@ __device__ __forceinline__ void fft_l(float2 (&v)[32], float2* xp, const float2*
   }
 }
 
-__device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m, int mp, int k, int weighting,
-                                             float floor) {
+__device__ __forceinline__ float2 cross_phat(const float2* spec, int Kp1, int m, int mp, int k, const Phat& ph) {
   const float2 a = spec[m * Kp1 + k];
   const float2 b = spec[mp * Kp1 + k];
-  float2 raw = cmulc(a, b);
-  if (weighting) {
-    // raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158)
-    const float mag2 = raw.x * raw.x + raw.y * raw.y;
-    const float inv = (mag2 > floor * floor && mag2 > 0.f) ? rsqrtf(mag2) : (floor > 0.f ? 1.0f / floor : 0.f);
-    raw.x *= inv;
-    raw.y *= inv;
-  }
-  return raw;
+  return ph(cmulc(a, b));
 }
 
 // forward FFTs of one frame (R channel pairs per round, rounds split over the frame's warps)
@@ -203,7 +194,7 @@ __device__ __forceinline__ float forward_frame(const WarpParams& prm, int64_t st
 template <int LP, int kWpf, class Put>
 __device__ __forceinline__ void inverse_frame(const WarpParams& prm, const float2* spec, float2* work, float2* xp,
                                               const float2* twT, const int* s_pairs, const int* s_counts,
-                                              const int* s_off, float floor, int lane, int mi, const Put& put) {
+                                              const int* s_off, const Phat& ph, int lane, int mi, const Put& put) {
   using G = Geo<LP>;
   constexpr int L = G::L, K = G::K, R = G::R, Kp1 = K + 1, B = K - 1;
   const int P = prm.P;
@@ -218,8 +209,8 @@ __device__ __forceinline__ void inverse_frame(const WarpParams& prm, const float
       const int ma = s_pairs[2 * pa], mpa = s_pairs[2 * pa + 1];
       const int mb = (pb < P) ? s_pairs[2 * pb] : 0, mpb = (pb < P) ? s_pairs[2 * pb + 1] : 0;
       for (int k = 1 + lane; k < K; k += 32) {
-        sq[k - 1] = cross_phat(spec, Kp1, ma, mpa, k, prm.weighting, floor);
-        sq[B + k - 1] = (pb < P) ? cross_phat(spec, Kp1, mb, mpb, k, prm.weighting, floor)
+        sq[k - 1] = cross_phat(spec, Kp1, ma, mpa, k, ph);
+        sq[B + k - 1] = (pb < P) ? cross_phat(spec, Kp1, mb, mpb, k, ph)
                                  : make_float2(0.f, 0.f);
       }
     }
@@ -365,13 +356,14 @@ frontend_warp_kernel(const WarpParams prm) {
       for (int w = 0; w < kWpf; ++w) e += s_energy[fg * kWpf + w];
       floor = prm.floor_value * e;
     }
+    const Phat ph(prm.weighting, floor);
 
     if (OUT == W_OUT_GCC) {
       float2* dst = prm.gcc_out + f * prm.gcc_ld;
       for (int p = mi; p < P; p += kWpf) {
         const int m = s_pairs[2 * p], mp = s_pairs[2 * p + 1];
         for (int k = 1 + lane; k < K; k += 32) {
-          float2 val = cross_phat(spec, Kp1, m, mp, k, prm.weighting, floor);
+          float2 val = cross_phat(spec, Kp1, m, mp, k, ph);
           if (prm.round_tf32) val = make_float2(tf32_rne(val.x), tf32_rne(val.y));
           dst[p * B + k - 1] = val;
         }
@@ -381,7 +373,7 @@ frontend_warp_kernel(const WarpParams prm) {
     } else {
       float* dst = prm.xi_out + (prm.xi_ld ? f : f * (int64_t)prm.S);
       const int64_t sst = prm.xi_ld ? prm.xi_ld : 1;
-      inverse_frame<LP, kWpf>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, floor, lane, mi,
+      inverse_frame<LP, kWpf>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, ph, lane, mi,
                               GlobalXi{prm, dst, sst, f});
       if (prm.xi_planes && !prm.planes_ld && mi == 0) {   // zero the planes' pad columns [S, cols8)
         uint16_t* pl = prm.xi_planes + f * prm.cols8;
@@ -458,7 +450,8 @@ frontend_sspi_kernel(const WarpParams prm, const SellMap mp) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
       const float floor = (prm.weighting && prm.floor_mode == 0) ? prm.floor_value * energy : prm.floor_value;
-      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, floor, lane, 0, SmemXi{xs, wid});
+      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, Phat(prm.weighting, floor), lane, 0,
+                           SmemXi{xs, wid});
     } else {
       for (int s = lane; s < S; s += 32) xs[s * 4 + wid] = 0.f;
     }

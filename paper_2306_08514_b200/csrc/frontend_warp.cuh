@@ -34,6 +34,24 @@ struct WarpParams {
   int64_t planes_ld;    // 0: planes frame-major [2][F][cols8]; > 0: lag-major [2][cols8][planes_ld]
 };
 
+// PHAT weighting raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158), with the
+// per-frame constants hoisted: rsqrt(|raw|^2) above the floor, 1 / floor below it.
+struct Phat {
+  int weighting;
+  float floor2, inv_floor;
+  __device__ __forceinline__ Phat(int w, float floor)
+      : weighting(w), floor2(floor * floor), inv_floor(floor > 0.f ? 1.0f / floor : 0.f) {}
+  __device__ __forceinline__ float2 operator()(float2 raw) const {
+    if (weighting) {
+      const float mag2 = raw.x * raw.x + raw.y * raw.y;
+      const float inv = (mag2 > floor2 && mag2 > 0.f) ? rsqrtf(mag2) : inv_floor;
+      raw.x *= inv;
+      raw.y *= inv;
+    }
+    return raw;
+  }
+};
+
 // one xi sample (storage index d of a pair block at offset o with N lags a side): the
 // f32 output and, when requested, its bf16 hi/lo planes (storage or natural lag order)
 __device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_t sst, int64_t f, int o, int N, int d,

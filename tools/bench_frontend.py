@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--frames", default="", help="comma list overriding the workload's frame count")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--kernels", default="warp,task,block")
+    ap.add_argument("--rounds", type=int, default=1, help="alternate the kernels this many times (median)")
     a = ap.parse_args()
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     for name in a.workloads.split(","):
@@ -59,18 +60,22 @@ def main():
         x = torch.from_numpy(wl.samples).cuda()
         planes, natural = PLANES.get(name, (False, False))
         for frames in frame_list:
-            for k in a.kernels.split(","):
-                with frontend_kernel(k):
-                    try:
-                        ms = time_graph(lambda: s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(frames),
-                                                                    planes=planes, natural=natural),
-                                        a.reps, flush)
-                    except Exception as exc:  # noqa: BLE001
-                        print(json.dumps({"workload": name, "frames": frames, "kernel": k, "error": str(exc)}))
-                        continue
+            times = {k: [] for k in a.kernels.split(",")}
+            for _ in range(a.rounds):
+                for k in times:
+                    with frontend_kernel(k):
+                        try:
+                            times[k].append(time_graph(
+                                lambda: s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(frames),
+                                                            planes=planes, natural=natural), a.reps, flush))
+                        except Exception as exc:  # noqa: BLE001
+                            times[k].append(float("nan"))
+                            print(json.dumps({"workload": name, "frames": frames, "kernel": k, "error": str(exc)}))
+            for k, ts in times.items():
+                ms = sorted(ts)[len(ts) // 2]
                 print(json.dumps({"workload": name, "frames": frames, "kernel": k, "planes": planes,
-                                  "natural": natural, "ms": ms, "ns_per_frame": ms * 1e6 / frames}), flush=True)
-
+                                  "natural": natural, "ms": ms, "ns_per_frame": ms * 1e6 / frames,
+                                  "all_ms": ts}), flush=True)
 
 if __name__ == "__main__":
     main()
