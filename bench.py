@@ -325,18 +325,21 @@ def run_ours(args):
     fused = pipe.uses_fused_chain()
     # ---- per-kernel times for the roofline: each stage captured alone, CUDA events
     if fused:
-        t_front, t_map = 0.0, fused_time(s, wl, op, x_dev, count, flush)
+        t_front, t_map = 0.0, fused_time(s, wl, args.variant, op, x_dev, count, flush)
     else:
         t_front, t_map = stage_times(s, wl, args.variant, op, x_dev, count, flush, engine=args.engine)
     hbm, bf16, peak_src = peaks()
     abytes = algorithmic_bytes(wl, args.variant, count, op, args.engine)
     tf32_peak, fp32_peak, xsrc = extra_peaks()
     if fused:
-        sell = _maps.sell_from_sparse(op)
-        fbytes = abytes["frontend"] - count * 4 * wl.spec.total_samples \
-            + count * 4 * wl.grid.num_points + sell.cols.numel() * 6 + sell.chunk_off.numel() * 4
+        if args.variant == "sspi":
+            sell = _maps.sell_from_sparse(op)
+            op_bytes = sell.cols.numel() * 6 + sell.chunk_off.numel() * 4
+        else:
+            op_bytes = 4 * op.tall.shape[1] * (wl.grid.num_points + wl.spec.total_samples)
+        fbytes = abytes["frontend"] - count * 4 * wl.spec.total_samples + count * 4 * wl.grid.num_points + op_bytes
         achieved = fbytes / (t_map / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "frontend_sspi_kernel (fused chain)", "achieved": achieved,
+        roof = {"bound": "hbm", "kernel": f"frontend_map_kernel ({args.variant} fused chain)", "achieved": achieved,
                 "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": fbytes,
                 "traffic": ncu_traffic(args.workload, args.variant, "fused")}
@@ -542,11 +545,12 @@ def ring_timed(slots, steps, warmup, world, dev, total):
     return float(t.item()) / steps
 
 
-def fused_time(s, wl, op, x_dev, count, flush, reps=10):
-    """Median device time of the fused frames -> SSPI map -> argmax kernel, in its own graph."""
+def fused_time(s, wl, variant, op, x_dev, count, flush, reps=10):
+    """Median device time of the fused frames -> map -> argmax kernel, in its own graph."""
     import torch
     from paper_2306_08514_b200 import maps
-    fn = lambda: maps.frames_to_sspi_map(op, x_dev, wl.frame, wl.pairs, wl.spec, range(0, count))
+    chain = maps.frames_to_sspi_map if variant == "sspi" else maps.frames_to_slri_map
+    fn = lambda: chain(op, x_dev, wl.frame, wl.pairs, wl.spec, range(0, count))
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()

@@ -135,6 +135,18 @@ int srpgpu_frames_to_sspi_map(const float* samples, int32_t num_channels, int64_
                               const float* sell_vals, const int32_t* sell_chunk_off, int64_t num_candidates,
                               float* z, int64_t* index, uint64_t* keys, srpgpu_stream_t stream);
 
+/* The SLRI chain in one launch (stft_frame + fd_gcc + td_gcc_samples + slri_map + locate;
+ * interpolation.py:178-185): y = fat [R][S] . xi per frame in shared memory, then
+ * z = tall . y with the tall factor transposed, tall_t [R][J] (candidates contiguous).
+ * Outputs as srpgpu_frames_to_sspi_map; f32 throughout. */
+int srpgpu_frames_to_slri_map(const float* samples, int32_t num_channels, int64_t num_samples,
+                              int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
+                              int64_t first_frame, int64_t num_frames, const int32_t* pairs, int32_t num_pairs,
+                              int32_t weighting, int32_t floor_mode, double floor_value, const int32_t* counts,
+                              const int32_t* offsets, int32_t total_samples, const float* fat, const float* tall_t,
+                              int32_t rank, int64_t num_candidates, float* z, int64_t* index, uint64_t* keys,
+                              srpgpu_stream_t stream);
+
 /* fused fd_gcc + td_gcc_samples on precomputed spectra [F][M][K+1]. */
 int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t num_channels,
                               int32_t half_len, const int32_t* pairs, int32_t num_pairs,

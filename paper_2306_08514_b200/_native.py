@@ -39,6 +39,8 @@ SIGNATURES = {
                                         _I32, _I32, _F64, _P, _P, _I32, _P, _I64, _P, _I32, _I64, _I32, _P, _P],
     "srpgpu_frames_to_sspi_map": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _I32, _I32, _I32,
                                   _F64, _P, _P, _I32, _P, _P, _P, _I64, _P, _P, _P, _P],
+    "srpgpu_frames_to_slri_map": [_P, _I32, _I64, _I64, _P, _I32, _I32, _I64, _I64, _P, _I32, _I32, _I32,
+                                  _F64, _P, _P, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_spectra_to_samples": [_P, _I64, _I32, _I32, _P, _I32, _I32, _I32, _F64, _P, _P, _I32,
                                   _P, _I64, _P],
     "srpgpu_sspi_map": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _I64, _I64, _P, _P, _P],

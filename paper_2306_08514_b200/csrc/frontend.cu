@@ -517,6 +517,36 @@ extern "C" int srpgpu_frames_to_sspi_map(const float* samples, int32_t num_chann
   return frontend_sspi_launch(wp, mp, as_stream(stream), "frames_to_sspi_map");
 }
 
+extern "C" int srpgpu_frames_to_slri_map(const float* samples, int32_t num_channels, int64_t num_samples,
+                                         int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,
+                                         int64_t first_frame, int64_t num_frames, const int32_t* pairs,
+                                         int32_t num_pairs, int32_t weighting, int32_t floor_mode,
+                                         double floor_value, const int32_t* counts, const int32_t* offsets,
+                                         int32_t total_samples, const float* fat, const float* tall_t, int32_t rank,
+                                         int64_t num_candidates, float* z, int64_t* index, uint64_t* keys,
+                                         srpgpu_stream_t stream) {
+  FrontendParams prm = {};
+  int st = fill_common(prm, frame_len, "frames_to_slri_map");
+  if (st) return st;
+  SRPGPU_CHECK_ARG(weighting == 0 || weighting == 1, SRPGPU_ERR_VALUE, "frames_to_slri_map: unknown weighting");
+  SRPGPU_CHECK_ARG(num_channels >= 2 && num_pairs >= 1 && total_samples >= 1 && rank >= 1 && rank <= 4096 &&
+                       num_candidates >= 1 && num_candidates < (1ll << 31),
+                   SRPGPU_ERR_DIMENSION, "frames_to_slri_map: bad shape");
+  SRPGPU_CHECK_ARG(fat && tall_t, SRPGPU_ERR_VALUE, "frames_to_slri_map: missing factors");
+  prm.samples = samples; prm.ld_samples = ld_samples; prm.window = window;
+  prm.M = num_channels; prm.hop = hop; prm.first_frame = first_frame; prm.F = num_frames;
+  if ((st = check_frames(prm, num_samples, "frames_to_slri_map"))) return st;
+  WarpParams wp = {};
+  wp.samples = samples; wp.ld_samples = ld_samples; wp.window = window;
+  wp.M = num_channels; wp.L = prm.L; wp.K = prm.K; wp.hop = hop;
+  wp.first_frame = first_frame; wp.F = num_frames; wp.pairs = pairs; wp.P = num_pairs;
+  wp.weighting = weighting; wp.floor_mode = floor_mode; wp.floor_value = (float)floor_value;
+  wp.counts = counts; wp.offsets = offsets; wp.S = total_samples;
+  SlriMap mp = {fat, tall_t, rank, total_samples, num_candidates, z, index, keys};
+  if (num_frames == 0) return SRPGPU_OK;
+  return frontend_slri_launch(wp, mp, as_stream(stream), "frames_to_slri_map");
+}
+
 extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels,
                                                int64_t num_samples, int64_t ld_samples, const float* window,
                                                int32_t frame_len, int32_t hop, int64_t first_frame,

@@ -387,15 +387,6 @@ frontend_warp_kernel(const WarpParams prm) {
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// Fused chain for latency-scale batches (SURVEY 8(f) #1): samples -> spectra -> PHAT ->
-// pruned inverse FFT -> SSPI map -> per-frame argmax in ONE kernel.  A CTA's 4 warps each
-// run one frame's frontend (the warp-per-frame code above) with the TD-GCC samples kept in
-// shared memory as xs[S][4] (frame fastest); then the 4 warps evaluate the sparse map for
-// all 4 frames at once: one float4 shared load per operator entry feeds 4 FMAs.  The
-// operator is a sliced ELL (chunks of 32 candidates, per-chunk width, column-major within a
-// chunk) read coalesced through L1.  z is written once; one CTA owns its frames, so the
-// argmax index is written directly (no key reset, no atomics, no decode launch).
 struct SmemXi {
   float* xs;
   int fg;
@@ -404,59 +395,41 @@ struct SmemXi {
 
 constexpr int kMapW = 16;   // operator entries per chunk taken by the unrolled (all loads first) path
 
-template <int LP>
-__global__ void __launch_bounds__(kWarps * 32)
-frontend_sspi_kernel(const WarpParams prm, const SellMap mp) {
-  using G = Geo<LP>;
-  constexpr int L = G::L, K = G::K;
-  constexpr int Kp1 = K + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
-  int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
-  int* s_counts = s_pairs + 2 * prm.P;                                  // [P]
-  int* s_off = s_counts + prm.P;                                        // [P+1]
-  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
-  const int M = prm.M, P = prm.P, S = prm.S;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t frame_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
-  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * frame_bytes);  // [M][K+1]
-  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
-  float* xs = reinterpret_cast<float*>(smem_raw + head + kWarps * frame_bytes);    // [S][4]
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(xs + 4 * (size_t)S);   // [4 warps][4]
-  int* s_choff = reinterpret_cast<int*>(s_keys + 16);                                       // [nch + 1]
-  float2* xp = work + (lane / LP) * G::XP;
-
-  for (int e = threadIdx.x; e < 32 * LP; e += blockDim.x) {
-    const int k2 = e / LP, l = e % LP;
-    float sn, cs;
-    sincospif(2.0f * (float)(k2 * l) / (float)L, &sn, &cs);
-    twT[e] = make_float2(cs, -sn);
-  }
-  for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) s_pairs[i] = prm.pairs[i];
-  for (int i = threadIdx.x; i < P; i += blockDim.x) s_counts[i] = prm.counts[i];
-  for (int i = threadIdx.x; i <= P; i += blockDim.x) s_off[i] = prm.offsets[i];
-  const int64_t J = mp.J;
-  const int nch = (int)((J + 31) / 32);
-  for (int i = threadIdx.x; i <= nch; i += blockDim.x) s_choff[i] = mp.chunk_off[i];
-  __syncthreads();
-
-  const float4* xs4 = reinterpret_cast<const float4*>(xs);
-  const int64_t groups = (prm.F + 3) / 4;
-  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
-    const int64_t f = g * 4 + wid;
-    if (f < prm.F) {
-      const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
-      float energy = forward_frame<LP, 1>(prm, start, spec, work, xp, twT, lane, 0);
+// one candidate's map values for the CTA's 4 frames: z stores + running argmax keys
+__device__ __forceinline__ void emit4(float4 acc, int64_t i, int64_t J, int64_t g, int64_t F, float* z,
+                                      unsigned long long (&best)[4]) {
+  if (i >= J) return;
+  const float a[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
-      const float floor = (prm.weighting && prm.floor_mode == 0) ? prm.floor_value * energy : prm.floor_value;
-      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, Phat(prm.weighting, floor), lane, 0,
-                           SmemXi{xs, wid});
-    } else {
-      for (int s = lane; s < S; s += 32) xs[s * 4 + wid] = 0.f;
-    }
-    __syncthreads();                                  // xs of the CTA's 4 frames complete
-    unsigned long long best[4] = {0ull, 0ull, 0ull, 0ull};
+  for (int fr = 0; fr < 4; ++fr) {
+    if (z && g * 4 + fr < F) __stcs(z + (g * 4 + fr) * J + i, a[fr]);
+    best[fr] = key_max(best[fr], make_key(a[fr], (uint32_t)i));
+  }
+}
+
+__device__ __forceinline__ void fma4(float4& acc, float w, float4 x) {
+  acc.x = fmaf(w, x.x, acc.x);
+  acc.y = fmaf(w, x.y, acc.y);
+  acc.z = fmaf(w, x.z, acc.z);
+  acc.w = fmaf(w, x.w, acc.w);
+}
+
+// SSPI map phase: sliced-ELL sparse operator (interpolation.py:188-195)
+struct SellPhase {
+  SellMap mp;
+  static size_t smem(const SellMap& m, int) { return (size_t)((m.J + 31) / 32 + 1) * 4; }
+  __device__ __forceinline__ const SellMap& out() const { return mp; }
+  __device__ __forceinline__ void setup(void* extra) const {
+    int* s_choff = reinterpret_cast<int*>(extra);
+    const int nch = (int)((mp.J + 31) / 32);
+    for (int i = threadIdx.x; i <= nch; i += blockDim.x) s_choff[i] = mp.chunk_off[i];
+  }
+  __device__ __forceinline__ void prepare(const float4*, void*, int, int) const {}
+  __device__ __forceinline__ void candidates(const float4* xs4, const void* extra, int64_t g, int64_t F, int wid,
+                                             int lane, unsigned long long (&best)[4]) const {
+    const int* s_choff = reinterpret_cast<const int*>(extra);
+    const int64_t J = mp.J;
+    const int nch = (int)((J + 31) / 32);
     // two chunks per warp at a time, all their entries loaded before any is used (the
     // operator streams from L2: issue every load of both chunks, then do the FMAs)
     for (int c = wid; c < nch; c += 2 * kWarps) {
@@ -477,41 +450,128 @@ frontend_sspi_kernel(const WarpParams prm, const SellMap mp) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int t = 0; t < kMapW; ++t) {
-            const float4 x = xs4[col[h][t]];
-            acc[h].x = fmaf(wv[h][t], x.x, acc[h].x);
-            acc[h].y = fmaf(wv[h][t], x.y, acc[h].y);
-            acc[h].z = fmaf(wv[h][t], x.z, acc[h].z);
-            acc[h].w = fmaf(wv[h][t], x.w, acc[h].w);
-          }
+          for (int t = 0; t < kMapW; ++t) fma4(acc[h], wv[h][t], xs4[col[h][t]]);
       } else {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           const int e0 = h ? eb : ea, n = h ? nb : na;
 #pragma unroll 4
-          for (int e = e0; e < e0 + n; ++e) {
-            const float w = __ldg(mp.vals + (int64_t)e * 32 + lane);
-            const float4 x = xs4[__ldg(mp.cols + (int64_t)e * 32 + lane)];
-            acc[h].x = fmaf(w, x.x, acc[h].x);
-            acc[h].y = fmaf(w, x.y, acc[h].y);
-            acc[h].z = fmaf(w, x.z, acc[h].z);
-            acc[h].w = fmaf(w, x.w, acc[h].w);
-          }
+          for (int e = e0; e < e0 + n; ++e)
+            fma4(acc[h], __ldg(mp.vals + (int64_t)e * 32 + lane), xs4[__ldg(mp.cols + (int64_t)e * 32 + lane)]);
         }
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t i = (int64_t)(h ? cb : c) * 32 + lane;
-        if (i < J) {
-          const float a[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
-#pragma unroll
-          for (int fr = 0; fr < 4; ++fr) {
-            if (mp.z && g * 4 + fr < prm.F) __stcs(mp.z + (g * 4 + fr) * J + i, a[fr]);
-            best[fr] = key_max(best[fr], make_key(a[fr], (uint32_t)i));
-          }
-        }
-      }
+      emit4(acc[0], (int64_t)c * 32 + lane, J, g, F, mp.z, best);
+      emit4(acc[1], (int64_t)cb * 32 + lane, J, g, F, mp.z, best);
     }
+  }
+};
+
+// SLRI map phase: z = tall (fat xi) (interpolation.py:178-185); y [R][4 frames] in shared memory
+struct SlriPhase {
+  SlriMap mp;
+  static size_t smem(const SlriMap& m, int) { return (size_t)m.R * 16; }
+  __device__ __forceinline__ const SlriMap& out() const { return mp; }
+  __device__ __forceinline__ void setup(void*) const {}
+  __device__ __forceinline__ void prepare(const float4* xs4, void* extra, int wid, int lane) const {
+    float4* ys = reinterpret_cast<float4*>(extra);
+    for (int r = wid; r < mp.R; r += kWarps) {        // y[r] = fat[r] . xi for the 4 frames
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* fr = mp.fat + (int64_t)r * mp.S;
+      for (int s = lane; s < mp.S; s += 32) fma4(acc, __ldg(fr + s), xs4[s]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+      }
+      if (lane == 0) ys[r] = acc;
+    }
+  }
+  __device__ __forceinline__ void candidates(const float4*, const void* extra, int64_t g, int64_t F, int wid,
+                                             int lane, unsigned long long (&best)[4]) const {
+    const float4* ys = reinterpret_cast<const float4*>(extra);
+    const int64_t J = mp.J;
+    for (int64_t c = wid; c * 32 < J; c += kWarps) {
+      const int64_t i = c * 32 + lane;
+      const float* tc = mp.tallT + (i < J ? i : 0);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int r = 0;
+      for (; r + 8 <= mp.R; r += 8) {                // 8 loads in flight, then 8 x 4 FMAs
+        float t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = __ldg(tc + (int64_t)(r + u) * J);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) fma4(acc, t[u], ys[r + u]);
+      }
+      for (; r < mp.R; ++r) fma4(acc, __ldg(tc + (int64_t)r * J), ys[r]);
+      emit4(acc, i, J, g, F, mp.z, best);
+    }
+  }
+};
+
+// Fused chain for latency-scale batches (SURVEY 8(f) #1): samples -> spectra -> PHAT ->
+// pruned inverse FFT -> map -> per-frame argmax in ONE kernel.  A CTA's 4 warps each run
+// one frame's frontend (the warp-per-frame code above) with the TD-GCC samples kept in
+// shared memory as xs[S][4] (frame fastest); then the 4 warps evaluate the map for all 4
+// frames at once (one float4 shared load feeds 4 FMAs): the SSPI sliced-ELL operator or
+// the SLRI factors, read coalesced through L1 / L2.  z is written once; one CTA owns its
+// frames, so the argmax index is written directly (no key reset, no atomics, no decode).
+template <int LP, class Phase>
+__global__ void __launch_bounds__(kWarps * 32)
+frontend_map_kernel(const WarpParams prm, const Phase ph) {
+  using G = Geo<LP>;
+  constexpr int L = G::L, K = G::K;
+  constexpr int Kp1 = K + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
+  int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
+  int* s_counts = s_pairs + 2 * prm.P;                                  // [P]
+  int* s_off = s_counts + prm.P;                                        // [P+1]
+  const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
+  const int M = prm.M, P = prm.P, S = prm.S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t frame_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
+  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * frame_bytes);  // [M][K+1]
+  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
+  float* xs = reinterpret_cast<float*>(smem_raw + head + kWarps * frame_bytes);    // [S][4]
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(xs + 4 * (size_t)S);   // [4 warps][4]
+  void* extra = s_keys + 16;                                                                // phase data
+  float2* xp = work + (lane / LP) * G::XP;
+
+  for (int e = threadIdx.x; e < 32 * LP; e += blockDim.x) {
+    const int k2 = e / LP, l = e % LP;
+    float sn, cs;
+    sincospif(2.0f * (float)(k2 * l) / (float)L, &sn, &cs);
+    twT[e] = make_float2(cs, -sn);
+  }
+  for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) s_pairs[i] = prm.pairs[i];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) s_counts[i] = prm.counts[i];
+  for (int i = threadIdx.x; i <= P; i += blockDim.x) s_off[i] = prm.offsets[i];
+  ph.setup(extra);
+  __syncthreads();
+
+  const float4* xs4 = reinterpret_cast<const float4*>(xs);
+  const int64_t groups = (prm.F + 3) / 4;
+  const auto& out = ph.out();
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    const int64_t f = g * 4 + wid;
+    if (f < prm.F) {
+      const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
+      float energy = forward_frame<LP, 1>(prm, start, spec, work, xp, twT, lane, 0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+      const float floor = (prm.weighting && prm.floor_mode == 0) ? prm.floor_value * energy : prm.floor_value;
+      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, Phat(prm.weighting, floor), lane, 0,
+                           SmemXi{xs, wid});
+    } else {
+      for (int s = lane; s < S; s += 32) xs[s * 4 + wid] = 0.f;
+    }
+    __syncthreads();                                  // xs of the CTA's 4 frames complete
+    ph.prepare(xs4, extra, wid, lane);
+    __syncthreads();
+    unsigned long long best[4] = {0ull, 0ull, 0ull, 0ull};
+    ph.candidates(xs4, extra, g, prm.F, wid, lane, best);
 #pragma unroll
     for (int fr = 0; fr < 4; ++fr) best[fr] = warp_key_max(best[fr]);
     if (lane == 0) {
@@ -523,22 +583,22 @@ frontend_sspi_kernel(const WarpParams prm, const SellMap mp) {
       unsigned long long k = s_keys[lane];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) k = key_max(k, s_keys[w * 4 + lane]);
-      if (mp.keys) mp.keys[g * 4 + lane] = k;
-      if (mp.index) mp.index[g * 4 + lane] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+      if (out.keys) out.keys[g * 4 + lane] = k;
+      if (out.index) out.index[g * 4 + lane] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
     }
   }
 }
 
-template <int LP>
-static int launch_sspi(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what) {
+template <int LP, class Phase, class Map>
+static int launch_fused(const WarpParams& wp, const Map& mp, cudaStream_t st, const char* what) {
   using G = Geo<LP>;
   const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1) * 4) + 15) & ~(size_t)15;
   const size_t frame_bytes = ((size_t)wp.M * (G::K + 1) + G::WORK) * sizeof(float2);
-  const size_t smem = head + kWarps * frame_bytes + (size_t)wp.S * 16 + 16 * 8 + (size_t)((mp.J + 31) / 32 + 1) * 4;
+  const size_t smem = head + kWarps * frame_bytes + (size_t)wp.S * 16 + 16 * 8 + Phase::smem(mp, wp.S);
   SRPGPU_CHECK_ARG(smem <= 227 * 1024, SRPGPU_ERR_UNSUPPORTED,
                    "%s: %d channels x %d samples per frame and %d TD-GCC samples need %zu B of shared memory",
                    what, wp.M, wp.L, wp.S, smem);
-  auto kern = frontend_sspi_kernel<LP>;
+  auto kern = frontend_map_kernel<LP, Phase>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("%s: cannot reserve %zu B shared memory", what, smem);
     return SRPGPU_ERR_LAUNCH;
@@ -548,7 +608,7 @@ static int launch_sspi(const WarpParams& wp, const SellMap& mp, cudaStream_t st,
   if (per_sm < 1) per_sm = 1;
   const int64_t grid = std::min<int64_t>((wp.F + 3) / 4, (int64_t)num_sms() * per_sm);
   if (grid <= 0) return SRPGPU_OK;
-  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp, mp);
+  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp, Phase{mp});
   SRPGPU_CHECK_LAUNCH(what);
   return SRPGPU_OK;
 }
@@ -592,9 +652,20 @@ static int by_len(const WarpParams& wp, cudaStream_t st, const char* what) {
 // a negative status on error.
 int frontend_sspi_launch(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what) {
   switch (wp.L) {
-    case 256: return wf::launch_sspi<8>(wp, mp, st, what);
-    case 512: return wf::launch_sspi<16>(wp, mp, st, what);
-    case 1024: return wf::launch_sspi<32>(wp, mp, st, what);
+    case 256: return wf::launch_fused<8, wf::SellPhase>(wp, mp, st, what);
+    case 512: return wf::launch_fused<16, wf::SellPhase>(wp, mp, st, what);
+    case 1024: return wf::launch_fused<32, wf::SellPhase>(wp, mp, st, what);
+    default:
+      set_error("%s: the fused chain needs a frame length of 256, 512 or 1024 (got %d)", what, wp.L);
+      return SRPGPU_ERR_UNSUPPORTED;
+  }
+}
+
+int frontend_slri_launch(const WarpParams& wp, const SlriMap& mp, cudaStream_t st, const char* what) {
+  switch (wp.L) {
+    case 256: return wf::launch_fused<8, wf::SlriPhase>(wp, mp, st, what);
+    case 512: return wf::launch_fused<16, wf::SlriPhase>(wp, mp, st, what);
+    case 1024: return wf::launch_fused<32, wf::SlriPhase>(wp, mp, st, what);
     default:
       set_error("%s: the fused chain needs a frame length of 256, 512 or 1024 (got %d)", what, wp.L);
       return SRPGPU_ERR_UNSUPPORTED;

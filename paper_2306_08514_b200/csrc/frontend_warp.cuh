@@ -85,8 +85,20 @@ struct SellMap {
   uint64_t* keys;            // [F] packed argmax keys or null
 };
 
-// frontend + SSPI map + argmax in one launch (frame lengths 256 / 512 / 1024).
+// SLRI factors + outputs of the fused frames -> SLRI map chain.
+struct SlriMap {
+  const float* fat;          // [R][S]
+  const float* tallT;        // [R][J] (tall transposed: candidates contiguous)
+  int32_t R, S;
+  int64_t J;
+  float* z;                  // [F][J] or null
+  int64_t* index;            // [F] argmax index or null
+  uint64_t* keys;            // [F] packed argmax keys or null
+};
+
+// frontend + SSPI / SLRI map + argmax in one launch (frame lengths 256 / 512 / 1024).
 int frontend_sspi_launch(const WarpParams& wp, const SellMap& mp, cudaStream_t st, const char* what);
+int frontend_slri_launch(const WarpParams& wp, const SlriMap& mp, cudaStream_t st, const char* what);
 
 // 0: launched; 1: shape not covered (use the block kernel); < 0: error status.
 int frontend_warp_launch(const WarpParams& wp, int out, cudaStream_t st, const char* what);

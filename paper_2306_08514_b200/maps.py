@@ -833,26 +833,36 @@ def sell_from_sparse(sp) -> SellOperator:
 def fused_eligible(sp, frame, spec, frames: int, num_channels: int) -> bool:
     """Whether frames_to_sspi_map takes this operator / frame shape / batch (the pipeline's
     choice for latency-scale batches: cfg1 / cfg2)."""
-    if not hasattr(sp, "row_splits") or frame.frame_len not in FUSED_FRAME_LENS:
-        return False
-    s_tot = int(spec_offsets(spec)[-1])
-    if s_tot > 4096 or int(sp.num_cols) != s_tot or frames > FUSED_MAX_FRAMES_PER_SM * dev.num_sms():
+    if not hasattr(sp, "row_splits") or int(sp.num_cols) != int(spec_offsets(spec)[-1]):
         return False
     nnz = np.diff(np.asarray(sp.row_splits))
     if nnz.size == 0 or int(nnz.max()) > FUSED_MAX_NNZ:
         return False
+    return _fused_shape_ok(frame, spec, frames, num_channels, 4 * ((nnz.size + 31) // 32 + 1))
+
+
+def _fused_shape_ok(frame, spec, frames: int, num_channels: int, extra_smem: int) -> bool:
+    if frame.frame_len not in FUSED_FRAME_LENS or frames > FUSED_MAX_FRAMES_PER_SM * dev.num_sms():
+        return False
+    s_tot = int(spec_offsets(spec)[-1])
+    if s_tot > 4096:
+        return False
     k = frame.frame_len // 2
     lp = frame.frame_len // 32
-    smem = 4 * ((num_channels * (k + 1) + (32 // lp) * 32 * (lp + 1)) * 8) + 16 * s_tot + 8 * 1024
+    smem = 4 * ((num_channels * (k + 1) + (32 // lp) * 32 * (lp + 1)) * 8) + 16 * s_tot + 8 * 1024 + extra_smem
     return smem <= 220 * 1024
 
 
-def frames_to_sspi_map(sp, samples, frame, pairs, spec, frames=None, weighting: str = "phat", floor=None,
-                       *, argmax: bool = True, out_map: bool = True):
-    """The SSPI chain in one kernel: stft_frame -> fd_gcc -> td_gcc_samples -> sspi_map ->
-    locate over a range of frames (frontend.py:89-160, sampling.py:106-134,
-    interpolation.py:188-195, srp.py:74-80).  The TD-GCC samples stay in shared memory.
-    Returns z (F, J) (None without out_map) and, with argmax, the per-frame argmax (F,)."""
+def fused_slri_eligible(lr, frame, spec, frames: int, num_channels: int) -> bool:
+    """Whether frames_to_slri_map takes this factorization / frame shape / batch."""
+    fat = np.asarray(lr.fat)
+    if fat.ndim != 2 or fat.shape[1] != int(spec_offsets(spec)[-1]):
+        return False
+    return _fused_shape_ok(frame, spec, frames, num_channels, 16 * fat.shape[0])
+
+
+def _fused_call(name, samples, frame, pairs, spec, frames, weighting, floor, num_cols, num_rows, op_args,
+                argmax, out_map):
     from . import frontend as fe
     from .sampling import _spec_device
     x = fe._signal(samples)
@@ -861,21 +871,43 @@ def frames_to_sspi_map(sp, samples, frame, pairs, spec, frames=None, weighting: 
     if spec.num_pairs != pairs.num_pairs or spec.half_len != frame.half_len:
         raise DimensionError("sample spec does not match the pairs / frame")
     s_tot = int(spec_offsets(spec)[-1])
-    if int(sp.num_cols) != s_tot:
-        raise DimensionError(f"operator with {int(sp.num_cols)} columns does not match {s_tot} samples")
+    if num_cols != s_tot:
+        raise DimensionError(f"operator with {num_cols} columns does not match {s_tot} samples")
     first, count, batched = fe._frame_range(frames, fe.num_frames(frame, x.shape[1]))
     fe._check_range(frame, first, count, x.shape[1])
     w, mode, fval = fe._floor_args(weighting, floor)
     counts, offsets = _spec_device(spec)
-    op = sell_from_sparse(sp)
-    z = torch.empty((count, op.num_rows), dtype=torch.float32, device=x.device) if out_map else None
+    z = torch.empty((count, num_rows), dtype=torch.float32, device=x.device) if out_map else None
     idx = torch.empty(count, dtype=torch.int64, device=x.device) if argmax else None
-    nat.call("srpgpu_frames_to_sspi_map", dev.ptr(x), x.shape[0], x.shape[1], x.shape[1],
-             dev.ptr(fe._window_device(frame)), frame.frame_len, frame.hop, first, count,
-             dev.ptr(fe._pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts), dev.ptr(offsets),
-             s_tot, dev.ptr(op.cols), dev.ptr(op.vals), dev.ptr(op.chunk_off), op.num_rows, dev.ptr(z),
-             dev.ptr(idx), None, dev.stream_ptr())
+    nat.call(name, dev.ptr(x), x.shape[0], x.shape[1], x.shape[1], dev.ptr(fe._window_device(frame)),
+             frame.frame_len, frame.hop, first, count, dev.ptr(fe._pairs_device(pairs)), pairs.num_pairs, w, mode,
+             fval, dev.ptr(counts), dev.ptr(offsets), s_tot, *op_args, num_rows, dev.ptr(z), dev.ptr(idx), None,
+             dev.stream_ptr())
     zz = None if z is None else (z if batched else z[0])
     if not argmax:
         return zz
     return zz, (idx if batched else idx[0])
+
+
+def frames_to_slri_map(lr, samples, frame, pairs, spec, frames=None, weighting: str = "phat", floor=None,
+                       *, argmax: bool = True, out_map: bool = True):
+    """The SLRI chain in one kernel: stft_frame -> fd_gcc -> td_gcc_samples -> slri_map ->
+    locate (interpolation.py:178-185 for the map): y = fat . xi per frame in shared
+    memory, z = tall . y, fp32.  Returns z (F, J) (None without out_map) and the argmax."""
+    d_fat, d_tall = _slri_device(lr)
+    tall_t = dev.CACHE.get(lr, "slri_tall_t", lambda: d_tall.t().contiguous())
+    r, j = d_fat.shape[0], d_tall.shape[0]
+    return _fused_call("srpgpu_frames_to_slri_map", samples, frame, pairs, spec, frames, weighting, floor,
+                       int(d_fat.shape[1]), j, (dev.ptr(d_fat), dev.ptr(tall_t), r), argmax, out_map)
+
+
+def frames_to_sspi_map(sp, samples, frame, pairs, spec, frames=None, weighting: str = "phat", floor=None,
+                       *, argmax: bool = True, out_map: bool = True):
+    """The SSPI chain in one kernel: stft_frame -> fd_gcc -> td_gcc_samples -> sspi_map ->
+    locate over a range of frames (frontend.py:89-160, sampling.py:106-134,
+    interpolation.py:188-195, srp.py:74-80).  The TD-GCC samples stay in shared memory.
+    Returns z (F, J) (None without out_map) and, with argmax, the per-frame argmax (F,)."""
+    op = sell_from_sparse(sp)
+    return _fused_call("srpgpu_frames_to_sspi_map", samples, frame, pairs, spec, frames, weighting, floor,
+                       op.num_cols, op.num_rows, (dev.ptr(op.cols), dev.ptr(op.vals), dev.ptr(op.chunk_off)),
+                       argmax, out_map)

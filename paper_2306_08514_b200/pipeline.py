@@ -3,8 +3,8 @@
 The per-frame reference loop (cli.py:241-258: stft_frame -> fd_gcc ->
 evaluate_map -> locate) becomes one graph replay per batch of frames:
 
-    sspi (latency-scale batches, small sparse rows): frames_to_sspi_map -- the whole chain,
-                       argmax included, in one kernel
+    sspi / slri (latency-scale batches; sspi with short sparse rows): frames_to_sspi_map /
+                       frames_to_slri_map -- the whole chain, argmax included, in one kernel
     sspi / si / slri :  frames_to_samples (1 fused kernel) -> map kernel(s) with fused argmax
     lr / conv        :  gcc_frames (1 fused kernel)        -> map kernel(s) with fused argmax
 
@@ -61,7 +61,8 @@ class MapPipeline:
         v = self.variant
         if self.uses_fused_chain():
             # latency-scale batches: the whole chain in one kernel (xi never leaves shared memory)
-            return maps.frames_to_sspi_map(self.op, self.input, self.frame, self.pairs, self.spec, rng,
+            fused = maps.frames_to_sspi_map if v == "sspi" else maps.frames_to_slri_map
+            return fused(self.op, self.input, self.frame, self.pairs, self.spec, rng,
                                            self.weighting, self.floor, argmax=True, out_map=self.out_map)
         if v in ("sspi", "si", "slri"):
             eng = maps.map_engine(v, self.op, self.engine, self.frames)
@@ -80,15 +81,22 @@ class MapPipeline:
                                   out_map=self.out_map)
 
     def uses_fused_chain(self) -> bool:
-        """sspi on latency-scale batches with short sparse rows: frames_to_sspi_map."""
-        if self.variant != "sspi" or self.engine not in ("auto", "fused"):
+        """Latency-scale sspi / slri batches: the whole chain in one kernel
+        (frames_to_sspi_map for short sparse rows, frames_to_slri_map)."""
+        if self.variant not in ("sspi", "slri") or self.engine not in ("auto", "fused"):
             return False
-        ok = maps.fused_eligible(self.op, self.frame, self.spec, self.frames, self.input.shape[0])
+        m = self.input.shape[0]
+        if self.variant == "sspi":
+            ok = maps.fused_eligible(self.op, self.frame, self.spec, self.frames, m)
+            auto = ok and maps.map_engine("sspi", self.op, "auto", self.frames) == "band"
+        else:
+            ok = maps.fused_slri_eligible(self.op, self.frame, self.spec, self.frames, m)
+            auto = ok and self.frames * np.asarray(self.op.tall).shape[0] < maps.LOWRANK_TC_MIN_OUTPUTS
         if self.engine == "fused":
             if not ok:
-                raise ValueError("the fused SSPI chain does not take this operator / frame shape / batch")
+                raise ValueError(f"the fused {self.variant} chain does not take this operator / frame shape / batch")
             return True
-        return ok and maps.map_engine("sspi", self.op, "auto", self.frames) == "band"
+        return auto
 
     def _run_eager(self):
         return self._chain()

@@ -161,6 +161,29 @@ def test_fused_sspi_chain(golden_scene):
         s.maps.frames_to_sspi_map(sparse_from_golden(g, keep_tags(g)[0]), x[:-1], frame, pairs, spec)
 
 
+def test_fused_slri_chain(golden_scene):
+    """frames_to_slri_map (frontend + fat.xi + tall.y + argmax in one kernel) against the
+    reference SLRI maps and the unfused chain; the fused pipeline matches its own eager run."""
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, range(F))
+    for r in g["ranks"]:
+        lr = s.LowRankInterp(g[f"slri_{r}_tall"], g[f"slri_{r}_fat"], np.zeros(r))
+        z, idx = s.maps.frames_to_slri_map(lr, x, frame, pairs, spec, range(F))
+        assert_map_close(z, g[f"z_slri_{r}"])
+        assert_argmax_agrees(idx, g[f"z_slri_{r}"])
+        zu, iu = s.slri_map(lr, xi, argmax=True, engine="simt")
+        assert O.normalized_max_error(np_(z), np_(zu)).max() < 1e-5
+        zo, io = s.maps.frames_to_slri_map(lr, x, frame, pairs, spec, range(F), out_map=False)
+        assert zo is None and torch.equal(io, idx)
+    pipe = MapPipeline("slri", lr, frame, pairs, spec, frames=F, engine="fused")
+    zp, ip = pipe.run(x)
+    assert torch.equal(zp, z) and torch.equal(ip, idx)
+
+
 def test_fused_sspi_pipeline(golden_scene):
     """MapPipeline engine 'fused' (one kernel per replay) matches its eager run and the band chain."""
     from paper_2306_08514_b200.pipeline import MapPipeline
