@@ -17,7 +17,7 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 
 
 def key_of(name: str, variant: str):
-    if "frontend_sspi" in name:
+    if "frontend_map_kernel" in name or "frontend_sspi" in name:
         return "fused"
     if "untile" in name:
         return f"{variant}_untile"

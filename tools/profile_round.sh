@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file $out/${tag}_launches_cfg2_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
   > $out/${tag}_launches_ncu.log 2>&1
 echo "launches rc=$?"
-full cfg2_sspi cfg2 sspi "frontend_sspi" 1000 1 2 fused
+full cfg2_sspi cfg2 sspi "frontend_map" 1000 1 2 fused
 full cfg3_sspi cfg3 sspi "frontend|sspi|interp_tc" 10000
 full cfg3_slri cfg3 slri "frontend|gemm|splitk|interp_tc|split_bf16" 10000 5 5
 full cfg3_conv cfg3 conv "frontend|conv_gen" 10000
