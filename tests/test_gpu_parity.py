@@ -184,6 +184,26 @@ def test_fused_slri_chain(golden_scene):
     assert torch.equal(zp, z) and torch.equal(ip, idx)
 
 
+@pytest.mark.parametrize("weighting,floor", [("none", None), ("phat", 0.5), ("phat", 0.0)])
+def test_fused_chains_weighting_and_floor(golden_scene, weighting, floor):
+    """The fused chains honour fd_gcc's weighting / floor arguments (frontend.py:127-160)
+    exactly as the unfused frontend + map does."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    F = g["psi"].shape[0]
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, range(F), weighting=weighting, floor=floor)
+    sp = sparse_from_golden(g, [t for t in keep_tags(g) if t != "all"][0])
+    z, idx = s.maps.frames_to_sspi_map(sp, x, frame, pairs, spec, range(F), weighting=weighting, floor=floor)
+    zu, iu = s.sspi_map(sp, xi, argmax=True, engine="band")
+    assert O.normalized_max_error(np_(z), np_(zu)).max() < 1e-5
+    r = g["ranks"][0]
+    lr = s.LowRankInterp(g[f"slri_{r}_tall"], g[f"slri_{r}_fat"], np.zeros(r))
+    z2, i2 = s.maps.frames_to_slri_map(lr, x, frame, pairs, spec, range(F), weighting=weighting, floor=floor)
+    zu2, iu2 = s.slri_map(lr, xi, argmax=True, engine="simt")
+    assert O.normalized_max_error(np_(z2), np_(zu2)).max() < 1e-5
+
+
 def test_fused_sspi_pipeline(golden_scene):
     """MapPipeline engine 'fused' (one kernel per replay) matches its eager run and the band chain."""
     from paper_2306_08514_b200.pipeline import MapPipeline
