@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU per step (default: config)")
     ap.add_argument("--variant", default="sspi", choices=["sspi", "slri", "lr", "conv", "conv_h", "si"])
     ap.add_argument("--nnz", default="2jp", help="SSPI sparsity token (reference `xjp` semantics)")
+    ap.add_argument("--fit", default="global", choices=["global", "fixed"],
+                    help="SSPI fit where the dense operator is infeasible (cfg4): the reference's global "
+                         "top-Q rule, streamed (global), or nnz per (candidate, pair) (fixed)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
     ap.add_argument("--engine", default="auto", choices=["auto", "fused", "tc", "tile", "band"],
                     help="SSPI / SI map engine (maps.interp_engine)")
@@ -180,7 +183,11 @@ def fit_operator(wl, variant, args):
     import paper_2306_08514_b200 as s
     dense_bytes = 8 * wl.grid.num_points * wl.spec.total_samples
     if variant == "sspi" and dense_bytes > DENSE_LAMBDA_CAP:
-        # cfg4: Lambda is 18.7 GB -> fixed nnz per (candidate, pair), built pair by pair
+        # cfg4: Lambda is 18.7 GB -> never built dense
+        if args.fit == "global":   # the reference's global top-Q (truncate_sparse), two streamed passes
+            keep = s.resolve_sparsity(args.nnz, wl.grid.num_points, wl.pairs.num_pairs,
+                                      wl.grid.num_points * wl.spec.total_samples)
+            return s.truncate_sparse_streamed(wl.tdoa, wl.spec, wl.frame, keep)
         nnz = int(round(float(args.nnz[:-2]))) if args.nnz.endswith("jp") else int(args.nnz)
         return s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, max(1, nnz))
     if variant in ("si", "slri", "lr") and dense_bytes > DENSE_LAMBDA_CAP:
@@ -475,7 +482,7 @@ def run_ours(args):
                        "candidates": wl.grid.num_points, "pairs": wl.pairs.num_pairs,
                        "frame_len": wl.frame.frame_len, "total_lags": wl.spec.total_samples,
                        "variant": args.variant,
-                       "operator": ((args.nnz if not hasattr(op, "kept") else
+                       "operator": ((f"{args.nnz} (global top-Q, the reference rule)" if not hasattr(op, "kept") else
                                      f"{int(op.values.shape[2])} nnz per (candidate, pair)")
                                     if args.variant == "sspi" else
                                     f"rank {args.rank_r}" if args.variant in ("lr", "slri") else "dense"),

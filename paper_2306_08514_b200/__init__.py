@@ -29,7 +29,7 @@ from .operators import (DEFAULT_MATRIX_CAP_BYTES, FixedNnzInterp, InterpMatrix, 
                         SparseInterp, SrpMatrix, build_interp_matrix, build_srp_matrix,
                         check_capacity, low_rank_interp_from_svd, low_rank_srp_from_svd,
                         resolve_sparsity, srp_matrix_shape, truncate_low_rank, truncate_sparse,
-                        truncate_sparse_fixed, truncate_srp_matrix)
+                        truncate_sparse_fixed, truncate_sparse_streamed, truncate_srp_matrix)
 from .sampling import (SampleSpec, TdGccSamples, frames_to_samples, sample_spec,
                        spectra_to_samples, td_gcc_samples)
 from .scene import (CandidateGrid, MicrophoneArray, PairTable, TdoaTable, build_ff_grid,

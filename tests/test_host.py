@@ -220,3 +220,18 @@ def test_fixed_nnz_from_tdoa_matches_dense_fit(golden_scene):
         assert_array_equal(cols, a.col_indices)
         assert_array_equal(splits, a.row_splits)
         assert_array_equal(vals, a.values.astype(np.float32))
+
+
+def test_streamed_global_fit_matches_reference(golden_scene):
+    """truncate_sparse_streamed (row-blocked, two-pass histogram selection, never the dense
+    operator) reproduces the reference's global top-Q CSR bit for bit (interpolation.py:155-175)."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    for tag in keep_tags(g):
+        ref = sparse_from_golden(g, tag)
+        got = s.truncate_sparse_streamed(tdoa, spec, frame, int(ref.values.shape[0]), block_bytes=1 << 14)
+        assert np.array_equal(got.col_indices, ref.col_indices)
+        assert np.array_equal(got.row_splits, ref.row_splits)
+        assert np.array_equal(got.values, ref.values)
+    with pytest.raises(ValueError):
+        s.truncate_sparse_streamed(tdoa, spec, frame, -1)
