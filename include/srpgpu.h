@@ -154,6 +154,18 @@ int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames, int32_t 
                               const int32_t* counts, const int32_t* offsets, int32_t total_samples,
                               float* samples_out, int64_t samples_ld, srpgpu_stream_t stream);
 
+/* ---- scene synthesis (srpmap/simulate.py) -------------------------------- */
+
+/* synthesize (simulate.py:232-265), room-response part: for every microphone m and image
+ * source i (num_images per microphone, image order shared by all microphones)
+ *   out[m][n] += gain[m][i] * sum_t taps[m][i][t] * dry[n - start[m][i] - t]   (t < 64)
+ * accumulated in image order into direct [M][N] (is_direct[i] != 0) or reverb [M][N];
+ * float64 throughout.  start = floor(delay) - 31, taps = the 64-tap fractional-delay
+ * kernel, gain = image gain / distance, all computed on the host. */
+int srpgpu_render_images(const double* dry, int64_t num_samples, int32_t num_mics, int32_t num_images,
+                         const int64_t* start, const double* gain, const double* taps,
+                         const int32_t* is_direct, double* direct, double* reverb, srpgpu_stream_t stream);
+
 /* ---- maps (srpmap/interpolation.py, lowrank.py, srp.py) ------------------- */
 
 /* sspi_map (interpolation.py:188-195) and, with a keep-all operator, si_map

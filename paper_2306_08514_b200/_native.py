@@ -43,6 +43,7 @@ SIGNATURES = {
                                   _F64, _P, _P, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_spectra_to_samples": [_P, _I64, _I32, _I32, _P, _I32, _I32, _I32, _F64, _P, _P, _I32,
                                   _P, _I64, _P],
+    "srpgpu_render_images": [_P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P],
     "srpgpu_sspi_map": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _I64, _I64, _P, _P, _P],
     "srpgpu_transpose": [_P, _I64, _I64, _I64, _P, _I64, _P],
     "srpgpu_interp_map_tc": [_P, _I64, _P, _I64, _I32, _P, _P, _P],
