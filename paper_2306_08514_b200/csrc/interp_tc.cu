@@ -32,10 +32,11 @@ constexpr int IM = 128;   // frames per tile (TMEM lanes)
 constexpr int IN = 256;   // candidates per tile (TMEM columns per accumulator)
 constexpr int IK = 64;    // bf16 per k-block = 128 bytes = one swizzle atom row
 constexpr int UK = 16;    // kind::f16 MMA K
-constexpr int NS = 2;     // operand stages
-constexpr int kEpi = 4;   // epilogue warps
-constexpr int kThreads = 32 * (2 + kEpi);
-
+// Two configurations: <2 stages, 4 epilogue warps> for operators with several k-blocks
+// (SSPI / SI: MMA-bound), <1 stage, 8 epilogue warps> for a single k-block (the SLRI / LR
+// candidate products, K = R or 2R: bound by the z write, so the epilogue gets twice the
+// warps -- two per TMEM lane quarter, each draining half of the columns).
+template <int NS, int kEpi>
 struct __align__(1024) Smem {
   uint16_t a[NS][2][IM * IK];        // xi hi / lo, 16 KB per plane
   uint16_t b[NS][2][IN * IK];        // Lambda hi / lo, 32 KB per plane
@@ -52,13 +53,15 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NS, int kEpi>
+__global__ void __launch_bounds__(32 * (2 + kEpi), 1)
 interp_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                  const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                  const __grid_constant__ CUtensorMap mz, int64_t F, int64_t J, int32_t nkb, float* __restrict__ z,
                  int32_t z_tma, unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  Smem<NS, kEpi>& sm =
+      *reinterpret_cast<Smem<NS, kEpi>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (int)((F + IM - 1) / IM);
   const int n_tiles = (int)((J + IN - 1) / IN);
@@ -153,8 +156,10 @@ interp_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       const int64_t f0w = (int64_t)m_blk * IM + q * 32;       // first frame of this warp
       uint32_t best_ob = 0, best_j = 0;
       bool have = false;
+      constexpr int kCpw = (IN / 32) / (kEpi / 4);   // 32-column chunks per epilogue warp
+      const int c_lo = ((warp - 2) / 4) * kCpw;
 #pragma unroll 1
-      for (int c = 0; c < IN / 32; ++c) {
+      for (int c = c_lo; c < c_lo + kCpw; ++c) {
         uint32_t r[32];
         tmem_ld32(lane_base + acc * IN + c * 32, r);
         const int64_t jc = j0 + c * 32;
@@ -366,17 +371,23 @@ extern "C" int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_fram
   if (z_tma && (s = make_map_2d(&mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, z, num_frames, num_candidates,
                                 num_candidates, 32, 32, "interp_map_tc")))
     return s;
-  const size_t smem = sizeof(Smem) + 1024;
-  if (cudaFuncSetAttribute(interp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-    set_error("interp_map_tc: cannot reserve %zu B shared memory", smem);
-    return SRPGPU_ERR_LAUNCH;
-  }
   const int64_t tiles = ((num_frames + IM - 1) / IM) * ((num_candidates + IN - 1) / IN);
   SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "interp_map_tc: too many tiles");
   const int nkb = (cols8 + IK - 1) / IK;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
-  interp_tc_kernel<<<grid, kThreads, smem, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, mz, num_frames, num_candidates, nkb, z,
-                                                 z_tma, reinterpret_cast<unsigned long long*>(keys));
+  auto run = [&](auto kern, size_t smem, int threads) -> int {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      set_error("interp_map_tc: cannot reserve %zu B shared memory", smem);
+      return SRPGPU_ERR_LAUNCH;
+    }
+    kern<<<grid, threads, smem, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, mz, num_frames, num_candidates, nkb, z, z_tma,
+                                      reinterpret_cast<unsigned long long*>(keys));
+    return SRPGPU_OK;
+  };
+  // one k-block (the low-rank candidate products): z-write bound -> 8 epilogue warps
+  s = nkb == 1 ? run(interp_tc_kernel<1, 8>, sizeof(Smem<1, 8>) + 1024, 32 * (2 + 8))
+               : run(interp_tc_kernel<2, 4>, sizeof(Smem<2, 4>) + 1024, 32 * (2 + 4));
+  if (s) return s;
   SRPGPU_CHECK_LAUNCH("interp_map_tc");
   return SRPGPU_OK;
 }
