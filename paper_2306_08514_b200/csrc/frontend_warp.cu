@@ -395,15 +395,36 @@ struct SmemXi {
 
 constexpr int kMapW = 16;   // operator entries per chunk taken by the unrolled (all loads first) path
 
-// one candidate's map values for the CTA's 4 frames: z stores + running argmax keys
-__device__ __forceinline__ void emit4(float4 acc, int64_t i, int64_t J, int64_t g, int64_t F, float* z,
-                                      unsigned long long (&best)[4]) {
+// running per-lane argmax of the CTA's 4 frames: ordered float bits (the packed-key order:
+// largest value, NaN above everything, -0 == +0) and the first candidate reaching it
+struct Best4 {
+  uint32_t ob[4];
+  int32_t idx[4];
+  __device__ __forceinline__ Best4() {
+#pragma unroll
+    for (int fr = 0; fr < 4; ++fr) {
+      ob[fr] = 0u;
+      idx[fr] = -1;
+    }
+  }
+  __device__ __forceinline__ unsigned long long key(int fr) const {
+    return idx[fr] < 0 ? 0ull : ((unsigned long long)ob[fr] << 32) | (0xFFFFFFFFull - (uint32_t)idx[fr]);
+  }
+};
+
+// one candidate's map values for the CTA's 4 frames: z stores + running argmax (a lane's
+// candidates arrive in increasing index order, so strict '>' keeps the first maximum)
+__device__ __forceinline__ void emit4(float4 acc, int64_t i, int64_t J, int64_t g, int64_t F, float* z, Best4& best) {
   if (i >= J) return;
   const float a[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
   for (int fr = 0; fr < 4; ++fr) {
     if (z && g * 4 + fr < F) __stcs(z + (g * 4 + fr) * J + i, a[fr]);
-    best[fr] = key_max(best[fr], make_key(a[fr], (uint32_t)i));
+    const uint32_t ob = ordered_bits(a[fr]);
+    if (best.idx[fr] < 0 || ob > best.ob[fr]) {
+      best.ob[fr] = ob;
+      best.idx[fr] = (int32_t)i;
+    }
   }
 }
 
@@ -426,7 +447,7 @@ struct SellPhase {
   }
   __device__ __forceinline__ void prepare(const float4*, void*, int, int) const {}
   __device__ __forceinline__ void candidates(const float4* xs4, const void* extra, int64_t g, int64_t F, int wid,
-                                             int lane, unsigned long long (&best)[4]) const {
+                                             int lane, Best4& best) const {
     const int* s_choff = reinterpret_cast<const int*>(extra);
     const int64_t J = mp.J;
     const int nch = (int)((J + 31) / 32);
@@ -437,20 +458,33 @@ struct SellPhase {
       const int ea = s_choff[c], na = s_choff[c + 1] - ea;
       const int eb = cb < nch ? s_choff[cb] : 0, nb = cb < nch ? s_choff[cb + 1] - eb : 0;
       float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-      if (na <= kMapW && nb <= kMapW) {
+      const bool has_b = cb < nch;
+      if (na == kMapW && (!has_b || nb == kMapW)) {
+        // chunks padded to kMapW entries on the host: unconditional loads at fixed offsets
+        const uint16_t* ca = mp.cols + (int64_t)ea * 32 + lane;
+        const float* va = mp.vals + (int64_t)ea * 32 + lane;
+        const uint16_t* cbp = mp.cols + (int64_t)eb * 32 + lane;
+        const float* vb = mp.vals + (int64_t)eb * 32 + lane;
         uint32_t col[2][kMapW];
         float wv[2][kMapW];
 #pragma unroll
         for (int t = 0; t < kMapW; ++t) {
-          col[0][t] = t < na ? __ldg(mp.cols + (int64_t)(ea + t) * 32 + lane) : 0u;
-          wv[0][t] = t < na ? __ldg(mp.vals + (int64_t)(ea + t) * 32 + lane) : 0.f;
-          col[1][t] = t < nb ? __ldg(mp.cols + (int64_t)(eb + t) * 32 + lane) : 0u;
-          wv[1][t] = t < nb ? __ldg(mp.vals + (int64_t)(eb + t) * 32 + lane) : 0.f;
+          col[0][t] = __ldg(ca + t * 32);
+          wv[0][t] = __ldg(va + t * 32);
+        }
+        if (has_b) {
+#pragma unroll
+          for (int t = 0; t < kMapW; ++t) {
+            col[1][t] = __ldg(cbp + t * 32);
+            wv[1][t] = __ldg(vb + t * 32);
+          }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int t = 0; t < kMapW; ++t) fma4(acc[0], wv[0][t], xs4[col[0][t]]);
+        if (has_b) {
 #pragma unroll
-          for (int t = 0; t < kMapW; ++t) fma4(acc[h], wv[h][t], xs4[col[h][t]]);
+          for (int t = 0; t < kMapW; ++t) fma4(acc[1], wv[1][t], xs4[col[1][t]]);
+        }
       } else {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
@@ -489,7 +523,7 @@ struct SlriPhase {
     }
   }
   __device__ __forceinline__ void candidates(const float4*, const void* extra, int64_t g, int64_t F, int wid,
-                                             int lane, unsigned long long (&best)[4]) const {
+                                             int lane, Best4& best) const {
     const float4* ys = reinterpret_cast<const float4*>(extra);
     const int64_t J = mp.J;
     for (int64_t c = wid; c * 32 < J; c += kWarps) {
@@ -570,10 +604,11 @@ frontend_map_kernel(const WarpParams prm, const Phase ph) {
     __syncthreads();                                  // xs of the CTA's 4 frames complete
     ph.prepare(xs4, extra, wid, lane);
     __syncthreads();
-    unsigned long long best[4] = {0ull, 0ull, 0ull, 0ull};
-    ph.candidates(xs4, extra, g, prm.F, wid, lane, best);
+    Best4 lane_best;
+    ph.candidates(xs4, extra, g, prm.F, wid, lane, lane_best);
+    unsigned long long best[4];
 #pragma unroll
-    for (int fr = 0; fr < 4; ++fr) best[fr] = warp_key_max(best[fr]);
+    for (int fr = 0; fr < 4; ++fr) best[fr] = warp_key_max(lane_best.key(fr));
     if (lane == 0) {
 #pragma unroll
       for (int fr = 0; fr < 4; ++fr) s_keys[wid * 4 + fr] = best[fr];

@@ -788,6 +788,7 @@ def evaluate_map(kind, op, spec, frame, gcc, path="ifft", **kw):
 # ----------------------------------------------------------------- fused chain (SSPI)
 
 FUSED_MAX_NNZ = 32            # widest sparse row the fused chain takes (its cost grows with nnz)
+FUSED_PAD = 16                # sliced-ELL chunk width of the kernel's unrolled path (kMapW)
 FUSED_MAX_FRAMES_PER_SM = 8   # latency-scale batches only (a warp per frame, one wave)
 FUSED_FRAME_LENS = (256, 512, 1024)
 
@@ -808,6 +809,9 @@ class SellOperator:
         width = np.zeros(nch * 32, dtype=np.int64)
         width[:j] = nnz
         width = width.reshape(nch, 32).max(axis=1)
+        # chunks up to FUSED_PAD entries wide are padded to exactly FUSED_PAD: the kernel then
+        # loads them unconditionally at fixed offsets (frontend_warp.cu kMapW)
+        width = np.where(width <= FUSED_PAD, FUSED_PAD, width)
         off = np.zeros(nch + 1, dtype=np.int64)
         np.cumsum(width, out=off[1:])
         rows = int(off[-1])
