@@ -137,7 +137,8 @@ int srpgpu_frames_to_sspi_map(const float* samples, int32_t num_channels, int64_
 
 /* The SLRI chain in one launch (stft_frame + fd_gcc + td_gcc_samples + slri_map + locate;
  * interpolation.py:178-185): y = fat [R][S] . xi per frame in shared memory, then
- * z = tall . y with the tall factor transposed, tall_t [R][J] (candidates contiguous).
+ * z = tall . y with the tall factor transposed, tall_t [round16(R)][J] (candidates
+ * contiguous; rows R.. zero).
  * Outputs as srpgpu_frames_to_sspi_map; f32 throughout. */
 int srpgpu_frames_to_slri_map(const float* samples, int32_t num_channels, int64_t num_samples,
                               int64_t ld_samples, const float* window, int32_t frame_len, int32_t hop,

@@ -503,11 +503,13 @@ struct SellPhase {
 // SLRI map phase: z = tall (fat xi) (interpolation.py:178-185); y [R][4 frames] in shared memory
 struct SlriPhase {
   SlriMap mp;
-  static size_t smem(const SlriMap& m, int) { return (size_t)m.R * 16; }
+  static size_t smem(const SlriMap& m, int) { return (size_t)((m.R + 15) / 16 * 16) * 16; }
   __device__ __forceinline__ const SlriMap& out() const { return mp; }
   __device__ __forceinline__ void setup(void*) const {}
   __device__ __forceinline__ void prepare(const float4* xs4, void* extra, int wid, int lane) const {
     float4* ys = reinterpret_cast<float4*>(extra);
+    for (int r = mp.R + threadIdx.x; r < (mp.R + 15) / 16 * 16; r += blockDim.x)
+      ys[r] = make_float4(0.f, 0.f, 0.f, 0.f);       // padding rows of tall_t are zero too
     for (int r = wid; r < mp.R; r += kWarps) {        // y[r] = fat[r] . xi for the 4 frames
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       const float* fr = mp.fat + (int64_t)r * mp.S;
@@ -526,20 +528,33 @@ struct SlriPhase {
                                              int lane, Best4& best) const {
     const float4* ys = reinterpret_cast<const float4*>(extra);
     const int64_t J = mp.J;
-    for (int64_t c = wid; c * 32 < J; c += kWarps) {
-      const int64_t i = c * 32 + lane;
-      const float* tc = mp.tallT + (i < J ? i : 0);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      int r = 0;
-      for (; r + 8 <= mp.R; r += 8) {                // 8 loads in flight, then 8 x 4 FMAs
-        float t[8];
+    const int nch = (int)((J + 31) / 32);
+    // two 32-candidate chunks per warp at a time; tall_t has R rounded up to 16 rows (zero
+    // padded on the host), loaded 16 rows x 2 chunks before any FMA
+    for (int c = wid; c < nch; c += 2 * kWarps) {
+      const int cb = c + kWarps;
+      const bool has_b = cb < nch;
+      const int64_t ia = (int64_t)c * 32 + lane, ib = (int64_t)cb * 32 + lane;
+      const float* ta = mp.tallT + (ia < J ? ia : 0);
+      const float* tb = mp.tallT + (has_b && ib < J ? ib : 0);
+      float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+      for (int r0 = 0; r0 < mp.R; r0 += 16) {
+        float t[2][16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = __ldg(tc + (int64_t)(r + u) * J);
+        for (int u = 0; u < 16; ++u) t[0][u] = __ldg(ta + (int64_t)(r0 + u) * J);
+        if (has_b) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) fma4(acc, t[u], ys[r + u]);
+          for (int u = 0; u < 16; ++u) t[1][u] = __ldg(tb + (int64_t)(r0 + u) * J);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) fma4(acc[0], t[0][u], ys[r0 + u]);
+        if (has_b) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) fma4(acc[1], t[1][u], ys[r0 + u]);
+        }
       }
-      for (; r < mp.R; ++r) fma4(acc, __ldg(tc + (int64_t)r * J), ys[r]);
-      emit4(acc, i, J, g, F, mp.z, best);
+      emit4(acc[0], ia, J, g, F, mp.z, best);
+      if (has_b) emit4(acc[1], ib, J, g, F, mp.z, best);
     }
   }
 };

@@ -88,7 +88,7 @@ struct SellMap {
 // SLRI factors + outputs of the fused frames -> SLRI map chain.
 struct SlriMap {
   const float* fat;          // [R][S]
-  const float* tallT;        // [R][J] (tall transposed: candidates contiguous)
+  const float* tallT;        // [round16(R)][J] (tall transposed: candidates contiguous; rows >= R zero)
   int32_t R, S;
   int64_t J;
   float* z;                  // [F][J] or null

@@ -899,7 +899,12 @@ def frames_to_slri_map(lr, samples, frame, pairs, spec, frames=None, weighting: 
     locate (interpolation.py:178-185 for the map): y = fat . xi per frame in shared
     memory, z = tall . y, fp32.  Returns z (F, J) (None without out_map) and the argmax."""
     d_fat, d_tall = _slri_device(lr)
-    tall_t = dev.CACHE.get(lr, "slri_tall_t", lambda: d_tall.t().contiguous())
+    def build_t():
+        r16 = (d_tall.shape[1] + 15) // 16 * 16
+        t = torch.zeros((r16, d_tall.shape[0]), dtype=torch.float32, device=d_tall.device)
+        t[:d_tall.shape[1]] = d_tall.t()
+        return t
+    tall_t = dev.CACHE.get(lr, "slri_tall_t16", build_t)
     r, j = d_fat.shape[0], d_tall.shape[0]
     return _fused_call("srpgpu_frames_to_slri_map", samples, frame, pairs, spec, frames, weighting, floor,
                        int(d_fat.shape[1]), j, (dev.ptr(d_fat), dev.ptr(tall_t), r), argmax, out_map)
