@@ -203,9 +203,11 @@ int srpgpu_interp_map_tc(const void* samples_planes, int64_t num_frames, const v
  * each tile row (ascending, -1 pad; rows 0-127 half 0);
  * num_ctas persistent CTAs take the work units (group of 8 frame tiles, tile, frame tile)
  * round-robin (num_ctas = the SM count).
- * z [F][J] and keys [F] optional; a map is written in tile order into z_tiles
- * [F][num_tiles * 256] (full 32-byte sectors) and gathered back to grid order by
- * tile_pos [J] (= tile * 256 + row of each candidate). */
+ * z [F][J] and keys [F] optional.  With z_tiles the map is written in tile order into
+ * z_tiles [F][num_tiles * 256] (full 32-byte sectors) and gathered back to grid order by
+ * tile_pos [J] (= tile * 256 + row of each candidate); with z_tiles NULL it is written
+ * straight into grid order (no gather pass, but 32-byte sectors shared between tiles are
+ * read-modify-written: 2.3x slower at cfg4). */
 int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, int32_t num_cols,
                                 int64_t planes_ld,
                                 const void* slab_planes, int64_t num_slabs, const int32_t* group_col,

@@ -97,7 +97,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
                  const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int64_t F,
                  int64_t J, int32_t T, const int32_t* __restrict__ group_col, const int32_t* __restrict__ tile_blk,
                  const int32_t* __restrict__ tile_nkb, const int32_t* __restrict__ tile_rows,
-                 float* __restrict__ zt, unsigned long long* __restrict__ keys) {
+                 float* __restrict__ zt, float* __restrict__ zg, unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -237,7 +237,19 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
         tmem_ld32(lane_base + c * 32, rr);
         const int64_t f0 = (int64_t)w.n * GN + c * 32;
         if (f0 >= F || !any) continue;               // warp-uniform (after the aligned load)
-        if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
+        if (zg) {   // grid order: the tile's rows are ascending candidates (runs of neighbours)
+          if (jrow >= 0) {
+            float* zc = zg + f0 * J + jrow;
+            if (f0 + 32 <= F) {
+#pragma unroll
+              for (int t = 0; t < 32; ++t) __stcs(zc + t * J, __uint_as_float(rr[t]));
+            } else {
+#pragma unroll
+              for (int t = 0; t < 32; ++t)
+                if (f0 + t < F) __stcs(zc + t * J, __uint_as_float(rr[t]));
+            }
+          }
+        } else if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
           float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
           if (f0 + 32 <= F) {
 #pragma unroll
@@ -337,8 +349,8 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
                    SRPGPU_ERR_VALUE, "interp_map_gather_tc: operands must be 16-byte aligned");
   SRPGPU_CHECK_ARG(num_frames < (1ll << 31) && num_candidates < (1ll << 31) && num_slabs * GM < (1ll << 31),
                    SRPGPU_ERR_DIMENSION, "interp_map_gather_tc: too large");
-  SRPGPU_CHECK_ARG(!z || (z_tiles && tile_pos), SRPGPU_ERR_VALUE,
-                   "interp_map_gather_tc: a map needs the tile-order scratch [F][num_tiles * 128] and tile_pos");
+  SRPGPU_CHECK_ARG(!z || !z_tiles || tile_pos, SRPGPU_ERR_VALUE,
+                   "interp_map_gather_tc: a tile-order map needs tile_pos");
   cudaStream_t st = as_stream(stream);
   int s = reset_keys(keys, num_frames, st);
   if (s) return s;
@@ -363,9 +375,9 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
   }
   gather_tc_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nkb, tile_rows,
-      z ? z_tiles : nullptr, reinterpret_cast<unsigned long long*>(keys));
+      z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
-  if (z) {
+  if (z && z_tiles) {
     dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
               (unsigned)std::min<int64_t>(num_frames, 65535));
     untile_kernel<<<grid, 256, 0, st>>>(z_tiles, (int64_t)num_tiles * GT, tile_pos, num_candidates, num_frames, z);

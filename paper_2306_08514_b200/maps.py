@@ -372,10 +372,17 @@ def tile_from_sparse(sp, offsets: np.ndarray) -> TileOperator:
                          lambda: TileOperator(sp, offsets, num_rows))
 
 
+# Gathered-window maps straight into grid order (no untile pass): measured 2.3x SLOWER at
+# cfg4 (76 vs 33.5 ms; 166 GB of DRAM reads: the L2 read-modify-writes partial 32-byte
+# sectors shared between tiles), so the tile-order store + untile gather stays the default.
+TILE_GRID_ORDER = False
+
+
 def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
     planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
-    zt = torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device) if out_map else None
+    zt = (torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
+          if out_map and not TILE_GRID_ORDER else None)
     keys = _new_keys(f, argmax)
     nat.call("srpgpu_interp_map_gather_tc", dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes),
              op.num_slabs,
