@@ -489,9 +489,23 @@ struct SellPhase {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           const int e0 = h ? eb : ea, n = h ? nb : na;
+          if (n == 2 * kMapW) {        // chunks padded to 32 entries: one chunk, all loads first
+            const uint16_t* cp = mp.cols + (int64_t)e0 * 32 + lane;
+            const float* vp = mp.vals + (int64_t)e0 * 32 + lane;
+            uint32_t col[2 * kMapW];
+            float wv[2 * kMapW];
+#pragma unroll
+            for (int t = 0; t < 2 * kMapW; ++t) {
+              col[t] = __ldg(cp + t * 32);
+              wv[t] = __ldg(vp + t * 32);
+            }
+#pragma unroll
+            for (int t = 0; t < 2 * kMapW; ++t) fma4(acc[h], wv[t], xs4[col[t]]);
+          } else {
 #pragma unroll 4
-          for (int e = e0; e < e0 + n; ++e)
-            fma4(acc[h], __ldg(mp.vals + (int64_t)e * 32 + lane), xs4[__ldg(mp.cols + (int64_t)e * 32 + lane)]);
+            for (int e = e0; e < e0 + n; ++e)
+              fma4(acc[h], __ldg(mp.vals + (int64_t)e * 32 + lane), xs4[__ldg(mp.cols + (int64_t)e * 32 + lane)]);
+          }
         }
       }
       emit4(acc[0], (int64_t)c * 32 + lane, J, g, F, mp.z, best);

@@ -816,9 +816,10 @@ class SellOperator:
         width = np.zeros(nch * 32, dtype=np.int64)
         width[:j] = nnz
         width = width.reshape(nch, 32).max(axis=1)
-        # chunks up to FUSED_PAD entries wide are padded to exactly FUSED_PAD: the kernel then
-        # loads them unconditionally at fixed offsets (frontend_warp.cu kMapW)
-        width = np.where(width <= FUSED_PAD, FUSED_PAD, width)
+        # chunks up to FUSED_PAD (2 FUSED_PAD) entries wide are padded to exactly FUSED_PAD
+        # (2 FUSED_PAD): the kernel then loads them unconditionally at fixed offsets
+        # (frontend_warp.cu kMapW)
+        width = np.where(width <= FUSED_PAD, FUSED_PAD, np.where(width <= 2 * FUSED_PAD, 2 * FUSED_PAD, width))
         off = np.zeros(nch + 1, dtype=np.int64)
         np.cumsum(width, out=off[1:])
         rows = int(off[-1])

@@ -88,7 +88,7 @@ class MapPipeline:
         m = self.input.shape[0]
         if self.variant == "sspi":
             ok = maps.fused_eligible(self.op, self.frame, self.spec, self.frames, m)
-            auto = ok and maps.map_engine("sspi", self.op, "auto", self.frames) == "band"
+            auto = ok
         else:
             ok = maps.fused_slri_eligible(self.op, self.frame, self.spec, self.frames, m)
             auto = ok and self.frames * np.asarray(self.op.tall).shape[0] < maps.LOWRANK_TC_MIN_OUTPUTS
