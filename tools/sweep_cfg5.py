@@ -129,7 +129,7 @@ def main():
         fit_s = time.perf_counter() - t0
         pipe = pipe_for("sspi", sp, f_main)
         ms = graph_ms(pipe, 10)
-        eng = maps.map_engine("sspi", sp, "auto", f_main)
+        eng = "fused" if pipe.uses_fused_chain() else maps.map_engine("sspi", sp, "auto", f_main)
         row = {"sweep": "nnz", "nnz_per_cand_pair": q, "kept": int(sp.values.shape[0]), "frames": f_main,
                "ms_per_batch": ms, "maps_per_s": f_main / (ms / 1e3), "engine": eng,
                "host_fit_s": fit_s, **errors("sspi", sp, pipe)}
@@ -140,7 +140,8 @@ def main():
         pipe = pipe_for("slri", lr, f_main)
         ms = graph_ms(pipe, 10)
         row = {"sweep": "rank", "rank": r, "frames": f_main, "ms_per_batch": ms,
-               "maps_per_s": f_main / (ms / 1e3), **errors("slri", lr, pipe)}
+               "maps_per_s": f_main / (ms / 1e3), "engine": "fused" if pipe.uses_fused_chain() else "unfused",
+               **errors("slri", lr, pipe)}
         print(json.dumps(row), flush=True)
         del pipe
 
