@@ -278,10 +278,13 @@ int srpgpu_srp_map_simt(const float* gcc, int64_t num_frames, int32_t gcc_len, c
  * row pitches gcc_ld / h2_ld (floats) that are multiples of 4 (16 bytes); the K
  * tail and out-of-range rows are zero-filled by TMA.  kind::tf32 truncates fp32
  * operands, so callers pass TF32-rounded (RNE) operands: srpgpu_round_tf32 or
- * srpgpu_gcc_frames(flags=1). */
+ * srpgpu_gcc_frames(flags=1).  ksplit > 1 splits K into that many slices of whole
+ * 16-k-block chunks (for grids with fewer output tiles than SMs: small batches): the
+ * partial maps go to work [ksplit][F][J] f32 and a second kernel sums them in slice order
+ * and forms the argmax keys; ksplit = 1 needs no work buffer (NULL). */
 int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
-                      const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,
-                      uint64_t* keys, srpgpu_stream_t stream);
+                      const float* h2, int64_t h2_ld, int64_t num_candidates, int32_t ksplit,
+                      float* work, float* z, uint64_t* keys, srpgpu_stream_t stream);
 
 /* srp_map_exact with the steering matrix generated on chip (never stored): for
  * candidate i, pair p, bin k: H = exp(j pi k x[i][p] / K), x = xtab [J][P] f32 = dt * fs
@@ -289,10 +292,11 @@ int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int3
  * (gcc_ld floats per frame, 16-byte pitch).  The operator for grids whose H does not
  * fit in memory (BASELINE cfg4: 164 GB).  split = 1 selects 3xTF32 (near-fp32 accuracy,
  * 3 MMAs per k-step): gcc then holds the hi plane [F][gcc_ld] followed by the lo plane
- * (srpgpu_split_tf32), and the steering residual is generated on chip as well. */
+ * (srpgpu_split_tf32), and the steering residual is generated on chip as well.
+ * ksplit / work: split-K as for srpgpu_srp_map_tc. */
 int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t num_pairs,
                         int32_t half_len, const float* xtab, int64_t num_candidates, int32_t split,
-                        float* z, uint64_t* keys, srpgpu_stream_t stream);
+                        int32_t ksplit, float* work, float* z, uint64_t* keys, srpgpu_stream_t stream);
 
 /* dst = [hi plane rows][lo plane rows]: hi = tf32_rne(src), lo = tf32_rne(src - hi). */
 int srpgpu_split_tf32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t rows,

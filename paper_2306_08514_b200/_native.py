@@ -57,8 +57,8 @@ SIGNATURES = {
     "srpgpu_lr_map_tc": [_P, _I64, _I32, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "srpgpu_lr_map": [_P, _I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_srp_map_simt": [_P, _I64, _I32, _P, _I64, _P, _P, _P],
-    "srpgpu_srp_map_tc": [_P, _I64, _I64, _I32, _P, _I64, _I64, _P, _P, _P],
-    "srpgpu_srp_map_tdoa": [_P, _I64, _I64, _I32, _I32, _P, _I64, _I32, _P, _P, _P],
+    "srpgpu_srp_map_tc": [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _P, _P, _P, _P],
+    "srpgpu_srp_map_tdoa": [_P, _I64, _I64, _I32, _I32, _P, _I64, _I32, _I32, _P, _P, _P, _P],
     "srpgpu_split_tf32": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "srpgpu_round_tf32": [_P, _I64, _P, _I64, _I64, _I64, _P],
     "srpgpu_c128_to_steering": [_P, _I64, _I64, _I64, _P, _I64, _I32, _P],

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreadsC, 1)
 conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_b2,
                         const __grid_constant__ CUtensorMap map_a, int64_t J, int64_t F, int32_t Kd,
                         float* __restrict__ z, unsigned long long* __restrict__ keys, float alpha,
-                        const GenParams gp) {
+                        const GenParams gp, int32_t ksplit, float* __restrict__ zpart) {
   constexpr int BN = 256;
   using SM = SmemC<SPLIT>;
   constexpr int NS = SM::NS;
@@ -225,7 +225,9 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (int)((J + BLOCK_M - 1) / BLOCK_M);
   const int n_tiles = (int)((F + BN - 1) / BN);
-  const int tile = blockIdx.x;
+  // split-K (small grids): CTA = (output tile, K slice); K slices are whole chunks
+  const int ks = blockIdx.x % ksplit;
+  const int tile = blockIdx.x / ksplit;
   // raster: with a stored operator, groups of GROUP_M candidate tiles sweep the frame
   // tiles (both operands reused from L2); with on-chip steering only psi is read, so all
   // candidate tiles of one frame tile run together and psi is read from HBM once
@@ -235,7 +237,10 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
   const int gsize = min(m_tiles - first_m, gm);
   const int m_blk = first_m + (tile % (gm * n_tiles)) % gsize;
   const int n_blk = (tile % (gm * n_tiles)) / gsize;
-  const int num_kb = (Kd + BLOCK_K - 1) / BLOCK_K;
+  const int kb_total = (Kd + BLOCK_K - 1) / BLOCK_K;
+  const int kper = ((kb_total + ksplit - 1) / ksplit + CHUNK - 1) / CHUNK * CHUNK;
+  const int kb0 = ks * kper;                                   // first k-block of this slice
+  const int num_kb = max(0, min(kb_total - kb0, kper));        // k-blocks of this slice
   const int num_chunks = (num_kb + CHUNK - 1) / CHUNK;
 
   if (warp == 0 && lane == 0) {
@@ -275,9 +280,10 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
     if (warp == 0) {
     if (lane == 0) {
       constexpr uint32_t kBytes = (BN * SM::NP + (GEN ? 0 : BLOCK_M)) * BLOCK_K * sizeof(float);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % NS;
-        const uint32_t round = kb / NS;
+      for (int kbl = 0; kbl < num_kb; ++kbl) {
+        const int kb = kb0 + kbl;
+        const int s = kbl % NS;
+        const uint32_t round = kbl / NS;
         mbar_wait(&sm.empty[s], (round & 1) ^ 1);
         mbar_expect_tx(&sm.full[s], kBytes);
         if (!GEN) tma_load_2d(sm.a[s][0], &map_a, &sm.full[s], kb * BLOCK_K, m_blk * BLOCK_M);
@@ -353,7 +359,7 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.tempty[b])) : "memory");
     };
     GenState g;
-    gen_state_init(g, kNB * part, gp.B > 0 ? gp.B : 1);
+    gen_state_init(g, kb0 * (BLOCK_K / 2) + kNB * part, gp.B > 0 ? gp.B : 1);
     const int64_t gi_c = gi < J ? gi : J - 1;          // rows past J: any finite values (discarded)
     constexpr uint32_t kPlane = BLOCK_M * BLOCK_K * sizeof(float), kStage = SM::NP * kPlane;
     const uint32_t a_row = smem_u32(&sm.a[0][0][0]) + row * 128;
@@ -389,6 +395,16 @@ conv_gen_chunked_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_
     while (folded < num_chunks) fold(folded++);
     const int64_t i = (int64_t)m_blk * BLOCK_M + quarter * 32 + lane;
     const bool row_ok = i < J;
+    if (zpart) {                                   // split-K: this slice's partial map
+#pragma unroll
+      for (int c = 0; c < kFoldCols; ++c) {
+        const int64_t f = (int64_t)n_blk * BN + cslice * kFoldCols + c;
+        if (f >= F) break;
+        if (row_ok) zpart[((int64_t)ks * F + f) * J + i] = alpha * sum[c];
+      }
+      end_sync();
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < kFoldCols; ++c) {
       const int64_t f = (int64_t)n_blk * BN + cslice * kFoldCols + c;
@@ -457,10 +473,27 @@ __global__ void split_tf32_kernel(const float* __restrict__ src, int64_t ld_src,
   }
 }
 
+// split-K combine: z[f][i] = sum over slices (fixed order) + the per-frame argmax keys
+__global__ void splitk_reduce_kernel(const float* __restrict__ zpart, int32_t ksplit, int64_t F, int64_t J,
+                                     float* __restrict__ z, unsigned long long* __restrict__ keys) {
+  const int64_t f = blockIdx.y;
+  unsigned long long best = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < J; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int k = 0; k < ksplit; ++k) v += __ldcs(zpart + ((int64_t)k * F + f) * J + i);
+    if (z) __stcs(z + f * J + i, v);
+    best = key_max(best, make_key(v, (uint32_t)i));
+  }
+  if (keys) {
+    best = warp_key_max(best);
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(keys + f, best);
+  }
+}
+
 template <bool SPLIT, bool GEN = true>
 static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t Kd, int64_t J, float* z,
                           uint64_t* keys, cudaStream_t st, const GenParams& gp, const float* h2 = nullptr,
-                          int64_t h2_ld = 0) {
+                          int64_t h2_ld = 0, int32_t ksplit = 1, float* work = nullptr) {
   CUtensorMap mb, mb2, ma;
   int s = make_map(&mb, gcc, F, Kd, gcc_ld, 256);
   if (s) return s;
@@ -476,8 +509,12 @@ static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t K
   }
   const int64_t tiles = ((J + BLOCK_M - 1) / BLOCK_M) * ((F + 255) / 256);
   SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "srp_map_tdoa: too many tiles");
-  kern<<<(unsigned)tiles, kThreadsC, smem, st>>>(mb, mb2, ma, J, F, Kd, z,
-                                                  reinterpret_cast<unsigned long long*>(keys), 2.0f, gp);
+  const int kb_total = (Kd + BLOCK_K - 1) / BLOCK_K;
+  ksplit = std::max(1, std::min<int32_t>(ksplit, (kb_total + CHUNK - 1) / CHUNK));
+  SRPGPU_CHECK_ARG(ksplit == 1 || work, SRPGPU_ERR_VALUE, "srp_map: split-K needs a work buffer");
+  kern<<<(unsigned)(tiles * ksplit), kThreadsC, smem, st>>>(mb, mb2, ma, J, F, Kd, z,
+                                                            reinterpret_cast<unsigned long long*>(keys), 2.0f, gp,
+                                                            ksplit, ksplit > 1 ? work : nullptr);
   {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -489,6 +526,12 @@ static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t K
       return SRPGPU_ERR_LAUNCH;
     }
     count_launch();
+  }
+  if (ksplit > 1) {
+    SRPGPU_CHECK_ARG(F <= 65535, SRPGPU_ERR_DIMENSION, "srp_map: split-K for at most 65535 frames");
+    dim3 grid((unsigned)std::min<int64_t>((J + 255) / 256, 64), (unsigned)F);
+    splitk_reduce_kernel<<<grid, 256, 0, st>>>(work, ksplit, F, J, z, reinterpret_cast<unsigned long long*>(keys));
+    SRPGPU_CHECK_LAUNCH("srp_map(split-K reduce)");
   }
   return SRPGPU_OK;
 }
@@ -549,8 +592,8 @@ extern "C" int srpgpu_split_tf32(const float* src, int64_t ld_src, float* dst, i
 }
 
 extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t gcc_len,
-                                 const float* h2, int64_t h2_ld, int64_t num_candidates, float* z,
-                                 uint64_t* keys, srpgpu_stream_t stream) {
+                                 const float* h2, int64_t h2_ld, int64_t num_candidates, int32_t ksplit,
+                                 float* work, float* z, uint64_t* keys, srpgpu_stream_t stream) {
   const int32_t Kd = 2 * gcc_len;
   SRPGPU_CHECK_ARG(gcc_len >= 1 && num_candidates >= 1, SRPGPU_ERR_DIMENSION, "srp_map_tc: empty operator");
   SRPGPU_CHECK_ARG(gcc_ld >= Kd && h2_ld >= Kd && gcc_ld % 4 == 0 && h2_ld % 4 == 0, SRPGPU_ERR_VALUE,
@@ -567,12 +610,13 @@ extern "C" int srpgpu_srp_map_tc(const float* gcc, int64_t gcc_ld, int64_t num_f
   (void)m_tiles; (void)n256;
   // chunked TMEM accumulation folded into fp32 registers (see conv_gen_chunked_kernel)
   return tc::launch_chunked<false, false>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp, h2,
-                                          h2_ld);
+                                          h2_ld, ksplit, work);
 }
 
 extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num_frames, int32_t num_pairs,
                                    int32_t half_len, const float* xtab, int64_t num_candidates,
-                                   int32_t split, float* z, uint64_t* keys, srpgpu_stream_t stream) {
+                                   int32_t split, int32_t ksplit, float* work, float* z, uint64_t* keys,
+                                   srpgpu_stream_t stream) {
   const int32_t bins = half_len - 1;
   const int32_t Kd = 2 * num_pairs * bins;
   SRPGPU_CHECK_ARG(num_pairs >= 1 && bins >= 1 && num_candidates >= 1, SRPGPU_ERR_DIMENSION,
@@ -591,6 +635,8 @@ extern "C" int srpgpu_srp_map_tdoa(const float* gcc, int64_t gcc_ld, int64_t num
   (void)m_tiles; (void)n256;
   // chunked TMEM accumulation folded into fp32 registers (bounded in-pipe accumulation)
   if (split)   // 3xTF32: gcc holds the hi plane [F][gcc_ld] followed by the lo plane
-    return tc::launch_chunked<true>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp);
-  return tc::launch_chunked<false>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp);
+    return tc::launch_chunked<true>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp, nullptr, 0,
+                                    ksplit, work);
+  return tc::launch_chunked<false>(gcc, gcc_ld, num_frames, Kd, num_candidates, z, keys, st, gp, nullptr, 0,
+                                   ksplit, work);
 }

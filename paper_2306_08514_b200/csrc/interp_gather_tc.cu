@@ -302,11 +302,15 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
   }
 }
 
+#ifndef UNTILE_U
+#define UNTILE_U 4
+#endif
+
 // tile order -> grid order: z[f][j] = zt[f][pos[j]] (coalesced writes; the reads follow
 // the tiles' ascending rows, mostly short contiguous runs)
 __global__ void untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
                               int64_t F, float* __restrict__ z) {
-  constexpr int U = 4;   // independent gathers in flight per thread
+  constexpr int U = UNTILE_U;   // independent gathers in flight per thread
   for (int64_t f = blockIdx.y; f < F; f += gridDim.y) {
     const float* src = zt + f * ldt;
     float* dst = z + f * J;

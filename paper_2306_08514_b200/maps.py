@@ -696,9 +696,26 @@ def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, ou
             vp = torch.empty((f, ld), dtype=torch.float32, device=h2.device)
             nat.call("srpgpu_round_tf32", dev.ptr(v), 2 * n, dev.ptr(vp), ld, f, 2 * n,
                      dev.stream_ptr())
-        nat.call("srpgpu_srp_map_tc", dev.ptr(vp), ld, f, n, dev.ptr(h2), ld, j, dev.ptr(z),
+        ks, work = _conv_split(f, j, n)
+        nat.call("srpgpu_srp_map_tc", dev.ptr(vp), ld, f, n, dev.ptr(h2), ld, j, ks, dev.ptr(work), dev.ptr(z),
                  dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
+
+
+CONV_CHUNK_FLOATS = 16 * 32      # one TMEM accumulation chunk of the tcgen05 map (16 k-blocks of 32)
+CONV_SPLIT_MAX = 16
+
+
+def _conv_split(frames: int, num_candidates: int, num_cols: int):
+    """Split-K factor of the tensor-core conventional map: grids with fewer output tiles
+    (128 candidates x 256 frames) than SMs split K into whole chunks so every SM works
+    (cfg2: 56 tiles -> 2 slices; cfg1: 14 tiles -> 10); (ksplit, work buffer or None)."""
+    tiles = -(-num_candidates // 128) * -(-frames // 256)
+    chunks = -(-2 * num_cols // CONV_CHUNK_FLOATS)
+    ks = max(1, min(dev.num_sms() // max(tiles, 1), chunks, CONV_SPLIT_MAX))
+    if ks < 2 or frames > 65535:
+        return 1, None
+    return ks, torch.empty((ks, frames, num_candidates), dtype=torch.float32, device=dev.device())
 
 
 def _xtab_device(op) -> torch.Tensor:
@@ -734,8 +751,9 @@ def _srp_map_tdoa(op, gcc, argmax: bool, out_map: bool, split: bool = False):
     xt = _xtab_device(op)
     z = torch.empty((f, j), dtype=torch.float32, device=vp.device) if out_map else None
     keys = _new_keys(f, argmax)
+    ks, work = _conv_split(f, j, n)
     nat.call("srpgpu_srp_map_tdoa", dev.ptr(vp), ld, f, op.num_pairs, op.num_bins + 1, dev.ptr(xt), j,
-             1 if split else 0, dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+             1 if split else 0, ks, dev.ptr(work), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 

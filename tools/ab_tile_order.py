@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=10000)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--modes", default="tile,grid")
     a = ap.parse_args()
     wl = workloads.make("cfg4", num_frames=a.frames)
     op = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
@@ -27,7 +28,8 @@ def main():
     xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(a.frames), planes=True, natural=True)
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     out = {}
-    for mode in (False, True):
+    modes = [m == "grid" for m in a.modes.split(",")]
+    for mode in modes:
         maps.TILE_GRID_ORDER = mode
         z, idx = s.sspi_map(op, xi, argmax=True, engine="tile")
         torch.cuda.synchronize()
@@ -43,9 +45,12 @@ def main():
         out["grid" if mode else "tile"] = {"ms": sorted(ts)[len(ts) // 2], "all": ts}
         out[f"z_{mode}"] = z.clone() if mode else z
         out[f"i_{mode}"] = idx.clone()
-    same = bool(torch.equal(out.pop("z_True"), out.pop("z_False")) and torch.equal(out.pop("i_True"),
-                                                                                   out.pop("i_False")))
-    out["bit_identical"] = same
+    if len(modes) == 2:
+        same = bool(torch.equal(out.pop("z_True"), out.pop("z_False")) and torch.equal(out.pop("i_True"),
+                                                                                       out.pop("i_False")))
+        out["bit_identical"] = same
+    for k in [k for k in out if k.startswith(("z_", "i_"))]:
+        out.pop(k)
     print(json.dumps(out))
 
 
