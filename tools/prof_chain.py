@@ -48,9 +48,10 @@ def main():
         else:
             op = interp
         from paper_2306_08514_b200 import maps
-        if a.engine == "fused":          # frontend + SSPI map + argmax in one kernel
+        if a.engine == "fused":          # frontend + map + argmax in one kernel
+            chain = maps.frames_to_slri_map if a.variant == "slri" else maps.frames_to_sspi_map
             for _ in range(a.reps):
-                z, idx = maps.frames_to_sspi_map(op, x, wl.frame, wl.pairs, wl.spec, rng)
+                z, idx = chain(op, x, wl.frame, wl.pairs, wl.spec, rng)
             torch.cuda.synchronize()
             return
         fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
