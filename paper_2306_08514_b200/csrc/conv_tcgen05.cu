@@ -479,8 +479,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ zpart, int32_t ks
   const int64_t f = blockIdx.y;
   unsigned long long best = 0ull;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < J; i += (int64_t)gridDim.x * blockDim.x) {
-    float v = 0.f;
-    for (int k = 0; k < ksplit; ++k) v += __ldcs(zpart + ((int64_t)k * F + f) * J + i);
+    float v = __ldcs(zpart + f * J + i);
+#pragma unroll 4
+    for (int k = 1; k < ksplit; ++k) v += __ldcs(zpart + ((int64_t)k * F + f) * J + i);
     if (z) __stcs(z + f * J + i, v);
     best = key_max(best, make_key(v, (uint32_t)i));
   }
@@ -529,7 +530,8 @@ static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t K
   }
   if (ksplit > 1) {
     SRPGPU_CHECK_ARG(F <= 65535, SRPGPU_ERR_DIMENSION, "srp_map: split-K for at most 65535 frames");
-    dim3 grid((unsigned)std::min<int64_t>((J + 255) / 256, 64), (unsigned)F);
+    // ~8 candidates per thread: one warp key reduction and atomic per 8 outputs
+    dim3 grid((unsigned)std::min<int64_t>((J + 2047) / 2048, 64), (unsigned)F);
     splitk_reduce_kernel<<<grid, 256, 0, st>>>(work, ksplit, F, J, z, reinterpret_cast<unsigned long long*>(keys));
     SRPGPU_CHECK_LAUNCH("srp_map(split-K reduce)");
   }
