@@ -530,8 +530,10 @@ static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t K
   }
   if (ksplit > 1) {
     SRPGPU_CHECK_ARG(F <= 65535, SRPGPU_ERR_DIMENSION, "srp_map: split-K for at most 65535 frames");
-    // ~8 candidates per thread: one warp key reduction and atomic per 8 outputs
-    dim3 grid((unsigned)std::min<int64_t>((J + 2047) / 2048, 64), (unsigned)F);
+    // enough blocks for ~4 per SM, then up to ~8 candidates per thread (one warp key
+    // reduction and atomic per several outputs)
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((J + 255) / 256, (4 * num_sms() + F - 1) / F));
+    dim3 grid((unsigned)gx, (unsigned)F);
     splitk_reduce_kernel<<<grid, 256, 0, st>>>(work, ksplit, F, J, z, reinterpret_cast<unsigned long long*>(keys));
     SRPGPU_CHECK_LAUNCH("srp_map(split-K reduce)");
   }
