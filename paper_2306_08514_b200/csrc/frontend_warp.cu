@@ -305,8 +305,21 @@ __device__ __forceinline__ void frame_sync(int fg) {
 
 // kWpf warps per frame share its spectra: 1 (latency-bound small batches: a warp per
 // frame) or 2 (large batches: half the spectra buffers per warp -> more resident warps)
+// register budget: 4 CTAs per SM (<= 128 registers, no spills; left free the compiler takes
+// up to ~250 and only 2 CTAs fit) -- cfg3, 10^4 frames: 0.37 vs 0.47 ms; 10^4 cfg2-shaped
+// frames: 0.20 vs 0.24 ms.  The 1-warp-per-frame L = 1024 kernel of small batches keeps the
+// free allocation (a few % faster at 1000 frames).  -DWARP_MINB_ALL=n overrides (A/B builds).
+template <int LP, int kWpf>
+struct WarpMinBlocks {
+#ifdef WARP_MINB_ALL
+  static constexpr int value = WARP_MINB_ALL;
+#else
+  static constexpr int value = (LP == 32 && kWpf == 1) ? 1 : 4;
+#endif
+};
+
 template <int LP, int OUT, int kWpf>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, WarpMinBlocks<LP, kWpf>::value)
 frontend_warp_kernel(const WarpParams prm) {
   using G = Geo<LP>;
   constexpr int L = G::L, K = G::K, R = G::R;
