@@ -427,12 +427,13 @@ struct Best4 {
 
 // one candidate's map values for the CTA's 4 frames: z stores + running argmax (a lane's
 // candidates arrive in increasing index order, so strict '>' keeps the first maximum)
-__device__ __forceinline__ void emit4(float4 acc, int64_t i, int64_t J, int64_t g, int64_t F, float* z, Best4& best) {
+__device__ __forceinline__ void emit4(float4 acc, int64_t i, int64_t J, int64_t fbase, int nvalid, float* z,
+                                      Best4& best) {
   if (i >= J) return;
   const float a[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
   for (int fr = 0; fr < 4; ++fr) {
-    if (z && g * 4 + fr < F) __stcs(z + (g * 4 + fr) * J + i, a[fr]);
+    if (z && fr < nvalid) __stcs(z + (fbase + fr) * J + i, a[fr]);
     const uint32_t ob = ordered_bits(a[fr]);
     if (best.idx[fr] < 0 || ob > best.ob[fr]) {
       best.ob[fr] = ob;
@@ -459,8 +460,8 @@ struct SellPhase {
     for (int i = threadIdx.x; i <= nch; i += blockDim.x) s_choff[i] = mp.chunk_off[i];
   }
   __device__ __forceinline__ void prepare(const float4*, void*, int, int) const {}
-  __device__ __forceinline__ void candidates(const float4* xs4, const void* extra, int64_t g, int64_t F, int wid,
-                                             int lane, Best4& best) const {
+  __device__ __forceinline__ void candidates(const float4* xs4, const void* extra, int64_t fbase, int nvalid,
+                                             int wid, int lane, Best4& best) const {
     const int* s_choff = reinterpret_cast<const int*>(extra);
     const int64_t J = mp.J;
     const int nch = (int)((J + 31) / 32);
@@ -521,8 +522,8 @@ struct SellPhase {
           }
         }
       }
-      emit4(acc[0], (int64_t)c * 32 + lane, J, g, F, mp.z, best);
-      emit4(acc[1], (int64_t)cb * 32 + lane, J, g, F, mp.z, best);
+      emit4(acc[0], (int64_t)c * 32 + lane, J, fbase, nvalid, mp.z, best);
+      emit4(acc[1], (int64_t)cb * 32 + lane, J, fbase, nvalid, mp.z, best);
     }
   }
 };
@@ -551,7 +552,7 @@ struct SlriPhase {
       if (lane == 0) ys[r] = acc;
     }
   }
-  __device__ __forceinline__ void candidates(const float4*, const void* extra, int64_t g, int64_t F, int wid,
+  __device__ __forceinline__ void candidates(const float4*, const void* extra, int64_t fbase, int nvalid, int wid,
                                              int lane, Best4& best) const {
     const float4* ys = reinterpret_cast<const float4*>(extra);
     const int64_t J = mp.J;
@@ -580,8 +581,8 @@ struct SlriPhase {
           for (int u = 0; u < 16; ++u) fma4(acc[1], t[1][u], ys[r0 + u]);
         }
       }
-      emit4(acc[0], ia, J, g, F, mp.z, best);
-      if (has_b) emit4(acc[1], ib, J, g, F, mp.z, best);
+      emit4(acc[0], ia, J, fbase, nvalid, mp.z, best);
+      if (has_b) emit4(acc[1], ib, J, fbase, nvalid, mp.z, best);
     }
   }
 };
@@ -593,12 +594,15 @@ struct SlriPhase {
 // frames at once (one float4 shared load feeds 4 FMAs): the SSPI sliced-ELL operator or
 // the SLRI factors, read coalesced through L1 / L2.  z is written once; one CTA owns its
 // frames, so the argmax index is written directly (no key reset, no atomics, no decode).
-template <int LP, class Phase>
+// kWpf warps per frame: 1 (4 frames per CTA: the map phase reuses each operator load for 4
+// frames) or 4 (1 frame per CTA for tiny batches: the frame's FFT rounds run side by side)
+template <int LP, class Phase, int kWpf>
 __global__ void __launch_bounds__(kWarps * 32)
 frontend_map_kernel(const WarpParams prm, const Phase ph) {
   using G = Geo<LP>;
   constexpr int L = G::L, K = G::K;
   constexpr int Kp1 = K + 1;
+  constexpr int kFpc = kWarps / kWpf;                                   // frames per CTA
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* twT = reinterpret_cast<float2*>(smem_raw);                    // [32][LP]
   int* s_pairs = reinterpret_cast<int*>(twT + 32 * LP);                 // [2P]
@@ -607,12 +611,14 @@ frontend_map_kernel(const WarpParams prm, const Phase ph) {
   const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * prm.P + 1) * 4) + 15) & ~(size_t)15;
   const int M = prm.M, P = prm.P, S = prm.S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t frame_bytes = ((size_t)M * Kp1 + G::WORK) * sizeof(float2);
-  float2* spec = reinterpret_cast<float2*>(smem_raw + head + wid * frame_bytes);  // [M][K+1]
-  float2* work = spec + (size_t)M * Kp1;                                           // [R][XP]
-  float* xs = reinterpret_cast<float*>(smem_raw + head + kWarps * frame_bytes);    // [S][4]
+  const int fg = wid / kWpf, mi = wid % kWpf;
+  const size_t frame_bytes = ((size_t)M * Kp1 + kWpf * G::WORK) * sizeof(float2);
+  float2* spec = reinterpret_cast<float2*>(smem_raw + head + fg * frame_bytes);   // [M][K+1]
+  float2* work = spec + (size_t)M * Kp1 + mi * G::WORK;                           // [R][XP]
+  float* xs = reinterpret_cast<float*>(smem_raw + head + kFpc * frame_bytes);     // [S][4]
   unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(xs + 4 * (size_t)S);   // [4 warps][4]
-  void* extra = s_keys + 16;                                                                // phase data
+  float* s_energy = reinterpret_cast<float*>(s_keys + 16);                                  // [4 warps]
+  void* extra = s_energy + kWarps;                                                          // phase data
   float2* xp = work + (lane / LP) * G::XP;
 
   for (int e = threadIdx.x; e < 32 * LP; e += blockDim.x) {
@@ -624,30 +630,42 @@ frontend_map_kernel(const WarpParams prm, const Phase ph) {
   for (int i = threadIdx.x; i < 2 * P; i += blockDim.x) s_pairs[i] = prm.pairs[i];
   for (int i = threadIdx.x; i < P; i += blockDim.x) s_counts[i] = prm.counts[i];
   for (int i = threadIdx.x; i <= P; i += blockDim.x) s_off[i] = prm.offsets[i];
+  if (kFpc < 4)                                       // columns no frame writes stay zero
+    for (int i = threadIdx.x; i < 4 * S; i += blockDim.x) xs[i] = 0.f;
   ph.setup(extra);
   __syncthreads();
 
   const float4* xs4 = reinterpret_cast<const float4*>(xs);
-  const int64_t groups = (prm.F + 3) / 4;
+  const int64_t groups = (prm.F + kFpc - 1) / kFpc;
   const auto& out = ph.out();
   for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
-    const int64_t f = g * 4 + wid;
-    if (f < prm.F) {
+    const int64_t fbase = g * kFpc;
+    const int64_t left = prm.F - fbase;
+    const int nvalid = left < kFpc ? (int)left : kFpc;
+    const int64_t f = fbase + fg;
+    if (fg < nvalid) {                                // warp-uniform per frame group
       const int64_t start = (prm.first_frame + f) * (int64_t)prm.hop;
-      float energy = forward_frame<LP, 1>(prm, start, spec, work, xp, twT, lane, 0);
+      float energy = forward_frame<LP, kWpf>(prm, start, spec, work, xp, twT, lane, mi);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, o);
+      if (kWpf > 1) {
+        if (lane == 0) s_energy[wid] = energy;
+        frame_sync<kWpf>(fg);                         // spectra + energy of the frame complete
+        energy = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWpf; ++w) energy += s_energy[fg * kWpf + w];
+      }
       const float floor = (prm.weighting && prm.floor_mode == 0) ? prm.floor_value * energy : prm.floor_value;
-      inverse_frame<LP, 1>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, Phat(prm.weighting, floor), lane, 0,
-                           SmemXi{xs, wid});
-    } else {
-      for (int s = lane; s < S; s += 32) xs[s * 4 + wid] = 0.f;
+      inverse_frame<LP, kWpf>(prm, spec, work, xp, twT, s_pairs, s_counts, s_off, Phat(prm.weighting, floor), lane,
+                              mi, SmemXi{xs, fg});
+    } else if (mi == 0) {
+      for (int s = lane; s < S; s += 32) xs[s * 4 + fg] = 0.f;
     }
-    __syncthreads();                                  // xs of the CTA's 4 frames complete
+    __syncthreads();                                  // xs of the CTA's frames complete
     ph.prepare(xs4, extra, wid, lane);
     __syncthreads();
     Best4 lane_best;
-    ph.candidates(xs4, extra, g, prm.F, wid, lane, lane_best);
+    ph.candidates(xs4, extra, fbase, nvalid, wid, lane, lane_best);
     unsigned long long best[4];
 #pragma unroll
     for (int fr = 0; fr < 4; ++fr) best[fr] = warp_key_max(lane_best.key(fr));
@@ -656,26 +674,27 @@ frontend_map_kernel(const WarpParams prm, const Phase ph) {
       for (int fr = 0; fr < 4; ++fr) s_keys[wid * 4 + fr] = best[fr];
     }
     __syncthreads();                                  // xs free; s_keys complete
-    if (wid == 0 && lane < 4 && g * 4 + lane < prm.F) {
+    if (wid == 0 && lane < nvalid) {
       unsigned long long k = s_keys[lane];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) k = key_max(k, s_keys[w * 4 + lane]);
-      if (out.keys) out.keys[g * 4 + lane] = k;
-      if (out.index) out.index[g * 4 + lane] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+      if (out.keys) out.keys[fbase + lane] = k;
+      if (out.index) out.index[fbase + lane] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
     }
   }
 }
 
-template <int LP, class Phase, class Map>
-static int launch_fused(const WarpParams& wp, const Map& mp, cudaStream_t st, const char* what) {
+template <int LP, class Phase, int kWpf, class Map>
+static int launch_fused_w(const WarpParams& wp, const Map& mp, cudaStream_t st, const char* what) {
   using G = Geo<LP>;
+  constexpr int kFpc = kWarps / kWpf;
   const size_t head = (((size_t)32 * LP * 8 + (size_t)(4 * wp.P + 1) * 4) + 15) & ~(size_t)15;
-  const size_t frame_bytes = ((size_t)wp.M * (G::K + 1) + G::WORK) * sizeof(float2);
-  const size_t smem = head + kWarps * frame_bytes + (size_t)wp.S * 16 + 16 * 8 + Phase::smem(mp, wp.S);
+  const size_t frame_bytes = ((size_t)wp.M * (G::K + 1) + kWpf * G::WORK) * sizeof(float2);
+  const size_t smem = head + kFpc * frame_bytes + (size_t)wp.S * 16 + 16 * 8 + kWarps * 4 + Phase::smem(mp, wp.S);
   SRPGPU_CHECK_ARG(smem <= 227 * 1024, SRPGPU_ERR_UNSUPPORTED,
                    "%s: %d channels x %d samples per frame and %d TD-GCC samples need %zu B of shared memory",
                    what, wp.M, wp.L, wp.S, smem);
-  auto kern = frontend_map_kernel<LP, Phase>;
+  auto kern = frontend_map_kernel<LP, Phase, kWpf>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     set_error("%s: cannot reserve %zu B shared memory", what, smem);
     return SRPGPU_ERR_LAUNCH;
@@ -683,11 +702,18 @@ static int launch_fused(const WarpParams& wp, const Map& mp, cudaStream_t st, co
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t grid = std::min<int64_t>((wp.F + 3) / 4, (int64_t)num_sms() * per_sm);
+  const int64_t grid = std::min<int64_t>((wp.F + kFpc - 1) / kFpc, (int64_t)num_sms() * per_sm);
   if (grid <= 0) return SRPGPU_OK;
   kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(wp, Phase{mp});
   SRPGPU_CHECK_LAUNCH(what);
   return SRPGPU_OK;
+}
+
+// tiny batches (<= 2 frames per SM): a CTA of 4 warps per frame; else 4 frames per CTA
+template <int LP, class Phase, class Map>
+static int launch_fused(const WarpParams& wp, const Map& mp, cudaStream_t st, const char* what) {
+  if (wp.F <= 2 * (int64_t)num_sms()) return launch_fused_w<LP, Phase, 4>(wp, mp, st, what);
+  return launch_fused_w<LP, Phase, 1>(wp, mp, st, what);
 }
 
 template <int LP, int OUT, int kWpf>
