@@ -16,7 +16,9 @@ namespace srpgpu {
 
 constexpr int kGI = 64, kGF = 64, kGK = 16;
 
-template <bool BT>   // BT: B stored transposed, element (f, k) at B[k * ldb + f]
+// TI x TF output tile (TI * TF = 4096, 256 threads x 4 x 4): 64 x 64, or 32 x 128 for
+// factor products with at most 32 rank rows (LR at R = 16: 2R = 32), so no half-empty tiles
+template <bool BT, int TI = 64>   // BT: B stored transposed, element (f, k) at B[k * ldb + f]
 __global__ void __launch_bounds__(256)
 gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                float* __restrict__ out, int64_t ldo, int64_t I, int64_t F, int64_t K, float alpha,
@@ -26,36 +28,61 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
   const int64_t kbeg = (int64_t)blockIdx.z * k_chunk;
   const int64_t kend = kbeg + k_chunk < K ? kbeg + k_chunk : K;
   out += (int64_t)blockIdx.z * F * ldo;
-  __shared__ __align__(16) float As[kGK][kGI + 4];
-  __shared__ __align__(16) float Bs[kGK][kGF + 4];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  constexpr int TF = 4096 / TI, TX = TI / 4;
+  __shared__ __align__(16) float As[kGK][TI + 4];
+  __shared__ __align__(16) float Bs[kGK][TF + 4];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   // frame tiles run fastest: co-resident CTAs then cover many frames, so their per-frame
   // key atomics spread over many addresses (candidate-fastest order had ~1000 CTAs
   // hammering the same 64 keys); both operands are small and stay L2-resident
-  const int64_t f0 = (int64_t)blockIdx.x * kGF, i0 = (int64_t)blockIdx.y * kGI;
+  const int64_t f0 = (int64_t)blockIdx.x * TF, i0 = (int64_t)blockIdx.y * TI;
   float acc[4][4];
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
 
-  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK) {
+  // the next k-tile is loaded into registers while the current one is multiplied
+  // (register double buffering: the global loads' latency hides behind 256 FMAs)
+  constexpr int NA = TI * kGK / 256, NB = TF * kGK / 256;
+  float ra[NA], rb[NB];
+  auto load_tile = [&](int64_t k0) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * 256;        // 0..1023 over a 64 x 16 tile, k fastest
-      const int row = idx >> 4, kk = idx & 15;
-      const int64_t gi = i0 + row, gk = k0 + kk;
-      As[kk][row] = (gi < I && gk < kend) ? __ldg(A + gi * lda + gk) : 0.f;
+    for (int r = 0; r < NA; ++r) {
+      const int idx = tid + r * 256;        // over a TI x 16 tile, k fastest
+      const int64_t gi = i0 + (idx >> 4), gk = k0 + (idx & 15);
+      ra[r] = (gi < I && gk < kend) ? __ldg(A + gi * lda + gk) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const int idx = tid + r * 256;
       if (!BT) {
-        const int64_t gf = f0 + row;
-        Bs[kk][row] = (gf < F && gk < kend) ? __ldg(B + gf * ldb + gk) : 0.f;
+        const int64_t gf = f0 + (idx >> 4), gk = k0 + (idx & 15);
+        rb[r] = (gf < F && gk < kend) ? __ldg(B + gf * ldb + gk) : 0.f;
       } else {                              // frames fastest: coalesced along f
-        const int fr = idx & 63, kb = idx >> 6;
-        const int64_t gf = f0 + fr, gkb = k0 + kb;
-        Bs[kb][fr] = (gf < F && gkb < kend) ? __ldg(B + gkb * ldb + gf) : 0.f;
+        const int64_t gf = f0 + idx % TF, gkb = k0 + idx / TF;
+        rb[r] = (gf < F && gkb < kend) ? __ldg(B + gkb * ldb + gf) : 0.f;
       }
     }
+  };
+  auto store_tile = [&]() {
+#pragma unroll
+    for (int r = 0; r < NA; ++r) {
+      const int idx = tid + r * 256;
+      As[idx & 15][idx >> 4] = ra[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const int idx = tid + r * 256;
+      if (!BT) Bs[idx & 15][idx >> 4] = rb[r];
+      else Bs[idx / TF][idx % TF] = rb[r];
+    }
+  };
+  if (kbeg < kend) load_tile(kbeg);
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kGK) {
+    store_tile();
     __syncthreads();
+    if (k0 + kGK < kend) load_tile(k0 + kGK);
 #pragma unroll
     for (int kk = 0; kk < kGK; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[kk][tx * 4]);
@@ -100,9 +127,9 @@ gemm_nt_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict
       }
     }
     if (keys) {
-      // reduce over the 16 lanes sharing ty (half-warp)
+      // reduce over the TX lanes sharing ty
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) key = key_max(key, __shfl_xor_sync(0xffffffffu, key, o));
+      for (int o = TX / 2; o > 0; o >>= 1) key = key_max(key, __shfl_xor_sync(0xffffffffu, key, o));
       if (tx == 0 && f < F && key) atomicMax(keys + f, key);
     }
   }
@@ -303,23 +330,27 @@ int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out
             int64_t I, int64_t F, int64_t K, float alpha, uint64_t* keys, cudaStream_t st,
             const char* what, bool b_trans = false, float* split_ws = nullptr) {
   if (I <= 0 || F <= 0) return SRPGPU_OK;
-  const int64_t ctas = ((I + kGI - 1) / kGI) * ((F + kGF - 1) / kGF);
+  const bool narrow = I <= 32;                       // 32 x 128 tiles (no half-empty 64-row tiles)
+  const int64_t ti = narrow ? 32 : kGI, tf = 4096 / ti;
+  const int64_t ctas = ((I + ti - 1) / ti) * ((F + tf - 1) / tf);
   int64_t split = 1;
   if (split_ws && !keys && ldo == I && ctas < 2 * num_sms())
     split = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, (2 * num_sms() + ctas - 1) / ctas,
                                                     K / 256}));
   const int64_t chunk = ((K + split - 1) / split + kGK - 1) / kGK * kGK;
   split = (K + chunk - 1) / chunk;
-  SRPGPU_CHECK_ARG((I + kGI - 1) / kGI <= 65535, SRPGPU_ERR_DIMENSION, "%s: too many candidates", what);
-  dim3 grid((unsigned)((F + kGF - 1) / kGF), (unsigned)((I + kGI - 1) / kGI), (unsigned)split);
+  SRPGPU_CHECK_ARG((I + ti - 1) / ti <= 65535, SRPGPU_ERR_DIMENSION, "%s: too many candidates", what);
+  dim3 grid((unsigned)((F + tf - 1) / tf), (unsigned)((I + ti - 1) / ti), (unsigned)split);
   float* dst = split > 1 ? split_ws : out;
   const float a = split > 1 ? 1.0f : alpha;
-  if (b_trans)
-    gemm_nt_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a,
-                                               reinterpret_cast<unsigned long long*>(keys), 0, chunk);
-  else
-    gemm_nt_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a,
-                                                reinterpret_cast<unsigned long long*>(keys), 0, chunk);
+  auto* kp = reinterpret_cast<unsigned long long*>(keys);
+  if (b_trans) {
+    if (narrow) gemm_nt_kernel<true, 32><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a, kp, 0, chunk);
+    else gemm_nt_kernel<true, 64><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a, kp, 0, chunk);
+  } else {
+    if (narrow) gemm_nt_kernel<false, 32><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a, kp, 0, chunk);
+    else gemm_nt_kernel<false, 64><<<grid, 256, 0, st>>>(A, lda, B, ldb, dst, ldo, I, F, K, a, kp, 0, chunk);
+  }
   SRPGPU_CHECK_LAUNCH(what);
   if (split > 1) {
     const int64_t n = F * I;
