@@ -368,6 +368,10 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
     roof["kernel_ms"] = {"fused_chain": t_map} if fused else {"frontend": t_front, "map": t_map}
+    if not fused and args.variant not in ("conv", "conv_h"):
+        # both stages against the HBM roofline (the north-star target is per stage)
+        roof["stages_hbm_frac"] = {k: abytes[k] / (t / 1e3) / 1e9 / hbm
+                                   for k, t in (("frontend", t_front), ("map", t_map)) if k in abytes and t > 0}
     eng = "fused" if fused else _maps.map_engine(args.variant, op, "auto" if args.engine == "fused" else args.engine,
                                                  count)
     if eng == "tc":
