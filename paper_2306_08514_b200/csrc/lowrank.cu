@@ -334,8 +334,8 @@ int gemm_nt(const float* A, int64_t lda, const float* B, int64_t ldb, float* out
   const int64_t ti = narrow ? 32 : kGI, tf = 4096 / ti;
   const int64_t ctas = ((I + ti - 1) / ti) * ((F + tf - 1) / tf);
   int64_t split = 1;
-  if (split_ws && !keys && ldo == I && ctas < 2 * num_sms())
-    split = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, (2 * num_sms() + ctas - 1) / ctas,
+  if (split_ws && !keys && ldo == I && ctas < 4 * num_sms())
+    split = std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, (4 * num_sms() + ctas - 1) / ctas,
                                                     K / 256}));
   const int64_t chunk = ((K + split - 1) / split + kGK - 1) / kGK * kGK;
   split = (K + chunk - 1) / chunk;
