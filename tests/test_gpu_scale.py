@@ -103,6 +103,32 @@ def test_cfg2_conventional(cfg2):
         check(z, z_ref, idx)
 
 
+def test_cfg2_fused_chains_and_splitk(cfg2):
+    """The bench's headline path at full batch (1000 frames, one fused kernel per step) for
+    SSPI (global 2JP fit) and SLRI (R = 16), and the split-K on-chip conventional map,
+    against the float64 oracle on the first 32 frames."""
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    wl, x, xi, psi_ref, xi_ref = cfg2
+    interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame)
+    sp = s.truncate_sparse(interp, s.resolve_sparsity("2jp", wl.grid.num_points, wl.pairs.num_pairs,
+                                                      interp.matrix.size))
+    lr = s.truncate_low_rank(interp, 16)
+    F = wl.num_frames
+    n = (F - 1) * wl.frame.hop + wl.frame.frame_len
+    for variant, op, z_ref in (
+            ("sspi", sp, O.sspi_map(sp.values, sp.col_indices, sp.row_splits, xi_ref)),
+            ("slri", lr, O.slri_map(lr.tall, lr.fat, xi_ref))):
+        pipe = MapPipeline(variant, op, wl.frame, wl.pairs, wl.spec, frames=F)
+        assert pipe.uses_fused_chain()
+        z, idx = pipe.run(x[:, :n])
+        torch.cuda.synchronize()
+        check(z, z_ref, idx)
+    steer = s.steering_operator(wl.tdoa, wl.frame)
+    gcc = s.gcc_frames(x, wl.frame, wl.pairs, tf32=True)
+    z, idx = s.srp_map_exact(steer, gcc, argmax=True)          # 56 output tiles -> 2 K slices
+    check(z, O.srp_map_exact(s.build_srp_matrix(wl.tdoa, wl.frame).matrix, psi_ref), idx)
+
+
 @pytest.fixture(scope="module")
 def cfg3():
     wl = workloads.make("cfg3", num_frames=256)
