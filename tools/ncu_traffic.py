@@ -32,6 +32,8 @@ def key_of(name: str, variant: str):
         return f"{variant}_map"
     if "lowrank_out" in name:
         return f"{variant}_map"
+    if "splitk" in name and variant in ("conv", "conv_h"):
+        return "srp_map_splitk_reduce"
     if "gemm_nt" in name or "splitk" in name or "split_bf16" in name:
         return f"{variant}_factor"
     return None
