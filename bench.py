@@ -435,6 +435,26 @@ def run_ours(args):
                  "steps": e2e_steps}
     assert last.shape == (count,)
     del stream
+    # the e2e bound: the same pinned host->device copy alone (no chain), CUDA events
+    link_buf = torch.empty_like(x_dev)
+    for _ in range(3):
+        link_buf.copy_(pinned, non_blocking=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(e2e_steps):
+        link_buf.copy_(pinned, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    copy_ms = a.elapsed_time(b) / e2e_steps
+    del link_buf
+    h2d = e2e_block["h2d_bytes_per_step"]
+    e2e_block["host_link"] = {
+        "h2d_gbps": h2d / (e2e_ms / 1e3) / 1e9,
+        "copy_alone_gbps": h2d / (copy_ms / 1e3) / 1e9,
+        "copy_alone_ms": copy_ms,
+        "frac": copy_ms / e2e_ms,
+        "bound": "host link (the pinned H2D copy of the samples)" if copy_ms >= 0.8 * e2e_ms
+                 else "device chain / host submission"}
 
     parity = None
     if rank == 0:

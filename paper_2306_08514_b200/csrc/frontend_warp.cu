@@ -12,6 +12,7 @@
 //   * the inverse is pruned: only the 2N_p+1 kept lags (|n| <= N_p) are produced,
 //     i.e. outputs k1 in {0, LP-1} of the second step when N_p < 32.
 //   * frame energy for the PHAT floor by warp shuffles.
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "frontend_warp.cuh"
@@ -712,7 +713,13 @@ static int launch_fused_w(const WarpParams& wp, const Map& mp, cudaStream_t st, 
 // tiny batches (<= 2 frames per SM): a CTA of 4 warps per frame; else 4 frames per CTA
 template <int LP, class Phase, class Map>
 static int launch_fused(const WarpParams& wp, const Map& mp, cudaStream_t st, const char* what) {
-  if (wp.F <= 2 * (int64_t)num_sms()) return launch_fused_w<LP, Phase, 4>(wp, mp, st, what);
+  static const int forced = [] {                      // tuning override: SRPGPU_FUSED_WPF=1|2|4
+    const char* v = std::getenv("SRPGPU_FUSED_WPF");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (forced == 2) return launch_fused_w<LP, Phase, 2>(wp, mp, st, what);
+  if (forced == 4 || (forced != 1 && wp.F <= 2 * (int64_t)num_sms()))
+    return launch_fused_w<LP, Phase, 4>(wp, mp, st, what);
   return launch_fused_w<LP, Phase, 1>(wp, mp, st, what);
 }
 
