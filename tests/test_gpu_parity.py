@@ -184,6 +184,23 @@ def test_fused_slri_chain(golden_scene):
     assert torch.equal(zp, z) and torch.equal(ip, idx)
 
 
+@pytest.mark.parametrize("wpf", ["1", "2", "4"])
+def test_fused_chains_every_warps_per_frame(wpf):
+    """The fused chains with 1, 2 and 4 warps per frame forced (SRPGPU_FUSED_WPF, read once
+    per process, hence a child pytest) pass the same golden parity tests."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, SRPGPU_FUSED_WPF=wpf)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-m", "gpu",
+                        "-k", "fused_sspi_chain or fused_slri_chain or fused_chains_weighting"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 @pytest.mark.parametrize("weighting,floor", [("none", None), ("phat", 0.5), ("phat", 0.0)])
 def test_fused_chains_weighting_and_floor(golden_scene, weighting, floor):
     """The fused chains honour fd_gcc's weighting / floor arguments (frontend.py:127-160)
