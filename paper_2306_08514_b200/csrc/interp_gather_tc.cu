@@ -26,6 +26,7 @@
 // restores grid order: scattered 4-byte stores made the L2 read-modify-write each
 // sector), and the per-frame argmax is a butterfly max across the lanes plus a ballot
 // for the lowest winning candidate (tile rows are ascending).
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include "tc_common.cuh"
@@ -307,26 +308,43 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 #endif
 
 // tile order -> grid order: z[f][j] = zt[f][pos[j]] (coalesced writes; the reads follow
-// the tiles' ascending rows, mostly short contiguous runs)
+// the tiles' ascending rows, mostly short contiguous runs).  FB frames per CTA share each
+// thread's pos loads (the kernel is L1-wavefront bound: ncu r1j, L1 86% of peak)
+template <int FB>
 __global__ void untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
                               int64_t F, float* __restrict__ z) {
-  constexpr int U = UNTILE_U;   // independent gathers in flight per thread
-  for (int64_t f = blockIdx.y; f < F; f += gridDim.y) {
-    const float* src = zt + f * ldt;
-    float* dst = z + f * J;
+  constexpr int U = UNTILE_U;   // independent gathers in flight per thread (per frame)
+  for (int64_t f0 = (int64_t)blockIdx.y * FB; f0 < F; f0 += (int64_t)gridDim.y * FB) {
+    const int nf = F - f0 < FB ? (int)(F - f0) : FB;
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < J; j0 += U * step) {
       int32_t p[U];
-      float v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) p[u] = j0 + u * step < J ? __ldg(pos + j0 + u * step) : 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = __ldcs(src + p[u]);
+      for (int fb = 0; fb < FB; ++fb) {
+        if (fb < nf) {
+          const float* src = zt + (f0 + fb) * ldt;
+          float* dst = z + (f0 + fb) * J;
+          float v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (j0 + u * step < J) __stcs(dst + j0 + u * step, v[u]);
+          for (int u = 0; u < U; ++u) v[u] = __ldcs(src + p[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (j0 + u * step < J) __stcs(dst + j0 + u * step, v[u]);
+        }
+      }
     }
   }
+}
+
+static int untile_frames() {                          // tuning override: SRPGPU_UNTILE_FB=1|2|4
+  static const int fb = [] {
+    const char* v = std::getenv("SRPGPU_UNTILE_FB");
+    const int x = v ? std::atoi(v) : 4;           // cfg4 map+untile 33.8 -> 33.4 ms (r1k A/B)
+    return (x == 1 || x == 2) ? x : 4;
+  }();
+  return fb;
 }
 
 }  // namespace gtc
@@ -382,9 +400,13 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
       z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
   if (z && z_tiles) {
+    const int fb = untile_frames();
     dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
-              (unsigned)std::min<int64_t>(num_frames, 65535));
-    untile_kernel<<<grid, 256, 0, st>>>(z_tiles, (int64_t)num_tiles * GT, tile_pos, num_candidates, num_frames, z);
+              (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
+    const int64_t ldt = (int64_t)num_tiles * GT;
+    if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+    else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+    else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
     SRPGPU_CHECK_LAUNCH("interp_map_gather_tc(untile)");
   }
   return SRPGPU_OK;
