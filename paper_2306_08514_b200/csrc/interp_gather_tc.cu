@@ -311,7 +311,7 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 // the tiles' ascending rows, mostly short contiguous runs).  FB frames per CTA share each
 // thread's pos loads (the kernel is L1-wavefront bound: ncu r1j, L1 86% of peak)
 template <int FB>
-__global__ void untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
+__global__ void __launch_bounds__(256) untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
                               int64_t F, float* __restrict__ z) {
   constexpr int U = UNTILE_U;   // independent gathers in flight per thread (per frame)
   for (int64_t f0 = (int64_t)blockIdx.y * FB; f0 < F; f0 += (int64_t)gridDim.y * FB) {
