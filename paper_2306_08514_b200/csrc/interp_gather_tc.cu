@@ -338,13 +338,17 @@ __global__ void __launch_bounds__(256) untile_kernel(const float* __restrict__ z
   }
 }
 
-static int untile_frames() {                          // tuning override: SRPGPU_UNTILE_FB=1|2|4
-  static const int fb = [] {
+// frames per CTA of the untile pass (tuning override: SRPGPU_UNTILE_FB=1|2|4).  4 frames share
+// each pos load on large batches (cfg4, 10^4 frames: map + untile 33.8 -> 33.4 ms); small
+// batches keep 1 (the cfg5 sweep at 16-256 frames lost 7-11% with 4: fewer CTAs per frame)
+static int untile_frames(int64_t num_frames) {
+  static const int forced = [] {
     const char* v = std::getenv("SRPGPU_UNTILE_FB");
-    const int x = v ? std::atoi(v) : 4;           // cfg4 map+untile 33.8 -> 33.4 ms (r1k A/B)
-    return (x == 1 || x == 2) ? x : 4;
+    const int x = v ? std::atoi(v) : 0;
+    return (x == 1 || x == 2 || x == 4) ? x : 0;
   }();
-  return fb;
+  if (forced) return forced;
+  return num_frames >= 4096 ? 4 : 1;
 }
 
 }  // namespace gtc
@@ -400,7 +404,7 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
       z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
   if (z && z_tiles) {
-    const int fb = untile_frames();
+    const int fb = untile_frames(num_frames);
     dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
               (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
     const int64_t ldt = (int64_t)num_tiles * GT;
