@@ -608,7 +608,7 @@ def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto")
         from paper_2306_08514_b200 import maps
         eng = maps.map_engine(variant, op, engine, count)   # the pipeline's frontend also writes the planes
         front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames,
-                                            planes=eng in ("tc", "tile"), natural=eng == "tile")
+                                            **maps.plane_args(eng))
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]
         if variant != "slri":
             mapf0 = mapf

@@ -107,9 +107,11 @@ int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t
  * tensor-core interpolation maps' operand), written by the same kernel; cols8 >=
  * total_samples, a multiple of 8.  planes_ld > 0: lag-major planes [2][cols8][planes_ld]
  * instead (planes_ld >= F, a multiple of 8; needs lag-major samples, samples_ld > 0).
- * natural != 0: sample index in natural lag order -N_p..N_p per pair
+ * natural bit 0: sample index in natural lag order -N_p..N_p per pair
  * (srpgpu_interp_map_gather_tc); natural_src [S] int32 maps each natural index to its
- * storage index (used when a non-warp kernel produced the samples). */
+ * storage index (used when a non-warp kernel produced the samples).  natural bit 1:
+ * fp32 TF32 planes (hi = tf32_rne(x), lo = tf32_rne(x - hi); lag-major only) for
+ * srpgpu_interp_map_gather_tf32. */
 int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels, int64_t num_samples,
                                     int64_t ld_samples, const float* window, int32_t frame_len,
                                     int32_t hop, int64_t first_frame, int64_t num_frames,
@@ -215,6 +217,23 @@ int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, 
                                 int32_t num_tiles, int64_t num_candidates, int32_t num_ctas,
                                 const int32_t* tile_pos, float* z_tiles, float* z,
                                 uint64_t* keys, srpgpu_stream_t stream);
+
+/* The same map with 3xTF32 operands (FP32-class: hi = tf32_rne(x), lo = tf32_rne(x - hi),
+ * z ~= Lh.xh + Lh.xl + Ll.xh accumulated in fp32 by tcgen05 kind::tf32): samples_planes
+ * fp32 [2][round8(S)][planes_ld] (planes_ld a multiple of 32, 128-byte aligned; natural lag
+ * order), slab_planes fp32 [2][num_slabs * 128][64] (srpgpu_split_tf32 of the slabs); the
+ * other arguments as srpgpu_interp_map_gather_tc.  Replaces interpolation.py:188-195
+ * (sspi_map) at long sample vectors. */
+int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
+                                  int64_t planes_ld, const float* slab_planes, int64_t num_slabs,
+                                  const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nkb,
+                                  const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
+                                  int32_t num_ctas, const int32_t* tile_pos, float* z_tiles, float* z,
+                                  uint64_t* keys, srpgpu_stream_t stream);
+
+/* srpgpu_split_bf16_rows into fp32 TF32 hi / lo planes (hi = tf32_rne(x), lo = tf32_rne(x - hi)). */
+int srpgpu_split_tf32_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols, const int32_t* row_src,
+                           float* dst, int64_t ld_dst, int64_t rows_dst, srpgpu_stream_t stream);
 
 /* row-wise bf16 hi/lo split: dst[p][r][c] for r < rows, c < cols (pitch ld_dst, plane
  * stride rows_dst * ld_dst) from src[row_src[r]][c] (row_src NULL: identity). */

@@ -51,7 +51,10 @@ SIGNATURES = {
     "srpgpu_split_bf16_cols": [_P, _I64, _I32, _I64, _I32, _P, _P, _I32, _P],
     "srpgpu_interp_map_gather_tc": [_P, _I64, _I32, _I64, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P,
                                     _P, _P, _P],
+    "srpgpu_interp_map_gather_tf32": [_P, _I64, _I32, _I64, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P,
+                                      _P, _P, _P],
     "srpgpu_split_bf16_rows": [_P, _I64, _I64, _I64, _P, _P, _I64, _I64, _P],
+    "srpgpu_split_tf32_rows": [_P, _I64, _I64, _I64, _P, _P, _I64, _I64, _P],
     "srpgpu_slri_map": [_P, _I64, _I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P],
     "srpgpu_slri_map_tc": [_P, _I64, _I64, _I32, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P],
     "srpgpu_lr_map_tc": [_P, _I64, _I32, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P],

@@ -512,6 +512,10 @@ static int launch_chunked(const float* gcc, int64_t gcc_ld, int64_t F, int32_t K
   SRPGPU_CHECK_ARG(tiles < (1ll << 31), SRPGPU_ERR_DIMENSION, "srp_map_tdoa: too many tiles");
   const int kb_total = (Kd + BLOCK_K - 1) / BLOCK_K;
   ksplit = std::max(1, std::min<int32_t>(ksplit, (kb_total + CHUNK - 1) / CHUNK));
+  {   // slices hold whole chunks: drop the slices that rounding left empty
+    const int kper = ((kb_total + ksplit - 1) / ksplit + CHUNK - 1) / CHUNK * CHUNK;
+    ksplit = (kb_total + kper - 1) / kper;
+  }
   SRPGPU_CHECK_ARG(ksplit == 1 || work, SRPGPU_ERR_VALUE, "srp_map: split-K needs a work buffer");
   kern<<<(unsigned)(tiles * ksplit), kThreadsC, smem, st>>>(mb, mb2, ma, J, F, Kd, z,
                                                             reinterpret_cast<unsigned long long*>(keys), 2.0f, gp,

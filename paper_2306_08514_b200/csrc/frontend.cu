@@ -45,6 +45,7 @@ struct FrontendParams {
   int32_t cols8;
   int32_t xi_natural;         // planes in natural lag order per pair
   int64_t planes_ld;          // 0: frame-major planes; > 0: lag-major [2][cols8][planes_ld]
+  int32_t planes_tf32;        // fp32 hi / lo TF32 planes instead of bf16 (lag-major only)
   int32_t* warp_used;         // set to 1 when the warp-per-frame kernel ran
 };
 
@@ -313,7 +314,7 @@ static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* 
     wp.gcc_out = prm.gcc_out; wp.gcc_ld = prm.gcc_ld; wp.round_tf32 = prm.round_tf32;
     wp.xi_out = prm.xi_out; wp.xi_ld = prm.xi_ld;
     wp.xi_planes = prm.xi_planes; wp.cols8 = prm.cols8; wp.xi_natural = prm.xi_natural;
-    wp.planes_ld = prm.planes_ld;
+    wp.planes_ld = prm.planes_ld; wp.planes_tf32 = prm.planes_tf32;
     const int wout = OUT == OUT_GCC ? W_OUT_GCC : W_OUT_XI;
     const int choice = frontend_kernel_choice();
     int r = 1;
@@ -567,8 +568,10 @@ extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num
   prm.pairs = pairs; prm.P = num_pairs; prm.weighting = weighting; prm.floor_mode = floor_mode;
   prm.floor_value = (float)floor_value; prm.counts = counts; prm.offsets = offsets;
   prm.S = total_samples; prm.xi_out = samples_out; prm.xi_ld = samples_ld;
-  prm.xi_planes = reinterpret_cast<uint16_t*>(planes); prm.cols8 = cols8; prm.xi_natural = natural ? 1 : 0;
-  prm.planes_ld = planes_ld;
+  prm.xi_planes = reinterpret_cast<uint16_t*>(planes); prm.cols8 = cols8; prm.xi_natural = (natural & 1) ? 1 : 0;
+  prm.planes_ld = planes_ld; prm.planes_tf32 = (natural & 2) ? 1 : 0;
+  SRPGPU_CHECK_ARG(!prm.planes_tf32 || planes_ld > 0, SRPGPU_ERR_VALUE,
+                   "frames_to_samples: TF32 planes are lag-major only (planes_ld > 0)");
   SRPGPU_CHECK_ARG(planes_ld == 0 || (planes_ld >= num_frames && planes_ld % 8 == 0), SRPGPU_ERR_VALUE,
                    "frames_to_samples: lag-major planes need a pitch >= F, a multiple of 8");
   SRPGPU_CHECK_ARG(!natural || natural_src, SRPGPU_ERR_VALUE, "frames_to_samples: natural planes need the column map");
@@ -580,11 +583,16 @@ extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num
   if ((st = launch_frontend<IN_SAMPLES, OUT_XI>(prm, as_stream(stream), "frames_to_samples"))) return st;
   if (warp_used || num_frames == 0) return SRPGPU_OK;
   // block-kernel frame lengths: split the f32 samples afterwards
+  if (prm.planes_tf32)
+    return srpgpu_split_tf32_rows(samples_out, samples_ld, total_samples, num_frames,
+                                  prm.xi_natural ? natural_src : nullptr, reinterpret_cast<float*>(planes), planes_ld,
+                                  cols8, stream);
   if (planes_ld)   // lag-major planes from the lag-major f32 samples
-    return srpgpu_split_bf16_rows(samples_out, samples_ld, total_samples, num_frames, natural ? natural_src : nullptr,
-                                  planes, planes_ld, cols8, stream);
+    return srpgpu_split_bf16_rows(samples_out, samples_ld, total_samples, num_frames,
+                                  prm.xi_natural ? natural_src : nullptr, planes, planes_ld, cols8, stream);
   return srpgpu_split_bf16_cols(samples_out, samples_ld ? samples_ld : total_samples, samples_ld ? 1 : 0,
-                                num_frames, total_samples, natural ? natural_src : nullptr, planes, cols8, stream);
+                                num_frames, total_samples, prm.xi_natural ? natural_src : nullptr, planes, cols8,
+                                stream);
 }
 
 extern "C" int srpgpu_spectra_to_samples(const float* spectra, int64_t num_frames,

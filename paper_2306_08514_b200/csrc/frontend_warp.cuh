@@ -32,6 +32,7 @@ struct WarpParams {
   int32_t cols8;
   int32_t xi_natural;   // planes in natural lag order -N_p..N_p per pair (gathered-window engine)
   int64_t planes_ld;    // 0: planes frame-major [2][F][cols8]; > 0: lag-major [2][cols8][planes_ld]
+  int32_t planes_tf32;  // planes are fp32 hi = tf32_rne(x), lo = tf32_rne(x - hi) (lag-major only)
 };
 
 // PHAT weighting raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158), with the
@@ -59,6 +60,13 @@ __device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_
   dst[(o + d) * sst] = v;
   if (prm.xi_planes) {
     const int col = o + (prm.xi_natural ? (d <= N ? N + d : d - N - 1) : d);
+    if (prm.planes_tf32) {                    // lag-major fp32 [2][cols8][planes_ld]
+      float* pl = reinterpret_cast<float*>(prm.xi_planes) + (int64_t)col * prm.planes_ld + f;
+      const float hi = tf32_rne(v);
+      pl[0] = hi;
+      pl[(int64_t)prm.cols8 * prm.planes_ld] = tf32_rne(v - hi);
+      return;
+    }
     const __nv_bfloat16 hi = __float2bfloat16_rn(v);
     const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
     __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(prm.xi_planes);

@@ -93,6 +93,91 @@ __device__ __forceinline__ bool decode(int u, int T, int n_tiles, Unit& out) {
   return out.n < n_tiles;
 }
 
+// Epilogue warps (2 + 4 * half + quarter): per unit, wait for the accumulator, drain the
+// warp's TMEM lane quarter of its tile half 32 frames at a time, store the map (tile order
+// or grid order) and fold the per-frame argmax (butterfly max across the lanes + a ballot
+// for the lowest winning candidate: tile rows are ascending); then free the accumulator.
+__device__ __forceinline__ void epilogue(uint32_t tmem, int warp, int lane, int64_t F, int64_t J, int32_t T,
+                                         int n_tiles, int u_total, uint64_t* tfull, uint64_t* tempty,
+                                         const int32_t* __restrict__ tile_rows, float* __restrict__ zt,
+                                         float* __restrict__ zg, unsigned long long* __restrict__ keys) {
+  const int q = warp & 3;                          // TMEM lane quarter this warp may access
+  const int half = (warp - 2) >> 2;                // which tile half (TMEM columns half * 256)
+  const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
+  const int64_t ldt = (int64_t)T * GT;
+  uint32_t it = 0;
+  for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
+    Unit w;
+    if (!decode(u, T, n_tiles, w)) continue;
+    const int r = half * GM + q * 32 + lane;         // tile row
+    const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);   // -1: padding row
+    mbar_wait(tfull, it & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool any = __any_sync(0xffffffffu, jrow >= 0);
+#pragma unroll 1
+    for (int c = 0; c < GN / 32; ++c) {
+      uint32_t rr[32];
+      tmem_ld32(lane_base + c * 32, rr);
+      const int64_t f0 = (int64_t)w.n * GN + c * 32;
+      if (f0 >= F || !any) continue;               // warp-uniform (after the aligned load)
+      if (zg) {   // grid order: the tile's rows are ascending candidates (runs of neighbours)
+        if (jrow >= 0) {
+          float* zc = zg + f0 * J + jrow;
+          if (f0 + 32 <= F) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) __stcs(zc + t * J, __uint_as_float(rr[t]));
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (f0 + t < F) __stcs(zc + t * J, __uint_as_float(rr[t]));
+          }
+        }
+      } else if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
+        float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
+        if (f0 + 32 <= F) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (f0 + t < F) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
+        }
+      }
+      if (keys) {
+        uint32_t ob[32], v[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = ob[t] = jrow >= 0 ? ordered_bits(__uint_as_float(rr[t])) : 0u;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int t = 0; t < o; ++t) {
+            const uint32_t send = up ? v[t] : v[t + o];
+            const uint32_t keep = up ? v[t + o] : v[t];
+            v[t] = max(keep, __shfl_xor_sync(0xffffffffu, send, o));
+          }
+        }
+        // lane t holds frame f0 + t's maximum in v[0]; the lowest lane (= lowest candidate) wins
+        uint32_t win = 0;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const uint32_t vt = __shfl_sync(0xffffffffu, v[0], t);
+          const uint32_t m = __ballot_sync(0xffffffffu, ob[t] == vt);
+          if (lane == t) win = (uint32_t)(__ffs(m) - 1);
+        }
+        const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
+        if (f0 + lane < F && v[0] != 0u)
+          atomicMax(keys + f0 + lane,
+                    ((unsigned long long)v[0] << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tempty);
+    ++it;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                  const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int64_t F,
@@ -219,80 +304,289 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
       }
     }
   } else {
-    const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;                // which tile half (TMEM columns half * 256)
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
-    const int64_t ldt = (int64_t)T * GT;
-    uint32_t it = 0;
-    for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
-      Unit w;
-      if (!decode(u, T, n_tiles, w)) continue;
-      const int r = half * GM + q * 32 + lane;         // tile row
-      const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);   // -1: padding row
-      mbar_wait(&sm.tfull, it & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const bool any = __any_sync(0xffffffffu, jrow >= 0);
-#pragma unroll 1
-      for (int c = 0; c < GN / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(lane_base + c * 32, rr);
-        const int64_t f0 = (int64_t)w.n * GN + c * 32;
-        if (f0 >= F || !any) continue;               // warp-uniform (after the aligned load)
-        if (zg) {   // grid order: the tile's rows are ascending candidates (runs of neighbours)
-          if (jrow >= 0) {
-            float* zc = zg + f0 * J + jrow;
-            if (f0 + 32 <= F) {
-#pragma unroll
-              for (int t = 0; t < 32; ++t) __stcs(zc + t * J, __uint_as_float(rr[t]));
-            } else {
-#pragma unroll
-              for (int t = 0; t < 32; ++t)
-                if (f0 + t < F) __stcs(zc + t * J, __uint_as_float(rr[t]));
-            }
-          }
-        } else if (zt) {   // tile order: a warp's 32 rows are 128 contiguous bytes of the frame's row
-          float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
-          if (f0 + 32 <= F) {
-#pragma unroll
-            for (int t = 0; t < 32; ++t) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
+    epilogue(tmem, warp, lane, F, J, T, n_tiles, u_total, &sm.tfull, &sm.tempty, tile_rows, zt, zg, keys);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+
+// ---- 3xTF32 variant with fp32 chunk folds (FP32-class) -------------------------------
+// Operands hi = tf32_rne(x), lo = tf32_rne(x - hi) (21+ significant bits; the lo.lo term
+// is dropped).  The tensor pipe's own accumulation is not IEEE fp32: its error grows with
+// the number of MMAs accumulated into one TMEM tile (measured ~1.6e-8 of max|z| per MMA
+// step: 7.3e-6 at cfg4 with whole-tile accumulation), so the MMAs accumulate a CHUNK of
+// CH stages (CH * 2 K steps x 3 passes) into one of two TMEM buffers and the epilogue
+// warps fold each finished chunk into fp32 registers (round-to-nearest adds) while the
+// MMAs fill the other buffer.  Two buffers x two tile halves fit the 512 TMEM columns
+// with units of 128 frames (N = 128).
+//   stage = 16 lags: A (slab) per half and plane 128 rows x 16 lags fp32 (64-byte rows,
+//     64-byte swizzle, 8 KB); B (gathered xi) per plane and group 4 frame blocks of
+//     [8 lags][32 frames] fp32 (1 KB each = two 512-byte atoms of the 32-byte-granular
+//     128-byte swizzle MN-major tf32 requires), all 4 fetched by ONE 3D TMA box
+//     {32 frames, 8 lags, 4 frame blocks} over the lag-major planes viewed as
+//     {32, lags, frames / 32} (fallback: four 2D boxes when the 3D view cannot be encoded).
+namespace g32 {
+constexpr int GK = 16;               // lags per stage
+constexpr int NG = GK / GG;          // groups per stage
+constexpr int GN = 128;              // frames per unit
+constexpr int GA = 32;               // frames per frame block (128 bytes of fp32)
+constexpr int NA = GN / GA;          // frame blocks per group
+constexpr int UK = 8;                // kind::tf32 MMA K
+constexpr int NS = 4;                // operand stages (48 KB each)
+
+struct __align__(1024) Smem {
+  float b[NS][2][NG][GN * GG];       // [plane][group] 4 frame blocks (4 KB)
+  float a[NS][2][2][GM * GK];        // [half][plane] slab columns (8 KB)
+  int32_t rows[2][kMaxGroups];
+  uint64_t full[NS], empty[NS], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+// units (frame-tile group of fg frame tiles, tile, frame tile), frame tile fastest: the
+// group's gathered samples stay L2-resident while every tile's slabs stream through once
+__device__ __forceinline__ bool decode32(int u, int T, int fg, int n_tiles, Unit& out) {
+  const int per = T * fg;
+  const int g = u / per, rem = u - g * per;
+  out.t = rem / fg;
+  out.n = g * fg + (rem - out.t * fg);
+  return out.n < n_tiles;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// MN-major fp32 operand: tf32 takes only the 128-byte swizzle with 32-byte atoms
+// (SWIZZLE_128B_BASE32B, layout type 1; the TMA side is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
+// 512-byte atoms of 4 K rows x 32 frames.  A group's 8 lags x 32 frames are two atoms,
+// 512 B apart (SBO, along K); the next 32 frames are 1 KB on (LBO, along N).
+__device__ __forceinline__ uint64_t desc_mn128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(1024 >> 4) << 16;            // LBO: next 32 frames
+  d |= (uint64_t)(512 >> 4) << 32;             // SBO: next 4 lags
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;                      // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// chunks of a tile with nk 64-lag blocks
+__device__ __forceinline__ int num_chunks(int nk, int ch) { return ((GB / GK) * nk + ch - 1) / ch; }
+
+__global__ void __launch_bounds__(kThreads, 1)
+gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                   const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int b3d,
+                   int fg, int CH, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                   const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
+                   const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
+                   unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)((F + GN - 1) / GN);
+  const int u_total = ((n_tiles + fg - 1) / fg) * T * fg;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ma_hi);
+    prefetch_tmap(&ma_lo);
+    prefetch_tmap(&mb_hi);
+    prefetch_tmap(&mb_lo);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.tfull[b], 1);
+      mbar_init(&sm.tempty[b], kEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // lanes 0-3: one (plane, group) of gathered samples each; lanes 4-7: one (half, plane) slab
+    constexpr uint32_t kBytes = 2u * (2 * GM * GK + GN * GK) * sizeof(float);
+    const int plane = (lane >> 1) & 1, grp = lane & 1;
+    const int ah = ((lane - 4) >> 1) & 1, ap = (lane - 4) & 1;
+    const uint64_t keep = policy_evict_last();
+    auto next_unit = [&](int u, Unit& w) {
+      while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += gridDim.x;
+      return u;
+    };
+    auto stage_rows = [&](int buf, const Unit& w) {
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int i = lane; i < nk * (GB / GG); i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
+    };
+    uint32_t g = 0;
+    int buf = 0;
+    Unit w;
+    int u = next_unit(blockIdx.x, w);
+    if (u < u_total) stage_rows(0, w);
+    while (u < u_total) {
+      Unit wn;
+      const int un = next_unit(u + gridDim.x, wn);
+      if (un < u_total) stage_rows(buf ^ 1, wn);
+      __syncwarp();
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int kq = 0; kq < (GB / GK) * nk; ++kq, ++g) {     // 16-lag stages: a quarter block each
+        const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
+        const int row = sm.rows[buf][kq * NG + grp];
+        const int s = g % NS;
+        if (lane == 0) {
+          mbar_wait(&sm.empty[s], ((g / NS) & 1) ^ 1);
+          mbar_expect_tx(&sm.full[s], kBytes);
+        }
+        __syncwarp();
+        if (lane < 4) {
+          const CUtensorMap* mb = plane ? &mb_lo : &mb_hi;
+          if (b3d) {
+            tma_load_3d(sm.b[s][plane][grp], mb, &sm.full[s], 0, row, w.n * NA);
           } else {
 #pragma unroll
-            for (int t = 0; t < 32; ++t)
-              if (f0 + t < F) __stcs(zc + t * ldt, __uint_as_float(rr[t]));
+            for (int a = 0; a < NA; ++a)
+              tma_load_2d(sm.b[s][plane][grp] + a * GA * GG, mb, &sm.full[s], w.n * GN + a * GA, row);
           }
-        }
-        if (keys) {
-          uint32_t ob[32], v[32];
-#pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] = ob[t] = jrow >= 0 ? ordered_bits(__uint_as_float(rr[t])) : 0u;
-#pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) {
-            const bool up = (lane & o) != 0;
-#pragma unroll
-            for (int t = 0; t < o; ++t) {
-              const uint32_t send = up ? v[t] : v[t + o];
-              const uint32_t keep = up ? v[t + o] : v[t];
-              v[t] = max(keep, __shfl_xor_sync(0xffffffffu, send, o));
-            }
-          }
-          // lane t holds frame f0 + t's maximum in v[0]; the lowest lane (= lowest candidate) wins
-          uint32_t win = 0;
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const uint32_t vt = __shfl_sync(0xffffffffu, v[0], t);
-            const uint32_t m = __ballot_sync(0xffffffffu, ob[t] == vt);
-            if (lane == t) win = (uint32_t)(__ffs(m) - 1);
-          }
-          const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
-          if (f0 + lane < F && v[0] != 0u)
-            atomicMax(keys + f0 + lane,
-                      ((unsigned long long)v[0] << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+        } else if (lane < 8) {
+          tma_load_2d_hint(sm.a[s][ah][ap], ap ? &ma_lo : &ma_hi, &sm.full[s], sub * GK, (2 * blk + ah) * GM, keep);
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty);
-      ++it;
+      buf ^= 1;
+      u = un;
+      w = wn;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // D f32, A/B tf32, A K-major, B MN-major (bit 16), N = 128, M = 128
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(GN >> 3) << 17) |
+                                 ((uint32_t)(GM >> 4) << 24);
+      uint32_t g = 0, c = 0;     // stage and chunk counters (chunk c uses TMEM buffer c & 1)
+      for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
+        Unit w;
+        if (!decode32(u, T, fg, n_tiles, w)) continue;
+        const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
+        for (int kq = 0; kq < ns; ++kq, ++g) {
+          const int s = g % NS;
+          const int first = kq % CH == 0;
+          if (first) {
+            mbar_wait(&sm.tempty[c & 1], ((c >> 1) & 1) ^ 1);    // the epilogue folded this buffer
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          mbar_wait(&sm.full[s], (g / NS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t dbuf = tmem + (c & 1) * 256;
+#pragma unroll
+          for (int k = 0; k < GK / UK; ++k) {
+            const uint64_t aoff = (uint64_t)((k * UK * 4) >> 4);
+            const uint64_t bh = desc_mn128(sm.b[s][0][k]), bl = desc_mn128(sm.b[s][1][k]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t d = dbuf + h * GN;
+              const uint64_t a_h = smem_desc_sw64(sm.a[s][h][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][h][1]) + aoff;
+              mma_tf32(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
+              mma_tf32(d, a_h, bl, idesc, 1u);
+              mma_tf32(d, a_l, bh, idesc, 1u);
+            }
+          }
+          mma_commit(&sm.empty[s]);
+          if (kq % CH == CH - 1 || kq == ns - 1) {
+            mma_commit(&sm.tfull[c & 1]);
+            ++c;
+          }
+        }
+      }
+    }
+  } else {
+    // epilogue: warp = (half, TMEM lane quarter); each thread folds its candidate row's
+    // 128 frames of every chunk into fp32 registers, then stores the unit's map (tile
+    // order) and folds the per-frame argmax as the bf16 kernel's epilogue does
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
+    const int64_t ldt = (int64_t)T * GT;
+    uint32_t c = 0;
+    for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
+      Unit w;
+      if (!decode32(u, T, fg, n_tiles, w)) continue;
+      const int r = half * GM + q * 32 + lane;
+      const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);
+      const int nc = num_chunks(__ldg(tile_nkb + w.t), CH);
+      float rs[GN];
+      for (int j = 0; j < nc; ++j, ++c) {
+        mbar_wait(&sm.tfull[c & 1], (c >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = lane_base + (c & 1) * 256;
+#pragma unroll
+        for (int cc = 0; cc < GN / 32; ++cc) {
+          uint32_t rr[32];
+          tmem_ld32(base + cc * 32, rr);
+          if (j == 0) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) rs[cc * 32 + t] = __uint_as_float(rr[t]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) rs[cc * 32 + t] += __uint_as_float(rr[t]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[c & 1]);
+      }
+      const bool any = __any_sync(0xffffffffu, jrow >= 0);
+      if (!any) continue;
+#pragma unroll
+      for (int cc = 0; cc < GN / 32; ++cc) {
+        const int64_t f0 = (int64_t)w.n * GN + cc * 32;
+        if (f0 >= F) break;
+        if (zg) {
+          if (jrow >= 0) {
+            float* zc = zg + f0 * J + jrow;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (f0 + t < F) __stcs(zc + t * J, rs[cc * 32 + t]);
+          }
+        } else if (zt) {
+          float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (f0 + t < F) __stcs(zc + t * ldt, rs[cc * 32 + t]);
+        }
+        if (keys) {   // per frame: warp max of the ordered bits (redux), lowest winning lane (ballot)
+          uint32_t best = 0u, win = 0u;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const uint32_t mine = jrow >= 0 ? ordered_bits(rs[cc * 32 + t]) : 0u;
+            const uint32_t m = __reduce_max_sync(0xffffffffu, mine);
+            const uint32_t who = __ballot_sync(0xffffffffu, mine == m);
+            if (lane == t) {
+              best = m;
+              win = (uint32_t)(__ffs(who) - 1);
+            }
+          }
+          const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
+          if (f0 + lane < F && best != 0u)
+            atomicMax(keys + f0 + lane,
+                      ((unsigned long long)best << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -302,6 +596,245 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
 }
+// ---- the same on CTA pairs (cta_group::2, a 2-CTA cluster per tile) ---------------------
+// One tcgen05.mma.cta_group::2 (M = 256 candidates, N = 256 frames, K = 8) covers the whole
+// tile: CTA r of the pair holds tile half r (rows 128r..128r+127) of the slabs and frames
+// 128r..128r+127 of the unit's gathered samples, so each SM streams half the operand bytes
+// of the one-CTA kernel per MMA (32 KB per 16-lag stage), and its accumulator is its 128
+// candidates x 256 frames, which leaves room for the two fold buffers.  The leader (rank
+// 0) issues the MMAs; both CTAs' TMA loads complete on the leader's stage barrier, the MMA
+// commits arrive on both CTAs' barriers, and both CTAs' epilogues release a fold buffer on
+// the leader's barrier.
+constexpr int PN = 256;              // frames per unit (pair)
+constexpr int PNC = PN / 2;          // frames per CTA (B half)
+constexpr int PNA = PNC / GA;        // frame blocks per group per CTA
+constexpr int PNS = 6;               // operand stages (32 KB each)
+constexpr int PEpi = kEpi;          // epilogue warps
+constexpr int PThreads = kThreads;
+constexpr int PCols = PN / (PEpi / 4);         // accumulator columns folded per epilogue thread
+
+struct __align__(1024) PairSmem {
+  float b[PNS][2][NG][PNC * GG];     // [plane][group] 4 frame blocks (4 KB)
+  float a[PNS][2][GM * GK];          // [plane] this CTA's slab half (8 KB)
+  int32_t rows[2][kMaxGroups];
+  uint64_t full[PNS], empty[PNS], tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
+gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                        const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+                        int fg, int CH, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                        const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
+                        const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
+                        unsigned long long* __restrict__ keys) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  PairSmem& sm = *reinterpret_cast<PairSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int n_tiles = (int)((F + PN - 1) / PN);
+  const int u_total = ((n_tiles + fg - 1) / fg) * T * fg;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ma_hi);
+    prefetch_tmap(&ma_lo);
+    prefetch_tmap(&mb_hi);
+    prefetch_tmap(&mb_lo);
+    for (int s = 0; s < PNS; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.tfull[b], 1);
+      mbar_init(&sm.tempty[b], 2 * PEpi);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // lanes 0-3: (plane, group) of this CTA's frame half; lanes 4-5: this CTA's slab half
+    constexpr uint32_t kBytes = 2u * (GM * GK + PNC * GK) * sizeof(float);   // one CTA's stage
+    const int plane = (lane >> 1) & 1, grp = lane & 1, ap = (lane - 4) & 1;
+    const uint64_t keep = policy_evict_last();
+    auto next_unit = [&](int u, Unit& w) {
+      while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += ncl;
+      return u;
+    };
+    auto stage_rows = [&](int buf, const Unit& w) {
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int i = lane; i < nk * (GB / GG); i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
+    };
+    uint32_t g = 0;
+    int buf = 0;
+    Unit w;
+    int u = next_unit(cid, w);
+    if (u < u_total) stage_rows(0, w);
+    while (u < u_total) {
+      Unit wn;
+      const int un = next_unit(u + ncl, wn);
+      if (un < u_total) stage_rows(buf ^ 1, wn);
+      __syncwarp();
+      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
+      for (int kq = 0; kq < (GB / GK) * nk; ++kq, ++g) {
+        const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
+        const int row = sm.rows[buf][kq * NG + grp];
+        const int s = g % PNS;
+        const uint32_t bar = mapa_shared(smem_u32(&sm.full[s]), 0);    // the leader's stage barrier
+        if (lane == 0) {
+          mbar_wait(&sm.empty[s], ((g / PNS) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * kBytes);     // both CTAs' loads
+        }
+        __syncwarp();
+        if (lane < 4) {
+          tma_load_3d_pair(sm.b[s][plane][grp], plane ? &mb_lo : &mb_hi, bar, 0, row,
+                           w.n * (PN / GA) + (int)rank * PNA);
+        } else if (lane < 6) {
+          tma_load_2d_pair(sm.a[s][ap], ap ? &ma_lo : &ma_hi, bar, sub * GK, (2 * blk + (int)rank) * GM, keep);
+        }
+      }
+      __syncwarp();
+      buf ^= 1;
+      u = un;
+      w = wn;
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      // D f32, A/B tf32, A K-major, B MN-major (bit 16), N = 256, M = 256 (the pair)
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(PN >> 3) << 17) |
+                                 ((uint32_t)((2 * GM) >> 4) << 24);
+      uint32_t g = 0, c = 0;
+      for (int u = cid; u < u_total; u += ncl) {
+        Unit w;
+        if (!decode32(u, T, fg, n_tiles, w)) continue;
+        const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
+        for (int kq = 0; kq < ns; ++kq, ++g) {
+          const int s = g % PNS;
+          const int first = kq % CH == 0;
+          if (first) {
+            mbar_wait(&sm.tempty[c & 1], ((c >> 1) & 1) ^ 1);    // both epilogues folded this buffer
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          mbar_wait(&sm.full[s], (g / PNS) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + (c & 1) * PN;
+#pragma unroll
+          for (int k = 0; k < GK / UK; ++k) {
+            const uint64_t aoff = (uint64_t)((k * UK * 4) >> 4);
+            const uint64_t bh = desc_mn128(sm.b[s][0][k]), bl = desc_mn128(sm.b[s][1][k]);
+            const uint64_t a_h = smem_desc_sw64(sm.a[s][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][1]) + aoff;
+            mma_tf32_pair(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
+            mma_tf32_pair(d, a_h, bl, idesc, 1u);
+            mma_tf32_pair(d, a_l, bh, idesc, 1u);
+          }
+          mma_commit_pair(&sm.empty[s]);
+          if (kq % CH == CH - 1 || kq == ns - 1) {
+            mma_commit_pair(&sm.tfull[c & 1]);
+            ++c;
+          }
+        }
+      }
+    }
+  } else {
+    // epilogue: warp = (column half ch, TMEM lane quarter q) of this CTA's 128 candidates x
+    // 256 frames; folds every chunk into fp32 registers, then map + argmax as above
+    const int q = warp & 3;
+    const int ch = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * PCols);
+    const int64_t ldt = (int64_t)T * GT;
+    uint32_t c = 0;
+    for (int u = cid; u < u_total; u += ncl) {
+      Unit w;
+      if (!decode32(u, T, fg, n_tiles, w)) continue;
+      const int r = (int)rank * GM + q * 32 + lane;
+      const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);
+      const int nc = num_chunks(__ldg(tile_nkb + w.t), CH);
+      float rs[PCols];
+      for (int j = 0; j < nc; ++j, ++c) {
+        mbar_wait(&sm.tfull[c & 1], (c >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = lane_base + (c & 1) * PN;
+#pragma unroll
+        for (int cc = 0; cc < PCols / 32; ++cc) {
+          uint32_t rr[32];
+          tmem_ld32(base + cc * 32, rr);
+          if (j == 0) {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) rs[cc * 32 + t] = __uint_as_float(rr[t]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) rs[cc * 32 + t] += __uint_as_float(rr[t]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sm.tempty[c & 1]), 0));
+      }
+      const bool any = __any_sync(0xffffffffu, jrow >= 0);
+      if (!any) continue;
+#pragma unroll
+      for (int cc = 0; cc < PCols / 32; ++cc) {
+        const int64_t f0 = (int64_t)w.n * PN + ch * PCols + cc * 32;
+        if (f0 >= F) break;
+        if (zg) {
+          if (jrow >= 0) {
+            float* zc = zg + f0 * J + jrow;
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (f0 + t < F) __stcs(zc + t * J, rs[cc * 32 + t]);
+          }
+        } else if (zt) {
+          float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (f0 + t < F) __stcs(zc + t * ldt, rs[cc * 32 + t]);
+        }
+        if (keys) {   // per frame: warp max of the ordered bits (redux), lowest winning lane (ballot)
+          uint32_t best = 0u, win = 0u;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const uint32_t mine = jrow >= 0 ? ordered_bits(rs[cc * 32 + t]) : 0u;
+            const uint32_t m = __reduce_max_sync(0xffffffffu, mine);
+            const uint32_t who = __ballot_sync(0xffffffffu, mine == m);
+            if (lane == t) {
+              best = m;
+              win = (uint32_t)(__ffs(who) - 1);
+            }
+          }
+          const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
+          if (f0 + lane < F && best != 0u)
+            atomicMax(keys + f0 + lane,
+                      ((unsigned long long)best << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+}
+}  // namespace g32
 
 #ifndef UNTILE_U
 #define UNTILE_U 4
@@ -349,6 +882,19 @@ static int untile_frames(int64_t num_frames) {
   }();
   if (forced) return forced;
   return num_frames >= 4096 ? 4 : 1;
+}
+
+static int untile(const float* z_tiles, int32_t num_tiles, const int32_t* tile_pos, int64_t num_candidates,
+                  int64_t num_frames, float* z, cudaStream_t st) {
+  const int fb = untile_frames(num_frames);
+  dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
+            (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
+  const int64_t ldt = (int64_t)num_tiles * GT;
+  if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+  else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+  else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+  SRPGPU_CHECK_LAUNCH("interp_map_gather(untile)");
+  return SRPGPU_OK;
 }
 
 }  // namespace gtc
@@ -403,15 +949,116 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
       ma_hi, ma_lo, mb_hi, mb_lo, num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nkb, tile_rows,
       z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH("interp_map_gather_tc");
-  if (z && z_tiles) {
-    const int fb = untile_frames(num_frames);
-    dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
-              (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
-    const int64_t ldt = (int64_t)num_tiles * GT;
-    if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
-    else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
-    else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
-    SRPGPU_CHECK_LAUNCH("interp_map_gather_tc(untile)");
+  if (z && z_tiles && (s = gtc::untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
+                                             int64_t planes_ld, const float* slab_planes, int64_t num_slabs,
+                                             const int32_t* group_col, const int32_t* tile_slab,
+                                             const int32_t* tile_nkb, const int32_t* tile_rows, int32_t num_tiles,
+                                             int64_t num_candidates, int32_t num_ctas, const int32_t* tile_pos,
+                                             float* z_tiles, float* z, uint64_t* keys, srpgpu_stream_t stream) {
+  using namespace gtc;
+  SRPGPU_CHECK_ARG(num_frames >= 0 && num_cols >= 1 && planes_ld >= num_frames && planes_ld % 32 == 0 &&
+                       num_slabs >= 0 && num_tiles >= 0 && num_candidates >= 1 && num_ctas >= 0,
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_tf32: bad shape (planes pitch: a multiple of 32 >= F)");
+  SRPGPU_CHECK_ARG(((uintptr_t)samples_planes & 127) == 0 && ((uintptr_t)slab_planes & 15) == 0 &&
+                       ((uintptr_t)group_col & 15) == 0,
+                   SRPGPU_ERR_VALUE, "interp_map_gather_tf32: operands must be aligned (samples 128 B, slabs 16 B)");
+  SRPGPU_CHECK_ARG(num_frames < (1ll << 31) && num_candidates < (1ll << 31) && num_slabs * GM < (1ll << 31),
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_tf32: too large");
+  SRPGPU_CHECK_ARG(!z || !z_tiles || tile_pos, SRPGPU_ERR_VALUE,
+                   "interp_map_gather_tf32: a tile-order map needs tile_pos");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  if (num_frames == 0 || num_tiles == 0 || num_ctas == 0) return SRPGPU_OK;
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const int64_t arows = num_slabs * GM;
+  const int64_t c8 = (int64_t)((num_cols + 7) / 8 * 8);   // planes hold round8(S) rows each
+  const float* xs_lo = samples_planes + c8 * planes_ld;
+  if ((s = make_map_2d(&ma_hi, f32, 4, slab_planes, arows, GB, GB, g32::GK, GM, "interp_map_gather_tf32",
+                       CU_TENSOR_MAP_SWIZZLE_64B)) ||
+      (s = make_map_2d(&ma_lo, f32, 4, slab_planes + arows * GB, arows, GB, GB, g32::GK, GM,
+                       "interp_map_gather_tf32", CU_TENSOR_MAP_SWIZZLE_64B)))
+    return s;
+  // gathered samples: one 3D box per (plane, group) when the {32, lags, frame blocks} view encodes
+  const CUtensorMapSwizzle sw32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  int b3d = getenv("SRPGPU_GATHER_2D") ? 0 : 1;
+  {
+    const int64_t dims[3] = {g32::GA, num_cols, planes_ld / g32::GA};
+    const int box[3] = {g32::GA, GG, g32::NA};
+    if (make_map_3d(&mb_hi, f32, samples_planes, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32",
+                    sw32) ||
+        make_map_3d(&mb_lo, f32, xs_lo, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32", sw32))
+      b3d = 0;
   }
+  if (!b3d && ((s = make_map_2d(&mb_hi, f32, 4, samples_planes, num_cols, num_frames, planes_ld, g32::GA, GG,
+                                "interp_map_gather_tf32", sw32)) ||
+               (s = make_map_2d(&mb_lo, f32, 4, xs_lo, num_cols, num_frames, planes_ld, g32::GA, GG,
+                                "interp_map_gather_tf32", sw32))))
+    return s;
+  // CTA pairs (cta_group::2) unless SRPGPU_GATHER_PAIR=0 or no 2-CTA cluster fits; persistent
+  // grid = the co-resident clusters
+  static const int pair_env = [] {
+    const char* v = getenv("SRPGPU_GATHER_PAIR");
+    return v ? atoi(v) : 1;
+  }();
+  // frames per unit group: their fp32 hi / lo samples (F_g x S x 8 B; 58 MB at cfg4 with
+  // 1024 frames) stay L2-resident next to the slabs in flight (SRPGPU_GATHER_GROUP overrides)
+  static const int64_t frames_per_group = [] {
+    const char* v = getenv("SRPGPU_GATHER_GROUP");
+    const int64_t x = v ? atoll(v) : 0;
+    return x >= 256 && x % 256 == 0 ? x : (int64_t)1024;
+  }();
+  // 16-lag stages per TMEM accumulation chunk (fp32 fold; SRPGPU_GATHER_CHUNK overrides)
+  static const int chunk = [] {
+    const char* v = getenv("SRPGPU_GATHER_CHUNK");
+    const int x = v ? atoi(v) : 0;
+    return x >= 1 && x <= 64 ? x : 8;
+  }();
+  int clusters = 0;
+  if (pair_env && b3d) {
+    const size_t psmem = sizeof(g32::PairSmem) + 1024;
+    if (cudaFuncSetAttribute(g32::gather_tf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)psmem) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3((unsigned)(num_ctas & ~1));
+      cfg.blockDim = dim3(g32::PThreads);
+      cfg.dynamicSmemBytes = psmem;
+      cfg.stream = st;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&clusters, g32::gather_tf32_pair_kernel, &cfg) != cudaSuccess) clusters = 0;
+      cudaGetLastError();
+      clusters = std::min(clusters, num_ctas / 2);
+    }
+  }
+  if (clusters > 0) {
+    g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
+        ma_hi, ma_lo, mb_hi, mb_lo, frames_per_group / g32::PN, chunk, num_frames, num_candidates, num_tiles, group_col,
+        tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
+        reinterpret_cast<unsigned long long*>(keys));
+  } else {
+    const size_t smem = sizeof(g32::Smem) + 1024;
+    if (cudaFuncSetAttribute(g32::gather_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
+      return SRPGPU_ERR_LAUNCH;
+    }
+    g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
+        ma_hi, ma_lo, mb_hi, mb_lo, b3d, frames_per_group / g32::GN, chunk, num_frames, num_candidates, num_tiles,
+        group_col, tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
+        reinterpret_cast<unsigned long long*>(keys));
+  }
+  SRPGPU_CHECK_LAUNCH("interp_map_gather_tf32");
+  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
   return SRPGPU_OK;
 }

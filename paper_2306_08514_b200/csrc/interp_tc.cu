@@ -286,6 +286,20 @@ __global__ void split_rows_kernel(const float* __restrict__ src, int64_t ld_src,
   }
 }
 
+// the same into fp32 TF32 hi / lo planes: hi = tf32_rne(x), lo = tf32_rne(x - hi)
+__global__ void split_rows_tf32_kernel(const float* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
+                                       const int32_t* __restrict__ row_src, float* __restrict__ dst, int64_t ld_dst,
+                                       int64_t plane) {
+  const int64_t r = blockIdx.y;
+  const int64_t rs = row_src ? __ldg(row_src + r) : r;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+    const float x = __ldg(src + rs * ld_src + c);
+    const float hi = tf32_rne(x);
+    dst[r * ld_dst + c] = hi;
+    dst[plane + r * ld_dst + c] = tf32_rne(x - hi);
+  }
+}
+
 }  // namespace itc
 
 int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
@@ -331,6 +345,25 @@ extern "C" int srpgpu_split_bf16_rows(const float* src, int64_t ld_src, int64_t 
                                                  reinterpret_cast<__nv_bfloat16*>(dst) + r0 * ld_dst, ld_dst,
                                                  rows_dst * ld_dst);
     SRPGPU_CHECK_LAUNCH("split_bf16_rows");
+  }
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_split_tf32_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                      const int32_t* row_src, float* dst, int64_t ld_dst, int64_t rows_dst,
+                                      srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rows >= 0 && cols >= 0 && ld_src >= cols && ld_dst >= cols && rows_dst >= rows, SRPGPU_ERR_DIMENSION,
+                   "split_tf32_rows: bad shape");
+  SRPGPU_CHECK_ARG(((uintptr_t)dst & 15) == 0, SRPGPU_ERR_VALUE, "split_tf32_rows: destination must be 16-byte aligned");
+  if (rows == 0 || cols == 0) return SRPGPU_OK;
+  cudaStream_t st = as_stream(stream);
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((cols + 255) / 256, 64), (unsigned)nr);
+    itc::split_rows_tf32_kernel<<<grid, 256, 0, st>>>(row_src ? src : src + r0 * ld_src, ld_src, nr, cols,
+                                                      row_src ? row_src + r0 : nullptr, dst + r0 * ld_dst, ld_dst,
+                                                      rows_dst * ld_dst);
+    SRPGPU_CHECK_LAUNCH("split_tf32_rows");
   }
   return SRPGPU_OK;
 }

@@ -32,9 +32,11 @@ from .sampling import TdGccSamples, spec_offsets
 
 # ----------------------------------------------------------------- helpers
 
-def _new_keys(frames: int, want: bool):
+def _new_keys(frames: int, want: bool, num_candidates: int | None = None):
     if not want:
         return None
+    if num_candidates == 0:     # np.argmax of an empty map raises (srp.py:74-80)
+        raise ValueError("attempt to get argmax of an empty sequence (the map has no candidates)")
     return torch.empty(frames, dtype=torch.int64, device=dev.device())
 
 
@@ -242,7 +244,7 @@ def band_from_dense(interp, offsets: np.ndarray) -> BandOperator:
 def _band_map(op: BandOperator, samples, argmax: bool, out_map: bool):
     buf, f, batched = _lag_major(samples, op.num_cols)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=buf.device) if out_map else None
-    keys = _new_keys(f, argmax)
+    keys = _new_keys(f, argmax, op.num_rows)
     if op.num_rows == 0:
         return _finish(z, keys, batched, argmax)
     nat.call("srpgpu_sspi_map", dev.ptr(buf), buf.shape[1], f, op.num_cols, op.num_pairs,
@@ -263,7 +265,7 @@ def _check_cols(samples, num_cols: int) -> None:
 
 # ----------------------------------------------------------------- SSPI / SI on tensor cores
 
-ENGINES = ("auto", "tc", "tile", "band")
+ENGINES = ("auto", "tc", "tile", "tile_bf16", "band")
 TC_MAX_COLS = 2048          # dense rows beyond this many samples: gathered windows ("tile") or band
 TC_DENSITY = 12             # dense tensor cores while cols8 <= TC_DENSITY * kept entries per row
 TILE_DENSITY = 4            # gathered windows while the kept entries per row are sparse
@@ -321,8 +323,9 @@ TC_MIN_FRAMES = 0           # batches below this take the band engine (set from 
 
 def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None,
                   pairs: bool = True) -> str:
-    """'tc' (dense operator on the tensor cores), 'tile' (per-tile gathered lag windows on
-    the tensor cores, for long sample vectors) or 'band' (tiled-band SpMM on FP32)."""
+    """'tc' (dense operator on the tensor cores, bf16x3), 'tile' (per-tile gathered lag
+    windows on the tensor cores in 3xTF32, for long sample vectors; 'tile_bf16': the same
+    in bf16x3, opt-in) or 'band' (tiled-band SpMM on FP32)."""
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}")
     if engine != "auto":
@@ -338,24 +341,32 @@ def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", fram
 
 
 class TileOperator:
-    """Device image of the gathered-window operator (tiles.TileLayout) for engine "tile"."""
+    """Device image of the gathered-window operator (tiles.TileLayout) for engines "tile"
+    (3xTF32: fp32 slab planes hi = tf32_rne(v), lo = tf32_rne(v - hi)) and "tile_bf16"
+    (bf16 hi / lo slab planes)."""
 
     MAX_BLOCKS = 128            # 64-lag operator blocks per tile (interp_gather_tc.cu kMaxBlocks)
 
-    def __init__(self, sp, offsets, num_rows: int):
+    def __init__(self, sp, offsets, num_rows: int, tf32: bool = True):
         lay = tiles.TileLayout(sp, offsets, num_rows)
         if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
             raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
                              f"(> {self.MAX_BLOCKS}): use engine 'band'")
         d = dev.device()
+        self.tf32 = bool(tf32)
         self.num_rows, self.num_cols, self.cols8 = int(num_rows), int(lay.num_cols), _cols8(lay.num_cols)
         self.num_tiles, self.num_slabs, self.mean_k = lay.num_tiles, lay.num_slabs, lay.mean_k
-        self.planes = torch.empty((2, max(1, lay.num_slabs) * tiles.HALF, tiles.SLAB), dtype=torch.bfloat16,
+        rows = max(1, lay.num_slabs) * tiles.HALF
+        self.planes = torch.empty((2, rows, tiles.SLAB), dtype=torch.float32 if self.tf32 else torch.bfloat16,
                                   device=d)
         if lay.num_slabs:
             src = torch.from_numpy(lay.slabs.reshape(-1, tiles.SLAB)).to(d)
-            nat.call("srpgpu_split_bf16", dev.ptr(src), tiles.SLAB, 0, src.shape[0], tiles.SLAB,
-                     dev.ptr(self.planes), tiles.SLAB, dev.stream_ptr())
+            if self.tf32:
+                nat.call("srpgpu_split_tf32", dev.ptr(src), tiles.SLAB, dev.ptr(self.planes), tiles.SLAB,
+                         src.shape[0], tiles.SLAB, dev.stream_ptr())
+            else:
+                nat.call("srpgpu_split_bf16", dev.ptr(src), tiles.SLAB, 0, src.shape[0], tiles.SLAB,
+                         dev.ptr(self.planes), tiles.SLAB, dev.stream_ptr())
             del src
         self.group_col = dev.as_i32(lay.group_col if lay.group_col.size else np.zeros(8, np.int32))
         self.tile_slab = dev.as_i32(lay.tile_slab)
@@ -366,10 +377,10 @@ class TileOperator:
         lay.slabs = None                      # host copy no longer needed
 
 
-def tile_from_sparse(sp, offsets: np.ndarray) -> TileOperator:
+def tile_from_sparse(sp, offsets: np.ndarray, tf32: bool = True) -> TileOperator:
     num_rows = int(sp.values.shape[1]) if np.ndim(sp.values) == 3 else int(np.asarray(sp.row_splits).shape[0] - 1)
-    return dev.CACHE.get(sp, ("tile_bf16x2", tuple(int(o) for o in offsets)),
-                         lambda: TileOperator(sp, offsets, num_rows))
+    return dev.CACHE.get(sp, ("tile_tf32x3" if tf32 else "tile_bf16x3", tuple(int(o) for o in offsets)),
+                         lambda: TileOperator(sp, offsets, num_rows, tf32))
 
 
 # Gathered-window maps straight into grid order (no untile pass): measured 2.3x SLOWER at
@@ -379,21 +390,22 @@ TILE_GRID_ORDER = False
 
 
 def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
-    planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets)
+    planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets, tf32=op.tf32)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
     zt = (torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
           if out_map and not TILE_GRID_ORDER else None)
     keys = _new_keys(f, argmax)
-    nat.call("srpgpu_interp_map_gather_tc", dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes),
-             op.num_slabs,
+    fn = "srpgpu_interp_map_gather_tf32" if op.tf32 else "srpgpu_interp_map_gather_tc"
+    nat.call(fn, dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
              dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
              op.num_tiles, op.num_rows, dev.num_sms(), dev.ptr(op.tile_pos), dev.ptr(zt), dev.ptr(z),
              dev.ptr(keys), dev.stream_ptr())
     return _finish(z, keys, batched, argmax)
 
 
-def sample_planes(samples, num_cols: int, natural=None):
-    """(bf16 planes, frames, batched) of any samples input.
+def sample_planes(samples, num_cols: int, natural=None, tf32: bool = False):
+    """(planes, frames, batched) of any samples input (bf16 hi / lo; `tf32`: fp32 TF32 hi / lo,
+    natural lag-major only).
 
     natural None: frame-major planes [2][F][cols8] in storage column order (dense engine);
     natural = the pair offsets: lag-major planes [2][cols8][F8] in natural lag order
@@ -403,7 +415,7 @@ def sample_planes(samples, num_cols: int, natural=None):
     planes = getattr(samples, "bf16_planes", None)
     c8 = _cols8(num_cols)
     if planes is not None and bool(getattr(samples, "planes_natural", False)) == want_nat and \
-            planes.shape[1 if want_nat else 2] == c8:
+            bool(getattr(samples, "planes_tf32", False)) == bool(tf32) and planes.shape[1 if want_nat else 2] == c8:
         vals = samples.values
         batched = vals.dim() == 2
         return planes, (vals.shape[0] if batched else 1), batched
@@ -414,6 +426,12 @@ def sample_planes(samples, num_cols: int, natural=None):
         if src is None:
             src = _NAT_SRC.setdefault(key, dev.as_i32(tiles.natural_columns(np.asarray(natural))))
         buf, f, batched = _lag_major(samples, num_cols)
+        if tf32:
+            f32 = (f + 31) // 32 * 32
+            planes = torch.empty((2, c8, f32), dtype=torch.float32, device=buf.device)
+            nat.call("srpgpu_split_tf32_rows", dev.ptr(buf), buf.shape[1], num_cols, f, dev.ptr(src),
+                     dev.ptr(planes), f32, c8, dev.stream_ptr())
+            return planes, f, batched
         f8 = (f + 7) // 8 * 8
         planes = torch.empty((2, c8, f8), dtype=torch.bfloat16, device=buf.device)
         nat.call("srpgpu_split_bf16_rows", dev.ptr(buf), buf.shape[1], num_cols, f, dev.ptr(src), dev.ptr(planes),
@@ -441,7 +459,7 @@ _NAT_SRC: dict = {}
 def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
     planes, f, batched = sample_planes(samples, op.num_cols)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
-    keys = _new_keys(f, argmax)
+    keys = _new_keys(f, argmax, op.num_rows)
     if op.num_rows == 0:
         return _finish(z, keys, batched, argmax)
     nat.call("srpgpu_interp_map_tc", dev.ptr(planes), f, dev.ptr(op.planes), op.num_rows, op.cols8,
@@ -460,9 +478,17 @@ def map_engine(variant: str, op, engine: str = "auto", frames: int | None = None
     return None
 
 
+def plane_args(engine: str) -> dict:
+    """frames_to_samples keywords that make the frontend also write the operand planes the
+    map engine reads (bf16 frame-major for "tc", natural lag-major bf16 / TF32 for the
+    gathered-window engines)."""
+    return {"planes": engine in ("tc", "tile", "tile_bf16"), "natural": engine in ("tile", "tile_bf16"),
+            "tf32": engine == "tile"}
+
+
 def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -> bool:
     """Whether sspi_map / si_map on this operator (and batch size) run on the tensor cores."""
-    return map_engine(variant, op, engine, frames) in ("tc", "tile")
+    return map_engine(variant, op, engine, frames) in ("tc", "tile", "tile_bf16")
 
 
 def _num_frames(samples) -> int:
@@ -493,8 +519,9 @@ def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True, engine:
     eng = interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples), offsets.shape[0] > 2)
     if eng == "tc":
         return _tc_map(dense_from_sparse(sp), samples, argmax, out_map)
-    if eng == "tile":
-        return _tile_map(tile_from_sparse(sp, offsets), samples, offsets, argmax, out_map)
+    if eng in ("tile", "tile_bf16"):
+        op = tile_from_sparse(sp, offsets, tf32=(eng == "tile"))
+        return _tile_map(op, samples, offsets, argmax, out_map)
     op = band_from_sparse(sp, offsets)
     return _band_map(op, samples, argmax, out_map)
 
@@ -507,7 +534,7 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engin
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
     _check_cols(samples, num_cols)
-    if engine == "tile":
+    if engine in ("tile", "tile_bf16"):
         raise ValueError("si_map keeps every entry: use engine 'tc' or 'band'")
     if interp_engine(num_cols, num_cols, engine, _num_frames(samples)) == "tc":
         return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
@@ -713,6 +740,7 @@ def _conv_split(frames: int, num_candidates: int, num_cols: int):
     tiles = -(-num_candidates // 128) * -(-frames // 256)
     chunks = -(-2 * num_cols // CONV_CHUNK_FLOATS)
     ks = max(1, min(dev.num_sms() // max(tiles, 1), chunks, CONV_SPLIT_MAX))
+    ks = -(-chunks // -(-chunks // ks))          # slices of whole chunks, none left empty (the kernel's rule)
     if ks < 2 or frames > 65535:
         return 1, None
     return ks, torch.empty((ks, frames, num_candidates), dtype=torch.float32, device=dev.device())

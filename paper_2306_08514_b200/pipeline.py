@@ -33,10 +33,10 @@ class MapPipeline:
                  num_channels: int | None = None, weighting: str = "phat", floor=None,
                  out_map: bool = True, precision: str = "tf32", graph: bool = True,
                  engine: str = "auto"):
+        if variant == "conv_h":          # stored steering matrix: the same conventional chain
+            variant = "conv"
         if variant not in self.VARIANTS:
             raise ValueError(f"unknown map variant {variant!r}")
-        if variant == "conv_h":
-            variant = "conv"
         if variant in ("sspi", "si", "slri") and spec is None:
             raise ValueError(f"{variant} needs a SampleSpec")
         self.variant, self.op, self.frame, self.pairs, self.spec = variant, op, frame, pairs, spec
@@ -67,8 +67,7 @@ class MapPipeline:
         if v in ("sspi", "si", "slri"):
             eng = maps.map_engine(v, self.op, self.engine, self.frames)
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
-                                            self.weighting, self.floor, planes=eng in ("tc", "tile"),
-                                            natural=eng == "tile")
+                                            self.weighting, self.floor, **maps.plane_args(eng))
             if v == "slri":
                 return maps.slri_map(self.op, xi, argmax=True, out_map=self.out_map)
             fn = maps.sspi_map if v == "sspi" else maps.si_map

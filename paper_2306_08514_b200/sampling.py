@@ -91,6 +91,9 @@ class TdGccSamples:
     # samples in natural lag order per pair
     bf16_planes: object = field(default=None, repr=False, compare=False)
     planes_natural: bool = field(default=False, repr=False, compare=False)
+    # the planes are fp32 TF32 hi / lo (lag-major [2][cols8][F32], natural order) for the
+    # 3xTF32 gathered-window engine instead of bf16
+    planes_tf32: bool = field(default=False, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -123,9 +126,14 @@ def _new_samples(frames: int, s_total: int, dev_):
     return buf, ld, buf[:, :frames].t()
 
 
-def _wrap(view, buf, spec, batched: bool, planes=None, natural: bool = False) -> "TdGccSamples":
+def _wrap(view, buf, spec, batched: bool, planes=None, natural: bool = False,
+          tf32: bool = False) -> "TdGccSamples":
     return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf, bf16_planes=planes,
-                        planes_natural=natural)
+                        planes_natural=natural, planes_tf32=tf32)
+
+
+def pad32(n: int) -> int:
+    return (int(n) + 31) // 32 * 32
 
 
 def natural_source_device(spec):
@@ -156,14 +164,18 @@ def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
 
 
 def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
-                      floor=None, planes: bool = False, natural: bool = False) -> TdGccSamples:
+                      floor=None, planes: bool = False, natural: bool = False,
+                      tf32: bool = False) -> TdGccSamples:
     """Fused stft_frame -> fd_gcc -> td_gcc_samples for a range of frames.
 
     Neither the spectra nor the cross-spectra touch HBM; one kernel launch.  With
     `planes` the same kernel also writes the bf16 hi/lo planes the tensor-core
     interpolation maps read (`bf16_planes`; natural lag order per pair with `natural`,
-    the layout of the gathered-window engine).
+    the layout of the gathered-window engine; with `tf32` too, fp32 TF32 hi / lo planes
+    for its 3xTF32 kernel).
     """
+    if tf32 and not natural:
+        raise ValueError("TF32 planes are natural-order lag-major only (natural=True)")
     x = _signal(samples)
     if x.shape[0] != pairs.num_mics:
         raise DimensionError(f"expected {pairs.num_mics} channels, got {x.shape[0]}")
@@ -183,16 +195,19 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
         return _wrap(view, buf, spec, batched)
     cols8 = (s_total + 7) // 8 * 8
     src = natural_source_device(spec) if natural else None
-    if natural:     # lag-major natural-order planes [2][cols8][F8] (gathered-window engine)
+    if tf32:        # lag-major natural-order fp32 planes [2][cols8][F32] (3xTF32 gathered windows)
+        planes_ld = pad32(count)
+        pl = torch.empty((2, cols8, planes_ld), dtype=torch.float32, device=x.device)
+    elif natural:   # lag-major natural-order planes [2][cols8][F8] (gathered-window engine)
         f8 = pad8(count)
         pl = torch.empty((2, cols8, f8), dtype=torch.bfloat16, device=x.device)
         planes_ld = f8
     else:           # frame-major planes [2][F][cols8] (dense tensor-core engine)
         pl = torch.empty((2, count, cols8), dtype=torch.bfloat16, device=x.device)
         planes_ld = 0
-    nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, planes_ld, 1 if natural else 0,
-             dev.ptr(src), dev.stream_ptr())
-    return _wrap(view, buf, spec, batched, pl, natural)
+    nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, planes_ld,
+             (1 if natural else 0) | (2 if tf32 else 0), dev.ptr(src), dev.stream_ptr())
+    return _wrap(view, buf, spec, batched, pl, natural, tf32)
 
 
 def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:

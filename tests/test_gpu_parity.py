@@ -241,7 +241,7 @@ def test_fused_sspi_pipeline(golden_scene):
 
 # ------------------------------------------------------------------ maps
 
-@pytest.mark.parametrize("engine", ["tc", "tile", "band"])
+@pytest.mark.parametrize("engine", ["tc", "tile", "tile_bf16", "band"])
 def test_sspi_and_si_maps(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
@@ -257,7 +257,7 @@ def test_sspi_and_si_maps(golden_scene, engine):
         assert_argmax_agrees(idx, ref)
         zo, io = s.sspi_map(sp, xi, argmax=True, out_map=False, engine=engine)
         assert zo is None and torch.equal(io, idx)         # argmax-only output
-    if engine == "tile":                                   # keep-all SI is not a gathered-window case
+    if engine in ("tile", "tile_bf16"):                    # keep-all SI is not a gathered-window case
         return
     interp = s.InterpMatrix(g["interp"], spec)
     z_si = s.si_map(interp, xi, engine=engine)
@@ -277,10 +277,13 @@ def test_sspi_engines_agree_on_frame_batches(golden_scene):
     zt, it = s.sspi_map(sp, xt, argmax=True, engine="tc")
     zb, ib = s.sspi_map(sp, xt, argmax=True, engine="band")
     zg, ig = s.sspi_map(sp, xt, argmax=True, engine="tile")
+    zh, ih = s.sspi_map(sp, xt, argmax=True, engine="tile_bf16")
     z1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tc")
     assert torch.equal(zt[7], z1)
-    g1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tile")
-    assert torch.equal(zg[7], g1)
+    for eng, zz in (("tile", zg), ("tile_bf16", zh)):
+        g1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine=eng)
+        assert torch.equal(zz[7], g1)
+    assert_map_close(zh, O.sspi_map(sp.values, sp.col_indices, sp.row_splits, x.astype(np.float64)))
     ref = O.sspi_map(sp.values, sp.col_indices, sp.row_splits, x.astype(np.float64))
     assert_map_close(zt, ref)
     assert_map_close(zb, ref)
@@ -306,6 +309,18 @@ def test_natural_planes_from_frontend(golden_scene):
                                ref[:, :spec.total_samples, :f].view(torch.int16))
         else:
             assert torch.equal(xi.bf16_planes.view(torch.int16), ref.view(torch.int16))
+    # TF32 hi / lo planes (3xTF32 gathered-window engine): exactly the split of the f32 samples
+    xi = s.frames_to_samples(x, frame, pairs, spec, **s.maps.plane_args("tile"))
+    assert xi.planes_tf32 and xi.bf16_planes.dtype == torch.float32
+    plain = s.TdGccSamples(xi.values.clone(), spec)
+    ref, _, _ = s.maps.sample_planes(plain, spec.total_samples, natural=spec_offsets(spec), tf32=True)
+    f, st = xi.values.shape[0], spec.total_samples
+    assert torch.equal(xi.bf16_planes[:, :st, :f], ref[:, :st, :f])
+    hi, lo = xi.bf16_planes[0, :st, :f], xi.bf16_planes[1, :st, :f]
+    assert torch.all((hi.view(torch.int32) & 0x1FFF) == 0) and torch.all((lo.view(torch.int32) & 0x1FFF) == 0)
+    nat_cols = torch.from_numpy(s.tiles.natural_columns(spec_offsets(spec))).cuda()
+    v = xi.values.t()[nat_cols].double()
+    assert torch.all((hi.double() + lo.double() - v).abs() <= v.abs() * 2.0 ** -21)
 
 
 def test_sspi_tile_and_row_kernels_agree(golden_scene):

@@ -204,13 +204,12 @@ def cfg4_fit():
     return wl, s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
 
 
-@pytest.mark.parametrize("engine", ["tile", "band"])
+@pytest.mark.parametrize("engine", ["tile", "tile_bf16", "band"])
 def test_cfg4_full_grid_sspi(cfg4_fit, engine):
     wl, fx = cfg4_fit
     assert wl.grid.num_points == 334611 and wl.pairs.num_pairs == 120
     x = torch.from_numpy(wl.samples).cuda()
-    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, planes=(engine == "tile"),
-                             natural=(engine == "tile"))
+    xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, **s.maps.plane_args(engine))
     z, idx = s.sspi_map(fx, xi, argmax=True, engine=engine)
     nf = 4
     xi_ref = O.td_gcc_samples(oracle_psi(wl, nf), wl.spec.counts, wl.frame.half_len)

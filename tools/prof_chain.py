@@ -35,8 +35,7 @@ def main():
         op = s.sparse_interp_fixed(wl.tdoa, wl.spec, wl.frame, 2)
         eng = maps.map_engine("sspi", op, a.engine, frames)
         for _ in range(a.reps):
-            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=eng in ("tc", "tile"),
-                                     natural=eng == "tile")
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, **s.maps.plane_args(eng))
             z, idx = s.sspi_map(op, xi, argmax=True, engine=eng)
     elif a.variant in ("sspi", "slri", "si"):
         interp = s.build_interp_matrix(wl.tdoa, wl.spec, wl.frame, max_bytes=1 << 36)
@@ -57,8 +56,7 @@ def main():
         fn = {"sspi": s.sspi_map, "slri": s.slri_map, "si": s.si_map}[a.variant]
         eng = maps.map_engine(a.variant, op, a.engine, frames)
         for _ in range(a.reps):
-            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, planes=eng in ("tc", "tile"),
-                                     natural=eng == "tile")
+            xi = s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, rng, **s.maps.plane_args(eng))
             z, idx = fn(op, xi, argmax=True, engine=a.engine)
     elif a.variant == "conv":          # on-chip steering (bench variant "conv")
         op = s.steering_operator(wl.tdoa, wl.frame)
