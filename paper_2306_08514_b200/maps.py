@@ -681,18 +681,35 @@ def steering_device(srp, tf32: bool = True) -> torch.Tensor:
     return dev.CACHE.get(srp, "h2_tf32" if tf32 else "h2_f32", build)
 
 
-def srp_map_exact(srp, gcc, *, precision: str = "tf32", argmax: bool = False, out_map: bool = True):
+def conv_precision(srp, precision: str = "auto", gcc=None) -> str:
+    """Resolve the conventional map's arithmetic: "auto" is the parity-safe FP32-class
+    mode of the operator -- 3xTF32 on the tensor cores for on-chip steering
+    (steering_operator), fp32 SIMT for a stored SrpMatrix -- unless the cross-spectra
+    were already rounded to TF32 by their producer (gcc_frames(tf32=True), an explicit
+    upstream choice of the TF32 path).  "tf32" (one TF32 pass, ~1.5e-5 normalized error
+    on maps with a source, up to ~2e-4 on peakless maps) is the opt-in speed mode; its
+    error is reported next to its numbers."""
+    if precision not in ("auto", "tf32", "fp32", "tf32x3"):
+        raise ValueError(f"unknown precision {precision!r}")
+    if precision == "auto":
+        if gcc is not None and getattr(gcc, "tf32_rounded", False):
+            return "tf32"
+        return "fp32" if hasattr(srp, "matrix") else "tf32x3"
+    return precision
+
+
+def srp_map_exact(srp, gcc, *, precision: str = "auto", argmax: bool = False, out_map: bool = True):
     """Conventional SRP map z = 2 Re(H psi) (srp.py:65-71).
 
-    precision "tf32": tcgen05 tensor-core GEMM (kind::tf32 on round-to-nearest TF32
-    operands, fp32 accumulation in TMEM), normalized max error ~1e-5 vs float64;
-    "fp32": SIMT fp32 GEMM.
+    precision "auto" (default): "tf32x3" for on-chip steering, "fp32" for a stored
+    SrpMatrix (conv_precision); "tf32x3": tcgen05 GEMM on hi / lo TF32 operands (3 MMA
+    passes, fp32 folds of the TMEM chunks), <= 5e-6 normalized error; "tf32": one
+    kind::tf32 pass (opt-in speed mode, ~1.5e-5); "fp32": SIMT fp32 GEMM.
     """
     if (gcc.num_pairs, gcc.num_bins) != (srp.num_pairs, srp.num_bins):
         raise DimensionError(f"cross-spectra for {gcc.num_pairs} pairs x {gcc.num_bins} bins do not "
                              f"match a {srp.num_pairs} x {srp.num_bins} transform")
-    if precision not in ("tf32", "fp32", "tf32x3"):
-        raise ValueError(f"unknown precision {precision!r}")
+    precision = conv_precision(srp, precision, gcc)
     if precision == "tf32x3" and hasattr(srp, "matrix"):
         raise ValueError("3xTF32 is provided by the on-chip steering operator (steering_operator)")
     if not hasattr(srp, "matrix"):           # implicit operator: steering generated on chip

@@ -31,7 +31,7 @@ class MapPipeline:
 
     def __init__(self, variant: str, op, frame, pairs, spec=None, frames: int = 1,
                  num_channels: int | None = None, weighting: str = "phat", floor=None,
-                 out_map: bool = True, precision: str = "tf32", graph: bool = True,
+                 out_map: bool = True, precision: str = "auto", graph: bool = True,
                  engine: str = "auto"):
         if variant == "conv_h":          # stored steering matrix: the same conventional chain
             variant = "conv"
@@ -41,7 +41,8 @@ class MapPipeline:
             raise ValueError(f"{variant} needs a SampleSpec")
         self.variant, self.op, self.frame, self.pairs, self.spec = variant, op, frame, pairs, spec
         self.frames = int(frames)
-        self.weighting, self.floor, self.out_map, self.precision = weighting, floor, out_map, precision
+        self.weighting, self.floor, self.out_map = weighting, floor, out_map
+        self.precision = maps.conv_precision(op, precision) if variant == "conv" else precision
         self.engine = engine              # sspi / si: "auto" | "fused" | "tc" | "tile" | "band"
         m = num_channels or pairs.num_mics
         n = (self.frames - 1) * frame.hop + frame.frame_len

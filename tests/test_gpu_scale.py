@@ -218,3 +218,64 @@ def test_cfg4_full_grid_sspi(cfg4_fit, engine):
         k = int(fx.kept[p])
         z_ref += np.einsum("jk,fjk->fj", fx.values[p, :, :k], xi_ref[:, fx.cols[p, :, :k]])
     check(z, z_ref, idx)
+
+
+@pytest.fixture(scope="module")
+def cfg4_global():
+    """The bench headline's operator: cfg4 SSPI with the reference's global top-Q rule at
+    Q = 2JP (interpolation.py:155-175), streamed (the dense 18.7 GB Lambda is never built)."""
+    wl = workloads.make("cfg4", num_frames=300)
+    j, p = wl.grid.num_points, wl.pairs.num_pairs
+    keep = s.resolve_sparsity("2jp", j, p, j * wl.spec.total_samples)
+    return wl, s.truncate_sparse_streamed(wl.tdoa, wl.spec, wl.frame, keep)
+
+
+def _csr_rows(sp, rows):
+    """The CSR rows `rows` of a SparseInterp (oracle on a row block)."""
+    splits = np.asarray(sp.row_splits)
+    lo, hi = splits[rows], splits[rows + 1]
+    idx = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)])
+    sub_splits = np.concatenate([[0], np.cumsum(hi - lo)])
+    return np.asarray(sp.values)[idx], np.asarray(sp.col_indices)[idx], sub_splits
+
+
+@pytest.mark.parametrize("engine", ["auto", "tile_bf16"])
+def test_cfg4_global_fit_pipeline(cfg4_global, engine):
+    """The default bench path: MapPipeline (CUDA graph: fused frontend -> 3xTF32 gathered-window
+    map on CTA pairs -> argmax) at cfg4 with the global fit, 300 frames (two unit frame
+    tiles + a ragged one), against the float64 oracle on a row block: a 1/61 subsample plus
+    each checked frame's peak neighbourhood, so max|z_ref| is the map's true maximum."""
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    wl, sp = cfg4_global
+    assert wl.grid.num_points == 334611 and sp.num_kept == 2 * 334611 * 120
+    pipe = MapPipeline("sspi", sp, wl.frame, wl.pairs, wl.spec, frames=wl.num_frames, engine=engine)
+    assert not pipe.uses_fused_chain()
+    if engine == "auto":
+        assert s.maps.map_engine("sspi", sp, "auto", wl.num_frames) == "tile"
+    z, idx = pipe.run(torch.from_numpy(wl.samples).cuda())
+    torch.cuda.synchronize()
+    nf = 3
+    frames = np.array([0, 1, wl.num_frames - 1])                   # last frame: the ragged unit
+    x64 = wl.samples.astype(np.float64)
+    win = O.frame_window(wl.frame.frame_len, wl.frame.window)
+    psi = O.fd_gcc(O.stft_frames(x64, wl.frame.frame_len, wl.frame.hop, win, frames), wl.pairs.pairs)
+    xi_ref = O.td_gcc_samples(psi, wl.spec.counts, wl.frame.half_len)
+    peaks = idx[frames].cpu().numpy()
+    near = np.concatenate([np.arange(max(0, q - 400), min(wl.grid.num_points, q + 400)) for q in peaks])
+    rows = np.unique(np.concatenate([np.arange(0, wl.grid.num_points, 61), near]))
+    vals, cols, splits = _csr_rows(sp, rows)
+    z_ref = O.sspi_map(vals, cols, splits, xi_ref)
+    got = z[frames][:, rows].float().cpu().numpy()
+    err = O.normalized_max_error(got, z_ref)
+    assert err.max() <= TOL
+    if engine == "auto":
+        assert err.max() <= 2e-6, f"3xTF32 with fp32 folds: FP32-class error expected, got {err.max():.2e}"
+    for k in range(nf):       # the GPU argmax is the oracle's maximum over the checked rows
+        j = int(np.searchsorted(rows, peaks[k]))
+        assert z_ref[k, j] >= z_ref[k].max() * (1 - 2 * TOL)
+    # the map does not depend on the batch: a frame's row equals its single-frame map
+    xi1 = s.frames_to_samples(torch.from_numpy(wl.samples).cuda(), wl.frame, wl.pairs, wl.spec, range(1, 2),
+                              **s.maps.plane_args(s.maps.map_engine("sspi", sp, engine, 1)))
+    z1 = s.sspi_map(sp, xi1, engine=s.maps.map_engine("sspi", sp, engine, 1))
+    assert torch.equal(z1[0], z[1])
+    print(f"cfg4 global fit ({engine}): normalized max error {err.max():.2e} over {rows.size} rows")
