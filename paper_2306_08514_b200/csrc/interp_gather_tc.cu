@@ -331,7 +331,9 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 //     {32, lags, frames / 32} (fallback: four 2D boxes when the 3D view cannot be encoded).
 namespace g32 {
 constexpr int GK = 16;               // lags per stage
+constexpr int GG = 4;                // lags per gathered group (one 4-row MN atom of the tf32 layout)
 constexpr int NG = GK / GG;          // groups per stage
+constexpr int kMaxGroups = kMaxBlocks * (GB / GG);
 constexpr int GN = 128;              // frames per unit
 constexpr int GA = 32;               // frames per frame block (128 bytes of fp32)
 constexpr int NA = GN / GA;          // frame blocks per group
@@ -339,7 +341,7 @@ constexpr int UK = 8;                // kind::tf32 MMA K
 constexpr int NS = 4;                // operand stages (48 KB each)
 
 struct __align__(1024) Smem {
-  float b[NS][2][NG][GN * GG];       // [plane][group] 4 frame blocks (4 KB)
+  float b[NS][2][NG][GN * GG];       // [plane][group] 4 frame blocks of [4 lags][32 frames] (2 KB)
   float a[NS][2][2][GM * GK];        // [half][plane] slab columns (8 KB)
   int32_t rows[2][kMaxGroups];
   uint64_t full[NS], empty[NS], tfull[2], tempty[2];
@@ -366,14 +368,15 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
 
 // MN-major fp32 operand: tf32 takes only the 128-byte swizzle with 32-byte atoms
 // (SWIZZLE_128B_BASE32B, layout type 1; the TMA side is CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B):
-// 512-byte atoms of 4 K rows x 32 frames.  A group's 8 lags x 32 frames are two atoms,
-// 512 B apart (SBO, along K); the next 32 frames are 1 KB on (LBO, along N).
+// 512-byte atoms of 4 K rows x 32 frames.  A gathered group is 4 lags, stored as its 4
+// frame blocks one atom after the other (LBO = 512 B along N); a K = 8 step takes two
+// consecutive groups (SBO = one group's 2 KB along K).
 __device__ __forceinline__ uint64_t desc_mn128(const void* p) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
   d |= (addr & 0x3FFFFull) >> 4;
-  d |= (uint64_t)(1024 >> 4) << 16;            // LBO: next 32 frames
-  d |= (uint64_t)(512 >> 4) << 32;             // SBO: next 4 lags
+  d |= (uint64_t)(512 >> 4) << 16;             // LBO: next 32 frames
+  d |= (uint64_t)((128 * GG * 4) >> 4) << 32;  // SBO: next 4 lags (the next group)
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)1 << 61;                      // SWIZZLE_128B_BASE32B
   return d;
@@ -385,7 +388,7 @@ __device__ __forceinline__ int num_chunks(int nk, int ch) { return ((GB / GK) * 
 __global__ void __launch_bounds__(kThreads, 1)
 gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int b3d,
-                   int fg, int CH, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                   int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                    const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
                    const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
                    unsigned long long* __restrict__ keys) {
@@ -393,7 +396,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)((F + GN - 1) / GN);
-  const int u_total = ((n_tiles + fg - 1) / fg) * T * fg;
+  const int u_total = min(u_end, ((n_tiles + fg - 1) / fg) * T * fg);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&ma_hi);
@@ -422,11 +425,13 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // lanes 0-3: one (plane, group) of gathered samples each; lanes 4-7: one (half, plane) slab
+    // lanes 0-7: one (plane, group) of gathered samples each; lanes 8-11: one (half, plane) slab
     constexpr uint32_t kBytes = 2u * (2 * GM * GK + GN * GK) * sizeof(float);
-    const int plane = (lane >> 1) & 1, grp = lane & 1;
-    const int ah = ((lane - 4) >> 1) & 1, ap = (lane - 4) & 1;
-    const uint64_t keep = policy_evict_last();
+    const int plane = (lane >> 2) & 1, grp = lane & 3;
+    const int ah = ((lane - 8) >> 1) & 1, ap = (lane - 8) & 1;
+    // L2 policy: the unit group's gathered samples are re-read by every tile (keep them);
+    // a tile's slabs only by the few CTAs on its frame tiles at about the same time
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();
     auto next_unit = [&](int u, Unit& w) {
       while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += gridDim.x;
       return u;
@@ -438,7 +443,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
     uint32_t g = 0;
     int buf = 0;
     Unit w;
-    int u = next_unit(blockIdx.x, w);
+    int u = next_unit(u_begin + blockIdx.x, w);
     if (u < u_total) stage_rows(0, w);
     while (u < u_total) {
       Unit wn;
@@ -455,17 +460,17 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
           mbar_expect_tx(&sm.full[s], kBytes);
         }
         __syncwarp();
-        if (lane < 4) {
+        if (lane < 8) {
           const CUtensorMap* mb = plane ? &mb_lo : &mb_hi;
           if (b3d) {
-            tma_load_3d(sm.b[s][plane][grp], mb, &sm.full[s], 0, row, w.n * NA);
+            tma_load_3d(sm.b[s][plane][grp], mb, &sm.full[s], 0, row, w.n * NA, keep);
           } else {
 #pragma unroll
             for (int a = 0; a < NA; ++a)
               tma_load_2d(sm.b[s][plane][grp] + a * GA * GG, mb, &sm.full[s], w.n * GN + a * GA, row);
           }
-        } else if (lane < 8) {
-          tma_load_2d_hint(sm.a[s][ah][ap], ap ? &ma_lo : &ma_hi, &sm.full[s], sub * GK, (2 * blk + ah) * GM, keep);
+        } else if (lane < 12) {
+          tma_load_2d_hint(sm.a[s][ah][ap], ap ? &ma_lo : &ma_hi, &sm.full[s], sub * GK, (2 * blk + ah) * GM, once);
         }
       }
       __syncwarp();
@@ -479,7 +484,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(GN >> 3) << 17) |
                                  ((uint32_t)(GM >> 4) << 24);
       uint32_t g = 0, c = 0;     // stage and chunk counters (chunk c uses TMEM buffer c & 1)
-      for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
+      for (int u = u_begin + blockIdx.x; u < u_total; u += gridDim.x) {
         Unit w;
         if (!decode32(u, T, fg, n_tiles, w)) continue;
         const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
@@ -496,7 +501,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
 #pragma unroll
           for (int k = 0; k < GK / UK; ++k) {
             const uint64_t aoff = (uint64_t)((k * UK * 4) >> 4);
-            const uint64_t bh = desc_mn128(sm.b[s][0][k]), bl = desc_mn128(sm.b[s][1][k]);
+            const uint64_t bh = desc_mn128(sm.b[s][0][2 * k]), bl = desc_mn128(sm.b[s][1][2 * k]);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const uint32_t d = dbuf + h * GN;
@@ -523,7 +528,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * GN);
     const int64_t ldt = (int64_t)T * GT;
     uint32_t c = 0;
-    for (int u = blockIdx.x; u < u_total; u += gridDim.x) {
+    for (int u = u_begin + blockIdx.x; u < u_total; u += gridDim.x) {
       Unit w;
       if (!decode32(u, T, fg, n_tiles, w)) continue;
       const int r = half * GM + q * 32 + lane;
@@ -614,7 +619,7 @@ constexpr int PThreads = kThreads;
 constexpr int PCols = PN / (PEpi / 4);         // accumulator columns folded per epilogue thread
 
 struct __align__(1024) PairSmem {
-  float b[PNS][2][NG][PNC * GG];     // [plane][group] 4 frame blocks (4 KB)
+  float b[PNS][2][NG][PNC * GG];     // [plane][group] 4 frame blocks of [4 lags][32 frames] (2 KB)
   float a[PNS][2][GM * GK];          // [plane] this CTA's slab half (8 KB)
   int32_t rows[2][kMaxGroups];
   uint64_t full[PNS], empty[PNS], tfull[2], tempty[2];
@@ -632,7 +637,7 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint6
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
 gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                         const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
-                        int fg, int CH, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                        int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                         const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
                         const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
                         unsigned long long* __restrict__ keys) {
@@ -642,7 +647,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
   const uint32_t rank = cluster_ctarank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int n_tiles = (int)((F + PN - 1) / PN);
-  const int u_total = ((n_tiles + fg - 1) / fg) * T * fg;
+  const int u_total = min(u_end, ((n_tiles + fg - 1) / fg) * T * fg);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&ma_hi);
@@ -671,10 +676,10 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // lanes 0-3: (plane, group) of this CTA's frame half; lanes 4-5: this CTA's slab half
+    // lanes 0-7: (plane, group) of this CTA's frame half; lanes 8-9: this CTA's slab half
     constexpr uint32_t kBytes = 2u * (GM * GK + PNC * GK) * sizeof(float);   // one CTA's stage
-    const int plane = (lane >> 1) & 1, grp = lane & 1, ap = (lane - 4) & 1;
-    const uint64_t keep = policy_evict_last();
+    const int plane = (lane >> 2) & 1, grp = lane & 3, ap = (lane - 8) & 1;
+    const uint64_t keep = policy_evict_last(), once = policy_evict_first();   // as the one-CTA kernel
     auto next_unit = [&](int u, Unit& w) {
       while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += ncl;
       return u;
@@ -686,7 +691,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     uint32_t g = 0;
     int buf = 0;
     Unit w;
-    int u = next_unit(cid, w);
+    int u = next_unit(u_begin + cid, w);
     if (u < u_total) stage_rows(0, w);
     while (u < u_total) {
       Unit wn;
@@ -704,11 +709,11 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
           if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * kBytes);     // both CTAs' loads
         }
         __syncwarp();
-        if (lane < 4) {
+        if (lane < 8) {
           tma_load_3d_pair(sm.b[s][plane][grp], plane ? &mb_lo : &mb_hi, bar, 0, row,
-                           w.n * (PN / GA) + (int)rank * PNA);
-        } else if (lane < 6) {
-          tma_load_2d_pair(sm.a[s][ap], ap ? &ma_lo : &ma_hi, bar, sub * GK, (2 * blk + (int)rank) * GM, keep);
+                           w.n * (PN / GA) + (int)rank * PNA, keep);
+        } else if (lane < 10) {
+          tma_load_2d_pair(sm.a[s][ap], ap ? &ma_lo : &ma_hi, bar, sub * GK, (2 * blk + (int)rank) * GM, once);
         }
       }
       __syncwarp();
@@ -722,7 +727,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(PN >> 3) << 17) |
                                  ((uint32_t)((2 * GM) >> 4) << 24);
       uint32_t g = 0, c = 0;
-      for (int u = cid; u < u_total; u += ncl) {
+      for (int u = u_begin + cid; u < u_total; u += ncl) {
         Unit w;
         if (!decode32(u, T, fg, n_tiles, w)) continue;
         const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
@@ -739,7 +744,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
 #pragma unroll
           for (int k = 0; k < GK / UK; ++k) {
             const uint64_t aoff = (uint64_t)((k * UK * 4) >> 4);
-            const uint64_t bh = desc_mn128(sm.b[s][0][k]), bl = desc_mn128(sm.b[s][1][k]);
+            const uint64_t bh = desc_mn128(sm.b[s][0][2 * k]), bl = desc_mn128(sm.b[s][1][2 * k]);
             const uint64_t a_h = smem_desc_sw64(sm.a[s][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][1]) + aoff;
             mma_tf32_pair(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
             mma_tf32_pair(d, a_h, bl, idesc, 1u);
@@ -761,7 +766,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * PCols);
     const int64_t ldt = (int64_t)T * GT;
     uint32_t c = 0;
-    for (int u = cid; u < u_total; u += ncl) {
+    for (int u = u_begin + cid; u < u_total; u += ncl) {
       Unit w;
       if (!decode32(u, T, fg, n_tiles, w)) continue;
       const int r = (int)rank * GM + q * 32 + lane;
@@ -989,15 +994,15 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   int b3d = getenv("SRPGPU_GATHER_2D") ? 0 : 1;
   {
     const int64_t dims[3] = {g32::GA, num_cols, planes_ld / g32::GA};
-    const int box[3] = {g32::GA, GG, g32::NA};
+    const int box[3] = {g32::GA, g32::GG, g32::NA};
     if (make_map_3d(&mb_hi, f32, samples_planes, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32",
                     sw32) ||
         make_map_3d(&mb_lo, f32, xs_lo, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32", sw32))
       b3d = 0;
   }
-  if (!b3d && ((s = make_map_2d(&mb_hi, f32, 4, samples_planes, num_cols, num_frames, planes_ld, g32::GA, GG,
+  if (!b3d && ((s = make_map_2d(&mb_hi, f32, 4, samples_planes, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
                                 "interp_map_gather_tf32", sw32)) ||
-               (s = make_map_2d(&mb_lo, f32, 4, xs_lo, num_cols, num_frames, planes_ld, g32::GA, GG,
+               (s = make_map_2d(&mb_lo, f32, 4, xs_lo, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
                                 "interp_map_gather_tf32", sw32))))
     return s;
   // CTA pairs (cta_group::2) unless SRPGPU_GATHER_PAIR=0 or no 2-CTA cluster fits; persistent
@@ -1041,24 +1046,37 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
       clusters = std::min(clusters, num_ctas / 2);
     }
   }
-  if (clusters > 0) {
-    g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
-        ma_hi, ma_lo, mb_hi, mb_lo, frames_per_group / g32::PN, chunk, num_frames, num_candidates, num_tiles, group_col,
-        tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
-        reinterpret_cast<unsigned long long*>(keys));
-  } else {
-    const size_t smem = sizeof(g32::Smem) + 1024;
-    if (cudaFuncSetAttribute(g32::gather_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-      set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
-      return SRPGPU_ERR_LAUNCH;
-    }
-    g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
-        ma_hi, ma_lo, mb_hi, mb_lo, b3d, frames_per_group / g32::GN, chunk, num_frames, num_candidates, num_tiles,
-        group_col, tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
-        reinterpret_cast<unsigned long long*>(keys));
+  const size_t smem = sizeof(g32::Smem) + 1024;
+  if (clusters == 0 &&
+      cudaFuncSetAttribute(g32::gather_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess) {
+    set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
+    return SRPGPU_ERR_LAUNCH;
   }
-  SRPGPU_CHECK_LAUNCH("interp_map_gather_tf32");
+  const int unit_frames = clusters > 0 ? g32::PN : g32::GN;
+  const int fg = (int)(frames_per_group / unit_frames);
+  const int64_t units_per_group = (int64_t)num_tiles * fg;
+  const int64_t n_groups = (num_frames + frames_per_group - 1) / frames_per_group;
+  SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "interp_map_gather_tf32: too many units");
+  auto gather = [&](int64_t g0, int64_t g1) -> int {
+    const int ub = (int)(g0 * units_per_group), ue = (int)(g1 * units_per_group);
+    if (clusters > 0)
+      g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
+          ma_hi, ma_lo, mb_hi, mb_lo, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
+          tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
+          reinterpret_cast<unsigned long long*>(keys));
+    else
+      g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
+          ma_hi, ma_lo, mb_hi, mb_lo, b3d, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col,
+          tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
+          reinterpret_cast<unsigned long long*>(keys));
+    SRPGPU_CHECK_LAUNCH("interp_map_gather_tf32");
+    return SRPGPU_OK;
+  };
+  // one launch over every group; the untile pass follows (measured: running group g's untile
+  // on a side stream under group g + 1's gather launch was slower, 50 vs 42 ms at cfg4 --
+  // the two contend for the SMs' issue slots and L2)
+  if ((s = gather(0, n_groups))) return s;
   if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
   return SRPGPU_OK;
 }

@@ -348,7 +348,7 @@ class TileOperator:
     MAX_BLOCKS = 128            # 64-lag operator blocks per tile (interp_gather_tc.cu kMaxBlocks)
 
     def __init__(self, sp, offsets, num_rows: int, tf32: bool = True):
-        lay = tiles.TileLayout(sp, offsets, num_rows)
+        lay = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8)
         if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
             raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
                              f"(> {self.MAX_BLOCKS}): use engine 'band'")
@@ -863,39 +863,47 @@ FUSED_MAX_FRAMES_PER_SM = 8   # latency-scale batches only (a warp per frame, on
 FUSED_FRAME_LENS = (256, 512, 1024)
 
 
+def sell_layout(sp):
+    """Host image of the sliced-ELL operator: (cols [rows][32] uint16 sample index, vals
+    [rows][32] float32 weight, chunk_off [ceil(J/32) + 1] int64).  Candidates come in chunks
+    of 32; chunk c has width W_c = its longest row (padded to FUSED_PAD / 2 FUSED_PAD for the
+    kernel's unrolled path), entries stored [row][lane]; candidate i's k-th CSR entry is row
+    chunk_off[i // 32] + k, lane i % 32; padding entries have weight 0 and sample index 0."""
+    splits = np.asarray(sp.row_splits, dtype=np.int64)
+    cols = np.asarray(sp.col_indices, dtype=np.int64)
+    vals = np.asarray(sp.values, dtype=np.float64)
+    j = splits.shape[0] - 1
+    nnz = np.diff(splits)
+    nch = (j + 31) // 32
+    width = np.zeros(nch * 32, dtype=np.int64)
+    width[:j] = nnz
+    width = width.reshape(nch, 32).max(axis=1)
+    # chunks up to FUSED_PAD (2 FUSED_PAD) entries wide are padded to exactly FUSED_PAD
+    # (2 FUSED_PAD): the kernel then loads them unconditionally at fixed offsets
+    # (frontend_warp.cu kMapW)
+    width = np.where(width <= FUSED_PAD, FUSED_PAD, np.where(width <= 2 * FUSED_PAD, 2 * FUSED_PAD, width))
+    off = np.zeros(nch + 1, dtype=np.int64)
+    np.cumsum(width, out=off[1:])
+    rows = int(off[-1])
+    c = np.zeros((max(rows, 1), 32), dtype=np.uint16)
+    v = np.zeros((max(rows, 1), 32), dtype=np.float32)
+    cand = np.repeat(np.arange(j, dtype=np.int64), nnz)
+    slot = np.arange(cols.shape[0], dtype=np.int64) - np.repeat(splits[:-1], nnz)
+    c[off[cand // 32] + slot, cand % 32] = cols
+    v[off[cand // 32] + slot, cand % 32] = vals.astype(np.float32)
+    return c, v, off
+
+
 class SellOperator:
-    """Sliced-ELL device image of a sparse interpolation fit (CSR SparseInterp) for the
-    fused frames -> SSPI map chain: candidates in chunks of 32, chunk c has width W_c = its
-    longest row, entries stored [row][lane] so a warp reads 32 candidates' entry t with one
-    coalesced load.  Padding entries have weight 0 (and sample index 0)."""
+    """Device image of sell_layout for the fused frames -> SSPI map chain."""
 
     def __init__(self, sp):
-        splits = np.asarray(sp.row_splits, dtype=np.int64)
-        cols = np.asarray(sp.col_indices, dtype=np.int64)
-        vals = np.asarray(sp.values, dtype=np.float64)
-        j = splits.shape[0] - 1
-        nnz = np.diff(splits)
-        nch = (j + 31) // 32
-        width = np.zeros(nch * 32, dtype=np.int64)
-        width[:j] = nnz
-        width = width.reshape(nch, 32).max(axis=1)
-        # chunks up to FUSED_PAD (2 FUSED_PAD) entries wide are padded to exactly FUSED_PAD
-        # (2 FUSED_PAD): the kernel then loads them unconditionally at fixed offsets
-        # (frontend_warp.cu kMapW)
-        width = np.where(width <= FUSED_PAD, FUSED_PAD, np.where(width <= 2 * FUSED_PAD, 2 * FUSED_PAD, width))
-        off = np.zeros(nch + 1, dtype=np.int64)
-        np.cumsum(width, out=off[1:])
-        rows = int(off[-1])
-        c = np.zeros((max(rows, 1), 32), dtype=np.uint16)
-        v = np.zeros((max(rows, 1), 32), dtype=np.float32)
-        cand = np.repeat(np.arange(j, dtype=np.int64), nnz)
-        slot = np.arange(cols.shape[0], dtype=np.int64) - np.repeat(splits[:-1], nnz)
-        c[off[cand // 32] + slot, cand % 32] = cols
-        v[off[cand // 32] + slot, cand % 32] = vals.astype(np.float32)
+        c, v, off = sell_layout(sp)
+        nnz = np.diff(np.asarray(sp.row_splits, dtype=np.int64))
         d = dev.device()
-        self.num_rows, self.num_cols = j, int(sp.num_cols)
-        self.max_row_nnz = int(nnz.max()) if j else 0
-        self.padding = rows * 32 / max(1, cols.shape[0])
+        self.num_rows, self.num_cols = nnz.shape[0], int(sp.num_cols)
+        self.max_row_nnz = int(nnz.max()) if nnz.size else 0
+        self.padding = int(off[-1]) * 32 / max(1, int(nnz.sum()))
         self.cols = torch.from_numpy(c.view(np.int16)).to(d)
         self.vals = torch.from_numpy(v).to(d)
         self.chunk_off = torch.from_numpy(off.astype(np.int32)).to(d)

@@ -7,9 +7,11 @@ every gathered sample tile) that are compact in TDOA space (recursive bisection 
 the pair with the widest spread), and each tile only sees the union of its candidates'
 kept lag windows, pair by pair, rounded up to groups of 8 consecutive lags:
 
-    K(tile) = sum_p 8 * ceil(w_p / 8),   w_p = width of the tile's window of pair p
+    K(tile) = sum_p g * ceil(w_p / g),   w_p = width of the tile's window of pair p
 
-(cfg4: 1182 on average for 256-candidate tiles, 1074 for 128; against S = 7028).  The
+with g = 8 lags for the bf16 kernel (its MN atoms are 8 rows) and g = 4 for the 3xTF32
+kernel (the tf32 MN layout has 4-row atoms): cfg4 (fixed fit) 1160 / 966 on average for
+256-candidate tiles, against S = 7028.  The
 tile's operator is stored dense over that K in 64-lag blocks, each block as two slabs
 (`[2 * block + half][128 rows][64]`, zero where a candidate does not keep the lag), and
 the kernel gathers each 8-lag group as 8 rows of the lag-major samples.
@@ -95,7 +97,8 @@ class TileLayout:
     """Host image of the gathered-window operator (see the module docstring).
 
     slabs      (2 * num_blocks, 128, 64) float32 operator values: block b, half h -> 2b + h
-    group_col  (num_blocks * 8,) int32: first natural sample index (lag row) of each 8-lag group
+    group_col  (num_blocks * 64 / group,) int32: first natural sample index (lag row) of each
+               group of `group` lags
     tile_slab  (T,) int32 first 64-lag block of each tile; tile_nkb (T,) blocks per tile
     tile_rows  (T, 256) int32 candidate of each tile row (ascending; -1 = padding);
                rows 0-127 are half 0, 128-255 half 1
@@ -103,7 +106,11 @@ class TileLayout:
                in this tile order, fully coalesced; a gather pass restores grid order)
     """
 
-    def __init__(self, sp, offsets, num_rows: int):
+    def __init__(self, sp, offsets, num_rows: int, group: int = GROUP):
+        if group not in (4, 8):
+            raise ValueError("lag groups of 4 (tf32 kernel) or 8 (bf16 kernel)")
+        self.group = int(group)
+        GROUP = self.group
         offsets = np.asarray(offsets, dtype=np.int64)
         p_count = offsets.shape[0] - 1
         rows, pairs, ncol, vals = _entries(sp, offsets)
@@ -175,10 +182,12 @@ class TileLayout:
         """float64 reference of the gathered product (test helper): z (F, J)."""
         f = xi_nat.shape[0]
         z = np.zeros((f, self.num_rows))
-        pad = np.concatenate([xi_nat, np.zeros((f, SLAB + GROUP))], axis=1)
+        g = self.group
+        pad = np.concatenate([xi_nat, np.zeros((f, SLAB + g))], axis=1)
+        per = SLAB // g
         for t in range(self.num_tiles):
             b0, nk = int(self.tile_slab[t]), int(self.tile_nkb[t])
-            cols = self.group_col[b0 * 8:(b0 + nk) * 8][:, None] + np.arange(GROUP)[None, :]
+            cols = self.group_col[b0 * per:(b0 + nk) * per][:, None] + np.arange(g)[None, :]
             x = pad[:, cols.ravel()]                                     # (F, nk*64)
             for h in range(2):
                 a = self.slabs[2 * b0 + h:2 * (b0 + nk):2].transpose(1, 0, 2).reshape(HALF, nk * SLAB)

@@ -235,3 +235,79 @@ def test_streamed_global_fit_matches_reference(golden_scene):
         assert np.array_equal(got.values, ref.values)
     with pytest.raises(ValueError):
         s.truncate_sparse_streamed(tdoa, spec, frame, -1)
+
+
+def _nonzero_rows(splits, cols, vals):
+    """Per row: the (column, float32 weight) entries whose weight is not 0, in CSR order."""
+    out = []
+    for i in range(splits.shape[0] - 1):
+        a, b = int(splits[i]), int(splits[i + 1])
+        v = np.asarray(vals[a:b], dtype=np.float32)
+        keep = v != 0
+        out.append((np.asarray(cols[a:b])[keep].astype(np.int64), v[keep]))
+    return out
+
+
+def test_sell_layout_decodes_to_reference_csr(golden_scene):
+    """The fused chain's sliced-ELL image holds exactly the reference CSR (interpolation.py:
+    155-175): candidate i's k-th entry sits at row chunk_off[i // 32] + k, lane i % 32, with
+    the reference column and float32(value); every other slot is padding of weight 0."""
+    _, g = golden_scene
+    for tag in keep_tags(g):
+        sp = sparse_from_golden(g, tag)
+        c, v, off = s.maps.sell_layout(sp)
+        splits = np.asarray(sp.row_splits)
+        nnz = np.diff(splits)
+        j = nnz.shape[0]
+        used = np.zeros(v.shape, dtype=bool)
+        for i in range(j):
+            r0, lane = int(off[i // 32]), i % 32
+            k = int(nnz[i])
+            assert_array_equal(c[r0:r0 + k, lane].astype(np.int64), sp.col_indices[splits[i]:splits[i + 1]])
+            assert_array_equal(v[r0:r0 + k, lane], np.asarray(sp.values[splits[i]:splits[i + 1]], np.float32))
+            used[r0:r0 + k, lane] = True
+        assert np.all(v[~used] == 0)                       # padding never contributes
+        w = np.diff(off)
+        assert np.all(w >= np.pad(nnz, (0, (-j) % 32)).reshape(-1, 32).max(axis=1))
+
+
+@pytest.mark.parametrize("group", [4, 8])
+def test_tile_layout_holds_the_csr(golden_scene, group):
+    """The gathered-window image (tiles.TileLayout, 4-lag groups for the 3xTF32 kernel, 8 for
+    bf16): every candidate sits in exactly one tile row, and decoding the slabs (tile row,
+    group_col + lag offset, natural -> storage column) gives exactly the CSR's nonzero
+    entries with float32 weights; the remaining slab entries are 0."""
+    from paper_2306_08514_b200 import tiles
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    off = s.sampling.spec_offsets(spec)
+    perm = tiles.natural_columns(off)                      # natural index -> storage column
+    for tag in keep_tags(g):
+        sp = sparse_from_golden(g, tag)
+        j = int(np.asarray(sp.row_splits).shape[0] - 1)
+        lay = tiles.TileLayout(sp, off, j, group=group)
+        rows_used = lay.tile_rows[lay.tile_rows >= 0]
+        assert_array_equal(np.sort(rows_used), np.arange(j))
+        assert_array_equal(lay.tile_pos[lay.tile_rows[lay.tile_rows >= 0]], np.flatnonzero(lay.tile_rows.ravel() >= 0))
+        per = tiles.SLAB // group
+        got = [dict() for _ in range(j)]
+        for t in range(lay.num_tiles):
+            b0, nk = int(lay.tile_slab[t]), int(lay.tile_nkb[t])
+            cols = (lay.group_col[b0 * per:(b0 + nk) * per][:, None] + np.arange(group)[None, :]).ravel()
+            for h in range(2):
+                a = lay.slabs[2 * b0 + h:2 * (b0 + nk):2].transpose(1, 0, 2).reshape(tiles.HALF, nk * tiles.SLAB)
+                for r in range(tiles.HALF):
+                    cand = int(lay.tile_rows[t, h * tiles.HALF + r])
+                    nzk = np.flatnonzero(a[r])
+                    if cand < 0:
+                        assert nzk.size == 0
+                        continue
+                    for k in nzk:
+                        col = int(perm[cols[k]])
+                        assert col not in got[cand]
+                        got[cand][col] = a[r, k]
+        ref = _nonzero_rows(np.asarray(sp.row_splits), np.asarray(sp.col_indices), np.asarray(sp.values))
+        for i in range(j):
+            rc, rv = ref[i]
+            assert sorted(got[i]) == sorted(rc.tolist())
+            assert all(got[i][int(cc)] == vv for cc, vv in zip(rc, rv))

@@ -1,4 +1,4 @@
-# A/B of the 3xTF32 gathered-window kernel knobs (pair / one-CTA, fold chunk, unit group)
-for P in 1 0; do for C in 2 4 8 64; do
-  echo "pair=$P chunk=$C"; SRPGPU_GATHER_PAIR=$P SRPGPU_GATHER_CHUNK=$C timeout 300 python tools/bench_tile.py --fit fixed --engines tile 2>&1 | tail -1
-done; done
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "sspi_and_si or engines_agree" 2>&1 | tail -2
+for G in 512 1024 2048; do
+  echo "group=$G"; SRPGPU_GATHER_GROUP=$G timeout 300 python tools/bench_tile.py --fit fixed --engines tile 2>&1 | tail -1
+done
