@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--variants", default="sspi,slri,lr,conv,conv_h",
                     help="comma list of extra variants measured on the same workload (conv: TF32 speed "
                          "mode with its error reported)")
+    ap.add_argument("--partition", default="frames", choices=["frames", "candidates"],
+                    help="multi-GPU split: frame blocks per rank (weak scaling, default) or candidate-row "
+                         "blocks per rank with every rank on all frames (strong scaling; keys MAX-reduced)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -674,6 +677,79 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_candidates(args):
+    """Candidate partition (north_star: "or, for the largest grids, candidate locations"):
+    rank r owns a contiguous block of candidate rows (distributed.candidate_block) for all F
+    frames of the step; its chain's per-frame argmax is re-based to global indices and the
+    keys are MAX-reduced over NCCL inside the timed region.  Strong scaling: the step's work
+    (F frames x J candidates) is fixed as N grows; value = F / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_08514_b200 import distributed as D
+    from paper_2306_08514_b200 import maps as _maps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    frames = args.frames or DEFAULT_FRAMES[args.workload]
+    wl = build_scene(args, frames)
+    op = shared_fit(wl, args.variant, args, world, rank)
+    prec = "tf32" if args.precision == "auto" and args.variant == "conv" else args.precision
+    shard = D.CandidateShard("conv" if args.variant == "conv_h" else args.variant, op, wl.frame, wl.pairs, wl.spec,
+                             frames, rank, world, engine=args.engine, precision=prec)
+    shard.input.copy_(torch.from_numpy(wl.samples).to(dev))
+    for _ in range(max(3, args.warmup)):
+        keys = shard.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    with clocks:
+        a.record()
+        for _ in range(args.steps):
+            keys = shard.step()
+        b.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    idx, _ = D.decode_host_keys(keys)
+    parity = None
+    if rank == 0:
+        parity = {"combined_argmax_first_frames": idx[:4].cpu().tolist(),
+                  "rank0_block": [shard.first, shard.count]}
+    eng = headline_engine(args, wl, op, frames)
+    in_bytes = wl.array.num_mics * ((frames - 1) * wl.frame.hop + wl.frame.frame_len) * 4
+    cfg = make_config(args, wl, frames, frames, world, op, eng, in_bytes)
+    cfg["parallelism"] = f"candidates/{world}"
+    cfg["collective"] = "NCCL all_reduce MAX of the per-frame packed argmax keys, every step" if world > 1 else None
+    if rank == 0:
+        dtype, arith = arithmetic(args.variant, eng, _maps.conv_precision(op, prec)
+                                  if args.variant in ("conv", "conv_h") else None)
+        print(json.dumps({
+            "metric": METRIC, "value": frames / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype, "arithmetic": arith,
+            "data": "synthetic (seeded generator with the BASELINE config's geometry, sources and SNR)",
+            "config": cfg, "candidates_per_s": frames / (ms / 1e3) * wl.grid.num_points,
+            "partition": {"rows_per_rank": [D.partition(wl.grid.num_points, world, r)[1] for r in range(world)]},
+            "clocks": clocks.summary(), "parity": parity}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 DEFAULT_FRAMES = {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000, "cfg5": 1024}
 
 
@@ -1022,7 +1098,10 @@ def main():
         run_reference(args)
     else:
         maybe_spawn(args)
-        run_ours(args)
+        if args.partition == "candidates":
+            run_candidates(args)
+        else:
+            run_ours(args)
 
 
 if __name__ == "__main__":

@@ -13,6 +13,11 @@ path shards without any data-path exchange:
   flipped so signed MAX gives the unsigned order (largest value, lowest index).
 
 Maps stay on the GPU that computed them.
+
+`candidate_block` cuts an operator to a contiguous block of candidate rows (the same
+entries the reference would use for those rows: srp.py:51-62 row by row, the CSR rows of
+interpolation.py:155-175) and `CandidateShard` runs one rank's block as a MapPipeline
+whose per-frame (value, index) become global keys combined by `reduce_candidate_keys`.
 """
 
 from __future__ import annotations
@@ -84,6 +89,65 @@ def pipelined_steps(steps, n: int, total_frames: int, outs=None, group=None):
     for w in works:
         w.wait()
     return outs
+
+
+def candidate_block(op, first: int, count: int):
+    """The operator restricted to candidate rows [first, first + count).
+
+    SteeringTdoa (on-chip conventional steering): the TDOA table's rows; SparseInterp (the
+    reference CSR): its rows, column indices unchanged; FixedNnzInterp: its (P, J, k) rows.
+    Values are the very entries of the full operator, so a block map equals the full map's
+    columns bit for bit on the row-local engines.
+    """
+    import numpy as np
+    from .operators import FixedNnzInterp, SparseInterp, SteeringTdoa
+    from .scene import TdoaTable
+    if isinstance(op, SteeringTdoa):
+        t = op.tdoa
+        return SteeringTdoa(tdoa=TdoaTable(np.ascontiguousarray(t.delta_t[first:first + count]), t.limits),
+                            frame=op.frame)
+    if isinstance(op, SparseInterp):
+        splits = np.asarray(op.row_splits, dtype=np.int64)
+        a, b = int(splits[first]), int(splits[first + count])
+        return SparseInterp(np.asarray(op.values)[a:b], np.asarray(op.col_indices)[a:b],
+                            splits[first:first + count + 1] - a, int(op.num_cols))
+    if isinstance(op, FixedNnzInterp):
+        return FixedNnzInterp(values=np.ascontiguousarray(op.values[:, first:first + count]),
+                              cols=np.ascontiguousarray(op.cols[:, first:first + count]), kept=op.kept,
+                              num_cols=op.num_cols)
+    raise TypeError(f"no candidate partition for {type(op).__name__}")
+
+
+def block_keys(z: torch.Tensor, index: torch.Tensor, row_offset: int) -> torch.Tensor:
+    """Global packed keys of a block map: the kernel's per-frame argmax (first maximum of
+    the block) and its value, re-based to the block's first global candidate."""
+    f = index.shape[0]
+    vals = z.reshape(f, -1).gather(1, index.reshape(f, 1)).reshape(f)
+    return encode_host_keys(vals, index + row_offset)
+
+
+class CandidateShard:
+    """One rank of a candidate-partitioned map: a contiguous block of candidate rows for
+    every frame of the batch (MapPipeline on `candidate_block`), whose per-frame keys are
+    all-reduced (MAX) into the global first maximum (srp.py:74-80) every step."""
+
+    def __init__(self, variant, op, frame, pairs, spec, frames: int, rank: int, world: int, **kw):
+        from .pipeline import MapPipeline
+        j = op.num_candidates if hasattr(op, "num_candidates") else (
+            op.values.shape[1] if getattr(op, "values", None) is not None and op.values.ndim == 3
+            else int(len(op.row_splits) - 1))
+        self.first, self.count = partition(j, world, rank)
+        self.block = candidate_block(op, self.first, self.count)
+        self.pipe = MapPipeline(variant, self.block, frame, pairs, spec, frames=frames, **kw)
+        self.input = self.pipe.input
+
+    def step(self, group=None) -> torch.Tensor:
+        """Replay the block's chain; -> global packed keys (frames,) on every rank."""
+        z, idx = self.pipe.replay()
+        keys = block_keys(z, idx, self.first)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            keys = reduce_candidate_keys(keys, group)
+        return keys
 
 
 def reduce_candidate_keys(local_keys: torch.Tensor, group=None) -> torch.Tensor:

@@ -279,3 +279,71 @@ def test_cfg4_global_fit_pipeline(cfg4_global, engine):
     z1 = s.sspi_map(sp, xi1, engine=s.maps.map_engine("sspi", sp, engine, 1))
     assert torch.equal(z1[0], z[1])
     print(f"cfg4 global fit ({engine}): normalized max error {err.max():.2e} over {rows.size} rows")
+
+
+def _combine(keys_list):
+    """The all-reduce MAX of candidate_partition, in one process."""
+    from paper_2306_08514_b200 import distributed as D
+    k = D.keys_to_signed(keys_list[0].clone())
+    for other in keys_list[1:]:
+        k = torch.maximum(k, D.keys_to_signed(other))
+    return D.decode_host_keys(D.signed_to_keys(k))
+
+
+def test_candidate_partition_conventional_ties():
+    """Candidate partition (srp.py:71: rows are independent): two row blocks of the on-chip
+    conventional map, their kernel argmax re-based to global indices and MAX-combined, give
+    the full map's first maximum -- including a tie planted across the block boundary (rows
+    J/2 - 1 and J/2 copy the peak row's TDOAs, so three rows share the maximum bitwise)."""
+    from paper_2306_08514_b200 import distributed as D
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    wl = workloads.make("cfg2", num_frames=4096)          # >= 148 output tiles: no split-K
+    x = torch.from_numpy(wl.samples).cuda()
+    j = wl.grid.num_points
+    op = s.steering_operator(wl.tdoa, wl.frame)
+    pipe = MapPipeline("conv", op, wl.frame, wl.pairs, wl.spec, frames=wl.num_frames)
+    z0, i0 = pipe.run(x)
+    peak = int(i0[0])
+    dt = wl.tdoa.delta_t.copy()
+    dt[j // 2 - 1] = dt[peak]
+    dt[j // 2] = dt[peak]
+    op2 = s.steering_operator(s.TdoaTable(dt, wl.tdoa.limits), wl.frame)
+    full = MapPipeline("conv", op2, wl.frame, wl.pairs, wl.spec, frames=wl.num_frames)
+    zf, idf = full.run(x)
+    zf, idf = zf.clone(), idf.clone()
+    keys = []
+    for r in range(2):
+        sh = D.CandidateShard("conv", op2, wl.frame, wl.pairs, wl.spec, wl.num_frames, r, 2)
+        sh.pipe.run(x)
+        z_b, _ = sh.pipe.z, sh.pipe.index
+        assert torch.equal(z_b, zf[:, sh.first:sh.first + sh.count])        # row-local: bitwise
+        keys.append(sh.step())
+    idx, val = _combine(keys)
+    zc = zf.cpu().numpy()
+    assert np.array_equal(idx.cpu().numpy(), np.argmax(zc, axis=1))        # first maximum, ties
+    assert np.array_equal(idx.cpu().numpy(), idf.cpu().numpy())
+    assert int(idx[0]) == min(peak, j // 2 - 1)
+    assert np.array_equal(val.cpu().numpy(), zc.max(axis=1))
+
+
+def test_candidate_partition_cfg4_sspi(cfg4_global):
+    """The largest grid split by candidates (cfg4, global fit, 3xTF32 gathered windows):
+    two row blocks + the key MAX give the full map's argmax on every margin-qualified frame."""
+    from paper_2306_08514_b200 import distributed as D
+    from paper_2306_08514_b200.pipeline import MapPipeline
+    wl, sp = cfg4_global
+    x = torch.from_numpy(wl.samples).cuda()
+    zf, idf = MapPipeline("sspi", sp, wl.frame, wl.pairs, wl.spec, frames=wl.num_frames).run(x)
+    zf, idf = zf.clone(), idf.clone()
+    keys = []
+    for r in range(2):
+        sh = D.CandidateShard("sspi", sp, wl.frame, wl.pairs, wl.spec, wl.num_frames, r, 2)
+        sh.pipe.run(x)
+        keys.append(sh.step())
+        del sh
+    idx, val = _combine(keys)
+    z = zf.cpu().numpy()
+    part = np.partition(z, -2, axis=1)
+    ok = (part[:, -1] - part[:, -2]) / np.abs(z).max(axis=1) > TOL
+    assert ok.sum() > wl.num_frames // 2
+    assert np.array_equal(idx.cpu().numpy()[ok], idf.cpu().numpy()[ok])

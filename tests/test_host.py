@@ -311,3 +311,28 @@ def test_tile_layout_holds_the_csr(golden_scene, group):
             rc, rv = ref[i]
             assert sorted(got[i]) == sorted(rc.tolist())
             assert all(got[i][int(cc)] == vv for cc, vv in zip(rc, rv))
+
+
+def test_candidate_blocks_are_row_slices(golden_scene):
+    """candidate_block (the candidate partition's per-rank operator) keeps exactly the
+    operator's rows [first, first + count): CSR rows, fixed-nnz rows, TDOA rows."""
+    from paper_2306_08514_b200 import distributed as D
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    j = int(np.asarray(sp.row_splits).shape[0] - 1)
+    parts = [D.partition(j, 3, r) for r in range(3)]
+    blocks = [D.candidate_block(sp, a, n) for a, n in parts]
+    assert sum(b.num_rows for b in blocks) == j
+    dense = np.zeros((j, sp.num_cols))
+    dense[np.repeat(np.arange(j), np.diff(sp.row_splits)), sp.col_indices] = sp.values
+    for (a, n), b in zip(parts, blocks):
+        d = np.zeros((n, sp.num_cols))
+        d[np.repeat(np.arange(n), np.diff(b.row_splits)), b.col_indices] = b.values
+        assert_array_equal(d, dense[a:a + n])
+    fx = s.sparse_interp_fixed(tdoa, spec, frame, 2)
+    fb = D.candidate_block(fx, parts[1][0], parts[1][1])
+    assert_array_equal(fb.values, fx.values[:, parts[1][0]:parts[1][0] + parts[1][1]])
+    st = D.candidate_block(s.steering_operator(tdoa, frame), parts[2][0], parts[2][1])
+    assert_array_equal(st.tdoa.delta_t, tdoa.delta_t[parts[2][0]:])
+    assert st.num_candidates == parts[2][1]
