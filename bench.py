@@ -502,7 +502,7 @@ def run_ours(args):
             name, peak, psrc = "interp_tc_kernel", bf16, f"bf16 {peak_src} (MEASURED_PEAKS.json)"
         else:
             t = _maps.tile_from_sparse(op, _maps.spec_offsets(wl.spec), tf32=(eng == "tile"))
-            mma = 3 * 2.0 * t.num_slabs * 128 * 64 * count
+            mma = 3 * 2.0 * t.num_tiles * 256 * t.mean_k * count      # the K the kernel iterates
             if eng == "tile":
                 name, peak, psrc = "gather_tf32_pair_kernel", tf32_peak, f"TF32 cuBLAS {xsrc}"
             else:
@@ -640,9 +640,7 @@ def run_ours(args):
                                          else "stored steering matrix via TMA")
                 else:
                     ev = _maps.map_engine(v, opv, "auto", count)
-                    entry["dtype"] = arithmetic(v, ev if ev else ("tc" if v in ("slri", "lr") and count *
-                                                wl.grid.num_points >= _maps.LOWRANK_TC_MIN_OUTPUTS else "simt"),
-                                                "auto")[0]
+                    entry["dtype"] = arithmetic(v, ev if ev else "simt", "auto")[0]
                 if v in ("lr", "slri"):
                     entry["rank"] = args.rank_r
                 pv.run(x_dev)

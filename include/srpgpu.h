@@ -221,8 +221,10 @@ int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, 
 /* The same map with 3xTF32 operands (FP32-class: hi = tf32_rne(x), lo = tf32_rne(x - hi),
  * z ~= Lh.xh + Lh.xl + Ll.xh accumulated in fp32 by tcgen05 kind::tf32): samples_planes
  * fp32 [2][round8(S)][planes_ld] (planes_ld a multiple of 32, 128-byte aligned; natural lag
- * order), slab_planes fp32 [2][num_slabs * 128][64] (srpgpu_split_tf32 of the slabs); the
- * other arguments as srpgpu_interp_map_gather_tc.  Replaces interpolation.py:188-195
+ * order), slab_planes fp32 [2][num_slabs * 128][64] (srpgpu_split_tf32 of the slabs);
+ * tile_nkb here counts each tile's 16-lag stages (its window rounded up to 16 lags, not to
+ * the 64-lag block) and group_col holds 4-lag groups (16 per block); the other arguments
+ * as srpgpu_interp_map_gather_tc.  Replaces interpolation.py:188-195
  * (sspi_map) at long sample vectors. */
 int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
                                   int64_t planes_ld, const float* slab_planes, int64_t num_slabs,

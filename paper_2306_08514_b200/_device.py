@@ -74,7 +74,9 @@ class OperatorCache:
     """
 
     def __init__(self):
-        self._lock = threading.Lock()
+        # re-entrant, and no cached value is released while it is held: releasing one can
+        # run another entry's weakref finalizer (_drop) on this thread
+        self._lock = threading.RLock()
         self._entries: dict = {}
 
     def get(self, obj, variant, builder):
@@ -89,16 +91,21 @@ class OperatorCache:
         except TypeError:  # not weak-referenceable: keep a strong ref
             ref = (lambda o=obj: o)
         with self._lock:
+            old = self._entries.get(key)
             self._entries[key] = (ref, value)
+        del old                                  # released outside the lock
         return value
 
     def _drop(self, key):
         with self._lock:
-            self._entries.pop(key, None)
+            old = self._entries.pop(key, None)
+        del old
 
     def clear(self):
         with self._lock:
-            self._entries.clear()
+            old = self._entries
+            self._entries = {}
+        del old
 
 
 CACHE = OperatorCache()

@@ -383,13 +383,14 @@ __device__ __forceinline__ uint64_t desc_mn128(const void* p) {
 }
 
 // chunks of a tile with nk 64-lag blocks
-__device__ __forceinline__ int num_chunks(int nk, int ch) { return ((GB / GK) * nk + ch - 1) / ch; }
+// tile_nst[t] = the tile's 16-lag stages (its window K rounded up to 16, not to the 64-lag slab block)
+__device__ __forceinline__ int num_chunks(int nst, int ch) { return (nst + ch - 1) / ch; }
 
 __global__ void __launch_bounds__(kThreads, 1)
 gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                    const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo, int b3d,
                    int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
-                   const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
+                   const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
                    const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
                    unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -437,8 +438,8 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       return u;
     };
     auto stage_rows = [&](int buf, const Unit& w) {
-      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int i = lane; i < nk * (GB / GG); i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
+      const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
+      for (int i = lane; i < nst * NG; i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
     };
     uint32_t g = 0;
     int buf = 0;
@@ -450,8 +451,8 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       const int un = next_unit(u + gridDim.x, wn);
       if (un < u_total) stage_rows(buf ^ 1, wn);
       __syncwarp();
-      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int kq = 0; kq < (GB / GK) * nk; ++kq, ++g) {     // 16-lag stages: a quarter block each
+      const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
+      for (int kq = 0; kq < nst; ++kq, ++g) {     // 16-lag stages: a quarter block each
         const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
         const int row = sm.rows[buf][kq * NG + grp];
         const int s = g % NS;
@@ -487,7 +488,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       for (int u = u_begin + blockIdx.x; u < u_total; u += gridDim.x) {
         Unit w;
         if (!decode32(u, T, fg, n_tiles, w)) continue;
-        const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
+        const int ns = __ldg(tile_nst + w.t);
         for (int kq = 0; kq < ns; ++kq, ++g) {
           const int s = g % NS;
           const int first = kq % CH == 0;
@@ -533,7 +534,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       if (!decode32(u, T, fg, n_tiles, w)) continue;
       const int r = half * GM + q * 32 + lane;
       const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);
-      const int nc = num_chunks(__ldg(tile_nkb + w.t), CH);
+      const int nc = num_chunks(__ldg(tile_nst + w.t), CH);
       float rs[GN];
       for (int j = 0; j < nc; ++j, ++c) {
         mbar_wait(&sm.tfull[c & 1], (c >> 1) & 1);
@@ -638,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
 gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                         const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
                         int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
-                        const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nkb,
+                        const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
                         const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
                         unsigned long long* __restrict__ keys) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -685,8 +686,8 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       return u;
     };
     auto stage_rows = [&](int buf, const Unit& w) {
-      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int i = lane; i < nk * (GB / GG); i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
+      const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
+      for (int i = lane; i < nst * NG; i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
     };
     uint32_t g = 0;
     int buf = 0;
@@ -698,8 +699,8 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       const int un = next_unit(u + ncl, wn);
       if (un < u_total) stage_rows(buf ^ 1, wn);
       __syncwarp();
-      const int b0 = __ldg(tile_blk + w.t), nk = __ldg(tile_nkb + w.t);
-      for (int kq = 0; kq < (GB / GK) * nk; ++kq, ++g) {
+      const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
+      for (int kq = 0; kq < nst; ++kq, ++g) {
         const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
         const int row = sm.rows[buf][kq * NG + grp];
         const int s = g % PNS;
@@ -730,7 +731,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       for (int u = u_begin + cid; u < u_total; u += ncl) {
         Unit w;
         if (!decode32(u, T, fg, n_tiles, w)) continue;
-        const int ns = (GB / GK) * __ldg(tile_nkb + w.t);
+        const int ns = __ldg(tile_nst + w.t);
         for (int kq = 0; kq < ns; ++kq, ++g) {
           const int s = g % PNS;
           const int first = kq % CH == 0;
@@ -771,7 +772,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       if (!decode32(u, T, fg, n_tiles, w)) continue;
       const int r = (int)rank * GM + q * 32 + lane;
       const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);
-      const int nc = num_chunks(__ldg(tile_nkb + w.t), CH);
+      const int nc = num_chunks(__ldg(tile_nst + w.t), CH);
       float rs[PCols];
       for (int j = 0; j < nc; ++j, ++c) {
         mbar_wait(&sm.tfull[c & 1], (c >> 1) & 1);

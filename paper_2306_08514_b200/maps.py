@@ -323,9 +323,10 @@ TC_MIN_FRAMES = 0           # batches below this take the band engine (set from 
 
 def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None,
                   pairs: bool = True) -> str:
-    """'tc' (dense operator on the tensor cores, bf16x3), 'tile' (per-tile gathered lag
-    windows on the tensor cores in 3xTF32, for long sample vectors; 'tile_bf16': the same
-    in bf16x3, opt-in) or 'band' (tiled-band SpMM on FP32)."""
+    """'tile' (per-tile gathered lag windows on the tensor cores in 3xTF32 with fp32 chunk
+    folds: FP32-class, the default wherever the tensor cores pay), 'band' (tiled-band SpMM
+    on FP32 SIMT: latency-scale sparse maps, single-pair operators), or the opt-in bf16x3
+    engines 'tc' (dense operator) and 'tile_bf16' (gathered windows)."""
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}")
     if engine != "auto":
@@ -333,9 +334,8 @@ def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", fram
     if frames is not None and frames < TC_MIN_FRAMES:
         return "band"
     c8 = _cols8(num_cols)
-    if c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0):
-        return "tc"
-    if c8 > TC_MAX_COLS and kept_per_row * TILE_DENSITY < c8 and pairs:
+    dense_ok = c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0)
+    if pairs and (dense_ok or (c8 > TC_MAX_COLS and kept_per_row * TILE_DENSITY < c8)):
         return "tile"
     return "band"
 
@@ -348,14 +348,20 @@ class TileOperator:
     MAX_BLOCKS = 128            # 64-lag operator blocks per tile (interp_gather_tc.cu kMaxBlocks)
 
     def __init__(self, sp, offsets, num_rows: int, tf32: bool = True):
-        lay = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8)
+        # J % 8 == 0 (cfg3 / cfg5): tiles of aligned 8-candidate runs, so the 3xTF32 kernel
+        # stores the map straight into grid order in whole 32-byte sectors (no tile-order
+        # scratch, no gather pass; cfg3 K is even 4% smaller than with compact tiles)
+        self.grid_order = bool(tf32) and num_rows % 8 == 0
+        lay = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8, runs=self.grid_order)
         if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
             raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
                              f"(> {self.MAX_BLOCKS}): use engine 'band'")
         d = dev.device()
         self.tf32 = bool(tf32)
         self.num_rows, self.num_cols, self.cols8 = int(num_rows), int(lay.num_cols), _cols8(lay.num_cols)
-        self.num_tiles, self.num_slabs, self.mean_k = lay.num_tiles, lay.num_slabs, lay.mean_k
+        self.num_tiles, self.num_slabs = lay.num_tiles, lay.num_slabs
+        # the K the kernel iterates: 16-lag stages (3xTF32) or 64-lag blocks (bf16)
+        self.mean_k = lay.mean_k_stages if self.tf32 else lay.mean_k
         rows = max(1, lay.num_slabs) * tiles.HALF
         self.planes = torch.empty((2, rows, tiles.SLAB), dtype=torch.float32 if self.tf32 else torch.bfloat16,
                                   device=d)
@@ -370,7 +376,7 @@ class TileOperator:
             del src
         self.group_col = dev.as_i32(lay.group_col if lay.group_col.size else np.zeros(8, np.int32))
         self.tile_slab = dev.as_i32(lay.tile_slab)
-        self.tile_nkb = dev.as_i32(lay.tile_nkb)
+        self.tile_nkb = dev.as_i32(lay.tile_nst if self.tf32 else lay.tile_nkb)
         self.tile_rows = dev.as_i32(lay.tile_rows)
         self.tile_pos = dev.as_i32(lay.tile_pos)
         self._layout = lay
@@ -393,7 +399,7 @@ def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
     planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets, tf32=op.tf32)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
     zt = (torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
-          if out_map and not TILE_GRID_ORDER else None)
+          if out_map and not (TILE_GRID_ORDER or op.grid_order) else None)
     keys = _new_keys(f, argmax)
     fn = "srpgpu_interp_map_gather_tf32" if op.tf32 else "srpgpu_interp_map_gather_tc"
     nat.call(fn, dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
@@ -534,14 +540,26 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engin
     """
     num_cols = int(np.asarray(interp.matrix).shape[1])
     _check_cols(samples, num_cols)
-    if engine in ("tile", "tile_bf16"):
-        raise ValueError("si_map keeps every entry: use engine 'tc' or 'band'")
-    if interp_engine(num_cols, num_cols, engine, _num_frames(samples)) == "tc":
-        return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
         offsets = np.array([0, num_cols], dtype=np.int64)
+    eng = interp_engine(num_cols, num_cols, engine, _num_frames(samples), offsets.shape[0] > 2)
+    if eng == "tc":
+        return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
+    if eng in ("tile", "tile_bf16"):
+        sp = dev.CACHE.get(interp, "keep_all_csr", lambda: _keep_all_csr(interp))
+        return _tile_map(tile_from_sparse(sp, offsets, tf32=(eng == "tile")), samples, offsets, argmax, out_map)
     return _band_map(band_from_dense(interp, offsets), samples, argmax, out_map)
+
+
+def _keep_all_csr(interp):
+    """The keep-all sparse fit of a dense operator (truncate_sparse(interp, J * S): every
+    entry, row-major) -- the operator si_map shares with sspi_map(keep=all)."""
+    from .operators import SparseInterp
+    mat = np.asarray(interp.matrix)
+    j, n = mat.shape
+    return SparseInterp(mat.ravel().copy(), np.tile(np.arange(n, dtype=np.int64), j),
+                        np.arange(0, j * n + 1, n, dtype=np.int64), n)
 
 
 # ----------------------------------------------------------------- low rank
@@ -561,24 +579,20 @@ LOWRANK_TC_MIN_OUTPUTS = 1 << 24   # frames x candidates from which the tensor-c
 
 
 def _lowrank_engine(engine: str, outputs: int) -> str:
-    """'tc': the rank-R candidate product on the tensor cores (z-write bound); 'simt': fp32.
-
-    "auto" takes the tensor cores for large maps (cfg3: SLRI 0.88 -> 0.72 ms per 10^4
-    frames) and fp32 SIMT for small ones (cfg2: 70 vs 81 us, launch-latency bound).
-    """
+    """'simt': the rank-R candidate product in fp32 SIMT (the default: FP32 end to end);
+    'tc': on the tensor cores with bf16 hi / lo operands (opt-in speed mode, z-write bound:
+    cfg3 SLRI chain 0.88 -> 0.65 ms, normalized error up to ~2.6e-5 at low ranks)."""
     if engine not in ("auto", "tc", "simt"):
         raise ValueError(f"unknown engine {engine!r}")
-    if engine == "auto":
-        return "tc" if outputs >= LOWRANK_TC_MIN_OUTPUTS else "simt"
-    return engine
+    return "simt" if engine == "auto" else engine
 
 
 def slri_map(lr, samples, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
     """Low-rank interpolation map z = tall (fat xi) (interpolation.py:178-185).
 
-    The factor product fat.xi runs in fp32; engine "tc" (default) evaluates the
-    candidate product tall.(fat xi) on the tensor cores with bf16 hi/lo operands
-    (~1e-6 normalized error), "simt" in fp32 SIMT.
+    The factor product fat.xi runs in fp32; the candidate product tall.(fat xi) runs in
+    fp32 SIMT ("simt", the default) or, opt-in, on the tensor cores with bf16 hi/lo
+    operands ("tc", ~1e-6 - 2.6e-5 normalized error).
     """
     fat = np.asarray(lr.fat)
     buf, f, batched = _lag_major(samples, fat.shape[1])
@@ -616,7 +630,7 @@ def _lr_device(lr):
 def lr_map(lr, gcc, *, argmax: bool = False, out_map: bool = True, engine: str = "auto"):
     """Low-rank SRP map z = 2 Re(tall (fat psi)) (lowrank.py:51-57).
 
-    engine as for slri_map: "tc" (default) runs the candidate product on the tensor
+    engine as for slri_map: "simt" (default) fp32; "tc" runs the candidate product on the tensor
     cores, "simt" in fp32.
     """
     fat = np.asarray(lr.fat)

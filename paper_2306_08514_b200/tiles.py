@@ -26,7 +26,7 @@ from __future__ import annotations
 
 import numpy as np
 
-TILE, HALF, GROUP, SLAB = 256, 128, 8, 64
+TILE, HALF, GROUP, SLAB, STAGE = 256, 128, 8, 64, 16
 
 
 def natural_columns(offsets: np.ndarray) -> np.ndarray:
@@ -99,17 +99,23 @@ class TileLayout:
     slabs      (2 * num_blocks, 128, 64) float32 operator values: block b, half h -> 2b + h
     group_col  (num_blocks * 64 / group,) int32: first natural sample index (lag row) of each
                group of `group` lags
-    tile_slab  (T,) int32 first 64-lag block of each tile; tile_nkb (T,) blocks per tile
+    tile_slab  (T,) int32 first 64-lag block of each tile; tile_nkb (T,) blocks per tile;
+               tile_nst (T,) 16-lag stages per tile (what the 3xTF32 kernel iterates)
     tile_rows  (T, 256) int32 candidate of each tile row (ascending; -1 = padding);
                rows 0-127 are half 0, 128-255 half 1
     tile_pos   (J,) int32 position t * 256 + row of each candidate (the kernel writes the map
                in this tile order, fully coalesced; a gather pass restores grid order)
     """
 
-    def __init__(self, sp, offsets, num_rows: int, group: int = GROUP):
+    def __init__(self, sp, offsets, num_rows: int, group: int = GROUP, runs: bool = False):
+        """runs: tiles made of aligned runs of 8 consecutive candidates (each run one 32-byte
+        sector of a map row when J % 8 == 0), 8 tile rows per run in ascending order, so
+        the kernel can store the map straight into grid order with whole sectors (no
+        tile-order scratch, no gather pass); otherwise tiles of compact candidates."""
         if group not in (4, 8):
             raise ValueError("lag groups of 4 (tf32 kernel) or 8 (bf16 kernel)")
         self.group = int(group)
+        self.runs = bool(runs)
         GROUP = self.group
         offsets = np.asarray(offsets, dtype=np.int64)
         p_count = offsets.shape[0] - 1
@@ -126,15 +132,32 @@ class TileLayout:
         if empty.any():
             centre = ((offsets[:-1] + offsets[1:] - 1) * 0.5).astype(np.float32)
             feat = np.where(empty.reshape(num_rows, p_count), centre[None, :], feat)
-        tiles = bisect_tiles(feat) if num_rows else []
-        t_count = len(tiles)
-        tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
         tile_of = np.zeros(num_rows, dtype=np.int64)
         row_of = np.zeros(num_rows, dtype=np.int64)
-        for t, idx in enumerate(tiles):
-            tile_rows[t, :idx.shape[0]] = idx
-            tile_of[idx] = t
-            row_of[idx] = np.arange(idx.shape[0])
+        if self.runs and num_rows:
+            n_runs = (num_rows + 7) // 8
+            run = np.arange(num_rows) // 8
+            rfeat = np.zeros((n_runs, p_count))
+            np.add.at(rfeat, run, feat)
+            rfeat = (rfeat / np.bincount(run, minlength=n_runs)[:, None]).astype(np.float32)
+            tiles = bisect_tiles(rfeat, TILE, weight=np.full(n_runs, 8))       # lists of runs
+            t_count = len(tiles)
+            tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
+            for t, rr in enumerate(tiles):
+                cand = (rr[:, None] * 8 + np.arange(8)[None, :]).ravel()
+                pos = np.arange(cand.shape[0])
+                ok = cand < num_rows
+                tile_rows[t, pos[ok]] = cand[ok]
+                tile_of[cand[ok]] = t
+                row_of[cand[ok]] = pos[ok]
+        else:
+            tiles = bisect_tiles(feat) if num_rows else []
+            t_count = len(tiles)
+            tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
+            for t, idx in enumerate(tiles):
+                tile_rows[t, :idx.shape[0]] = idx
+                tile_of[idx] = t
+                row_of[idx] = np.arange(idx.shape[0])
         # per (tile, pair) window over the tile's candidates
         lo_tp = np.full(t_count * p_count, np.iinfo(np.int64).max)
         hi_tp = np.full(t_count * p_count, -1)
@@ -149,6 +172,7 @@ class TileLayout:
         gstart[:, 1:] = np.cumsum(ngroups, axis=1)[:, :-1]                # group index of pair p
         tile_groups = ngroups.sum(axis=1)
         tile_nkb = np.maximum(1, (tile_groups * GROUP + SLAB - 1) // SLAB)
+        tile_nst = np.maximum(1, (tile_groups * GROUP + STAGE - 1) // STAGE)   # 16-lag stages (tf32 kernel)
         tile_slab = np.zeros(t_count, dtype=np.int64)
         if t_count:
             tile_slab[1:] = np.cumsum(tile_nkb)[:-1]
@@ -171,12 +195,14 @@ class TileLayout:
         self.group_col = group_col.astype(np.int32)
         self.tile_slab = tile_slab.astype(np.int32)
         self.tile_nkb = tile_nkb.astype(np.int32)
+        self.tile_nst = tile_nst.astype(np.int32)
         self.tile_rows = tile_rows
         self.tile_pos = (tile_of * TILE + row_of).astype(np.int32)
         self.num_tiles = t_count
         self.num_blocks = num_blocks
         self.num_slabs = 2 * num_blocks
         self.mean_k = float(tile_nkb.mean() * SLAB) if t_count else 0.0
+        self.mean_k_stages = float(tile_nst.mean() * STAGE) if t_count else 0.0
 
     def emulate(self, xi_nat: np.ndarray) -> np.ndarray:
         """float64 reference of the gathered product (test helper): z (F, J)."""

@@ -257,8 +257,6 @@ def test_sspi_and_si_maps(golden_scene, engine):
         assert_argmax_agrees(idx, ref)
         zo, io = s.sspi_map(sp, xi, argmax=True, out_map=False, engine=engine)
         assert zo is None and torch.equal(io, idx)         # argmax-only output
-    if engine in ("tile", "tile_bf16"):                    # keep-all SI is not a gathered-window case
-        return
     interp = s.InterpMatrix(g["interp"], spec)
     z_si = s.si_map(interp, xi, engine=engine)
     assert_map_close(z_si, g["z_si"])

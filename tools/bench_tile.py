@@ -83,7 +83,7 @@ def main():
              "maps_per_s": args.frames / ((t_front + t_map) / 1e3), "err": float(err.max()), "argmax_agree": agree,
              "setup_s": setup}
         if op is not None:
-            mma = 3 * 2.0 * op.num_slabs * 128 * 64 * args.frames
+            mma = 3 * 2.0 * op.num_tiles * 256 * op.mean_k * args.frames
             r.update({"mean_k": op.mean_k, "tiles": op.num_tiles,
                       "mma_tflops": mma / (t_keys / 1e3) / 1e12})
         print(json.dumps(r), flush=True)
