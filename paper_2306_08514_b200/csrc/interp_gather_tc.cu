@@ -330,6 +330,10 @@ gather_tc_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constan
 //     {32 frames, 8 lags, 4 frame blocks} over the lag-major planes viewed as
 //     {32, lags, frames / 32} (fallback: four 2D boxes when the 3D view cannot be encoded).
 namespace g32 {
+__device__ __forceinline__ void named_barrier(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 constexpr int GK = 16;               // lags per stage
 constexpr int GG = 4;                // lags per gathered group (one 4-row MN atom of the tf32 layout)
 constexpr int NG = GK / GG;          // groups per stage
@@ -614,7 +618,7 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
 constexpr int PN = 256;              // frames per unit (pair)
 constexpr int PNC = PN / 2;          // frames per CTA (B half)
 constexpr int PNA = PNC / GA;        // frame blocks per group per CTA
-constexpr int PNS = 6;               // operand stages (32 KB each)
+constexpr int PNS = 5;               // operand stages (32 KB each)
 constexpr int PEpi = kEpi;          // epilogue warps
 constexpr int PThreads = kThreads;
 constexpr int PCols = PN / (PEpi / 4);         // accumulator columns folded per epilogue thread
@@ -622,6 +626,7 @@ constexpr int PCols = PN / (PEpi / 4);         // accumulator columns folded per
 struct __align__(1024) PairSmem {
   float b[PNS][2][NG][PNC * GG];     // [plane][group] 4 frame blocks of [4 lags][32 frames] (2 KB)
   float a[PNS][2][GM * GK];          // [plane] this CTA's slab half (8 KB)
+  float zs[2][32 * GM];              // [column half] one 32-frame slice of the map for a TMA store
   int32_t rows[2][kMaxGroups];
   uint64_t full[PNS], empty[PNS], tfull[2], tempty[2];
   uint32_t tmem_base;
@@ -638,6 +643,7 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint6
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
 gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                         const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+                        const __grid_constant__ CUtensorMap mz, int z_tma, int64_t zt_ld,
                         int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                         const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
                         const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
@@ -765,7 +771,10 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     const int q = warp & 3;
     const int ch = (warp - 2) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * PCols);
-    const int64_t ldt = (int64_t)T * GT;
+    const int64_t ldt = zt_ld >= 0 ? zt_ld : (int64_t)T * GT;   // zt_ld: diagnostic override
+    // map stores stream past L2 (evict_first): they must not push out the group's samples
+    const uint64_t zpol = policy_evict_first();
+    const bool issuer = z_tma && q == 0 && lane == 0;   // one TMA-store thread per column half
     uint32_t c = 0;
     for (int u = u_begin + cid; u < u_total; u += ncl) {
       Unit w;
@@ -795,25 +804,38 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sm.tempty[c & 1]), 0));
       }
       const bool any = __any_sync(0xffffffffu, jrow >= 0);
-      if (!any) continue;
+      if (!z_tma && !any) continue;
 #pragma unroll
       for (int cc = 0; cc < PCols / 32; ++cc) {
         const int64_t f0 = (int64_t)w.n * PN + ch * PCols + cc * 32;
-        if (f0 >= F) break;
-        if (zg) {
+        if (f0 >= F) break;                            // uniform over the column half's 4 warps
+        if (z_tma) {
+          // tile-order map through shared memory and one TMA store per 32-frame slice: the
+          // epilogue is back to folding as soon as the slice is staged
+          if (issuer) bulk_wait_read<0>();             // the previous slice's smem has been read
+          named_barrier(1 + ch, 128);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) sm.zs[ch][t * GM + q * 32 + lane] = rs[cc * 32 + t];
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          named_barrier(1 + ch, 128);
+          if (issuer) {
+            tma_store_2d(&mz, sm.zs[ch], w.t * GT + (int)rank * GM, (int)f0);
+            bulk_commit();
+          }
+        } else if (zg) {
           if (jrow >= 0) {
             float* zc = zg + f0 * J + jrow;
 #pragma unroll
             for (int t = 0; t < 32; ++t)
-              if (f0 + t < F) __stcs(zc + t * J, rs[cc * 32 + t]);
+              if (f0 + t < F) st_global_hint(zc + t * J, rs[cc * 32 + t], zpol);
           }
         } else if (zt) {
           float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
 #pragma unroll
           for (int t = 0; t < 32; ++t)
-            if (f0 + t < F) __stcs(zc + t * ldt, rs[cc * 32 + t]);
+            if (f0 + t < F) st_global_hint(zc + t * ldt, rs[cc * 32 + t], zpol);
         }
-        if (keys) {   // per frame: warp max of the ordered bits (redux), lowest winning lane (ballot)
+        if (keys && any) {   // per frame: warp max of the ordered bits (redux), lowest winning lane (ballot)
           uint32_t best = 0u, win = 0u;
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
@@ -832,6 +854,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
         }
       }
     }
+    if (issuer) bulk_wait_all();                       // the map's TMA stores have landed
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();
@@ -1025,6 +1048,19 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
     const int x = v ? atoi(v) : 0;
     return x >= 1 && x <= 64 ? x : 8;
   }();
+  // tile-order map through TMA stores (the pair kernel): box of 128 candidates x 32 frames
+  CUtensorMap mz = ma_hi;
+  int z_tma = 0;
+  if (z && z_tiles && !getenv("SRPGPU_GATHER_ZSTG")) {
+    const int64_t ldt = (int64_t)num_tiles * GT;
+    if ((s = make_map_2d(&mz, f32, 4, z_tiles, num_frames, ldt, ldt, GM, 32, "interp_map_gather_tf32",
+                         CU_TENSOR_MAP_SWIZZLE_NONE)))
+      return s;
+    z_tma = 1;
+  }
+  // diagnostic: SRPGPU_GATHER_ZTEST=1 writes every frame's tile-order row to the same place
+  // (isolates the cost of issuing the map stores from the cost of their DRAM traffic)
+  static const int64_t zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
   int clusters = 0;
   if (pair_env && b3d) {
     const size_t psmem = sizeof(g32::PairSmem) + 1024;
@@ -1063,7 +1099,7 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
     const int ub = (int)(g0 * units_per_group), ue = (int)(g1 * units_per_group);
     if (clusters > 0)
       g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
-          ma_hi, ma_lo, mb_hi, mb_lo, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
+          ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && zt_ld < 0, zt_ld, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
           tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
           reinterpret_cast<unsigned long long*>(keys));
     else
