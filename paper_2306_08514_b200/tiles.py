@@ -70,11 +70,20 @@ def _entries(sp, offsets):
     return rows, pairs, to_natural(cols, offsets), vals
 
 
-def bisect_tiles(feat: np.ndarray, tile: int = TILE, weight=None) -> list:
+def bisect_tiles(feat: np.ndarray, tile: int = TILE, weight=None, lo=None, hi=None, group: int = GROUP,
+                 tries: int = 1) -> list:
     """Recursive bisection of the rows of `feat` (n, D) into groups of total weight <=
-    `tile` (weight: rows per item, default 1), splitting along the widest coordinate at
-    a multiple of `tile` near the (weighted) median."""
+    `tile` (weight: rows per item, default 1), splitting at a multiple of `tile` near the
+    (weighted) median.  The split axis is the widest coordinate, or -- with the items'
+    per-pair lag windows `lo` / `hi` (n, D) and tries > 1 -- the one among the `tries`
+    widest whose two halves have the smallest summed window widths (rounded up to `group`
+    lags, each half weighted by its share of tiles): the K the kernel iterates."""
     w = np.ones(feat.shape[0], dtype=np.int64) if weight is None else np.asarray(weight, dtype=np.int64)
+
+    def cost(ix):
+        width = hi[ix].max(axis=0) - lo[ix].min(axis=0) + 1
+        return float(np.sum((width + group - 1) // group * group))
+
     out, stack = [], [np.arange(feat.shape[0], dtype=np.int64)]
     while stack:
         idx = stack.pop()
@@ -83,14 +92,27 @@ def bisect_tiles(feat: np.ndarray, tile: int = TILE, weight=None) -> list:
             out.append(np.sort(idx))
             continue
         sub = feat[idx]
-        p = int(np.argmax(sub.max(axis=0) - sub.min(axis=0)))
-        order = idx[np.argsort(sub[:, p], kind="stable")]
+        spread = sub.max(axis=0) - sub.min(axis=0)
         target = tile * max(1, int(round(total / (2 * tile)))) if total > 2 * tile else total // 2
-        cum = np.cumsum(w[order])
-        n1 = int(np.clip(np.searchsorted(cum, target, side="right"), 1, idx.shape[0] - 1))
-        stack.append(order[n1:])
-        stack.append(order[:n1])
+        axes = [int(np.argmax(spread))] if tries <= 1 or lo is None else list(np.argsort(-spread)[:tries])
+        best = None
+        for p in axes:
+            order = idx[np.argsort(sub[:, p], kind="stable")]
+            cum = np.cumsum(w[order])
+            n1 = int(np.clip(np.searchsorted(cum, target, side="right"), 1, idx.shape[0] - 1))
+            if len(axes) == 1:
+                best = (0.0, order[:n1], order[n1:])
+                break
+            a, b = order[:n1], order[n1:]
+            c = cost(a) * (w[a].sum() / tile) + cost(b) * (w[b].sum() / tile)
+            if best is None or c < best[0]:
+                best = (c, a, b)
+        stack.append(best[2])
+        stack.append(best[1])
     return out
+
+
+BISECT_TRIES = 8     # split axes tried per bisection step (1: widest only; 8: -4% window K at cfg4)
 
 
 class TileLayout:
@@ -140,7 +162,14 @@ class TileLayout:
             rfeat = np.zeros((n_runs, p_count))
             np.add.at(rfeat, run, feat)
             rfeat = (rfeat / np.bincount(run, minlength=n_runs)[:, None]).astype(np.float32)
-            tiles = bisect_tiles(rfeat, TILE, weight=np.full(n_runs, 8))       # lists of runs
+            rlo = np.full((n_runs, p_count), np.iinfo(np.int64).max)
+            rhi = np.full((n_runs, p_count), -1)
+            np.minimum.at(rlo, run, np.where(empty.reshape(num_rows, p_count), np.iinfo(np.int64).max,
+                                             lo_ip.reshape(num_rows, p_count)))
+            np.maximum.at(rhi, run, hi_ip.reshape(num_rows, p_count))
+            rlo = np.where(rhi < 0, 0, rlo)
+            tiles = bisect_tiles(rfeat, TILE, weight=np.full(n_runs, 8), lo=rlo, hi=rhi, group=GROUP,
+                                 tries=BISECT_TRIES)                                    # lists of runs
             t_count = len(tiles)
             tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
             for t, rr in enumerate(tiles):
@@ -151,7 +180,9 @@ class TileLayout:
                 tile_of[cand[ok]] = t
                 row_of[cand[ok]] = pos[ok]
         else:
-            tiles = bisect_tiles(feat) if num_rows else []
+            clo = np.where(empty, 0, lo_ip).reshape(num_rows, p_count)
+            chi = hi_ip.reshape(num_rows, p_count)
+            tiles = bisect_tiles(feat, lo=clo, hi=chi, group=GROUP, tries=BISECT_TRIES) if num_rows else []
             t_count = len(tiles)
             tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
             for t, idx in enumerate(tiles):
