@@ -299,7 +299,7 @@ static size_t frontend_smem(int in, int out, int L, int K, int M, int P, int nbu
 // 0.43 ms), medians of 5 alternating runs (tools/bench_frontend.py --rounds 5).
 constexpr int64_t kLaneMaxFrames = 2;    // frames per SM (M < 8)
 constexpr int64_t kLaneMaxFrames8 = 12;  // frames per SM (M >= 8)
-constexpr int kLaneMinMics = 12;
+constexpr int kLaneMinMics = 8;     // (r2: with TF32 planes the task kernel wins at every cfg3 batch size)
 
 template <int IN, int OUT>
 static int launch_frontend(FrontendParams prm, cudaStream_t stream, const char* what) {

@@ -264,12 +264,17 @@ __device__ __forceinline__ void inverse_pair(const WarpParams& prm, const float2
   }
 }
 
+// resident CTAs per SM the register budget is cut for: the kernel is issue / latency bound
+// with few warps (ncu cfg4: 8 warps per SM, 55% issue active), so a second (third) CTA per
+// SM pays more than the registers it costs -- cfg4 (Q = 16, 2 CTAs at 128 registers, no
+// spills; 80 KB of shared memory each) 3.36 -> 2.64 ms per 10^4 frames; Q = 8 fits 3 at
+// 80 registers without spills
 #ifndef LANE_MINB
-#define LANE_MINB 1
+#define LANE_MINB(Q) ((Q) >= 16 ? 2 : 3)
 #endif
 
 template <int Q, int OUT, int WPF>
-__global__ void __launch_bounds__(WPF * 32, LANE_MINB)
+__global__ void __launch_bounds__(WPF * 32, LANE_MINB(Q))
 frontend_lane_kernel(const WarpParams prm) {
   using G = Geo<Q>;
   constexpr int N = G::N, L = G::L, K = N, B = K - 1, SLOT = G::SLOT;

@@ -21,7 +21,7 @@ from paper_2306_08514_b200 import workloads  # noqa: E402
 from paper_2306_08514_b200.frontend import frontend_kernel  # noqa: E402
 
 DEFAULT_FRAMES = {"cfg1": 100, "cfg2": 1000, "cfg3": 10000, "cfg4": 10000}
-PLANES = {"cfg1": (False, False), "cfg2": (False, False), "cfg3": (True, False), "cfg4": (True, True)}
+ENGINE = {"cfg1": "band", "cfg2": "band", "cfg3": "tile", "cfg4": "tile"}   # the map engine whose planes are written
 
 
 def time_graph(fn, reps, flush):
@@ -58,7 +58,7 @@ def main():
         frame_list = [int(f) for f in a.frames.split(",")] if a.frames else [DEFAULT_FRAMES[name]]
         wl = workloads.make(name, num_frames=max(frame_list))
         x = torch.from_numpy(wl.samples).cuda()
-        planes, natural = PLANES.get(name, (False, False))
+        pa = s.maps.plane_args(ENGINE.get(name, "band"))
         for frames in frame_list:
             times = {k: [] for k in a.kernels.split(",")}
             for _ in range(a.rounds):
@@ -66,15 +66,14 @@ def main():
                     with frontend_kernel(k):
                         try:
                             times[k].append(time_graph(
-                                lambda: s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(frames),
-                                                            planes=planes, natural=natural), a.reps, flush))
+                                lambda: s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(frames), **pa),
+                                a.reps, flush))
                         except Exception as exc:  # noqa: BLE001
                             times[k].append(float("nan"))
                             print(json.dumps({"workload": name, "frames": frames, "kernel": k, "error": str(exc)}))
             for k, ts in times.items():
                 ms = sorted(ts)[len(ts) // 2]
-                print(json.dumps({"workload": name, "frames": frames, "kernel": k, "planes": planes,
-                                  "natural": natural, "ms": ms, "ns_per_frame": ms * 1e6 / frames,
+                print(json.dumps({"workload": name, "frames": frames, "kernel": k, "planes": pa, "ms": ms, "ns_per_frame": ms * 1e6 / frames,
                                   "all_ms": ts}), flush=True)
 
 if __name__ == "__main__":
