@@ -643,7 +643,7 @@ __device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint6
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
 gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
                         const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
-                        const __grid_constant__ CUtensorMap mz, int z_tma, int64_t zt_ld,
+                        const __grid_constant__ CUtensorMap mz, int z_tma, int l2pol, int64_t zt_ld,
                         int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                         const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
                         const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
@@ -686,7 +686,10 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     // lanes 0-7: (plane, group) of this CTA's frame half; lanes 8-9: this CTA's slab half
     constexpr uint32_t kBytes = 2u * (GM * GK + PNC * GK) * sizeof(float);   // one CTA's stage
     const int plane = (lane >> 2) & 1, grp = lane & 3, ap = (lane - 8) & 1;
-    const uint64_t keep = policy_evict_last(), once = policy_evict_first();   // as the one-CTA kernel
+    // L2 policies as the one-CTA kernel (l2pol: diagnostic override, 2 bits each for the
+    // samples / slabs: 0 evict_last, 1 evict_first, 2 evict_normal)
+    auto pol = [](int c) { return c == 0 ? policy_evict_last() : c == 1 ? policy_evict_first() : policy_evict_normal(); };
+    const uint64_t keep = pol(l2pol & 3), once = pol((l2pol >> 2) & 3);
     auto next_unit = [&](int u, Unit& w) {
       while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += ncl;
       return u;
@@ -1061,6 +1064,9 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   // diagnostic: SRPGPU_GATHER_ZTEST=1 writes every frame's tile-order row to the same place
   // (isolates the cost of issuing the map stores from the cost of their DRAM traffic)
   static const int64_t zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
+  // L2 policies: samples evict_last, slabs evict_normal (4096 frames: 23 GB of DRAM reads
+  // against 41 GB with evict_first slabs and 71 GB with both evict_first)
+  static const int l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (2 << 2));
   int clusters = 0;
   if (pair_env && b3d) {
     const size_t psmem = sizeof(g32::PairSmem) + 1024;
@@ -1099,7 +1105,7 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
     const int ub = (int)(g0 * units_per_group), ue = (int)(g1 * units_per_group);
     if (clusters > 0)
       g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
-          ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && zt_ld < 0, zt_ld, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
+          ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && zt_ld < 0, l2pol, zt_ld, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
           tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
           reinterpret_cast<unsigned long long*>(keys));
     else
