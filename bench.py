@@ -9,7 +9,7 @@ A step is one pass of the hot path over one batch of F frames of the workload
 M = 16, J = 334611, K = 512, F = 10^4 frames per GPU, SSPI with the reference's global
 top-Q fit at Q = 2JP):
     samples --(fused STFT + GCC/PHAT + iFFT sampling kernel)--> xi (TF32 hi / lo planes)
-            --(3xTF32 gathered-window tensor-core SSPI map, fused argmax)--> z [F][J] + argmax [F]
+            --(split-operand (fp16x3 / 3xTF32) gathered-window tensor-core SSPI map, fused argmax)--> z [F][J] + argmax [F]
 For N > 1 (one process per GPU; `--gpus N` re-launches itself under torchrun when
 WORLD_SIZE is unset) each rank maps its own contiguous block of frames (weak scaling)
 and the per-frame argmax keys are all-gathered over NCCL inside the timed region.
@@ -59,7 +59,7 @@ def parse():
                     help="SSPI fit where the dense operator is infeasible (cfg4): the reference's global "
                          "top-Q rule, streamed (global), or nnz per (candidate, pair) (fixed)")
     ap.add_argument("--rank-r", type=int, default=16, help="rank for LR / SLRI")
-    ap.add_argument("--engine", default="auto", choices=["auto", "fused", "tc", "tile", "tile_bf16", "band"],
+    ap.add_argument("--engine", default="auto", choices=["auto", "fused", "tc", "tile", "tile_f16", "tile_bf16", "band"],
                     help="SSPI / SI map engine (maps.interp_engine)")
     ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "tf32x3", "fp32"],
                     help="conventional map arithmetic (maps.conv_precision)")
@@ -230,9 +230,9 @@ def algorithmic_bytes(wl, variant, frames, op, eng="band"):
         c8 = (s_tot + 7) // 8 * 8
         if eng == "tc":                                 # dense bf16 hi/lo planes: 4 B per sample slot
             out["map"] = frames * (4 * c8 + 4 * j) + 4 * j * c8
-        elif eng in ("tile", "tile_bf16"):              # gathered windows: the tile slabs once
-            t = maps.tile_from_sparse(op, maps.spec_offsets(wl.spec), tf32=(eng == "tile"))
-            per = 8 if eng == "tile" else 4             # hi + lo planes: fp32 or bf16
+        elif eng in maps.TILE_ENGINES:                  # gathered windows: the tile slabs once
+            t = maps.tile_from_sparse(op, maps.spec_offsets(wl.spec), fmt=maps.TILE_ENGINES[eng])
+            per = 8 if eng == "tile" else 4             # hi + lo planes: fp32, or fp16 / bf16
             out["map"] = frames * (per * c8 + 4 * j) + per * t.num_slabs * 128 * 64
         else:
             nnz_stored = getattr(op, "num_kept", None)
@@ -311,6 +311,11 @@ def arithmetic(variant, eng, precision):
         return ("tf32x3", "FP32-class: frontend fp32 SIMT; map on tcgen05 kind::tf32 with hi = tf32_rne(x), "
                           "lo = tf32_rne(x - hi) operands (3 passes), TMEM chunks of 8 x 16 lags folded into "
                           "fp32 registers")
+    if eng == "tile_f16":
+        return ("f16x3", "FP32-class: frontend fp32 SIMT; map on tcgen05 kind::f16 with fp16 split operands hi = "
+                         "f16_rne(x), lo = f16_rne(x - hi) (11 + 11 significant bits, as the 3xTF32 split; PHAT "
+                         "samples are bounded by 2(K-1), slab weights pre-scaled by 2^8; 3 passes hi*hi + hi*lo + "
+                         "lo*hi), TMEM chunks of 8 x 32 lags folded into fp32 registers")
     if eng in ("tc", "tile_bf16"):
         return ("bf16x3", "frontend fp32 SIMT; map on tcgen05 kind::f16 with bf16 hi / lo operands (3 passes, "
                           "16 significant bits), fp32 accumulation")
@@ -336,7 +341,7 @@ def headline_engine(args, wl, op, count):
                 return "fused"
         except Exception:        # no device to size the fused kernel's grid: not the fused chain
             pass
-    return maps.map_engine(v, op, "auto" if args.engine == "fused" else args.engine, count)
+    return maps.map_engine(v, op, "auto" if args.engine == "fused" else args.engine, count, bounded=True)
 
 
 def make_config(args, wl, per_gpu, total, world, op, eng, in_bytes):
@@ -352,6 +357,8 @@ def make_config(args, wl, per_gpu, total, world, op, eng, in_bytes):
             "map_engine": {"fused": "fused chain: frontend + sliced-ELL SSPI map + argmax in one kernel",
                            "tc": "tensor cores (dense operator, bf16x3)",
                            "tile": "tensor cores (gathered lag windows on CTA pairs, 3xTF32 + fp32 folds)",
+                           "tile_f16": "tensor cores (gathered lag windows on CTA pairs, fp16x3 split operands + "
+                                       "fp32 folds)",
                            "tile_bf16": "tensor cores (gathered lag windows, bf16x3)",
                            "band": "FP32 tiled band"}.get(eng, eng),
             "parallelism": f"frames/{world}",
@@ -454,7 +461,7 @@ def run_ours(args):
     from paper_2306_08514_b200 import maps as _maps
     fused = pipe.uses_fused_chain()
     eng = "fused" if fused else _maps.map_engine(args.variant, op, "auto" if args.engine == "fused" else args.engine,
-                                                 count)
+                                                 count, bounded=True)   # the bench weights with PHAT
     # ---- per-kernel times for the roofline: each stage captured alone, CUDA events; a stage
     # measured alone carries its own launch latency, so the times are scaled to their share
     # of the ring-timed step whenever they add up to more than it
@@ -493,7 +500,7 @@ def run_ours(args):
                 "unit": "TFLOP/s", "frac": achieved / tf32_peak, "mma_passes": passes,
                 "peak_source": f"TF32 cuBLAS {xsrc}", "frac_of_bf16_peak": achieved / bf16,
                 "traffic": ncu_traffic(args.workload, args.variant, dom_name)}
-    elif eng in ("tile", "tile_bf16", "tc") and t_map >= t_front:
+    elif (eng == "tc" or eng in _maps.TILE_ENGINES) and t_map >= t_front:
         # tensor-core interpolation map: bound by the MMA work it issues (3 passes over the
         # dense per-tile lag windows), next to the useful flops (2 per kept entry) and HBM
         if eng == "tc":
@@ -501,10 +508,12 @@ def run_ours(args):
             mma = 3 * 2.0 * wl.grid.num_points * c8 * count
             name, peak, psrc = "interp_tc_kernel", bf16, f"bf16 {peak_src} (MEASURED_PEAKS.json)"
         else:
-            t = _maps.tile_from_sparse(op, _maps.spec_offsets(wl.spec), tf32=(eng == "tile"))
+            t = _maps.tile_from_sparse(op, _maps.spec_offsets(wl.spec), fmt=_maps.TILE_ENGINES[eng])
             mma = 3 * 2.0 * t.num_tiles * 256 * t.mean_k * count      # the K the kernel iterates
             if eng == "tile":
-                name, peak, psrc = "gather_tf32_pair_kernel", tf32_peak, f"TF32 cuBLAS {xsrc}"
+                name, peak, psrc = "gather_pair_kernel<PairTf32>", tf32_peak, f"TF32 cuBLAS {xsrc}"
+            elif eng == "tile_f16":     # kind::f16 runs at the bf16 rate: the driver-measured dense peak
+                name, peak, psrc = "gather_pair_kernel<PairF16>", bf16, f"bf16/fp16 dense {peak_src} (MEASURED_PEAKS.json)"
             else:
                 name, peak, psrc = "gather_tc_kernel", bf16, f"bf16 {peak_src} (MEASURED_PEAKS.json)"
         achieved = mma / (t_map / 1e3) / 1e12
@@ -541,7 +550,7 @@ def run_ours(args):
         "fused_chain": ((frontend_flops(wl, args.variant, count) + map_flops(wl, args.variant, op, count))
                         / (t_map / 1e3) / 1e12 / fp32_peak if fused else None),
         "map": (map_flops(wl, args.variant, op, count) / (t_map / 1e3) / 1e12 / fp32_peak
-                if args.variant not in ("conv", "conv_h") and eng not in ("tc", "tile", "tile_bf16", "fused")
+                if args.variant not in ("conv", "conv_h") and eng not in ("tc", "tile", "tile_f16", "tile_bf16", "fused")
                 else None),
         "fp32_peak_tflops": fp32_peak, "peak_source": f"FP32 SIMT cuBLAS {xsrc}"}
 
@@ -639,7 +648,7 @@ def run_ours(args):
                     entry["operator"] = ("steering generated on chip" if v == "conv"
                                          else "stored steering matrix via TMA")
                 else:
-                    ev = _maps.map_engine(v, opv, "auto", count)
+                    ev = _maps.map_engine(v, opv, "auto", count, bounded=True)
                     entry["dtype"] = arithmetic(v, ev if ev else "simt", "auto")[0]
                 if v in ("lr", "slri"):
                     entry["rank"] = args.rank_r
@@ -822,7 +831,7 @@ def stage_times(s, wl, variant, op, x_dev, count, flush, reps=10, engine="auto",
     frames = range(0, count)
     if variant in ("sspi", "si", "slri"):
         from paper_2306_08514_b200 import maps
-        eng = maps.map_engine(variant, op, engine, count)   # the pipeline's frontend also writes the planes
+        eng = maps.map_engine(variant, op, engine, count, bounded=True)   # the pipeline's frontend also writes the planes
         front = lambda: s.frames_to_samples(x_dev, wl.frame, wl.pairs, wl.spec, frames,
                                             **maps.plane_args(eng))
         mapf = {"sspi": s.sspi_map, "si": s.si_map, "slri": s.slri_map}[variant]

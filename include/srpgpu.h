@@ -111,7 +111,9 @@ int srpgpu_frames_to_samples(const float* samples, int32_t num_channels, int64_t
  * (srpgpu_interp_map_gather_tc); natural_src [S] int32 maps each natural index to its
  * storage index (used when a non-warp kernel produced the samples).  natural bit 1:
  * fp32 TF32 planes (hi = tf32_rne(x), lo = tf32_rne(x - hi); lag-major only) for
- * srpgpu_interp_map_gather_tf32. */
+ * srpgpu_interp_map_gather_tf32.  natural bit 2: fp16 planes (hi = f16_rne(x), lo =
+ * f16_rne(x - hi); lag-major only, planes_ld a multiple of 64) for
+ * srpgpu_interp_map_gather_f16 -- PHAT-weighted samples only (|xi| <= 2(K-1) fits fp16). */
 int srpgpu_frames_to_samples_planes(const float* samples, int32_t num_channels, int64_t num_samples,
                                     int64_t ld_samples, const float* window, int32_t frame_len,
                                     int32_t hop, int64_t first_frame, int64_t num_frames,
@@ -232,6 +234,26 @@ int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frame
                                   const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
                                   int32_t num_ctas, const int32_t* tile_pos, float* z_tiles, float* z,
                                   uint64_t* keys, srpgpu_stream_t stream);
+
+/* The same map with fp16x3 operands (FP32-class while the operands stay in fp16 range:
+ * hi = f16_rne(x), lo = f16_rne(x - hi) carry the same 11 + 11 significant bits as the TF32
+ * split; tcgen05 kind::f16 at twice the TF32 rate; TMEM chunks folded into fp32 registers):
+ * samples_planes fp16 [2][round8(S)][planes_ld] (planes_ld a multiple of 64, 128-byte
+ * aligned, natural lag order; PHAT samples are bounded by 2(K-1)), slab_planes fp16
+ * [2][num_slabs * 128][64] = srpgpu_split_f16_rows of the slabs scaled by 1 / z_scale (a
+ * power of two; the kernel multiplies the finished sums by z_scale, exactly); group_col
+ * holds 8-lag groups (8 per block) and tile_nst counts each tile's 32-lag stages.  CTA pairs
+ * (cta_group::2) only.  Replaces interpolation.py:188-195 (sspi_map) / :129-136 (si_map). */
+int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t num_frames, int32_t num_cols,
+                                 int64_t planes_ld, const void* slab_planes, int64_t num_slabs,
+                                 const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nst,
+                                 const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
+                                 int32_t num_ctas, const int32_t* tile_pos, float z_scale, float* z_tiles,
+                                 float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* srpgpu_split_bf16_rows into fp16 hi / lo planes of scale * x (hi = f16_rne, lo = f16_rne(. - hi)). */
+int srpgpu_split_f16_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols, const int32_t* row_src,
+                          float scale, void* dst, int64_t ld_dst, int64_t rows_dst, srpgpu_stream_t stream);
 
 /* srpgpu_split_bf16_rows into fp32 TF32 hi / lo planes (hi = tf32_rne(x), lo = tf32_rne(x - hi)). */
 int srpgpu_split_tf32_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols, const int32_t* row_src,

@@ -569,9 +569,9 @@ extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num
   prm.floor_value = (float)floor_value; prm.counts = counts; prm.offsets = offsets;
   prm.S = total_samples; prm.xi_out = samples_out; prm.xi_ld = samples_ld;
   prm.xi_planes = reinterpret_cast<uint16_t*>(planes); prm.cols8 = cols8; prm.xi_natural = (natural & 1) ? 1 : 0;
-  prm.planes_ld = planes_ld; prm.planes_tf32 = (natural & 2) ? 1 : 0;
+  prm.planes_ld = planes_ld; prm.planes_tf32 = (natural & 4) ? 2 : (natural & 2) ? 1 : 0;
   SRPGPU_CHECK_ARG(!prm.planes_tf32 || planes_ld > 0, SRPGPU_ERR_VALUE,
-                   "frames_to_samples: TF32 planes are lag-major only (planes_ld > 0)");
+                   "frames_to_samples: TF32 / fp16 planes are lag-major only (planes_ld > 0)");
   SRPGPU_CHECK_ARG(planes_ld == 0 || (planes_ld >= num_frames && planes_ld % 8 == 0), SRPGPU_ERR_VALUE,
                    "frames_to_samples: lag-major planes need a pitch >= F, a multiple of 8");
   SRPGPU_CHECK_ARG(!natural || natural_src, SRPGPU_ERR_VALUE, "frames_to_samples: natural planes need the column map");
@@ -583,6 +583,9 @@ extern "C" int srpgpu_frames_to_samples_planes(const float* samples, int32_t num
   if ((st = launch_frontend<IN_SAMPLES, OUT_XI>(prm, as_stream(stream), "frames_to_samples"))) return st;
   if (warp_used || num_frames == 0) return SRPGPU_OK;
   // block-kernel frame lengths: split the f32 samples afterwards
+  if (prm.planes_tf32 == 2)
+    return srpgpu_split_f16_rows(samples_out, samples_ld, total_samples, num_frames,
+                                 prm.xi_natural ? natural_src : nullptr, 1.0f, planes, planes_ld, cols8, stream);
   if (prm.planes_tf32)
     return srpgpu_split_tf32_rows(samples_out, samples_ld, total_samples, num_frames,
                                   prm.xi_natural ? natural_src : nullptr, reinterpret_cast<float*>(planes), planes_ld,

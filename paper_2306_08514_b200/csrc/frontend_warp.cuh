@@ -1,6 +1,7 @@
 // Parameters of the warp-per-frame frontend (frontend_warp.cu), shared with frontend.cu.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -32,7 +33,8 @@ struct WarpParams {
   int32_t cols8;
   int32_t xi_natural;   // planes in natural lag order -N_p..N_p per pair (gathered-window engine)
   int64_t planes_ld;    // 0: planes frame-major [2][F][cols8]; > 0: lag-major [2][cols8][planes_ld]
-  int32_t planes_tf32;  // planes are fp32 hi = tf32_rne(x), lo = tf32_rne(x - hi) (lag-major only)
+  int32_t planes_tf32;  // 1: planes are fp32 hi = tf32_rne(x), lo = tf32_rne(x - hi); 2: fp16 hi = f16_rne(x),
+                        // lo = f16_rne(x - hi) (both lag-major only; fp16 needs |x| in fp16 range: PHAT)
 };
 
 // PHAT weighting raw / max(|raw|, floor), 0 where that is 0 (frontend.py:154-158), with the
@@ -60,6 +62,13 @@ __device__ __forceinline__ void put_xi(const WarpParams& prm, float* dst, int64_
   dst[(o + d) * sst] = v;
   if (prm.xi_planes) {
     const int col = o + (prm.xi_natural ? (d <= N ? N + d : d - N - 1) : d);
+    if (prm.planes_tf32 == 2) {               // lag-major fp16 [2][cols8][planes_ld]
+      __half* pl = reinterpret_cast<__half*>(prm.xi_planes) + (int64_t)col * prm.planes_ld + f;
+      const __half hi = __float2half_rn(v);
+      pl[0] = hi;
+      pl[(int64_t)prm.cols8 * prm.planes_ld] = __float2half_rn(v - __half2float(hi));
+      return;
+    }
     if (prm.planes_tf32) {                    // lag-major fp32 [2][cols8][planes_ld]
       float* pl = reinterpret_cast<float*>(prm.xi_planes) + (int64_t)col * prm.planes_ld + f;
       const float hi = tf32_rne(v);

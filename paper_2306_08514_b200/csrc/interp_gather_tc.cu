@@ -607,49 +607,95 @@ gather_tf32_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
   }
 }
 // ---- the same on CTA pairs (cta_group::2, a 2-CTA cluster per tile) ---------------------
-// One tcgen05.mma.cta_group::2 (M = 256 candidates, N = 256 frames, K = 8) covers the whole
+// One tcgen05.mma.cta_group::2 (M = 256 candidates, N = 256 frames) covers the whole
 // tile: CTA r of the pair holds tile half r (rows 128r..128r+127) of the slabs and frames
 // 128r..128r+127 of the unit's gathered samples, so each SM streams half the operand bytes
-// of the one-CTA kernel per MMA (32 KB per 16-lag stage), and its accumulator is its 128
+// of the one-CTA kernel per MMA (32 KB per stage), and its accumulator is its 128
 // candidates x 256 frames, which leaves room for the two fold buffers.  The leader (rank
 // 0) issues the MMAs; both CTAs' TMA loads complete on the leader's stage barrier, the MMA
 // commits arrive on both CTAs' barriers, and both CTAs' epilogues release a fold buffer on
 // the leader's barrier.
+//
+// Two operand formats share the kernel (same bytes per stage, same barriers, same epilogue):
+//   PairTf32: fp32 planes hi = tf32_rne(x), lo = tf32_rne(x - hi); kind::tf32, K = 8 per MMA,
+//             16-lag stages, 4-lag gathered groups (512-byte MN atoms of 4 lags x 32 frames);
+//   PairF16:  fp16 planes hi = f16_rne(x), lo = f16_rne(x - hi) -- the same 11 + 11
+//             significant bits as the TF32 split while |x| stays in fp16 range (PHAT samples
+//             are bounded by 2(K-1); the slab weights are scaled by a power of two on the
+//             host and the epilogue undoes it exactly) -- kind::f16, K = 16 per MMA at twice
+//             the TF32 rate, 32-lag stages, 8-lag groups (1 KB MN atoms of 8 lags x 64 frames).
 constexpr int PN = 256;              // frames per unit (pair)
 constexpr int PNC = PN / 2;          // frames per CTA (B half)
-constexpr int PNA = PNC / GA;        // frame blocks per group per CTA
 constexpr int PNS = 5;               // operand stages (32 KB each)
-constexpr int PEpi = kEpi;          // epilogue warps
+constexpr int PEpi = kEpi;           // epilogue warps
 constexpr int PThreads = kThreads;
 constexpr int PCols = PN / (PEpi / 4);         // accumulator columns folded per epilogue thread
+constexpr int PGroupBytes = 2048;    // one (plane, group) of a CTA's 128 frames
+constexpr int PSlabBytes = 8192;     // one plane of a CTA's slab half per stage
+constexpr int PNG = 4;               // groups per stage
 
+struct PairTf32 {
+  static constexpr int GK = 16, GG = 4, UK = 8, GA = 32, ES = 4;
+  static constexpr uint32_t kFmt = 2;          // instruction descriptor operand format: tf32
+  static __device__ __forceinline__ uint64_t desc_b(const void* p) { return desc_mn128(p); }
+  static __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+};
+
+struct PairF16 {
+  static constexpr int GK = 32, GG = 8, UK = 16, GA = 64, ES = 2;
+  static constexpr uint32_t kFmt = 0;          // f16
+  // MN-major fp16 operand, 128-byte swizzle: 1 KB atoms of 8 lags x 64 frames; a group's two
+  // frame blocks follow one another (LBO = 1 KB along N), the next 8 lags are the next group
+  // (SBO = 2 KB along K)
+  static __device__ __forceinline__ uint64_t desc_b(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    uint64_t d = 0;
+    d |= (addr & 0x3FFFFull) >> 4;
+    d |= (uint64_t)(1024 >> 4) << 16;
+    d |= (uint64_t)(PGroupBytes >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+    return d;
+  }
+  static __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+};
+
+template <class TR>
 struct __align__(1024) PairSmem {
-  float b[PNS][2][NG][PNC * GG];     // [plane][group] 4 frame blocks of [4 lags][32 frames] (2 KB)
-  float a[PNS][2][GM * GK];          // [plane] this CTA's slab half (8 KB)
-  float zs[2][32 * GM];              // [column half] one 32-frame slice of the map for a TMA store
-  int32_t rows[2][kMaxGroups];
+  unsigned char b[PNS][2][PNG][PGroupBytes];   // [plane][group] the CTA's frame blocks of one lag group
+  unsigned char a[PNS][2][PSlabBytes];         // [plane] this CTA's slab half (64-byte rows, 64-byte swizzle)
+  float zs[2][32 * GM];                        // [column half] one 32-frame slice of the map for a TMA store
+  int32_t rows[2][kMaxBlocks * (GB / TR::GG)];
   uint64_t full[PNS], empty[PNS], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
+template <class TR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
-gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
-                        const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
-                        const __grid_constant__ CUtensorMap mz, int z_tma, int l2pol, int64_t zt_ld,
-                        int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
-                        const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
-                        const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
-                        unsigned long long* __restrict__ keys) {
+gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
+                   const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+                   const __grid_constant__ CUtensorMap mz, int z_tma, int l2pol, int64_t zt_ld, float zscale,
+                   int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                   const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
+                   const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
+                   unsigned long long* __restrict__ keys) {
+  constexpr int GK = TR::GK, GG = TR::GG, UK = TR::UK, GA = TR::GA, ES = TR::ES;
+  constexpr int PNA = PNC / GA;                // frame blocks per group per CTA
+  static_assert(GK / GG == PNG && PNC * GG * ES == PGroupBytes && GM * GK * ES == PSlabBytes, "stage geometry");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  PairSmem& sm = *reinterpret_cast<PairSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  PairSmem<TR>& sm = *reinterpret_cast<PairSmem<TR>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -684,7 +730,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
 
   if (warp == 0) {
     // lanes 0-7: (plane, group) of this CTA's frame half; lanes 8-9: this CTA's slab half
-    constexpr uint32_t kBytes = 2u * (GM * GK + PNC * GK) * sizeof(float);   // one CTA's stage
+    constexpr uint32_t kBytes = 2u * (PSlabBytes + PNG * PGroupBytes);   // one CTA's stage
     const int plane = (lane >> 2) & 1, grp = lane & 3, ap = (lane - 8) & 1;
     // L2 policies as the one-CTA kernel (l2pol: diagnostic override, 2 bits each for the
     // samples / slabs: 0 evict_last, 1 evict_first, 2 evict_normal)
@@ -696,7 +742,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     };
     auto stage_rows = [&](int buf, const Unit& w) {
       const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
-      for (int i = lane; i < nst * NG; i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
+      for (int i = lane; i < nst * PNG; i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
     };
     uint32_t g = 0;
     int buf = 0;
@@ -711,7 +757,7 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
       const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
       for (int kq = 0; kq < nst; ++kq, ++g) {
         const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
-        const int row = sm.rows[buf][kq * NG + grp];
+        const int row = sm.rows[buf][kq * PNG + grp];
         const int s = g % PNS;
         const uint32_t bar = mapa_shared(smem_u32(&sm.full[s]), 0);    // the leader's stage barrier
         if (lane == 0) {
@@ -733,9 +779,9 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
     }
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
-      // D f32, A/B tf32, A K-major, B MN-major (bit 16), N = 256, M = 256 (the pair)
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(PN >> 3) << 17) |
-                                 ((uint32_t)((2 * GM) >> 4) << 24);
+      // D f32, A K-major, B MN-major (bit 16), N = 256, M = 256 (the pair)
+      constexpr uint32_t idesc = (1u << 4) | (TR::kFmt << 7) | (TR::kFmt << 10) | (1u << 16) |
+                                 ((uint32_t)(PN >> 3) << 17) | ((uint32_t)((2 * GM) >> 4) << 24);
       uint32_t g = 0, c = 0;
       for (int u = u_begin + cid; u < u_total; u += ncl) {
         Unit w;
@@ -753,12 +799,12 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
           const uint32_t d = tmem + (c & 1) * PN;
 #pragma unroll
           for (int k = 0; k < GK / UK; ++k) {
-            const uint64_t aoff = (uint64_t)((k * UK * 4) >> 4);
-            const uint64_t bh = desc_mn128(sm.b[s][0][2 * k]), bl = desc_mn128(sm.b[s][1][2 * k]);
+            const uint64_t aoff = (uint64_t)((k * UK * ES) >> 4);
+            const uint64_t bh = TR::desc_b(sm.b[s][0][2 * k]), bl = TR::desc_b(sm.b[s][1][2 * k]);
             const uint64_t a_h = smem_desc_sw64(sm.a[s][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][1]) + aoff;
-            mma_tf32_pair(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
-            mma_tf32_pair(d, a_h, bl, idesc, 1u);
-            mma_tf32_pair(d, a_l, bh, idesc, 1u);
+            TR::mma(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
+            TR::mma(d, a_h, bl, idesc, 1u);
+            TR::mma(d, a_l, bh, idesc, 1u);
           }
           mma_commit_pair(&sm.empty[s]);
           if (kq % CH == CH - 1 || kq == ns - 1) {
@@ -805,6 +851,10 @@ gather_tf32_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sm.tempty[c & 1]), 0));
+      }
+      if (zscale != 1.0f) {   // undo the slabs' power-of-two scale (exact)
+#pragma unroll
+        for (int t = 0; t < PCols; ++t) rs[t] *= zscale;
       }
       const bool any = __any_sync(0xffffffffu, jrow >= 0);
       if (!z_tma && !any) continue;
@@ -985,6 +1035,126 @@ extern "C" int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t n
   return SRPGPU_OK;
 }
 
+namespace srpgpu {
+namespace gtc {
+
+// tuning overrides shared by the gathered-window entry points
+struct GatherTuning {
+  int pair;                   // CTA pairs (SRPGPU_GATHER_PAIR=0: the one-CTA kernel)
+  int64_t frames_per_group;   // frames whose gathered samples stay L2-resident (SRPGPU_GATHER_GROUP)
+  int chunk;                  // stages per TMEM accumulation chunk (SRPGPU_GATHER_CHUNK)
+  int l2pol;                  // L2 policies (SRPGPU_GATHER_L2)
+  int64_t zt_ld;              // diagnostic: SRPGPU_GATHER_ZTEST=1 writes every frame's row to the same place
+  int zstg;                   // SRPGPU_GATHER_ZSTG: tile-order map by register stores instead of TMA stores
+};
+
+static const GatherTuning& tuning() {
+  static const GatherTuning t = [] {
+    GatherTuning g;
+    const char* v = getenv("SRPGPU_GATHER_PAIR");
+    g.pair = v ? atoi(v) : 1;
+    v = getenv("SRPGPU_GATHER_GROUP");
+    const int64_t x = v ? atoll(v) : 0;
+    // their hi / lo samples (F_g x S x 8 B in fp32, 58 MB at cfg4 with 1024 frames) stay
+    // L2-resident next to the slabs in flight
+    g.frames_per_group = x >= 256 && x % 256 == 0 ? x : (int64_t)1024;
+    v = getenv("SRPGPU_GATHER_CHUNK");
+    const int c = v ? atoi(v) : 0;
+    g.chunk = c >= 1 && c <= 64 ? c : 8;
+    // samples evict_last, slabs evict_normal (4096 frames: 23 GB of DRAM reads against 41 GB
+    // with evict_first slabs and 71 GB with both evict_first)
+    g.l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (2 << 2));
+    g.zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
+    g.zstg = getenv("SRPGPU_GATHER_ZSTG") ? 1 : 0;
+    return g;
+  }();
+  return t;
+}
+
+// co-resident 2-CTA clusters of the pair kernel (0: it cannot run here)
+template <class TR>
+static int pair_clusters(int num_ctas, cudaStream_t st) {
+  const size_t psmem = sizeof(g32::PairSmem<TR>) + 1024;
+  if (cudaFuncSetAttribute(g32::gather_pair_kernel<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(num_ctas & ~1));
+  cfg.blockDim = dim3(g32::PThreads);
+  cfg.dynamicSmemBytes = psmem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, g32::gather_pair_kernel<TR>, &cfg) != cudaSuccess) clusters = 0;
+  cudaGetLastError();
+  return std::min(clusters, num_ctas / 2);
+}
+
+// operand maps of the pair kernel: slabs [2][num_slabs * 128][64] (64-byte swizzle, one
+// stage of GK lags per box) and the lag-major sample planes viewed as {GA frames, lags,
+// frame blocks} (one 3D box per (plane, group): the CTA's frame blocks of GG lag rows)
+template <class TR>
+static int pair_maps(CUtensorMapDataType dt, const void* samples_planes, int32_t num_cols, int64_t planes_ld,
+                     const void* slab_planes, int64_t num_slabs, CUtensorMap* ma_hi, CUtensorMap* ma_lo,
+                     CUtensorMap* mb_hi, CUtensorMap* mb_lo, const char* what) {
+  const int64_t arows = num_slabs * GM;
+  const int64_t c8 = (int64_t)((num_cols + 7) / 8 * 8);   // planes hold round8(S) rows each
+  const auto* slabs = reinterpret_cast<const unsigned char*>(slab_planes);
+  const auto* xs = reinterpret_cast<const unsigned char*>(samples_planes);
+  int s;
+  if ((s = make_map_2d(ma_hi, dt, TR::ES, slabs, arows, GB, GB, TR::GK, GM, what, CU_TENSOR_MAP_SWIZZLE_64B)) ||
+      (s = make_map_2d(ma_lo, dt, TR::ES, slabs + arows * GB * TR::ES, arows, GB, GB, TR::GK, GM, what,
+                       CU_TENSOR_MAP_SWIZZLE_64B)))
+    return s;
+  const CUtensorMapSwizzle swz = TR::ES == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const int64_t dims[3] = {TR::GA, num_cols, planes_ld / TR::GA};
+  const int box[3] = {TR::GA, TR::GG, g32::PNC / TR::GA};
+  if ((s = make_map_3d(mb_hi, dt, xs, dims, planes_ld * TR::ES, TR::GA * TR::ES, box, what, swz)) ||
+      (s = make_map_3d(mb_lo, dt, xs + c8 * planes_ld * TR::ES, dims, planes_ld * TR::ES, TR::GA * TR::ES, box, what, swz)))
+    return s;
+  return SRPGPU_OK;
+}
+
+template <class TR>
+static int launch_pair(int clusters, const CUtensorMap& ma_hi, const CUtensorMap& ma_lo, const CUtensorMap& mb_hi,
+                       const CUtensorMap& mb_lo, float zscale, int64_t num_frames, int64_t num_candidates,
+                       int32_t num_tiles, const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nst,
+                       const int32_t* tile_rows, float* z_tiles, float* z, uint64_t* keys, cudaStream_t st,
+                       const char* what) {
+  const GatherTuning& tn = tuning();
+  // tile-order map through TMA stores: box of 128 candidates x 32 frames
+  CUtensorMap mz = ma_hi;
+  int z_tma = 0, s;
+  if (z && z_tiles && !tn.zstg) {
+    const int64_t ldt = (int64_t)num_tiles * GT;
+    if ((s = make_map_2d(&mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, z_tiles, num_frames, ldt, ldt, GM, 32, what,
+                         CU_TENSOR_MAP_SWIZZLE_NONE)))
+      return s;
+    z_tma = 1;
+  }
+  const int fg = (int)(tn.frames_per_group / g32::PN);
+  const int64_t units_per_group = (int64_t)num_tiles * fg;
+  const int64_t n_groups = (num_frames + tn.frames_per_group - 1) / tn.frames_per_group;
+  SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "%s: too many units", what);
+  g32::gather_pair_kernel<TR><<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem<TR>) + 1024, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && tn.zt_ld < 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
+      (int)(n_groups * units_per_group), num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nst,
+      tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
+  SRPGPU_CHECK_LAUNCH(what);
+  return SRPGPU_OK;
+}
+
+}  // namespace gtc
+}  // namespace srpgpu
+
 extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
                                              int64_t planes_ld, const float* slab_planes, int64_t num_slabs,
                                              const int32_t* group_col, const int32_t* tile_slab,
@@ -1006,120 +1176,109 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   int s = reset_keys(keys, num_frames, st);
   if (s) return s;
   if (num_frames == 0 || num_tiles == 0 || num_ctas == 0) return SRPGPU_OK;
+  const GatherTuning& tn = tuning();
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const CUtensorMapDataType f32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  const int64_t arows = num_slabs * GM;
-  const int64_t c8 = (int64_t)((num_cols + 7) / 8 * 8);   // planes hold round8(S) rows each
-  const float* xs_lo = samples_planes + c8 * planes_ld;
-  if ((s = make_map_2d(&ma_hi, f32, 4, slab_planes, arows, GB, GB, g32::GK, GM, "interp_map_gather_tf32",
-                       CU_TENSOR_MAP_SWIZZLE_64B)) ||
-      (s = make_map_2d(&ma_lo, f32, 4, slab_planes + arows * GB, arows, GB, GB, g32::GK, GM,
-                       "interp_map_gather_tf32", CU_TENSOR_MAP_SWIZZLE_64B)))
-    return s;
-  // gathered samples: one 3D box per (plane, group) when the {32, lags, frame blocks} view encodes
-  const CUtensorMapSwizzle sw32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-  int b3d = getenv("SRPGPU_GATHER_2D") ? 0 : 1;
-  {
-    const int64_t dims[3] = {g32::GA, num_cols, planes_ld / g32::GA};
-    const int box[3] = {g32::GA, g32::GG, g32::NA};
-    if (make_map_3d(&mb_hi, f32, samples_planes, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32",
-                    sw32) ||
-        make_map_3d(&mb_lo, f32, xs_lo, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32", sw32))
-      b3d = 0;
-  }
-  if (!b3d && ((s = make_map_2d(&mb_hi, f32, 4, samples_planes, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
-                                "interp_map_gather_tf32", sw32)) ||
-               (s = make_map_2d(&mb_lo, f32, 4, xs_lo, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
-                                "interp_map_gather_tf32", sw32))))
-    return s;
-  // CTA pairs (cta_group::2) unless SRPGPU_GATHER_PAIR=0 or no 2-CTA cluster fits; persistent
-  // grid = the co-resident clusters
-  static const int pair_env = [] {
-    const char* v = getenv("SRPGPU_GATHER_PAIR");
-    return v ? atoi(v) : 1;
-  }();
-  // frames per unit group: their fp32 hi / lo samples (F_g x S x 8 B; 58 MB at cfg4 with
-  // 1024 frames) stay L2-resident next to the slabs in flight (SRPGPU_GATHER_GROUP overrides)
-  static const int64_t frames_per_group = [] {
-    const char* v = getenv("SRPGPU_GATHER_GROUP");
-    const int64_t x = v ? atoll(v) : 0;
-    return x >= 256 && x % 256 == 0 ? x : (int64_t)1024;
-  }();
-  // 16-lag stages per TMEM accumulation chunk (fp32 fold; SRPGPU_GATHER_CHUNK overrides)
-  static const int chunk = [] {
-    const char* v = getenv("SRPGPU_GATHER_CHUNK");
-    const int x = v ? atoi(v) : 0;
-    return x >= 1 && x <= 64 ? x : 8;
-  }();
-  // tile-order map through TMA stores (the pair kernel): box of 128 candidates x 32 frames
-  CUtensorMap mz = ma_hi;
-  int z_tma = 0;
-  if (z && z_tiles && !getenv("SRPGPU_GATHER_ZSTG")) {
-    const int64_t ldt = (int64_t)num_tiles * GT;
-    if ((s = make_map_2d(&mz, f32, 4, z_tiles, num_frames, ldt, ldt, GM, 32, "interp_map_gather_tf32",
-                         CU_TENSOR_MAP_SWIZZLE_NONE)))
-      return s;
-    z_tma = 1;
-  }
-  // diagnostic: SRPGPU_GATHER_ZTEST=1 writes every frame's tile-order row to the same place
-  // (isolates the cost of issuing the map stores from the cost of their DRAM traffic)
-  static const int64_t zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
-  // L2 policies: samples evict_last, slabs evict_normal (4096 frames: 23 GB of DRAM reads
-  // against 41 GB with evict_first slabs and 71 GB with both evict_first)
-  static const int l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (2 << 2));
+  // CTA pairs (cta_group::2) unless SRPGPU_GATHER_PAIR=0, the 3D sample view cannot be encoded
+  // or no 2-CTA cluster fits; persistent grid = the co-resident clusters
   int clusters = 0;
-  if (pair_env && b3d) {
-    const size_t psmem = sizeof(g32::PairSmem) + 1024;
-    if (cudaFuncSetAttribute(g32::gather_tf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)psmem) == cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 2;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3((unsigned)(num_ctas & ~1));
-      cfg.blockDim = dim3(g32::PThreads);
-      cfg.dynamicSmemBytes = psmem;
-      cfg.stream = st;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&clusters, g32::gather_tf32_pair_kernel, &cfg) != cudaSuccess) clusters = 0;
-      cudaGetLastError();
-      clusters = std::min(clusters, num_ctas / 2);
+  if (tn.pair && !getenv("SRPGPU_GATHER_2D") &&
+      pair_maps<g32::PairTf32>(f32, samples_planes, num_cols, planes_ld, slab_planes, num_slabs, &ma_hi, &ma_lo,
+                               &mb_hi, &mb_lo, "interp_map_gather_tf32") == SRPGPU_OK)
+    clusters = pair_clusters<g32::PairTf32>(num_ctas, st);
+  if (clusters > 0) {
+    if ((s = launch_pair<g32::PairTf32>(clusters, ma_hi, ma_lo, mb_hi, mb_lo, 1.0f, num_frames, num_candidates,
+                                        num_tiles, group_col, tile_slab, tile_nkb, tile_rows, z_tiles, z, keys, st,
+                                        "interp_map_gather_tf32")))
+      return s;
+  } else {
+    // one-CTA fallback (N = 128 frames per unit)
+    const int64_t arows = num_slabs * GM;
+    const int64_t c8 = (int64_t)((num_cols + 7) / 8 * 8);
+    const float* xs_lo = samples_planes + c8 * planes_ld;
+    if ((s = make_map_2d(&ma_hi, f32, 4, slab_planes, arows, GB, GB, g32::GK, GM, "interp_map_gather_tf32",
+                         CU_TENSOR_MAP_SWIZZLE_64B)) ||
+        (s = make_map_2d(&ma_lo, f32, 4, slab_planes + arows * GB, arows, GB, GB, g32::GK, GM,
+                         "interp_map_gather_tf32", CU_TENSOR_MAP_SWIZZLE_64B)))
+      return s;
+    const CUtensorMapSwizzle sw32 = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    int b3d = getenv("SRPGPU_GATHER_2D") ? 0 : 1;
+    {
+      const int64_t dims[3] = {g32::GA, num_cols, planes_ld / g32::GA};
+      const int box[3] = {g32::GA, g32::GG, g32::NA};
+      if (make_map_3d(&mb_hi, f32, samples_planes, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32",
+                      sw32) ||
+          make_map_3d(&mb_lo, f32, xs_lo, dims, planes_ld * 4, g32::GA * 4, box, "interp_map_gather_tf32", sw32))
+        b3d = 0;
     }
-  }
-  const size_t smem = sizeof(g32::Smem) + 1024;
-  if (clusters == 0 &&
-      cudaFuncSetAttribute(g32::gather_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess) {
-    set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
-    return SRPGPU_ERR_LAUNCH;
-  }
-  const int unit_frames = clusters > 0 ? g32::PN : g32::GN;
-  const int fg = (int)(frames_per_group / unit_frames);
-  const int64_t units_per_group = (int64_t)num_tiles * fg;
-  const int64_t n_groups = (num_frames + frames_per_group - 1) / frames_per_group;
-  SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "interp_map_gather_tf32: too many units");
-  auto gather = [&](int64_t g0, int64_t g1) -> int {
-    const int ub = (int)(g0 * units_per_group), ue = (int)(g1 * units_per_group);
-    if (clusters > 0)
-      g32::gather_tf32_pair_kernel<<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem) + 1024, st>>>(
-          ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && zt_ld < 0, l2pol, zt_ld, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col, tile_slab,
-          tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
-          reinterpret_cast<unsigned long long*>(keys));
-    else
-      g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
-          ma_hi, ma_lo, mb_hi, mb_lo, b3d, fg, chunk, ub, ue, num_frames, num_candidates, num_tiles, group_col,
-          tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr,
-          reinterpret_cast<unsigned long long*>(keys));
+    if (!b3d && ((s = make_map_2d(&mb_hi, f32, 4, samples_planes, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
+                                  "interp_map_gather_tf32", sw32)) ||
+                 (s = make_map_2d(&mb_lo, f32, 4, xs_lo, num_cols, num_frames, planes_ld, g32::GA, g32::GG,
+                                  "interp_map_gather_tf32", sw32))))
+      return s;
+    const size_t smem = sizeof(g32::Smem) + 1024;
+    if (cudaFuncSetAttribute(g32::gather_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
+      return SRPGPU_ERR_LAUNCH;
+    }
+    const int fg = (int)(tn.frames_per_group / g32::GN);
+    const int64_t units_per_group = (int64_t)num_tiles * fg;
+    const int64_t n_groups = (num_frames + tn.frames_per_group - 1) / tn.frames_per_group;
+    SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION,
+                     "interp_map_gather_tf32: too many units");
+    g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
+        ma_hi, ma_lo, mb_hi, mb_lo, b3d, fg, tn.chunk, 0, (int)(n_groups * units_per_group), num_frames,
+        num_candidates, num_tiles, group_col, tile_slab, tile_nkb, tile_rows, z ? z_tiles : nullptr,
+        z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
     SRPGPU_CHECK_LAUNCH("interp_map_gather_tf32");
-    return SRPGPU_OK;
-  };
+  }
   // one launch over every group; the untile pass follows (measured: running group g's untile
   // on a side stream under group g + 1's gather launch was slower, 50 vs 42 ms at cfg4 --
   // the two contend for the SMs' issue slots and L2)
-  if ((s = gather(0, n_groups))) return s;
+  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
+  return SRPGPU_OK;
+}
+
+// The same map in fp16x3 (PairF16): samples_planes fp16 [2][round8(S)][planes_ld] (hi / lo,
+// lag-major, natural lag order, planes_ld a multiple of 64), slab_planes fp16
+// [2][num_slabs * 128][64] = split of (slab * 1 / z_scale) with z_scale a power of two; the
+// layout's groups are 8 lags and tile_nst counts 32-lag stages.  CTA pairs only.
+extern "C" int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t num_frames, int32_t num_cols,
+                                            int64_t planes_ld, const void* slab_planes, int64_t num_slabs,
+                                            const int32_t* group_col, const int32_t* tile_slab,
+                                            const int32_t* tile_nst, const int32_t* tile_rows, int32_t num_tiles,
+                                            int64_t num_candidates, int32_t num_ctas, const int32_t* tile_pos,
+                                            float z_scale, float* z_tiles, float* z, uint64_t* keys,
+                                            srpgpu_stream_t stream) {
+  using namespace gtc;
+  SRPGPU_CHECK_ARG(num_frames >= 0 && num_cols >= 1 && planes_ld >= num_frames && planes_ld % 64 == 0 &&
+                       num_slabs >= 0 && num_tiles >= 0 && num_candidates >= 1 && num_ctas >= 0,
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_f16: bad shape (planes pitch: a multiple of 64 >= F)");
+  SRPGPU_CHECK_ARG(((uintptr_t)samples_planes & 127) == 0 && ((uintptr_t)slab_planes & 15) == 0 &&
+                       ((uintptr_t)group_col & 15) == 0,
+                   SRPGPU_ERR_VALUE, "interp_map_gather_f16: operands must be aligned (samples 128 B, slabs 16 B)");
+  SRPGPU_CHECK_ARG(num_frames < (1ll << 31) && num_candidates < (1ll << 31) && num_slabs * GM < (1ll << 31),
+                   SRPGPU_ERR_DIMENSION, "interp_map_gather_f16: too large");
+  SRPGPU_CHECK_ARG(!z || !z_tiles || tile_pos, SRPGPU_ERR_VALUE, "interp_map_gather_f16: a tile-order map needs tile_pos");
+  SRPGPU_CHECK_ARG(z_scale > 0.f, SRPGPU_ERR_VALUE, "interp_map_gather_f16: z_scale must be positive");
+  cudaStream_t st = as_stream(stream);
+  int s = reset_keys(keys, num_frames, st);
+  if (s) return s;
+  if (num_frames == 0 || num_tiles == 0 || num_ctas == 0) return SRPGPU_OK;
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  if ((s = pair_maps<g32::PairF16>(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, samples_planes, num_cols, planes_ld, slab_planes,
+                                   num_slabs, &ma_hi, &ma_lo, &mb_hi, &mb_lo, "interp_map_gather_f16")))
+    return s;
+  const int clusters = pair_clusters<g32::PairF16>(num_ctas, st);
+  if (clusters == 0) {
+    set_error("interp_map_gather_f16: no 2-CTA cluster of the pair kernel fits this device");
+    return SRPGPU_ERR_LAUNCH;
+  }
+  if ((s = launch_pair<g32::PairF16>(clusters, ma_hi, ma_lo, mb_hi, mb_lo, z_scale, num_frames, num_candidates,
+                                     num_tiles, group_col, tile_slab, tile_nst, tile_rows, z_tiles, z, keys, st,
+                                     "interp_map_gather_f16")))
+    return s;
   if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
   return SRPGPU_OK;
 }

@@ -20,6 +20,7 @@
 // tcgen05.ld 32 columns at a time, running per-frame argmax in registers (one
 // atomicMax per frame per tile), z through a swizzled shared tile and a TMA store.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "tc_common.cuh"
 
@@ -300,6 +301,21 @@ __global__ void split_rows_tf32_kernel(const float* __restrict__ src, int64_t ld
   }
 }
 
+// the same into fp16 hi / lo planes: hi = f16_rne(s x), lo = f16_rne(s x - hi) (s: a power of
+// two that keeps the operand in fp16 range; 11 + 11 significant bits, as the TF32 split)
+__global__ void split_rows_f16_kernel(const float* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
+                                      const int32_t* __restrict__ row_src, float scale, __half* __restrict__ dst,
+                                      int64_t ld_dst, int64_t plane) {
+  const int64_t r = blockIdx.y;
+  const int64_t rs = row_src ? __ldg(row_src + r) : r;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+    const float x = __ldg(src + rs * ld_src + c) * scale;
+    const __half hi = __float2half_rn(x);
+    dst[r * ld_dst + c] = hi;
+    dst[plane + r * ld_dst + c] = __float2half_rn(x - __half2float(hi));
+  }
+}
+
 }  // namespace itc
 
 int reset_keys(uint64_t* keys, int64_t F, cudaStream_t st);
@@ -364,6 +380,26 @@ extern "C" int srpgpu_split_tf32_rows(const float* src, int64_t ld_src, int64_t 
                                                       row_src ? row_src + r0 : nullptr, dst + r0 * ld_dst, ld_dst,
                                                       rows_dst * ld_dst);
     SRPGPU_CHECK_LAUNCH("split_tf32_rows");
+  }
+  return SRPGPU_OK;
+}
+
+extern "C" int srpgpu_split_f16_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                     const int32_t* row_src, float scale, void* dst, int64_t ld_dst,
+                                     int64_t rows_dst, srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(rows >= 0 && cols >= 0 && ld_src >= cols && ld_dst >= cols && rows_dst >= rows, SRPGPU_ERR_DIMENSION,
+                   "split_f16_rows: bad shape");
+  SRPGPU_CHECK_ARG(((uintptr_t)dst & 15) == 0, SRPGPU_ERR_VALUE, "split_f16_rows: destination must be 16-byte aligned");
+  if (rows == 0 || cols == 0) return SRPGPU_OK;
+  cudaStream_t st = as_stream(stream);
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+    dim3 grid((unsigned)std::min<int64_t>((cols + 255) / 256, 64), (unsigned)nr);
+    itc::split_rows_f16_kernel<<<grid, 256, 0, st>>>(row_src ? src : src + r0 * ld_src, ld_src, nr, cols,
+                                                     row_src ? row_src + r0 : nullptr, scale,
+                                                     reinterpret_cast<__half*>(dst) + r0 * ld_dst, ld_dst,
+                                                     rows_dst * ld_dst);
+    SRPGPU_CHECK_LAUNCH("split_f16_rows");
   }
   return SRPGPU_OK;
 }

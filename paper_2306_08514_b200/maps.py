@@ -265,7 +265,8 @@ def _check_cols(samples, num_cols: int) -> None:
 
 # ----------------------------------------------------------------- SSPI / SI on tensor cores
 
-ENGINES = ("auto", "tc", "tile", "tile_bf16", "band")
+ENGINES = ("auto", "tc", "tile", "tile_f16", "tile_bf16", "band")
+TILE_ENGINES = {"tile": "tf32", "tile_f16": "f16", "tile_bf16": "bf16"}   # engine -> operand format
 TC_MAX_COLS = 2048          # dense rows beyond this many samples: gathered windows ("tile") or band
 TC_DENSITY = 12             # dense tensor cores while cols8 <= TC_DENSITY * kept entries per row
 TILE_DENSITY = 4            # gathered windows while the kept entries per row are sparse
@@ -318,15 +319,20 @@ def dense_from_matrix(interp) -> DenseInterpOperator:
                          lambda: DenseInterpOperator(np.asarray(interp.matrix).astype(np.float32)))
 
 
+F16_AUTO = True             # auto: PHAT-bounded samples take the fp16x3 gathered-window engine
+F16_SLAB_SCALE = 256.0      # slab weights are split as fp16(w * 256): |w| <= 1, lo stays normal down to |w| ~ 1e-3
 TC_MIN_FRAMES = 0           # batches below this take the band engine (set from the cfg5 batch sweep)
 
 
 def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", frames: int | None = None,
-                  pairs: bool = True) -> str:
-    """'tile' (per-tile gathered lag windows on the tensor cores in 3xTF32 with fp32 chunk
-    folds: FP32-class, the default wherever the tensor cores pay), 'band' (tiled-band SpMM
-    on FP32 SIMT: latency-scale sparse maps, single-pair operators), or the opt-in bf16x3
-    engines 'tc' (dense operator) and 'tile_bf16' (gathered windows)."""
+                  pairs: bool = True, bounded: bool = False) -> str:
+    """'tile' / 'tile_f16' (per-tile gathered lag windows on the tensor cores with split
+    operands and fp32 chunk folds: FP32-class, the default wherever the tensor cores pay;
+    'tile_f16' -- fp16 hi / lo operands, the same 22 significant bits as the 3xTF32 split at
+    twice the MMA rate -- when the samples are `bounded` (PHAT: |xi| <= 2(K-1)), else 'tile'
+    = 3xTF32), 'band' (tiled-band SpMM on FP32 SIMT: latency-scale sparse maps, single-pair
+    operators), or the opt-in bf16x3 engines 'tc' (dense operator) and 'tile_bf16'
+    (gathered windows)."""
     if engine not in ENGINES:
         raise ValueError(f"unknown engine {engine!r}")
     if engine != "auto":
@@ -336,22 +342,25 @@ def interp_engine(num_cols: int, kept_per_row: float, engine: str = "auto", fram
     c8 = _cols8(num_cols)
     dense_ok = c8 <= TC_MAX_COLS and c8 <= TC_DENSITY * max(kept_per_row, 1.0)
     if pairs and (dense_ok or (c8 > TC_MAX_COLS and kept_per_row * TILE_DENSITY < c8)):
-        return "tile"
+        return "tile_f16" if bounded and F16_AUTO else "tile"
     return "band"
 
 
 class TileOperator:
     """Device image of the gathered-window operator (tiles.TileLayout) for engines "tile"
-    (3xTF32: fp32 slab planes hi = tf32_rne(v), lo = tf32_rne(v - hi)) and "tile_bf16"
-    (bf16 hi / lo slab planes)."""
+    (3xTF32: fp32 slab planes hi = tf32_rne(v), lo = tf32_rne(v - hi)), "tile_f16" (fp16 hi /
+    lo planes of v * F16_SLAB_SCALE) and "tile_bf16" (bf16 hi / lo slab planes)."""
 
     MAX_BLOCKS = 128            # 64-lag operator blocks per tile (interp_gather_tc.cu kMaxBlocks)
 
-    def __init__(self, sp, offsets, num_rows: int, tf32: bool = True):
-        # J % 8 == 0 (cfg3 / cfg5): tiles of aligned 8-candidate runs, so the 3xTF32 kernel
+    def __init__(self, sp, offsets, num_rows: int, tf32: bool = True, fmt: str | None = None):
+        fmt = fmt or ("tf32" if tf32 else "bf16")
+        tf32 = fmt == "tf32"
+        self.fmt = fmt
+        # J % 8 == 0 (cfg3 / cfg5): tiles of aligned 8-candidate runs, so the pair kernel
         # stores the map straight into grid order in whole 32-byte sectors (no tile-order
         # scratch, no gather pass; cfg3 K is even 4% smaller than with compact tiles)
-        self.grid_order = bool(tf32) and num_rows % 8 == 0
+        self.grid_order = fmt in ("tf32", "f16") and num_rows % 8 == 0
         lay = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8, runs=self.grid_order)
         if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
             raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
@@ -360,33 +369,37 @@ class TileOperator:
         self.tf32 = bool(tf32)
         self.num_rows, self.num_cols, self.cols8 = int(num_rows), int(lay.num_cols), _cols8(lay.num_cols)
         self.num_tiles, self.num_slabs = lay.num_tiles, lay.num_slabs
-        # the K the kernel iterates: 16-lag stages (3xTF32) or 64-lag blocks (bf16)
-        self.mean_k = lay.mean_k_stages if self.tf32 else lay.mean_k
+        # the K the kernel iterates: 16-lag stages (3xTF32), 32-lag stages (fp16x3) or 64-lag blocks (bf16)
+        self.mean_k = {"tf32": lay.mean_k_stages, "f16": lay.mean_k_stages32, "bf16": lay.mean_k}[fmt]
         rows = max(1, lay.num_slabs) * tiles.HALF
-        self.planes = torch.empty((2, rows, tiles.SLAB), dtype=torch.float32 if self.tf32 else torch.bfloat16,
-                                  device=d)
+        dt = {"tf32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[fmt]
+        self.planes = torch.empty((2, rows, tiles.SLAB), dtype=dt, device=d)
         if lay.num_slabs:
             src = torch.from_numpy(lay.slabs.reshape(-1, tiles.SLAB)).to(d)
             if self.tf32:
                 nat.call("srpgpu_split_tf32", dev.ptr(src), tiles.SLAB, dev.ptr(self.planes), tiles.SLAB,
                          src.shape[0], tiles.SLAB, dev.stream_ptr())
+            elif fmt == "f16":
+                nat.call("srpgpu_split_f16_rows", dev.ptr(src), tiles.SLAB, src.shape[0], tiles.SLAB, None,
+                         F16_SLAB_SCALE, dev.ptr(self.planes), tiles.SLAB, rows, dev.stream_ptr())
             else:
                 nat.call("srpgpu_split_bf16", dev.ptr(src), tiles.SLAB, 0, src.shape[0], tiles.SLAB,
                          dev.ptr(self.planes), tiles.SLAB, dev.stream_ptr())
             del src
         self.group_col = dev.as_i32(lay.group_col if lay.group_col.size else np.zeros(8, np.int32))
         self.tile_slab = dev.as_i32(lay.tile_slab)
-        self.tile_nkb = dev.as_i32(lay.tile_nst if self.tf32 else lay.tile_nkb)
+        self.tile_nkb = dev.as_i32({"tf32": lay.tile_nst, "f16": lay.tile_nst32, "bf16": lay.tile_nkb}[fmt])
         self.tile_rows = dev.as_i32(lay.tile_rows)
         self.tile_pos = dev.as_i32(lay.tile_pos)
         self._layout = lay
         lay.slabs = None                      # host copy no longer needed
 
 
-def tile_from_sparse(sp, offsets: np.ndarray, tf32: bool = True) -> TileOperator:
+def tile_from_sparse(sp, offsets: np.ndarray, tf32: bool = True, fmt: str | None = None) -> TileOperator:
+    fmt = fmt or ("tf32" if tf32 else "bf16")
     num_rows = int(sp.values.shape[1]) if np.ndim(sp.values) == 3 else int(np.asarray(sp.row_splits).shape[0] - 1)
-    return dev.CACHE.get(sp, ("tile_tf32x3" if tf32 else "tile_bf16x3", tuple(int(o) for o in offsets)),
-                         lambda: TileOperator(sp, offsets, num_rows, tf32))
+    return dev.CACHE.get(sp, (f"tile_{fmt}x3", tuple(int(o) for o in offsets)),
+                         lambda: TileOperator(sp, offsets, num_rows, fmt=fmt))
 
 
 # Gathered-window maps straight into grid order (no untile pass): measured 2.3x SLOWER at
@@ -396,32 +409,37 @@ TILE_GRID_ORDER = False
 
 
 def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
-    planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets, tf32=op.tf32)
+    planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets, fmt=op.fmt)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
     zt = (torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
           if out_map and not (TILE_GRID_ORDER or op.grid_order) else None)
     keys = _new_keys(f, argmax)
-    fn = "srpgpu_interp_map_gather_tf32" if op.tf32 else "srpgpu_interp_map_gather_tc"
-    nat.call(fn, dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
-             dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
-             op.num_tiles, op.num_rows, dev.num_sms(), dev.ptr(op.tile_pos), dev.ptr(zt), dev.ptr(z),
-             dev.ptr(keys), dev.stream_ptr())
+    head = (dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
+            dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
+            op.num_tiles, op.num_rows, dev.num_sms(), dev.ptr(op.tile_pos))
+    tail = (dev.ptr(zt), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+    if op.fmt == "f16":
+        nat.call("srpgpu_interp_map_gather_f16", *head, 1.0 / F16_SLAB_SCALE, *tail)
+    else:
+        nat.call("srpgpu_interp_map_gather_tf32" if op.tf32 else "srpgpu_interp_map_gather_tc", *head, *tail)
     return _finish(z, keys, batched, argmax)
 
 
-def sample_planes(samples, num_cols: int, natural=None, tf32: bool = False):
-    """(planes, frames, batched) of any samples input (bf16 hi / lo; `tf32`: fp32 TF32 hi / lo,
-    natural lag-major only).
+def sample_planes(samples, num_cols: int, natural=None, tf32: bool = False, fmt: str | None = None):
+    """(planes, frames, batched) of any samples input (bf16 hi / lo; fmt "tf32": fp32 TF32
+    hi / lo, "f16": fp16 hi / lo -- both natural lag-major only; fp16 needs bounded samples).
 
     natural None: frame-major planes [2][F][cols8] in storage column order (dense engine);
     natural = the pair offsets: lag-major planes [2][cols8][F8] in natural lag order
     (gathered-window engine).  Kernel-produced TdGccSamples may already carry them.
     """
+    fmt = fmt or ("tf32" if tf32 else "bf16")
+    tf32 = fmt == "tf32"
     want_nat = natural is not None
     planes = getattr(samples, "bf16_planes", None)
     c8 = _cols8(num_cols)
     if planes is not None and bool(getattr(samples, "planes_natural", False)) == want_nat and \
-            bool(getattr(samples, "planes_tf32", False)) == bool(tf32) and planes.shape[1 if want_nat else 2] == c8:
+            getattr(samples, "planes_fmt", "bf16") == fmt and planes.shape[1 if want_nat else 2] == c8:
         vals = samples.values
         batched = vals.dim() == 2
         return planes, (vals.shape[0] if batched else 1), batched
@@ -437,6 +455,12 @@ def sample_planes(samples, num_cols: int, natural=None, tf32: bool = False):
             planes = torch.empty((2, c8, f32), dtype=torch.float32, device=buf.device)
             nat.call("srpgpu_split_tf32_rows", dev.ptr(buf), buf.shape[1], num_cols, f, dev.ptr(src),
                      dev.ptr(planes), f32, c8, dev.stream_ptr())
+            return planes, f, batched
+        if fmt == "f16":
+            f64 = (f + 63) // 64 * 64
+            planes = torch.empty((2, c8, f64), dtype=torch.float16, device=buf.device)
+            nat.call("srpgpu_split_f16_rows", dev.ptr(buf), buf.shape[1], num_cols, f, dev.ptr(src), 1.0,
+                     dev.ptr(planes), f64, c8, dev.stream_ptr())
             return planes, f, batched
         f8 = (f + 7) // 8 * 8
         planes = torch.empty((2, c8, f8), dtype=torch.bfloat16, device=buf.device)
@@ -473,14 +497,15 @@ def _tc_map(op: DenseInterpOperator, samples, argmax: bool, out_map: bool):
     return _finish(z, keys, batched, argmax)
 
 
-def map_engine(variant: str, op, engine: str = "auto", frames: int | None = None):
+def map_engine(variant: str, op, engine: str = "auto", frames: int | None = None, bounded: bool = False):
     """Engine sspi_map / si_map take on this operator and batch size ("tc" | "tile" |
-    "band"; None for the other variants)."""
+    "tile_f16" | "band"; None for the other variants).  bounded: the samples are PHAT-weighted
+    (|xi| <= 2(K-1)), so the fp16x3 engine may take the tensor-core cases."""
     if variant == "si":
         n = int(np.asarray(op.matrix).shape[1])
-        return interp_engine(n, n, engine, frames)
+        return interp_engine(n, n, engine, frames, bounded=bounded)
     if variant == "sspi":
-        return interp_engine(int(op.num_cols), _kept_per_row(op), engine, frames)
+        return interp_engine(int(op.num_cols), _kept_per_row(op), engine, frames, bounded=bounded)
     return None
 
 
@@ -488,13 +513,19 @@ def plane_args(engine: str) -> dict:
     """frames_to_samples keywords that make the frontend also write the operand planes the
     map engine reads (bf16 frame-major for "tc", natural lag-major bf16 / TF32 for the
     gathered-window engines)."""
-    return {"planes": engine in ("tc", "tile", "tile_bf16"), "natural": engine in ("tile", "tile_bf16"),
-            "tf32": engine == "tile"}
+    return {"planes": engine == "tc" or engine in TILE_ENGINES, "natural": engine in TILE_ENGINES,
+            "fmt": TILE_ENGINES.get(engine, "bf16")}
 
 
 def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -> bool:
     """Whether sspi_map / si_map on this operator (and batch size) run on the tensor cores."""
-    return map_engine(variant, op, engine, frames) in ("tc", "tile", "tile_bf16")
+    eng = map_engine(variant, op, engine, frames)
+    return eng == "tc" or eng in TILE_ENGINES
+
+
+def _bounded(samples) -> bool:
+    """Kernel-produced PHAT samples (|xi| <= 2(K-1)): safe as fp16 hi / lo operands."""
+    return bool(getattr(samples, "phat", False))
 
 
 def _num_frames(samples) -> int:
@@ -522,11 +553,12 @@ def sspi_map(sp, samples, *, argmax: bool = False, out_map: bool = True, engine:
     num_cols = int(sp.num_cols)
     _check_cols(samples, num_cols)                 # reference DimensionError check first
     offsets = _sample_offsets(samples, num_cols)
-    eng = interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples), offsets.shape[0] > 2)
+    eng = interp_engine(num_cols, _kept_per_row(sp), engine, _num_frames(samples), offsets.shape[0] > 2,
+                        bounded=_bounded(samples))
     if eng == "tc":
         return _tc_map(dense_from_sparse(sp), samples, argmax, out_map)
-    if eng in ("tile", "tile_bf16"):
-        op = tile_from_sparse(sp, offsets, tf32=(eng == "tile"))
+    if eng in TILE_ENGINES:
+        op = tile_from_sparse(sp, offsets, fmt=TILE_ENGINES[eng])
         return _tile_map(op, samples, offsets, argmax, out_map)
     op = band_from_sparse(sp, offsets)
     return _band_map(op, samples, argmax, out_map)
@@ -543,12 +575,13 @@ def si_map(interp, samples, *, argmax: bool = False, out_map: bool = True, engin
     offsets = spec_offsets(interp.spec)
     if int(offsets[-1]) != num_cols:
         offsets = np.array([0, num_cols], dtype=np.int64)
-    eng = interp_engine(num_cols, num_cols, engine, _num_frames(samples), offsets.shape[0] > 2)
+    eng = interp_engine(num_cols, num_cols, engine, _num_frames(samples), offsets.shape[0] > 2,
+                        bounded=_bounded(samples))
     if eng == "tc":
         return _tc_map(dense_from_matrix(interp), samples, argmax, out_map)
-    if eng in ("tile", "tile_bf16"):
+    if eng in TILE_ENGINES:
         sp = dev.CACHE.get(interp, "keep_all_csr", lambda: _keep_all_csr(interp))
-        return _tile_map(tile_from_sparse(sp, offsets, tf32=(eng == "tile")), samples, offsets, argmax, out_map)
+        return _tile_map(tile_from_sparse(sp, offsets, fmt=TILE_ENGINES[eng]), samples, offsets, argmax, out_map)
     return _band_map(band_from_dense(interp, offsets), samples, argmax, out_map)
 
 

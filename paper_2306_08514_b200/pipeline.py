@@ -43,7 +43,7 @@ class MapPipeline:
         self.frames = int(frames)
         self.weighting, self.floor, self.out_map = weighting, floor, out_map
         self.precision = maps.conv_precision(op, precision) if variant == "conv" else precision
-        self.engine = engine              # sspi / si: "auto" | "fused" | "tc" | "tile" | "band"
+        self.engine = engine              # sspi / si: "auto" | "fused" | "tc" | "tile" | "tile_f16" | "tile_bf16" | "band"
         m = num_channels or pairs.num_mics
         n = (self.frames - 1) * frame.hop + frame.frame_len
         self.input = torch.zeros((m, n), dtype=torch.float32, device=device())
@@ -66,7 +66,7 @@ class MapPipeline:
             return fused(self.op, self.input, self.frame, self.pairs, self.spec, rng,
                                            self.weighting, self.floor, argmax=True, out_map=self.out_map)
         if v in ("sspi", "si", "slri"):
-            eng = maps.map_engine(v, self.op, self.engine, self.frames)
+            eng = maps.map_engine(v, self.op, self.engine, self.frames, bounded=(self.weighting == "phat"))
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
                                             self.weighting, self.floor, **maps.plane_args(eng))
             if v == "slri":

@@ -94,6 +94,11 @@ class TdGccSamples:
     # the planes are fp32 TF32 hi / lo (lag-major [2][cols8][F32], natural order) for the
     # 3xTF32 gathered-window engine instead of bf16
     planes_tf32: bool = field(default=False, repr=False, compare=False)
+    # plane format: "bf16" | "tf32" | "f16" (fp16 hi / lo, lag-major [2][cols8][F64], natural
+    # order: the fp16x3 gathered-window engine; PHAT samples only -- bounded by 2(K-1))
+    planes_fmt: str = field(default="bf16", repr=False, compare=False)
+    # produced with PHAT weighting by these kernels: |xi| <= 2(K-1), so fp16 operands are safe
+    phat: bool = field(default=False, repr=False, compare=False)
 
     @property
     def num_frames(self) -> int:
@@ -127,13 +132,17 @@ def _new_samples(frames: int, s_total: int, dev_):
 
 
 def _wrap(view, buf, spec, batched: bool, planes=None, natural: bool = False,
-          tf32: bool = False) -> "TdGccSamples":
+          fmt: str = "bf16", phat: bool = False) -> "TdGccSamples":
     return TdGccSamples(values=view if batched else view[0], spec=spec, lag_major=buf, bf16_planes=planes,
-                        planes_natural=natural, planes_tf32=tf32)
+                        planes_natural=natural, planes_tf32=(fmt == "tf32"), planes_fmt=fmt, phat=phat)
 
 
 def pad32(n: int) -> int:
     return (int(n) + 31) // 32 * 32
+
+
+def pad64(n: int) -> int:
+    return (int(n) + 63) // 64 * 64
 
 
 def natural_source_device(spec):
@@ -165,17 +174,23 @@ def td_gcc_samples(gcc, spec, path: str = "ifft") -> TdGccSamples:
 
 def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str = "phat",
                       floor=None, planes: bool = False, natural: bool = False,
-                      tf32: bool = False) -> TdGccSamples:
+                      tf32: bool = False, fmt: str | None = None) -> TdGccSamples:
     """Fused stft_frame -> fd_gcc -> td_gcc_samples for a range of frames.
 
     Neither the spectra nor the cross-spectra touch HBM; one kernel launch.  With
     `planes` the same kernel also writes the bf16 hi/lo planes the tensor-core
     interpolation maps read (`bf16_planes`; natural lag order per pair with `natural`,
-    the layout of the gathered-window engine; with `tf32` too, fp32 TF32 hi / lo planes
-    for its 3xTF32 kernel).
+    the layout of the gathered-window engine; with `tf32` (or fmt="tf32") too, fp32 TF32
+    hi / lo planes for its 3xTF32 kernel; fmt="f16": fp16 hi / lo planes for its fp16x3
+    kernel -- PHAT weighting only, whose samples are bounded by 2(K-1)).
     """
-    if tf32 and not natural:
-        raise ValueError("TF32 planes are natural-order lag-major only (natural=True)")
+    fmt = fmt or ("tf32" if tf32 else "bf16")
+    if fmt not in ("bf16", "tf32", "f16"):
+        raise ValueError(f"unknown plane format {fmt!r}")
+    if fmt != "bf16" and not natural:
+        raise ValueError("TF32 / fp16 planes are natural-order lag-major only (natural=True)")
+    if fmt == "f16" and planes and weighting != "phat":
+        raise ValueError("fp16 planes need PHAT weighting (bounded samples); use fmt='tf32'")
     x = _signal(samples)
     if x.shape[0] != pairs.num_mics:
         raise DimensionError(f"expected {pairs.num_mics} channels, got {x.shape[0]}")
@@ -192,12 +207,15 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
             dev.ptr(counts), dev.ptr(offsets), s_total, dev.ptr(buf), ld)
     if not planes:
         nat.call("srpgpu_frames_to_samples", *args, dev.stream_ptr())
-        return _wrap(view, buf, spec, batched)
+        return _wrap(view, buf, spec, batched, phat=(weighting == "phat"))
     cols8 = (s_total + 7) // 8 * 8
     src = natural_source_device(spec) if natural else None
-    if tf32:        # lag-major natural-order fp32 planes [2][cols8][F32] (3xTF32 gathered windows)
+    if fmt == "tf32":   # lag-major natural-order fp32 planes [2][cols8][F32] (3xTF32 gathered windows)
         planes_ld = pad32(count)
         pl = torch.empty((2, cols8, planes_ld), dtype=torch.float32, device=x.device)
+    elif fmt == "f16":  # lag-major natural-order fp16 planes [2][cols8][F64] (fp16x3 gathered windows)
+        planes_ld = pad64(count)
+        pl = torch.empty((2, cols8, planes_ld), dtype=torch.float16, device=x.device)
     elif natural:   # lag-major natural-order planes [2][cols8][F8] (gathered-window engine)
         f8 = pad8(count)
         pl = torch.empty((2, cols8, f8), dtype=torch.bfloat16, device=x.device)
@@ -206,8 +224,9 @@ def frames_to_samples(samples, frame, pairs, spec, frames=None, weighting: str =
         pl = torch.empty((2, count, cols8), dtype=torch.bfloat16, device=x.device)
         planes_ld = 0
     nat.call("srpgpu_frames_to_samples_planes", *args, dev.ptr(pl), cols8, planes_ld,
-             (1 if natural else 0) | (2 if tf32 else 0), dev.ptr(src), dev.stream_ptr())
-    return _wrap(view, buf, spec, batched, pl, natural, tf32)
+             (1 if natural else 0) | (2 if fmt == "tf32" else 0) | (4 if fmt == "f16" else 0), dev.ptr(src),
+             dev.stream_ptr())
+    return _wrap(view, buf, spec, batched, pl, natural, fmt, phat=(weighting == "phat"))
 
 
 def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None) -> TdGccSamples:
@@ -225,7 +244,7 @@ def spectra_to_samples(spectra, pairs, spec, weighting: str = "phat", floor=None
     nat.call("srpgpu_spectra_to_samples", dev.ptr(y), y.shape[0], y.shape[1], spec.half_len,
              dev.ptr(_pairs_device(pairs)), pairs.num_pairs, w, mode, fval, dev.ptr(counts),
              dev.ptr(offsets), s_total, dev.ptr(buf), ld, dev.stream_ptr())
-    return _wrap(view, buf, spec, batched)
+    return _wrap(view, buf, spec, batched, phat=(weighting == "phat"))
 
 
 __all__ = ["SampleSpec", "TdGccSamples", "sample_spec", "td_gcc_samples", "frames_to_samples",

@@ -9,7 +9,7 @@ kept lag windows, pair by pair, rounded up to groups of 8 consecutive lags:
 
     K(tile) = sum_p g * ceil(w_p / g),   w_p = width of the tile's window of pair p
 
-with g = 8 lags for the bf16 kernel (its MN atoms are 8 rows) and g = 4 for the 3xTF32
+with g = 8 lags for the bf16 / fp16 kernels (their MN atoms are 8 rows) and g = 4 for the 3xTF32
 kernel (the tf32 MN layout has 4-row atoms): cfg4 (fixed fit) 1160 / 966 on average for
 256-candidate tiles, against S = 7028.  The
 tile's operator is stored dense over that K in 64-lag blocks, each block as two slabs
@@ -122,7 +122,8 @@ class TileLayout:
     group_col  (num_blocks * 64 / group,) int32: first natural sample index (lag row) of each
                group of `group` lags
     tile_slab  (T,) int32 first 64-lag block of each tile; tile_nkb (T,) blocks per tile;
-               tile_nst (T,) 16-lag stages per tile (what the 3xTF32 kernel iterates)
+               tile_nst (T,) 16-lag stages per tile (what the 3xTF32 kernel iterates);
+               tile_nst32 (T,) 32-lag stages per tile (the fp16x3 kernel)
     tile_rows  (T, 256) int32 candidate of each tile row (ascending; -1 = padding);
                rows 0-127 are half 0, 128-255 half 1
     tile_pos   (J,) int32 position t * 256 + row of each candidate (the kernel writes the map
@@ -158,22 +159,51 @@ class TileLayout:
         row_of = np.zeros(num_rows, dtype=np.int64)
         if self.runs and num_rows:
             n_runs = (num_rows + 7) // 8
-            run = np.arange(num_rows) // 8
-            rfeat = np.zeros((n_runs, p_count))
-            np.add.at(rfeat, run, feat)
-            rfeat = (rfeat / np.bincount(run, minlength=n_runs)[:, None]).astype(np.float32)
-            rlo = np.full((n_runs, p_count), np.iinfo(np.int64).max)
-            rhi = np.full((n_runs, p_count), -1)
-            np.minimum.at(rlo, run, np.where(empty.reshape(num_rows, p_count), np.iinfo(np.int64).max,
-                                             lo_ip.reshape(num_rows, p_count)))
-            np.maximum.at(rhi, run, hi_ip.reshape(num_rows, p_count))
-            rlo = np.where(rhi < 0, 0, rlo)
-            tiles = bisect_tiles(rfeat, TILE, weight=np.full(n_runs, 8), lo=rlo, hi=rhi, group=GROUP,
-                                 tries=BISECT_TRIES)                                    # lists of runs
+            imax = np.iinfo(np.int64).max
+            pad = n_runs * 8 - num_rows
+            f3 = np.concatenate([feat, np.repeat(feat[-1:], pad, axis=0)]).reshape(n_runs, 8, p_count)
+            lo3 = np.concatenate([np.where(empty, imax, lo_ip).reshape(num_rows, p_count),
+                                  np.full((pad, p_count), imax)]).reshape(n_runs, 8, p_count)
+            hi3 = np.concatenate([hi_ip.reshape(num_rows, p_count),
+                                  np.full((pad, p_count), -1)]).reshape(n_runs, 8, p_count)
+            # a run that wraps around the grid's fastest axis holds two far-apart clusters (its
+            # candidates before / after the wrap): one jump between neighbours dwarfs the others
+            d = np.abs(np.diff(f3, axis=1)).max(axis=2)                              # (n_runs, 7)
+            ks = d.argmax(axis=1)
+            jump = d[np.arange(n_runs), ks]
+            d[np.arange(n_runs), ks] = -1.0
+            wraps = (jump > 4.0) & (jump > 4.0 * d.max(axis=1))
+            head = np.arange(8)[None, :] < np.where(wraps, ks + 1, 8)[:, None]       # candidates before the wrap
+
+            def part(mask):
+                m3 = mask[:, :, None]
+                cnt = np.maximum(1, mask.sum(axis=1))[:, None]
+                rf = (np.where(m3, f3, 0.0).sum(axis=1) / cnt).astype(np.float32)
+                rl = np.where(m3, lo3, imax).min(axis=1)
+                rh = np.where(m3, hi3, -1).max(axis=1)
+                return rf, np.where(rh < 0, 0, rl), rh
+
+            hf, hl, hh = part(head)
+            tf_, tl, th = part(~head)
+            tiles = []
+            plain = np.flatnonzero(~wraps)
+            if plain.size:
+                tiles += [plain[ix] for ix in bisect_tiles(hf[plain], TILE, weight=np.full(plain.size, 8),
+                                                           lo=hl[plain], hi=hh[plain], group=GROUP,
+                                                           tries=BISECT_TRIES)]
+            wrapped = np.flatnonzero(wraps)
+            if wrapped.size:      # bisected on both clusters' windows (2P coordinates)
+                tiles += [wrapped[ix] for ix in
+                          bisect_tiles(np.concatenate([hf[wrapped], tf_[wrapped]], axis=1), TILE,
+                                       weight=np.full(wrapped.size, 8),
+                                       lo=np.concatenate([hl[wrapped], tl[wrapped]], axis=1),
+                                       hi=np.concatenate([hh[wrapped], th[wrapped]], axis=1), group=GROUP,
+                                       tries=BISECT_TRIES)]
+            self.num_wrapped_runs = int(wrapped.size)
             t_count = len(tiles)
             tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
             for t, rr in enumerate(tiles):
-                cand = (rr[:, None] * 8 + np.arange(8)[None, :]).ravel()
+                cand = (np.sort(rr)[:, None] * 8 + np.arange(8)[None, :]).ravel()
                 pos = np.arange(cand.shape[0])
                 ok = cand < num_rows
                 tile_rows[t, pos[ok]] = cand[ok]
@@ -189,36 +219,49 @@ class TileLayout:
                 tile_rows[t, :idx.shape[0]] = idx
                 tile_of[idx] = t
                 row_of[idx] = np.arange(idx.shape[0])
-        # per (tile, pair) window over the tile's candidates
-        lo_tp = np.full(t_count * p_count, np.iinfo(np.int64).max)
-        hi_tp = np.full(t_count * p_count, -1)
-        ip = np.arange(num_rows * p_count)
-        tp = tile_of[ip // p_count] * p_count + ip % p_count
-        ok = ~empty
-        np.minimum.at(lo_tp, tp[ok], lo_ip[ok])
-        np.maximum.at(hi_tp, tp[ok], hi_ip[ok])
-        width = np.where(hi_tp >= 0, hi_tp - lo_tp + 1, 0).reshape(t_count, p_count)
-        ngroups = (width + GROUP - 1) // GROUP                           # (T, P)
-        gstart = np.zeros_like(ngroups)
-        gstart[:, 1:] = np.cumsum(ngroups, axis=1)[:, :-1]                # group index of pair p
+        # per (tile, pair): the kept lags of the tile's candidates, covered greedily by groups of
+        # GROUP consecutive lags (each group is gathered on its own, so a tile may hold several
+        # disjoint windows of a pair -- the two clusters of wrapped runs -- and skips the holes)
+        big = np.int64(self.num_cols + GROUP + 1)
+        tp_e = tile_of[rows] * p_count + pairs                                    # (tile, pair) of each entry
+        comb = np.unique(tp_e * big + ncol)                                       # distinct (tile, pair, lag), sorted
+        n_tp = t_count * p_count
+        ptr = np.searchsorted(comb, np.arange(n_tp, dtype=np.int64) * big)        # first lag of each (tile, pair)
+        end = np.searchsorted(comb, (np.arange(n_tp, dtype=np.int64) + 1) * big)
+        g_key, g_start = [], []
+        live = np.flatnonzero(ptr < end)
+        while live.size:
+            start = comb[ptr[live]]                                               # key * big + first uncovered lag
+            g_key.append(live)
+            g_start.append(start)
+            ptr[live] = np.searchsorted(comb, start + GROUP)
+            live = live[ptr[live] < end[live]]
+        if g_key:
+            g_comb = np.sort(np.concatenate(g_start))                             # groups in (tile, pair, lag) order
+        else:
+            g_comb = np.zeros(0, dtype=np.int64)
+        g_tp = g_comb // big
+        ngroups = np.bincount(g_tp, minlength=n_tp).reshape(t_count, p_count)     # (T, P)
         tile_groups = ngroups.sum(axis=1)
         tile_nkb = np.maximum(1, (tile_groups * GROUP + SLAB - 1) // SLAB)
         tile_nst = np.maximum(1, (tile_groups * GROUP + STAGE - 1) // STAGE)   # 16-lag stages (tf32 kernel)
+        tile_nst32 = np.maximum(1, (tile_groups * GROUP + 2 * STAGE - 1) // (2 * STAGE))   # 32-lag stages (fp16 kernel)
         tile_slab = np.zeros(t_count, dtype=np.int64)
         if t_count:
             tile_slab[1:] = np.cumsum(tile_nkb)[:-1]
         num_blocks = int(tile_nkb.sum()) if t_count else 0
+        # groups are sorted by (tile, pair, lag): group i of tile t sits at slot
+        # tile_slab[t] * (SLAB // GROUP) + (i - first group of t)
+        g_tile = g_tp // p_count
+        tile_g0 = np.zeros(t_count + 1, dtype=np.int64)
+        tile_g0[1:] = np.cumsum(tile_groups)
+        g_slot = tile_slab[g_tile] * (SLAB // GROUP) + (np.arange(g_comb.shape[0]) - tile_g0[g_tile])
         group_col = np.zeros(num_blocks * (SLAB // GROUP), dtype=np.int64)
-        lo2 = lo_tp.reshape(t_count, p_count)
-        for t in range(t_count):
-            g0 = tile_slab[t] * (SLAB // GROUP)
-            starts = [lo2[t, p] + GROUP * np.arange(ngroups[t, p]) for p in range(p_count) if ngroups[t, p]]
-            if starts:
-                s = np.concatenate(starts)
-                group_col[g0:g0 + s.shape[0]] = s
+        group_col[g_slot] = g_comb % big
         # scatter the entries into the slabs
+        g_e = np.searchsorted(g_comb, tp_e * big + ncol, side="right") - 1        # group of each entry
         t_e = tile_of[rows]
-        kpos = gstart[t_e, pairs] * GROUP + (ncol - lo2[t_e, pairs])
+        kpos = (g_e - tile_g0[t_e]) * GROUP + (ncol - g_comb[g_e] % big)
         r_e = row_of[rows]
         slab = 2 * (tile_slab[t_e] + kpos // SLAB) + r_e // HALF
         self.slabs = np.zeros((2 * num_blocks, HALF, SLAB), dtype=np.float32)
@@ -227,6 +270,7 @@ class TileLayout:
         self.tile_slab = tile_slab.astype(np.int32)
         self.tile_nkb = tile_nkb.astype(np.int32)
         self.tile_nst = tile_nst.astype(np.int32)
+        self.tile_nst32 = tile_nst32.astype(np.int32)
         self.tile_rows = tile_rows
         self.tile_pos = (tile_of * TILE + row_of).astype(np.int32)
         self.num_tiles = t_count
@@ -234,6 +278,7 @@ class TileLayout:
         self.num_slabs = 2 * num_blocks
         self.mean_k = float(tile_nkb.mean() * SLAB) if t_count else 0.0
         self.mean_k_stages = float(tile_nst.mean() * STAGE) if t_count else 0.0
+        self.mean_k_stages32 = float(tile_nst32.mean() * 2 * STAGE) if t_count else 0.0
 
     def emulate(self, xi_nat: np.ndarray) -> np.ndarray:
         """float64 reference of the gathered product (test helper): z (F, J)."""

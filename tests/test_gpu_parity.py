@@ -241,7 +241,7 @@ def test_fused_sspi_pipeline(golden_scene):
 
 # ------------------------------------------------------------------ maps
 
-@pytest.mark.parametrize("engine", ["tc", "tile", "tile_bf16", "band"])
+@pytest.mark.parametrize("engine", ["tc", "tile", "tile_f16", "tile_bf16", "band"])
 def test_sspi_and_si_maps(golden_scene, engine):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
@@ -276,9 +276,10 @@ def test_sspi_engines_agree_on_frame_batches(golden_scene):
     zb, ib = s.sspi_map(sp, xt, argmax=True, engine="band")
     zg, ig = s.sspi_map(sp, xt, argmax=True, engine="tile")
     zh, ih = s.sspi_map(sp, xt, argmax=True, engine="tile_bf16")
+    zf, i_f = s.sspi_map(sp, xt, argmax=True, engine="tile_f16")
     z1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine="tc")
     assert torch.equal(zt[7], z1)
-    for eng, zz in (("tile", zg), ("tile_bf16", zh)):
+    for eng, zz in (("tile", zg), ("tile_bf16", zh), ("tile_f16", zf)):
         g1 = s.sspi_map(sp, s.TdGccSamples(torch.from_numpy(x[7]).cuda(), spec), engine=eng)
         assert torch.equal(zz[7], g1)
     assert_map_close(zh, O.sspi_map(sp.values, sp.col_indices, sp.row_splits, x.astype(np.float64)))
@@ -286,8 +287,13 @@ def test_sspi_engines_agree_on_frame_batches(golden_scene):
     assert_map_close(zt, ref)
     assert_map_close(zb, ref)
     assert_map_close(zg, ref)
+    assert_map_close(zf, ref)
     assert_argmax_agrees(it, ref)
     assert_argmax_agrees(ig, ref)
+    assert_argmax_agrees(i_f, ref)
+    # fp16x3 carries the same 22 operand bits as 3xTF32: the two FP32-class engines agree far
+    # inside the parity bar
+    assert O.normalized_max_error(np_(zf), np_(zg).astype(np.float64)).max() < 5e-6
 
 
 def test_natural_planes_from_frontend(golden_scene):
@@ -319,6 +325,32 @@ def test_natural_planes_from_frontend(golden_scene):
     nat_cols = torch.from_numpy(s.tiles.natural_columns(spec_offsets(spec))).cuda()
     v = xi.values.t()[nat_cols].double()
     assert torch.all((hi.double() + lo.double() - v).abs() <= v.abs() * 2.0 ** -21)
+
+
+def test_f16_planes_from_frontend(golden_scene):
+    """The frontend's fp16 hi / lo planes (fp16x3 gathered-window engine) are exactly the split
+    of its f32 samples, carry >= 21 significant bits, and the auto engine takes them only for
+    PHAT-weighted (bounded) samples."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, **s.maps.plane_args("tile_f16"))
+    assert xi.planes_fmt == "f16" and xi.phat and xi.bf16_planes.dtype == torch.float16
+    assert xi.bf16_planes.shape[2] % 64 == 0
+    plain = s.TdGccSamples(xi.values.clone(), spec)
+    ref, _, _ = s.maps.sample_planes(plain, spec.total_samples, natural=spec_offsets(spec), fmt="f16")
+    f, st = xi.values.shape[0], spec.total_samples
+    assert torch.equal(xi.bf16_planes[:, :st, :f].view(torch.int16), ref[:, :st, :f].view(torch.int16))
+    hi, lo = xi.bf16_planes[0, :st, :f].double(), xi.bf16_planes[1, :st, :f].double()
+    nat_cols = torch.from_numpy(s.tiles.natural_columns(spec_offsets(spec))).cuda()
+    v = xi.values.t()[nat_cols].double()
+    assert torch.all((hi + lo - v).abs() <= torch.clamp(v.abs() * 2.0 ** -21, min=2.0 ** -25))
+    assert float(v.abs().max()) <= 2 * (frame.half_len - 1)          # the PHAT bound
+    with pytest.raises(ValueError):
+        s.frames_to_samples(x, frame, pairs, spec, weighting="none", **s.maps.plane_args("tile_f16"))
+    assert s.maps.interp_engine(8192, 240.0, "auto", 4096, True, bounded=True) == "tile_f16"
+    assert s.maps.interp_engine(8192, 240.0, "auto", 4096, True, bounded=False) == "tile"
+    assert not s.maps._bounded(plain) and s.maps._bounded(xi)
 
 
 def test_sspi_tile_and_row_kernels_agree(golden_scene):
@@ -504,7 +536,7 @@ def test_pipeline_graph_matches_eager(golden_scene):
     eng = s.maps.map_engine("sspi", sp, "auto", F)
     pipe = MapPipeline("sspi", sp, frame, pairs, spec, frames=F, engine=eng)   # the unfused chain
     z, idx = pipe.run(x)
-    z2, idx2 = s.sspi_map(sp, xi, argmax=True)
+    z2, idx2 = s.sspi_map(sp, xi, argmax=True, engine=eng)
     assert torch.equal(z, z2) and torch.equal(idx, idx2)
     auto = MapPipeline("sspi", sp, frame, pairs, spec, frames=F)               # fused where eligible
     za, ia = auto.run(x)

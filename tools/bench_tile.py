@@ -1,4 +1,4 @@
-"""A/B of the gathered-window SSPI engines (3xTF32 "tile" vs bf16x3 "tile_bf16") at cfg4:
+"""A/B of the gathered-window SSPI engines (fp16x3 "tile_f16" vs 3xTF32 "tile" vs bf16x3 "tile_bf16") at cfg4:
 device time of the frontend and of the map per 10^4 frames, and parity against the
 float64 oracle on a few frames.  Usage: python tools/bench_tile.py [--fit fixed|global]"""
 import argparse
@@ -37,7 +37,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--fit", default="fixed")
     ap.add_argument("--frames", type=int, default=10000)
-    ap.add_argument("--engines", default="tile,tile_bf16")
+    ap.add_argument("--engines", default="tile_f16,tile,tile_bf16")
     ap.add_argument("--workload", default="cfg4")
     args = ap.parse_args()
     t0 = time.time()
@@ -77,8 +77,8 @@ def main():
         t_front = timeit(lambda: s.frames_to_samples(x, wl.frame, wl.pairs, wl.spec, range(args.frames), **pa))
         t_map = timeit(lambda: s.sspi_map(sp, xi, argmax=True, engine=eng))
         t_keys = timeit(lambda: s.sspi_map(sp, xi, argmax=True, out_map=False, engine=eng))
-        op = s.maps.tile_from_sparse(sp, s.maps.spec_offsets(wl.spec), tf32=(eng == "tile")) \
-            if eng.startswith("tile") else None
+        op = s.maps.tile_from_sparse(sp, s.maps.spec_offsets(wl.spec), fmt=s.maps.TILE_ENGINES[eng]) \
+            if eng in s.maps.TILE_ENGINES else None
         r = {"engine": eng, "frontend_ms": t_front, "map_ms": t_map, "map_argmax_only_ms": t_keys,
              "maps_per_s": args.frames / ((t_front + t_map) / 1e3), "err": float(err.max()), "argmax_agree": agree,
              "setup_s": setup}
