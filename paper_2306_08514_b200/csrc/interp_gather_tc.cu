@@ -778,38 +778,61 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       w = wn;
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
+      // The pair's MMA issuer.  The whole warp runs the loop converged and one elected lane
+      // issues (elect.sync keeps the descriptors on the uniform datapath; a lane-0 branch made
+      // every tcgen05.mma an ELECT / R2UR.BROADCAST loop and the issuer, not the tensor pipe,
+      // set the pace: ncu r2e).  Stage and chunk positions are running counters, and the
+      // stage-0 descriptors are advanced by the stage pitch (address field = bytes >> 4).
       // D f32, A K-major, B MN-major (bit 16), N = 256, M = 256 (the pair)
       constexpr uint32_t idesc = (1u << 4) | (TR::kFmt << 7) | (TR::kFmt << 10) | (1u << 16) |
                                  ((uint32_t)(PN >> 3) << 17) | ((uint32_t)((2 * GM) >> 4) << 24);
-      uint32_t g = 0, c = 0;
+      constexpr int NK = GK / UK;
+      constexpr uint64_t kAPitch = sizeof(sm.a[0]) >> 4, kBPitch = sizeof(sm.b[0]) >> 4;
+      const uint64_t a0h = smem_desc_sw64(sm.a[0][0]), a0l = smem_desc_sw64(sm.a[0][1]);
+      uint64_t b0h[NK], b0l[NK];
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        b0h[k] = TR::desc_b(sm.b[0][0][2 * k]);
+        b0l[k] = TR::desc_b(sm.b[0][1][2 * k]);
+      }
+      uint32_t s = 0, ph = 0, c = 0;
       for (int u = u_begin + cid; u < u_total; u += ncl) {
         Unit w;
         if (!decode32(u, T, fg, n_tiles, w)) continue;
         const int ns = __ldg(tile_nst + w.t);
-        for (int kq = 0; kq < ns; ++kq, ++g) {
-          const int s = g % PNS;
-          const int first = kq % CH == 0;
-          if (first) {
+        int kc = 0;                                              // stage within the accumulation chunk
+        for (int kq = 0; kq < ns; ++kq) {
+          if (kc == 0) {
             mbar_wait(&sm.tempty[c & 1], ((c >> 1) & 1) ^ 1);    // both epilogues folded this buffer
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
-          mbar_wait(&sm.full[s], (g / PNS) & 1);
+          mbar_wait(&sm.full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t d = tmem + (c & 1) * PN;
+          const bool last = kc == CH - 1 || kq == ns - 1;
+          if (elect_one()) {
+            const uint32_t d = tmem + (c & 1) * PN;
+            const uint64_t ao = (uint64_t)s * kAPitch, bo = (uint64_t)s * kBPitch;
 #pragma unroll
-          for (int k = 0; k < GK / UK; ++k) {
-            const uint64_t aoff = (uint64_t)((k * UK * ES) >> 4);
-            const uint64_t bh = TR::desc_b(sm.b[s][0][2 * k]), bl = TR::desc_b(sm.b[s][1][2 * k]);
-            const uint64_t a_h = smem_desc_sw64(sm.a[s][0]) + aoff, a_l = smem_desc_sw64(sm.a[s][1]) + aoff;
-            TR::mma(d, a_h, bh, idesc, (first && k == 0) ? 0u : 1u);
-            TR::mma(d, a_h, bl, idesc, 1u);
-            TR::mma(d, a_l, bh, idesc, 1u);
+            for (int k = 0; k < NK; ++k) {
+              const uint64_t aoff = ao + (uint64_t)((k * UK * ES) >> 4);
+              TR::mma(d, a0h + aoff, b0h[k] + bo, idesc, (kc == 0 && k == 0) ? 0u : 1u);
+              TR::mma(d, a0h + aoff, b0l[k] + bo, idesc, 1u);
+              TR::mma(d, a0l + aoff, b0h[k] + bo, idesc, 1u);
+            }
+            mma_commit_pair(&sm.empty[s]);
+            if (last) mma_commit_pair(&sm.tfull[c & 1]);
           }
-          mma_commit_pair(&sm.empty[s]);
-          if (kq % CH == CH - 1 || kq == ns - 1) {
-            mma_commit_pair(&sm.tfull[c & 1]);
+          __syncwarp();
+          if (last) {
             ++c;
+            kc = 0;
+          } else {
+            ++kc;
+          }
+          if (++s == PNS) {
+            s = 0;
+            ph ^= 1;
           }
         }
       }

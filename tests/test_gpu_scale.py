@@ -275,9 +275,10 @@ def test_cfg4_global_fit_pipeline(cfg4_global, engine):
         j = int(np.searchsorted(rows, peaks[k]))
         assert z_ref[k, j] >= z_ref[k].max() * (1 - 2 * TOL)
     # the map does not depend on the batch: a frame's row equals its single-frame map
+    eng1 = s.maps.map_engine("sspi", sp, engine, 1, bounded=True)      # the pipeline weights with PHAT
     xi1 = s.frames_to_samples(torch.from_numpy(wl.samples).cuda(), wl.frame, wl.pairs, wl.spec, range(1, 2),
-                              **s.maps.plane_args(s.maps.map_engine("sspi", sp, engine, 1)))
-    z1 = s.sspi_map(sp, xi1, engine=s.maps.map_engine("sspi", sp, engine, 1))
+                              **s.maps.plane_args(eng1))
+    z1 = s.sspi_map(sp, xi1, engine=eng1)
     assert torch.equal(z1[0], z[1])
     print(f"cfg4 global fit ({engine}): normalized max error {err.max():.2e} over {rows.size} rows")
 
