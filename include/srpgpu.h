@@ -226,7 +226,9 @@ int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, 
  * order), slab_planes fp32 [2][num_slabs * 128][64] (srpgpu_split_tf32 of the slabs);
  * tile_nkb here counts each tile's 16-lag stages (its window rounded up to 16 lags, not to
  * the 64-lag block) and group_col holds 4-lag groups (16 per block); the other arguments
- * as srpgpu_interp_map_gather_tc.  Replaces interpolation.py:188-195
+ * as srpgpu_interp_map_gather_tc, except that z_tiles is scratch of round256(F) rows of
+ * num_tiles * 256 floats (the CTA-pair kernel stores it in blocks of 32 frames:
+ * [frame block][tile][32 frames][256 rows]).  Replaces interpolation.py:188-195
  * (sspi_map) at long sample vectors. */
 int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
                                   int64_t planes_ld, const float* slab_planes, int64_t num_slabs,
@@ -242,8 +244,8 @@ int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frame
  * aligned, natural lag order; PHAT samples are bounded by 2(K-1)), slab_planes fp16
  * [2][num_slabs * 128][64] = srpgpu_split_f16_rows of the slabs scaled by 1 / z_scale (a
  * power of two; the kernel multiplies the finished sums by z_scale, exactly); group_col
- * holds 8-lag groups (8 per block) and tile_nst counts each tile's 32-lag stages.  CTA pairs
- * (cta_group::2) only.  Replaces interpolation.py:188-195 (sspi_map) / :129-136 (si_map). */
+ * holds 8-lag groups (8 per block) and tile_nst counts each tile's 32-lag stages; z_tiles is
+ * scratch of round256(F) rows of num_tiles * 256 floats.  CTA pairs (cta_group::2) only.  Replaces interpolation.py:188-195 (sspi_map) / :129-136 (si_map). */
 int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t num_frames, int32_t num_cols,
                                  int64_t planes_ld, const void* slab_planes, int64_t num_slabs,
                                  const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nst,

@@ -637,7 +637,19 @@ constexpr int PNG = 4;               // groups per stage
 struct PairTf32 {
   static constexpr int GK = 16, GG = 4, UK = 8, GA = 32, ES = 4;
   static constexpr uint32_t kFmt = 2;          // instruction descriptor operand format: tf32
-  static __device__ __forceinline__ uint64_t desc_b(const void* p) { return desc_mn128(p); }
+  // MN-major tf32 operand, 128-byte swizzle on 32-byte atoms: 512-byte atoms of 4 lags x 32 frames; a
+  // group's four frame blocks follow one another (LBO = 512 B), the next 4 lags are the next
+  // group, one (group, plane) pair further (SBO = 4 KB)
+  static __device__ __forceinline__ uint64_t desc_b(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    uint64_t d = 0;
+    d |= (addr & 0x3FFFFull) >> 4;
+    d |= (uint64_t)(512 >> 4) << 16;
+    d |= (uint64_t)((2 * PGroupBytes) >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;                    // SWIZZLE_128B_BASE32B
+    return d;
+  }
   static __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -651,14 +663,14 @@ struct PairF16 {
   static constexpr int GK = 32, GG = 8, UK = 16, GA = 64, ES = 2;
   static constexpr uint32_t kFmt = 0;          // f16
   // MN-major fp16 operand, 128-byte swizzle: 1 KB atoms of 8 lags x 64 frames; a group's two
-  // frame blocks follow one another (LBO = 1 KB along N), the next 8 lags are the next group
-  // (SBO = 2 KB along K)
+  // frame blocks follow one another (LBO = 1 KB along MN), the next 8 lags are the next group,
+  // one (group, plane) pair further (SBO = 4 KB along K)
   static __device__ __forceinline__ uint64_t desc_b(const void* p) {
     const uint64_t addr = smem_u32(p);
     uint64_t d = 0;
     d |= (addr & 0x3FFFFull) >> 4;
     d |= (uint64_t)(1024 >> 4) << 16;
-    d |= (uint64_t)(PGroupBytes >> 4) << 32;
+    d |= (uint64_t)((2 * PGroupBytes) >> 4) << 32;
     d |= (uint64_t)1 << 46;
     d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
     return d;
@@ -674,18 +686,17 @@ struct PairF16 {
 
 template <class TR>
 struct __align__(1024) PairSmem {
-  unsigned char b[PNS][2][PNG][PGroupBytes];   // [plane][group] the CTA's frame blocks of one lag group
-  unsigned char a[PNS][2][PSlabBytes];         // [plane] this CTA's slab half (64-byte rows, 64-byte swizzle)
-  float zs[2][32 * GM];                        // [column half] one 32-frame slice of the map for a TMA store
-  int32_t rows[2][kMaxBlocks * (GB / TR::GG)];
+  unsigned char b[PNS][PNG][2][PGroupBytes];   // [group][plane] the CTA's frame blocks of one lag group (one TMA box per group)
+  unsigned char a[PNS][2][PSlabBytes];         // [plane] this CTA's slab half (64-byte rows, 64-byte swizzle; one TMA box)
+  float zs[PEpi][32 * 32];                     // [epilogue warp] 32 frames x 32 candidates of the map (128-byte swizzle) for a TMA store
+  alignas(16) int32_t rows[2][kMaxBlocks * (GB / TR::GG)];   // the current / next unit's group rows
   uint64_t full[PNS], empty[PNS], tfull[2], tempty[2];
   uint32_t tmem_base;
 };
 
 template <class TR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
-gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_constant__ CUtensorMap ma_lo,
-                   const __grid_constant__ CUtensorMap mb_hi, const __grid_constant__ CUtensorMap mb_lo,
+gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
                    const __grid_constant__ CUtensorMap mz, int z_tma, int l2pol, int64_t zt_ld, float zscale,
                    int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                    const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
@@ -703,10 +714,8 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
   const int u_total = min(u_end, ((n_tiles + fg - 1) / fg) * T * fg);
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&ma_hi);
-    prefetch_tmap(&ma_lo);
-    prefetch_tmap(&mb_hi);
-    prefetch_tmap(&mb_lo);
+    prefetch_tmap(&ma);
+    prefetch_tmap(&mb);
     for (int s = 0; s < PNS; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], 1);
@@ -729,11 +738,14 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // lanes 0-7: (plane, group) of this CTA's frame half; lanes 8-9: this CTA's slab half
+    // The producer runs converged; per stage one elected lane issues this CTA's five TMA
+    // loads -- four gathered lag groups (hi and lo planes in one 4D box each) and the slab
+    // half (both planes in one 3D box) -- with operands on the uniform datapath.  (Ten
+    // per-lane loads cost ~100 cycles each in ELECT / R2UR.BROADCAST loops and the producer,
+    // not the tensor pipe, set the pace: ncu r2e.)
     constexpr uint32_t kBytes = 2u * (PSlabBytes + PNG * PGroupBytes);   // one CTA's stage
-    const int plane = (lane >> 2) & 1, grp = lane & 3, ap = (lane - 8) & 1;
-    // L2 policies as the one-CTA kernel (l2pol: diagnostic override, 2 bits each for the
-    // samples / slabs: 0 evict_last, 1 evict_first, 2 evict_normal)
+    // L2 policies (l2pol: diagnostic override, 2 bits each for the samples / slabs:
+    // 0 evict_last, 1 evict_first, 2 evict_normal)
     auto pol = [](int c) { return c == 0 ? policy_evict_last() : c == 1 ? policy_evict_first() : policy_evict_normal(); };
     const uint64_t keep = pol(l2pol & 3), once = pol((l2pol >> 2) & 3);
     auto next_unit = [&](int u, Unit& w) {
@@ -744,7 +756,8 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
       for (int i = lane; i < nst * PNG; i += 32) sm.rows[buf][i] = __ldg(group_col + b0 * (GB / GG) + i);
     };
-    uint32_t g = 0;
+    const uint32_t full0 = mapa_shared(smem_u32(&sm.full[0]), rank & ~1u);   // the leader's stage barriers
+    uint32_t s = 0, ph = 1;
     int buf = 0;
     Unit w;
     int u = next_unit(u_begin + cid, w);
@@ -755,21 +768,23 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       if (un < u_total) stage_rows(buf ^ 1, wn);
       __syncwarp();
       const int b0 = __ldg(tile_blk + w.t), nst = __ldg(tile_nst + w.t);
-      for (int kq = 0; kq < nst; ++kq, ++g) {
-        const int blk = b0 + kq / (GB / GK), sub = kq % (GB / GK);
-        const int row = sm.rows[buf][kq * PNG + grp];
-        const int s = g % PNS;
-        const uint32_t bar = mapa_shared(smem_u32(&sm.full[s]), 0);    // the leader's stage barrier
-        if (lane == 0) {
-          mbar_wait(&sm.empty[s], ((g / PNS) & 1) ^ 1);
+      const int fblk = w.n * (PN / GA) + (int)rank * PNA;
+      for (int kq = 0; kq < nst; ++kq) {
+        const int4 rows = *reinterpret_cast<const int4*>(&sm.rows[buf][kq * PNG]);
+        mbar_wait(&sm.empty[s], ph);
+        if (elect_one()) {
           if (rank == 0) mbar_expect_tx(&sm.full[s], 2 * kBytes);     // both CTAs' loads
+          const uint32_t bar = full0 + s * (uint32_t)sizeof(uint64_t);
+          tma_load_4d_pair(sm.b[s][0][0], &mb, bar, 0, rows.x, fblk, 0, keep);
+          tma_load_4d_pair(sm.b[s][1][0], &mb, bar, 0, rows.y, fblk, 0, keep);
+          tma_load_4d_pair(sm.b[s][2][0], &mb, bar, 0, rows.z, fblk, 0, keep);
+          tma_load_4d_pair(sm.b[s][3][0], &mb, bar, 0, rows.w, fblk, 0, keep);
+          tma_load_3d_pair(sm.a[s][0], &ma, bar, (kq % (GB / GK)) * GK, (2 * (b0 + kq / (GB / GK)) + (int)rank) * GM, 0, once);
         }
         __syncwarp();
-        if (lane < 8) {
-          tma_load_3d_pair(sm.b[s][plane][grp], plane ? &mb_lo : &mb_hi, bar, 0, row,
-                           w.n * (PN / GA) + (int)rank * PNA, keep);
-        } else if (lane < 10) {
-          tma_load_2d_pair(sm.a[s][ap], ap ? &ma_lo : &ma_hi, bar, sub * GK, (2 * blk + (int)rank) * GM, once);
+        if (++s == PNS) {
+          s = 0;
+          ph ^= 1;
         }
       }
       __syncwarp();
@@ -784,17 +799,19 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       // every tcgen05.mma an ELECT / R2UR.BROADCAST loop and the issuer, not the tensor pipe,
       // set the pace: ncu r2e).  Stage and chunk positions are running counters, and the
       // stage-0 descriptors are advanced by the stage pitch (address field = bytes >> 4).
-      // D f32, A K-major, B MN-major (bit 16), N = 256, M = 256 (the pair)
-      constexpr uint32_t idesc = (1u << 4) | (TR::kFmt << 7) | (TR::kFmt << 10) | (1u << 16) |
-                                 ((uint32_t)(PN >> 3) << 17) | ((uint32_t)((2 * GM) >> 4) << 24);
+      // D f32 [M = 256 frames (the pair)][N = 256 candidates]: A = the gathered samples, MN-major
+      // (bit 15), B = the slabs, K-major -- an accumulator lane is a frame, so the epilogue's
+      // argmax runs down a thread's registers and a thread's candidates are contiguous map bytes
+      constexpr uint32_t idesc = (1u << 4) | (TR::kFmt << 7) | (TR::kFmt << 10) | (1u << 15) |
+                                 ((uint32_t)((2 * GM) >> 3) << 17) | ((uint32_t)(PN >> 4) << 24);
       constexpr int NK = GK / UK;
       constexpr uint64_t kAPitch = sizeof(sm.a[0]) >> 4, kBPitch = sizeof(sm.b[0]) >> 4;
       const uint64_t a0h = smem_desc_sw64(sm.a[0][0]), a0l = smem_desc_sw64(sm.a[0][1]);
       uint64_t b0h[NK], b0l[NK];
 #pragma unroll
       for (int k = 0; k < NK; ++k) {
-        b0h[k] = TR::desc_b(sm.b[0][0][2 * k]);
-        b0l[k] = TR::desc_b(sm.b[0][1][2 * k]);
+        b0h[k] = TR::desc_b(sm.b[0][2 * k][0]);
+        b0l[k] = TR::desc_b(sm.b[0][2 * k][1]);
       }
       uint32_t s = 0, ph = 0, c = 0;
       for (int u = u_begin + cid; u < u_total; u += ncl) {
@@ -816,9 +833,9 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
               const uint64_t aoff = ao + (uint64_t)((k * UK * ES) >> 4);
-              TR::mma(d, a0h + aoff, b0h[k] + bo, idesc, (kc == 0 && k == 0) ? 0u : 1u);
-              TR::mma(d, a0h + aoff, b0l[k] + bo, idesc, 1u);
-              TR::mma(d, a0l + aoff, b0h[k] + bo, idesc, 1u);
+              TR::mma(d, b0h[k] + bo, a0h + aoff, idesc, (kc == 0 && k == 0) ? 0u : 1u);
+              TR::mma(d, b0l[k] + bo, a0h + aoff, idesc, 1u);
+              TR::mma(d, b0h[k] + bo, a0l + aoff, idesc, 1u);
             }
             mma_commit_pair(&sm.empty[s]);
             if (last) mma_commit_pair(&sm.tfull[c & 1]);
@@ -838,21 +855,29 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
       }
     }
   } else {
-    // epilogue: warp = (column half ch, TMEM lane quarter q) of this CTA's 128 candidates x
-    // 256 frames; folds every chunk into fp32 registers, then map + argmax as above
+    // epilogue: warp = (column half ch, TMEM lane quarter q): this CTA's frames 32q..32q+31, one
+    // per lane, x tile rows 128ch..128ch+127 in the thread's registers.  Every chunk is folded
+    // into fp32 registers; then the argmax runs down the registers (no cross-lane work), and
+    // the map leaves in 32-candidate slices through the warp's own swizzled staging tile and a
+    // TMA store (tile order), or as whole 32-byte runs (grid order).
     const int q = warp & 3;
     const int ch = (warp - 2) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * PCols);
-    const int64_t ldt = zt_ld >= 0 ? zt_ld : (int64_t)T * GT;   // zt_ld: diagnostic override
     // map stores stream past L2 (evict_first): they must not push out the group's samples
     const uint64_t zpol = policy_evict_first();
-    const bool issuer = z_tma && q == 0 && lane == 0;   // one TMA-store thread per column half
+    float* zsw = sm.zs[warp - 2];
     uint32_t c = 0;
     for (int u = u_begin + cid; u < u_total; u += ncl) {
       Unit w;
       if (!decode32(u, T, fg, n_tiles, w)) continue;
-      const int r = (int)rank * GM + q * 32 + lane;
-      const int jrow = __ldg(tile_rows + (int64_t)w.t * GT + r);
+      const int64_t f0 = (int64_t)w.n * PN + (int)rank * PNC + q * 32;   // the warp's first frame
+      const int64_t f = f0 + lane;
+      const int32_t* trow = tile_rows + (int64_t)w.t * GT + ch * PCols;
+      // the tile's valid rows are a prefix: count this column half's
+      int nv = 0;
+#pragma unroll
+      for (int i = 0; i < PCols / 32; ++i) nv += __ldg(trow + i * 32 + lane) >= 0 ? 1 : 0;
+      nv = __reduce_add_sync(0xffffffffu, nv);
       const int nc = num_chunks(__ldg(tile_nst + w.t), CH);
       float rs[PCols];
       for (int j = 0; j < nc; ++j, ++c) {
@@ -873,64 +898,76 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sm.tempty[c & 1]), 0));
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&sm.tempty[c & 1]), rank & ~1u));
       }
+      if (nv == 0 || f0 >= F) continue;                // padding rows only / frames past the batch
       if (zscale != 1.0f) {   // undo the slabs' power-of-two scale (exact)
 #pragma unroll
         for (int t = 0; t < PCols; ++t) rs[t] *= zscale;
       }
-      const bool any = __any_sync(0xffffffffu, jrow >= 0);
-      if (!z_tma && !any) continue;
+      if (keys) {   // first maximum of the thread's valid candidates (rows ascend with the candidate)
+        float bv = rs[0];
+        int bc = 0;
+        if (nv == PCols) {
 #pragma unroll
-      for (int cc = 0; cc < PCols / 32; ++cc) {
-        const int64_t f0 = (int64_t)w.n * PN + ch * PCols + cc * 32;
-        if (f0 >= F) break;                            // uniform over the column half's 4 warps
-        if (z_tma) {
-          // tile-order map through shared memory and one TMA store per 32-frame slice: the
-          // epilogue is back to folding as soon as the slice is staged
-          if (issuer) bulk_wait_read<0>();             // the previous slice's smem has been read
-          named_barrier(1 + ch, 128);
+          for (int t = 1; t < PCols; ++t)
+            if (rs[t] > bv) {
+              bv = rs[t];
+              bc = t;
+            }
+        } else {
 #pragma unroll
-          for (int t = 0; t < 32; ++t) sm.zs[ch][t * GM + q * 32 + lane] = rs[cc * 32 + t];
+          for (int t = 1; t < PCols; ++t)
+            if (t < nv && rs[t] > bv) {
+              bv = rs[t];
+              bc = t;
+            }
+        }
+        if (f < F) atomicMax(keys + f, make_key(bv, (uint32_t)__ldg(trow + bc)));
+      }
+      if (z_tma) {
+#pragma unroll
+        for (int cc = 0; cc < PCols / 32; ++cc) {
+          if (cc * 32 >= nv) break;                    // uniform over the warp
+          if (lane == 0) bulk_wait_read<0>();          // the previous slice has left the staging tile
+          __syncwarp();
+          // row = this lane's frame (128 B); 16-byte chunk j sits at j ^ (row & 7) (SWIZZLE_128B)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(zsw + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                make_float4(rs[cc * 32 + 4 * j], rs[cc * 32 + 4 * j + 1], rs[cc * 32 + 4 * j + 2],
+                            rs[cc * 32 + 4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          named_barrier(1 + ch, 128);
-          if (issuer) {
-            tma_store_2d(&mz, sm.zs[ch], w.t * GT + (int)rank * GM, (int)f0);
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&mz, zsw, ch * PCols + cc * 32, 0, w.t, w.n * (PN / 32) + (int)rank * (PNC / 32) + q);
             bulk_commit();
           }
-        } else if (zg) {
-          if (jrow >= 0) {
-            float* zc = zg + f0 * J + jrow;
-#pragma unroll
-            for (int t = 0; t < 32; ++t)
-              if (f0 + t < F) st_global_hint(zc + t * J, rs[cc * 32 + t], zpol);
-          }
-        } else if (zt) {
-          float* zc = zt + f0 * ldt + (int64_t)w.t * GT + r;
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (f0 + t < F) st_global_hint(zc + t * ldt, rs[cc * 32 + t], zpol);
         }
-        if (keys && any) {   // per frame: warp max of the ordered bits (redux), lowest winning lane (ballot)
-          uint32_t best = 0u, win = 0u;
+      } else if (zg) {   // grid order: the tile's rows are aligned runs of 8 candidates
+        if (f < F) {
+          float* zf = zg + f * J;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const uint32_t mine = jrow >= 0 ? ordered_bits(rs[cc * 32 + t]) : 0u;
-            const uint32_t m = __reduce_max_sync(0xffffffffu, mine);
-            const uint32_t who = __ballot_sync(0xffffffffu, mine == m);
-            if (lane == t) {
-              best = m;
-              win = (uint32_t)(__ffs(who) - 1);
+          for (int r8 = 0; r8 < PCols / 8; ++r8) {
+            const int j8 = __ldg(trow + r8 * 8);
+            if (j8 >= 0) {
+              st_global_v4_hint(zf + j8, rs[r8 * 8], rs[r8 * 8 + 1], rs[r8 * 8 + 2], rs[r8 * 8 + 3], zpol);
+              st_global_v4_hint(zf + j8 + 4, rs[r8 * 8 + 4], rs[r8 * 8 + 5], rs[r8 * 8 + 6], rs[r8 * 8 + 7], zpol);
             }
           }
-          const int jw = __shfl_sync(0xffffffffu, jrow, (int)win);
-          if (f0 + lane < F && best != 0u)
-            atomicMax(keys + f0 + lane,
-                      ((unsigned long long)best << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)jw));
+        }
+      } else if (zt) {   // tile order by register stores (diagnostic: SRPGPU_GATHER_ZSTG)
+        if (f < F) {
+          // zt_ld == 0: diagnostic, every unit to one block
+          const int64_t blk = zt_ld == 0 ? 0 : (int64_t)(w.n * (PN / 32) + (int)rank * (PNC / 32) + q) * T + w.t;
+          float* zc = zt + (blk * 32 + lane) * GT + ch * PCols;
+#pragma unroll
+          for (int t = 0; t < PCols; t += 4)
+            st_global_v4_hint(zc + t, rs[t], rs[t + 1], rs[t + 2], rs[t + 3], zpol);
         }
       }
     }
-    if (issuer) bulk_wait_all();                       // the map's TMA stores have landed
+    if (lane == 0) bulk_wait_all();                    // the map's TMA stores have landed
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();
@@ -948,21 +985,32 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma_hi, const __grid_const
 // tile order -> grid order: z[f][j] = zt[f][pos[j]] (coalesced writes; the reads follow
 // the tiles' ascending rows, mostly short contiguous runs).  FB frames per CTA share each
 // thread's pos loads (the kernel is L1-wavefront bound: ncu r1j, L1 86% of peak)
+// blocked != 0 (the pair kernel): the tile-order map is stored in blocks of ZB = 32 frames,
+// zt[frame block][tile][32 frames][256 rows], so an epilogue warp's 32 frames x 128 candidates
+// land in one 32 KB block (with the frames' rows 1.3 MB apart the stores' latency stalled the
+// pair kernel's accumulator hand-back: +4.5 ms at cfg4; whole 256-frame units, on the other
+// hand, scatter this pass's reads over 343 MB per frame: 6.3 -> 14.4 ms); blocked = the number
+// of tiles T.
+constexpr int ZB = 32;
 template <int FB>
 __global__ void __launch_bounds__(256) untile_kernel(const float* __restrict__ zt, int64_t ldt, const int32_t* __restrict__ pos, int64_t J,
-                              int64_t F, float* __restrict__ z) {
+                              int64_t F, float* __restrict__ z, int64_t blocked) {
   constexpr int U = UNTILE_U;   // independent gathers in flight per thread (per frame)
   for (int64_t f0 = (int64_t)blockIdx.y * FB; f0 < F; f0 += (int64_t)gridDim.y * FB) {
     const int nf = F - f0 < FB ? (int)(F - f0) : FB;
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < J; j0 += U * step) {
-      int32_t p[U];
+      int64_t p[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) p[u] = j0 + u * step < J ? __ldg(pos + j0 + u * step) : 0;
+      for (int u = 0; u < U; ++u) {
+        const int32_t q = j0 + u * step < J ? __ldg(pos + j0 + u * step) : 0;
+        p[u] = blocked ? (int64_t)(q >> 8) * (GT * ZB) + (q & 255) : (int64_t)q;
+      }
 #pragma unroll
       for (int fb = 0; fb < FB; ++fb) {
         if (fb < nf) {
-          const float* src = zt + (f0 + fb) * ldt;
+          const int64_t f = f0 + fb;
+          const float* src = blocked ? zt + ((f / ZB) * blocked * ZB + (f % ZB)) * GT : zt + f * ldt;
           float* dst = z + (f0 + fb) * J;
           float v[U];
 #pragma unroll
@@ -990,14 +1038,15 @@ static int untile_frames(int64_t num_frames) {
 }
 
 static int untile(const float* z_tiles, int32_t num_tiles, const int32_t* tile_pos, int64_t num_candidates,
-                  int64_t num_frames, float* z, cudaStream_t st) {
+                  int64_t num_frames, float* z, cudaStream_t st, bool blocked = false) {
   const int fb = untile_frames(num_frames);
   dim3 grid((unsigned)std::min<int64_t>((num_candidates + 255) / 256, 64),
             (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
   const int64_t ldt = (int64_t)num_tiles * GT;
-  if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
-  else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
-  else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z);
+  const int64_t bt = blocked ? num_tiles : 0;
+  if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
+  else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
+  else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
   SRPGPU_CHECK_LAUNCH("interp_map_gather(untile)");
   return SRPGPU_OK;
 }
@@ -1121,45 +1170,47 @@ static int pair_clusters(int num_ctas, cudaStream_t st) {
   return std::min(clusters, num_ctas / 2);
 }
 
-// operand maps of the pair kernel: slabs [2][num_slabs * 128][64] (64-byte swizzle, one
-// stage of GK lags per box) and the lag-major sample planes viewed as {GA frames, lags,
-// frame blocks} (one 3D box per (plane, group): the CTA's frame blocks of GG lag rows)
+// operand maps of the pair kernel, hi and lo planes in one box each: the slabs
+// [2][num_slabs * 128][64] as {lags, rows, planes} (64-byte swizzle, one stage of GK lags of the
+// CTA's 128 rows per box) and the lag-major sample planes [2][round8(S)][planes_ld] as {GA
+// frames, lags, frame blocks, planes} (one box per gathered group: the CTA's frame blocks of
+// GG lag rows, both planes)
 template <class TR>
 static int pair_maps(CUtensorMapDataType dt, const void* samples_planes, int32_t num_cols, int64_t planes_ld,
-                     const void* slab_planes, int64_t num_slabs, CUtensorMap* ma_hi, CUtensorMap* ma_lo,
-                     CUtensorMap* mb_hi, CUtensorMap* mb_lo, const char* what) {
+                     const void* slab_planes, int64_t num_slabs, CUtensorMap* ma, CUtensorMap* mb, const char* what) {
   const int64_t arows = num_slabs * GM;
   const int64_t c8 = (int64_t)((num_cols + 7) / 8 * 8);   // planes hold round8(S) rows each
-  const auto* slabs = reinterpret_cast<const unsigned char*>(slab_planes);
-  const auto* xs = reinterpret_cast<const unsigned char*>(samples_planes);
   int s;
-  if ((s = make_map_2d(ma_hi, dt, TR::ES, slabs, arows, GB, GB, TR::GK, GM, what, CU_TENSOR_MAP_SWIZZLE_64B)) ||
-      (s = make_map_2d(ma_lo, dt, TR::ES, slabs + arows * GB * TR::ES, arows, GB, GB, TR::GK, GM, what,
-                       CU_TENSOR_MAP_SWIZZLE_64B)))
-    return s;
+  {
+    const int64_t dims[3] = {GB, arows, 2};
+    const int box[3] = {TR::GK, GM, 2};
+    if ((s = make_map_3d(ma, dt, slab_planes, dims, (int64_t)GB * TR::ES, arows * GB * TR::ES, box, what,
+                         CU_TENSOR_MAP_SWIZZLE_64B)))
+      return s;
+  }
   const CUtensorMapSwizzle swz = TR::ES == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-  const int64_t dims[3] = {TR::GA, num_cols, planes_ld / TR::GA};
-  const int box[3] = {TR::GA, TR::GG, g32::PNC / TR::GA};
-  if ((s = make_map_3d(mb_hi, dt, xs, dims, planes_ld * TR::ES, TR::GA * TR::ES, box, what, swz)) ||
-      (s = make_map_3d(mb_lo, dt, xs + c8 * planes_ld * TR::ES, dims, planes_ld * TR::ES, TR::GA * TR::ES, box, what, swz)))
-    return s;
-  return SRPGPU_OK;
+  const int64_t dims[4] = {TR::GA, num_cols, planes_ld / TR::GA, 2};
+  const int64_t strides[3] = {planes_ld * TR::ES, (int64_t)TR::GA * TR::ES, c8 * planes_ld * TR::ES};
+  const int box[4] = {TR::GA, TR::GG, g32::PNC / TR::GA, 2};
+  return make_map_4d(mb, dt, samples_planes, dims, strides, box, what, swz);
 }
 
 template <class TR>
-static int launch_pair(int clusters, const CUtensorMap& ma_hi, const CUtensorMap& ma_lo, const CUtensorMap& mb_hi,
-                       const CUtensorMap& mb_lo, float zscale, int64_t num_frames, int64_t num_candidates,
+static int launch_pair(int clusters, const CUtensorMap& ma, const CUtensorMap& mb, float zscale, int64_t num_frames, int64_t num_candidates,
                        int32_t num_tiles, const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nst,
                        const int32_t* tile_rows, float* z_tiles, float* z, uint64_t* keys, cudaStream_t st,
                        const char* what) {
   const GatherTuning& tn = tuning();
-  // tile-order map through TMA stores: box of 128 candidates x 32 frames
-  CUtensorMap mz = ma_hi;
+  // tile-order map through TMA stores in blocks of 32 frames ([frame block][tile][32 frames][256
+  // rows]): box of 32 candidates x 32 frames (an epilogue warp's 128-byte-swizzled staging tile)
+  CUtensorMap mz = ma;
   int z_tma = 0, s;
   if (z && z_tiles && !tn.zstg) {
-    const int64_t ldt = (int64_t)num_tiles * GT;
-    if ((s = make_map_2d(&mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, z_tiles, num_frames, ldt, ldt, GM, 32, what,
-                         CU_TENSOR_MAP_SWIZZLE_NONE)))
+    const int64_t dims[4] = {GT, ZB, num_tiles, (num_frames + ZB - 1) / ZB};
+    const int64_t strides[3] = {(int64_t)GT * 4, (int64_t)GT * ZB * 4, (int64_t)GT * ZB * 4 * num_tiles};
+    const int box[4] = {32, 32, 1, 1};
+    if ((s = make_map_4d(&mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z_tiles, dims, strides, box, what,
+                         CU_TENSOR_MAP_SWIZZLE_128B)))
       return s;
     z_tma = 1;
   }
@@ -1168,7 +1219,7 @@ static int launch_pair(int clusters, const CUtensorMap& ma_hi, const CUtensorMap
   const int64_t n_groups = (num_frames + tn.frames_per_group - 1) / tn.frames_per_group;
   SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "%s: too many units", what);
   g32::gather_pair_kernel<TR><<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem<TR>) + 1024, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, mz, z_tma && tn.zt_ld < 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
+      ma, mb, mz, z_tma && tn.zt_ld < 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
       (int)(n_groups * units_per_group), num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nst,
       tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH(what);
@@ -1206,11 +1257,11 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   // or no 2-CTA cluster fits; persistent grid = the co-resident clusters
   int clusters = 0;
   if (tn.pair && !getenv("SRPGPU_GATHER_2D") &&
-      pair_maps<g32::PairTf32>(f32, samples_planes, num_cols, planes_ld, slab_planes, num_slabs, &ma_hi, &ma_lo,
-                               &mb_hi, &mb_lo, "interp_map_gather_tf32") == SRPGPU_OK)
+      pair_maps<g32::PairTf32>(f32, samples_planes, num_cols, planes_ld, slab_planes, num_slabs, &ma_hi, &mb_hi,
+                               "interp_map_gather_tf32") == SRPGPU_OK)
     clusters = pair_clusters<g32::PairTf32>(num_ctas, st);
   if (clusters > 0) {
-    if ((s = launch_pair<g32::PairTf32>(clusters, ma_hi, ma_lo, mb_hi, mb_lo, 1.0f, num_frames, num_candidates,
+    if ((s = launch_pair<g32::PairTf32>(clusters, ma_hi, mb_hi, 1.0f, num_frames, num_candidates,
                                         num_tiles, group_col, tile_slab, tile_nkb, tile_rows, z_tiles, z, keys, st,
                                         "interp_map_gather_tf32")))
       return s;
@@ -1259,7 +1310,7 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   // one launch over every group; the untile pass follows (measured: running group g's untile
   // on a side stream under group g + 1's gather launch was slower, 50 vs 42 ms at cfg4 --
   // the two contend for the SMs' issue slots and L2)
-  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
+  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st, clusters > 0))) return s;
   return SRPGPU_OK;
 }
 
@@ -1289,19 +1340,19 @@ extern "C" int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t 
   int s = reset_keys(keys, num_frames, st);
   if (s) return s;
   if (num_frames == 0 || num_tiles == 0 || num_ctas == 0) return SRPGPU_OK;
-  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  CUtensorMap ma, mb;
   if ((s = pair_maps<g32::PairF16>(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, samples_planes, num_cols, planes_ld, slab_planes,
-                                   num_slabs, &ma_hi, &ma_lo, &mb_hi, &mb_lo, "interp_map_gather_f16")))
+                                   num_slabs, &ma, &mb, "interp_map_gather_f16")))
     return s;
   const int clusters = pair_clusters<g32::PairF16>(num_ctas, st);
   if (clusters == 0) {
     set_error("interp_map_gather_f16: no 2-CTA cluster of the pair kernel fits this device");
     return SRPGPU_ERR_LAUNCH;
   }
-  if ((s = launch_pair<g32::PairF16>(clusters, ma_hi, ma_lo, mb_hi, mb_lo, z_scale, num_frames, num_candidates,
+  if ((s = launch_pair<g32::PairF16>(clusters, ma, mb, z_scale, num_frames, num_candidates,
                                      num_tiles, group_col, tile_slab, tile_nst, tile_rows, z_tiles, z, keys, st,
                                      "interp_map_gather_f16")))
     return s;
-  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st))) return s;
+  if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st, true))) return s;
   return SRPGPU_OK;
 }

@@ -83,9 +83,12 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-// arrive on an mbarrier anywhere in the cluster (release at cluster scope)
+// arrive on an mbarrier anywhere in the cluster.  Default semantics (release at CTA scope): the
+// arrivals here hand back TMEM buffers, which tcgen05.wait::ld + fence::before_thread_sync
+// already order; a cluster-scope release compiles to MEMBAR.ALL.GPU and holds the arrival (and
+// with it the next accumulation chunk) until the thread's earlier map stores have landed.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // TMA loads of one CTA of a pair whose completion is counted on the leader CTA's mbarrier
@@ -105,6 +108,15 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
       "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
       : "memory");
 }
 
@@ -139,6 +151,12 @@ __device__ __forceinline__ void st_global_hint(float* p, float v, uint64_t polic
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy) : "memory");
 }
 
+__device__ __forceinline__ void st_global_v4_hint(float* p, float a, float b, float c, float d, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d),
+               "l"(policy)
+               : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -156,6 +174,13 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
 
@@ -284,6 +309,31 @@ inline int make_map_3d(CUtensorMap* map, CUtensorMapDataType dtype, const void* 
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("%s: cuTensorMapEncodeTiled (3D) failed (%d)", what, (int)r);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  return SRPGPU_OK;
+}
+
+// 4D tensor map: dims[0] contiguous (elements), dims[1..3] with byte strides (any order)
+inline int make_map_4d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, const int64_t (&dims)[4],
+                       const int64_t (&strides)[3], const int (&box)[4], const char* what,
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("%s: cuTensorMapEncodeTiled unavailable", what);
+    return SRPGPU_ERR_LAUNCH;
+  }
+  cuuint64_t d[4], st[3];
+  cuuint32_t b[4], estr[4] = {1, 1, 1, 1};
+  for (int i = 0; i < 4; ++i) {
+    d[i] = (cuuint64_t)dims[i];
+    b[i] = (cuuint32_t)box[i];
+  }
+  for (int i = 0; i < 3; ++i) st[i] = (cuuint64_t)strides[i];
+  CUresult r = enc(map, dtype, 4, const_cast<void*>(base), d, st, b, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("%s: cuTensorMapEncodeTiled (4D) failed (%d)", what, (int)r);
     return SRPGPU_ERR_LAUNCH;
   }
   return SRPGPU_OK;

@@ -411,7 +411,8 @@ TILE_GRID_ORDER = False
 def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
     planes, f, batched = sample_planes(samples, op.num_cols, natural=offsets, fmt=op.fmt)
     z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device) if out_map else None
-    zt = (torch.empty((f, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
+    # tile-order scratch: whole 256-frame units (the pair kernels store it unit by unit)
+    zt = (torch.empty(((f + 255) // 256 * 256, op.num_tiles * tiles.TILE), dtype=torch.float32, device=planes.device)
           if out_map and not (TILE_GRID_ORDER or op.grid_order) else None)
     keys = _new_keys(f, argmax)
     head = (dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
