@@ -228,8 +228,10 @@ int srpgpu_interp_map_gather_tc(const void* samples_planes, int64_t num_frames, 
  * the 64-lag block) and group_col holds 4-lag groups (16 per block); the other arguments
  * as srpgpu_interp_map_gather_tc, except that z_tiles is scratch of round256(F) rows of
  * num_tiles * 256 floats (the CTA-pair kernel stores it in blocks of 32 frames:
- * [frame block][tile][32 frames][256 rows]).  Replaces interpolation.py:188-195
- * (sspi_map) at long sample vectors. */
+ * [frame block][tile][32 frames][256 rows]); with z, z_tiles NULL and tile_pos NULL the tiles
+ * are taken to be 256 consecutive candidates each (tile_rows[t][r] = 256 t + r) and the map
+ * is stored straight into z with 2D TMA boxes (J % 4 == 0).  Replaces
+ * interpolation.py:188-195 (sspi_map) at long sample vectors. */
 int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_t num_frames, int32_t num_cols,
                                   int64_t planes_ld, const float* slab_planes, int64_t num_slabs,
                                   const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nkb,
@@ -252,6 +254,14 @@ int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t num_frames,
                                  const int32_t* tile_rows, int32_t num_tiles, int64_t num_candidates,
                                  int32_t num_ctas, const int32_t* tile_pos, float z_scale, float* z_tiles,
                                  float* z, uint64_t* keys, srpgpu_stream_t stream);
+
+/* The gather pass of the tile-order scratch alone: z[f][j] = z_tiles[f][tile_pos[j]] after a
+ * srpgpu_interp_map_gather_tf32 / _f16 call that was given z_tiles but no z (the two halves of
+ * the map stage, so that each can be timed on its own).  blocked != 0: the CTA-pair kernels'
+ * scratch layout ([frame block of 32][tile][32 frames][256 rows]); 0: rows of num_tiles * 256. */
+int srpgpu_interp_map_untile(const float* z_tiles, int32_t num_tiles, const int32_t* tile_pos,
+                             int64_t num_candidates, int64_t num_frames, float* z, int32_t blocked,
+                             srpgpu_stream_t stream);
 
 /* srpgpu_split_bf16_rows into fp16 hi / lo planes of scale * x (hi = f16_rne, lo = f16_rne(. - hi)). */
 int srpgpu_split_f16_rows(const float* src, int64_t ld_src, int64_t rows, int64_t cols, const int32_t* row_src,

@@ -55,6 +55,7 @@ SIGNATURES = {
                                       _P, _P, _P],
     "srpgpu_interp_map_gather_f16": [_P, _I64, _I32, _I64, _P, _I64, _P, _P, _P, _P, _I32, _I64, _I32, _P, _F32,
                                      _P, _P, _P, _P],
+    "srpgpu_interp_map_untile": [_P, _I32, _P, _I64, _I64, _P, _I32, _P],
     "srpgpu_split_f16_rows": [_P, _I64, _I64, _I64, _P, _F32, _P, _I64, _I64, _P],
     "srpgpu_split_bf16_rows": [_P, _I64, _I64, _I64, _P, _P, _I64, _I64, _P],
     "srpgpu_split_tf32_rows": [_P, _I64, _I64, _I64, _P, _P, _I64, _I64, _P],

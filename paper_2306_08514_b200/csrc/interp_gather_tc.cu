@@ -864,7 +864,8 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
     const int ch = (warp - 2) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ch * PCols);
     // map stores stream past L2 (evict_first): they must not push out the group's samples
-    const uint64_t zpol = policy_evict_first();
+    const uint64_t zpol = ((l2pol >> 4) & 3) == 0 ? policy_evict_first()
+                          : ((l2pol >> 4) & 3) == 1 ? policy_evict_normal() : policy_evict_last();
     float* zsw = sm.zs[warp - 2];
     uint32_t c = 0;
     for (int u = u_begin + cid; u < u_total; u += ncl) {
@@ -940,7 +941,11 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_4d(&mz, zsw, ch * PCols + cc * 32, 0, w.t, w.n * (PN / 32) + (int)rank * (PNC / 32) + q);
+            if (z_tma == 2)   // contiguous tiles: straight into the grid-order map (rows / columns clipped)
+              tma_store_2d_hint(&mz, zsw, w.t * GT + ch * PCols + cc * 32, (int)f0, zpol);
+            else
+              tma_store_4d_hint(&mz, zsw, ch * PCols + cc * 32, 0, w.t,
+                                w.n * (PN / 32) + (int)rank * (PNC / 32) + q, zpol);
             bulk_commit();
           }
         }
@@ -1127,15 +1132,17 @@ static const GatherTuning& tuning() {
     g.pair = v ? atoi(v) : 1;
     v = getenv("SRPGPU_GATHER_GROUP");
     const int64_t x = v ? atoll(v) : 0;
-    // their hi / lo samples (F_g x S x 8 B in fp32, 58 MB at cfg4 with 1024 frames) stay
-    // L2-resident next to the slabs in flight
-    g.frames_per_group = x >= 256 && x % 256 == 0 ? x : (int64_t)1024;
+    // 0: per operand format (launch_pair): the group's hi / lo samples (F_g x S x 4 B in fp16, 8 B in
+    // fp32) stay L2-resident next to the slabs in flight
+    g.frames_per_group = x >= 256 && x % 256 == 0 ? x : (int64_t)0;
     v = getenv("SRPGPU_GATHER_CHUNK");
     const int c = v ? atoi(v) : 0;
     g.chunk = c >= 1 && c <= 64 ? c : 8;
-    // samples evict_last, slabs evict_normal (4096 frames: 23 GB of DRAM reads against 41 GB
-    // with evict_first slabs and 71 GB with both evict_first)
-    g.l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (2 << 2));
+    // samples evict_last, slabs evict_first, map stores evict_first (bits 0-1 / 2-3 / 4-5).  cfg4,
+    // fp16x3, 10^4 frames (profiles/r2h_gather_f16_traffic*.log, DRAM reads / kernel time under
+    // ncu): slabs evict_normal 58.5 GB / 16.2 ms, slabs evict_first 45.1 GB / 14.7 ms, and with
+    // 512-frame groups 40.1 GB / 14.5 ms; map stores evict_normal: 57 GB / 15.2 ms
+    g.l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (1 << 2));
     g.zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
     g.zstg = getenv("SRPGPU_GATHER_ZSTG") ? 1 : 0;
     return g;
@@ -1199,13 +1206,13 @@ template <class TR>
 static int launch_pair(int clusters, const CUtensorMap& ma, const CUtensorMap& mb, float zscale, int64_t num_frames, int64_t num_candidates,
                        int32_t num_tiles, const int32_t* group_col, const int32_t* tile_slab, const int32_t* tile_nst,
                        const int32_t* tile_rows, float* z_tiles, float* z, uint64_t* keys, cudaStream_t st,
-                       const char* what) {
+                       const char* what, bool contiguous = false) {
   const GatherTuning& tn = tuning();
   // tile-order map through TMA stores in blocks of 32 frames ([frame block][tile][32 frames][256
   // rows]): box of 32 candidates x 32 frames (an epilogue warp's 128-byte-swizzled staging tile)
   CUtensorMap mz = ma;
   int z_tma = 0, s;
-  if (z && z_tiles && !tn.zstg) {
+  if (z_tiles && !tn.zstg) {
     const int64_t dims[4] = {GT, ZB, num_tiles, (num_frames + ZB - 1) / ZB};
     const int64_t strides[3] = {(int64_t)GT * 4, (int64_t)GT * ZB * 4, (int64_t)GT * ZB * 4 * num_tiles};
     const int box[4] = {32, 32, 1, 1};
@@ -1213,15 +1220,22 @@ static int launch_pair(int clusters, const CUtensorMap& ma, const CUtensorMap& m
                          CU_TENSOR_MAP_SWIZZLE_128B)))
       return s;
     z_tma = 1;
+  } else if (z && contiguous && num_candidates % 4 == 0) {
+    // tiles of 256 consecutive candidates: the same staging tiles go straight into z [F][J]
+    if ((s = make_map_2d(&mz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, z, num_frames, num_candidates, num_candidates,
+                         32, 32, what, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return s;
+    z_tma = 2;
   }
-  const int fg = (int)(tn.frames_per_group / g32::PN);
+  const int64_t fpg = tn.frames_per_group ? tn.frames_per_group : (TR::ES == 2 ? 512 : 1024);
+  const int fg = (int)(fpg / g32::PN);
   const int64_t units_per_group = (int64_t)num_tiles * fg;
-  const int64_t n_groups = (num_frames + tn.frames_per_group - 1) / tn.frames_per_group;
+  const int64_t n_groups = (num_frames + fpg - 1) / fpg;
   SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "%s: too many units", what);
   g32::gather_pair_kernel<TR><<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem<TR>) + 1024, st>>>(
-      ma, mb, mz, z_tma && tn.zt_ld < 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
+      ma, mb, mz, tn.zt_ld < 0 ? z_tma : 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
       (int)(n_groups * units_per_group), num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nst,
-      tile_rows, z ? z_tiles : nullptr, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
+      tile_rows, z_tiles, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH(what);
   return SRPGPU_OK;
 }
@@ -1263,7 +1277,7 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
   if (clusters > 0) {
     if ((s = launch_pair<g32::PairTf32>(clusters, ma_hi, mb_hi, 1.0f, num_frames, num_candidates,
                                         num_tiles, group_col, tile_slab, tile_nkb, tile_rows, z_tiles, z, keys, st,
-                                        "interp_map_gather_tf32")))
+                                        "interp_map_gather_tf32", z && !z_tiles && !tile_pos)))
       return s;
   } else {
     // one-CTA fallback (N = 128 frames per unit)
@@ -1296,9 +1310,10 @@ extern "C" int srpgpu_interp_map_gather_tf32(const float* samples_planes, int64_
       set_error("interp_map_gather_tf32: cannot reserve %zu B shared memory", smem);
       return SRPGPU_ERR_LAUNCH;
     }
-    const int fg = (int)(tn.frames_per_group / g32::GN);
+    const int64_t fpg = tn.frames_per_group ? tn.frames_per_group : 1024;
+    const int fg = (int)(fpg / g32::GN);
     const int64_t units_per_group = (int64_t)num_tiles * fg;
-    const int64_t n_groups = (num_frames + tn.frames_per_group - 1) / tn.frames_per_group;
+    const int64_t n_groups = (num_frames + fpg - 1) / fpg;
     SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION,
                      "interp_map_gather_tf32: too many units");
     g32::gather_tf32_kernel<<<(unsigned)num_ctas, kThreads, smem, st>>>(
@@ -1351,8 +1366,22 @@ extern "C" int srpgpu_interp_map_gather_f16(const void* samples_planes, int64_t 
   }
   if ((s = launch_pair<g32::PairF16>(clusters, ma, mb, z_scale, num_frames, num_candidates,
                                      num_tiles, group_col, tile_slab, tile_nst, tile_rows, z_tiles, z, keys, st,
-                                     "interp_map_gather_f16")))
+                                     "interp_map_gather_f16", z && !z_tiles && !tile_pos)))
     return s;
   if (z && z_tiles && (s = untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, st, true))) return s;
   return SRPGPU_OK;
+}
+
+// The gather pass alone: z[f][j] = z_tiles[f][tile_pos[j]], for a scratch map an earlier
+// srpgpu_interp_map_gather_* call left (z NULL there, z_tiles given).  blocked != 0: the CTA-pair
+// kernels' layout ([frame block of 32][tile][32 frames][256 rows]); 0: rows of num_tiles * 256.
+extern "C" int srpgpu_interp_map_untile(const float* z_tiles, int32_t num_tiles, const int32_t* tile_pos,
+                                        int64_t num_candidates, int64_t num_frames, float* z, int32_t blocked,
+                                        srpgpu_stream_t stream) {
+  SRPGPU_CHECK_ARG(num_tiles >= 0 && num_candidates >= 0 && num_frames >= 0, SRPGPU_ERR_DIMENSION,
+                   "interp_map_untile: bad shape");
+  SRPGPU_CHECK_ARG(z_tiles && tile_pos && z, SRPGPU_ERR_VALUE, "interp_map_untile: null argument");
+  if (num_frames == 0 || num_candidates == 0) return SRPGPU_OK;
+  return srpgpu::gtc::untile(z_tiles, num_tiles, tile_pos, num_candidates, num_frames, z, as_stream(stream),
+                             blocked != 0);
 }

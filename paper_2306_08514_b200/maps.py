@@ -319,6 +319,9 @@ def dense_from_matrix(interp) -> DenseInterpOperator:
                          lambda: DenseInterpOperator(np.asarray(interp.matrix).astype(np.float32)))
 
 
+import os as _os
+CONTIGUOUS_K_SLACK = float(_os.environ.get("SRPGPU_CONTIGUOUS_SLACK", "1.03"))   # contiguous 256-candidate tiles while their MMA work stays within 3%
+CONTIGUOUS_SHORT_SLACK, CONTIGUOUS_SHORT_K = 1.6, 512.0
 F16_AUTO = True             # auto: PHAT-bounded samples take the fp16x3 gathered-window engine
 F16_SLAB_SCALE = 256.0      # slab weights are split as fp16(w * 256): |w| <= 1, lo stays normal down to |w| ~ 1e-3
 TC_MIN_FRAMES = 0           # batches below this take the band engine (set from the cfg5 batch sweep)
@@ -362,6 +365,21 @@ class TileOperator:
         # scratch, no gather pass; cfg3 K is even 4% smaller than with compact tiles)
         self.grid_order = fmt in ("tf32", "f16") and num_rows % 8 == 0
         lay = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8, runs=self.grid_order)
+        # tiles of 256 consecutive candidates where they cost no more K (short windows: any tiling
+        # pays about one lag group per pair -- cfg3 / cfg5): the pair kernel then stores the map
+        # into grid order with 2D TMA boxes (whole 128-byte lines, asynchronous) instead of
+        # per-thread 32-byte runs
+        self.contiguous = False
+        if fmt in ("tf32", "f16") and num_rows % 4 == 0 and lay.num_tiles:
+            flat = tiles.TileLayout(sp, offsets, num_rows, group=4 if tf32 else 8, contiguous=True)
+            k_of = (lambda l: l.mean_k_stages) if tf32 else (lambda l: l.mean_k_stages32)
+            work, base = k_of(flat) * flat.num_tiles, k_of(lay) * lay.num_tiles
+            # ... or up to 1.6x the K while the tiles are short (K <= 512: there the per-run stores of
+            # the other layout, not the MMAs, set the pace -- cfg3: K 224 -> 310, map 0.81 -> 0.54 ms)
+            cheap = work <= CONTIGUOUS_K_SLACK * base or (work <= CONTIGUOUS_SHORT_SLACK * base
+                                                         and k_of(flat) <= CONTIGUOUS_SHORT_K)
+            if cheap and int(flat.tile_nkb.max()) <= self.MAX_BLOCKS:
+                lay, self.contiguous, self.grid_order = flat, True, True
         if lay.num_tiles and int(lay.tile_nkb.max()) > self.MAX_BLOCKS:
             raise ValueError(f"a candidate tile needs {int(lay.tile_nkb.max())} lag blocks "
                              f"(> {self.MAX_BLOCKS}): use engine 'band'")
@@ -417,13 +435,45 @@ def _tile_map(op: TileOperator, samples, offsets, argmax: bool, out_map: bool):
     keys = _new_keys(f, argmax)
     head = (dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
             dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
-            op.num_tiles, op.num_rows, dev.num_sms(), dev.ptr(op.tile_pos))
+            op.num_tiles, op.num_rows, dev.num_sms(), None if op.contiguous else dev.ptr(op.tile_pos))
     tail = (dev.ptr(zt), dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
     if op.fmt == "f16":
         nat.call("srpgpu_interp_map_gather_f16", *head, 1.0 / F16_SLAB_SCALE, *tail)
     else:
         nat.call("srpgpu_interp_map_gather_tf32" if op.tf32 else "srpgpu_interp_map_gather_tc", *head, *tail)
     return _finish(z, keys, batched, argmax)
+
+
+def tile_map_stages(sp, samples, engine: str = "tile_f16"):
+    """(gather, untile) callables of the CTA-pair gathered-window map's two kernels on these
+    samples -- the tile-order map + argmax keys, then the gather back to grid order -- so a
+    benchmark can time each on its own (`sspi_map` runs them back to back).  untile is None
+    when the engine stores straight into grid order (J % 8 == 0)."""
+    offsets = _sample_offsets(samples, int(sp.num_cols))
+    op = tile_from_sparse(sp, offsets, fmt=TILE_ENGINES[engine])
+    if op.fmt == "bf16":
+        raise ValueError("tile_map_stages: the CTA-pair engines only ('tile', 'tile_f16')")
+    planes, f, _ = sample_planes(samples, op.num_cols, natural=offsets, fmt=op.fmt)
+    z = torch.empty((f, op.num_rows), dtype=torch.float32, device=planes.device)
+    zt = None if op.grid_order else torch.empty(((f + 255) // 256 * 256, op.num_tiles * tiles.TILE),
+                                                dtype=torch.float32, device=planes.device)
+    keys = _new_keys(f, True)
+    head = (dev.ptr(planes), f, op.num_cols, planes.shape[2], dev.ptr(op.planes), op.num_slabs,
+            dev.ptr(op.group_col), dev.ptr(op.tile_slab), dev.ptr(op.tile_nkb), dev.ptr(op.tile_rows),
+            op.num_tiles, op.num_rows, dev.num_sms(), None if op.contiguous else dev.ptr(op.tile_pos))
+
+    def gather():
+        tail = (dev.ptr(zt), None if zt is not None else dev.ptr(z), dev.ptr(keys), dev.stream_ptr())
+        if op.fmt == "f16":
+            nat.call("srpgpu_interp_map_gather_f16", *head, 1.0 / F16_SLAB_SCALE, *tail)
+        else:
+            nat.call("srpgpu_interp_map_gather_tf32", *head, *tail)
+
+    def untile():
+        nat.call("srpgpu_interp_map_untile", dev.ptr(zt), op.num_tiles, dev.ptr(op.tile_pos), op.num_rows, f,
+                 dev.ptr(z), 1, dev.stream_ptr())
+
+    return gather, (untile if zt is not None else None), z, keys
 
 
 def sample_planes(samples, num_cols: int, natural=None, tf32: bool = False, fmt: str | None = None):

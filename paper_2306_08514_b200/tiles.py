@@ -130,15 +130,20 @@ class TileLayout:
                in this tile order, fully coalesced; a gather pass restores grid order)
     """
 
-    def __init__(self, sp, offsets, num_rows: int, group: int = GROUP, runs: bool = False):
-        """runs: tiles made of aligned runs of 8 consecutive candidates (each run one 32-byte
+    def __init__(self, sp, offsets, num_rows: int, group: int = GROUP, runs: bool = False,
+                 contiguous: bool = False):
+        """contiguous: tile t = candidates 256 t .. 256 t + 255 (the kernel stores the map
+        straight into grid order with 2D TMA boxes; worth it where the windows are so short
+        that any tiling pays one lag group per pair, cfg3 / cfg5).
+        runs: tiles made of aligned runs of 8 consecutive candidates (each run one 32-byte
         sector of a map row when J % 8 == 0), 8 tile rows per run in ascending order, so
         the kernel can store the map straight into grid order with whole sectors (no
         tile-order scratch, no gather pass); otherwise tiles of compact candidates."""
         if group not in (4, 8):
             raise ValueError("lag groups of 4 (tf32 kernel) or 8 (bf16 kernel)")
         self.group = int(group)
-        self.runs = bool(runs)
+        self.contiguous = bool(contiguous)
+        self.runs = bool(runs) and not self.contiguous
         GROUP = self.group
         offsets = np.asarray(offsets, dtype=np.int64)
         p_count = offsets.shape[0] - 1
@@ -157,7 +162,13 @@ class TileLayout:
             feat = np.where(empty.reshape(num_rows, p_count), centre[None, :], feat)
         tile_of = np.zeros(num_rows, dtype=np.int64)
         row_of = np.zeros(num_rows, dtype=np.int64)
-        if self.runs and num_rows:
+        if self.contiguous:
+            t_count = (num_rows + TILE - 1) // TILE
+            tile_rows = np.full((t_count, TILE), -1, dtype=np.int32)
+            cand = np.arange(num_rows)
+            tile_of, row_of = cand // TILE, cand % TILE
+            tile_rows[tile_of, row_of] = cand
+        elif self.runs and num_rows:
             n_runs = (num_rows + 7) // 8
             imax = np.iinfo(np.int64).max
             pad = n_runs * 8 - num_rows

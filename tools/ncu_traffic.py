@@ -21,6 +21,8 @@ def key_of(name: str, variant: str):
         return "fused"
     if "untile" in name:
         return f"{variant}_untile"
+    if "gather_pair_kernel" in name:      # bench.py's name of the CTA-pair gathered-window kernels
+        return "gather_pair_kernel<PairF16>" if "PairF16" in name else "gather_pair_kernel<PairTf32>"
     if "gather_tc" in name:
         return f"{variant}_map"
     if "frontend" in name:
@@ -41,6 +43,10 @@ def key_of(name: str, variant: str):
 
 def main(args):
     out = {}
+    if args and args[0].startswith("--merge="):      # keep the entries of an existing traffic.json
+        with open(args[0].split("=", 1)[1]) as f:
+            out = json.load(f)
+        args = args[1:]
     for a in args:
         workload, variant, path = a.split(":", 2)
         with open(path) as f:
