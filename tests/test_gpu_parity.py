@@ -353,6 +353,51 @@ def test_f16_planes_from_frontend(golden_scene):
     assert not s.maps._bounded(plain) and s.maps._bounded(xi)
 
 
+@pytest.mark.parametrize("engine", ["tile", "tile_f16"])
+def test_tile_map_stages_and_layouts(golden_scene, engine, monkeypatch):
+    """The CTA-pair map's two kernels called one after the other (tile-order map + keys, then
+    srpgpu_interp_map_untile) give sspi_map's result bit for bit; and the three tile layouts
+    (bisected tiles through the scratch, sector runs / 256 consecutive candidates straight
+    into grid order, where the grid size allows them) all match the oracle -- on a grid padded
+    to a multiple of 8 candidates too, so that every layout is exercised."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    tag = keep_tags(g)[0]
+    sp = sparse_from_golden(g, tag)
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, **s.maps.plane_args(engine))
+    z, idx = s.sspi_map(sp, xi, argmax=True, engine=engine)
+    op = s.maps.tile_from_sparse(sp, spec_offsets(spec), fmt=s.maps.TILE_ENGINES[engine])
+    gather, untile, z2, keys = s.maps.tile_map_stages(sp, xi, engine)
+    gather()
+    if untile is not None:
+        assert not op.grid_order
+        untile()
+    torch.cuda.synchronize()
+    assert torch.equal(z2, z)
+    assert torch.equal(s.maps.decode_keys(keys)[0], idx)
+    # the same operator on a grid padded with copies of its last rows to J % 8 == 0: bisected
+    # sector runs (slack 0) and contiguous tiles (any slack) store straight into grid order
+    j = int(np.asarray(sp.row_splits).shape[0] - 1)
+    pad = (-j) % 8 or 8
+    splits = np.asarray(sp.row_splits)
+    lo = int(splits[j - 1])
+    vals = np.concatenate([np.asarray(sp.values)] + [np.asarray(sp.values)[lo:]] * pad)
+    cols = np.concatenate([np.asarray(sp.col_indices)] + [np.asarray(sp.col_indices)[lo:]] * pad)
+    spl = np.concatenate([splits, splits[-1] + (np.arange(1, pad + 1) * (int(splits[j]) - lo))])
+    ref = O.sspi_map(vals, cols, spl, np_(xi.values).astype(np.float64))
+    for slack, contiguous in ((0.0, False), (1e9, True)):
+        monkeypatch.setattr(s.maps, "CONTIGUOUS_K_SLACK", slack)
+        monkeypatch.setattr(s.maps, "CONTIGUOUS_SHORT_SLACK", slack)
+        spp = s.SparseInterp(vals, cols, spl, int(sp.num_cols))
+        opp = s.maps.tile_from_sparse(spp, spec_offsets(spec), fmt=s.maps.TILE_ENGINES[engine])
+        assert opp.grid_order and opp.contiguous == contiguous
+        zp, ip = s.sspi_map(spp, xi, argmax=True, engine=engine)
+        assert_map_close(zp, ref)
+        assert_argmax_agrees(ip, ref)
+        assert O.normalized_max_error(np_(zp[:, :j]), np_(z).astype(np.float64)).max() < 5e-6
+
+
 def test_sspi_tile_and_row_kernels_agree(golden_scene):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)

@@ -271,12 +271,14 @@ def test_sell_layout_decodes_to_reference_csr(golden_scene):
         assert np.all(w >= np.pad(nnz, (0, (-j) % 32)).reshape(-1, 32).max(axis=1))
 
 
+@pytest.mark.parametrize("mode", ["compact", "runs", "contiguous"])
 @pytest.mark.parametrize("group", [4, 8])
-def test_tile_layout_holds_the_csr(golden_scene, group):
+def test_tile_layout_holds_the_csr(golden_scene, group, mode):
     """The gathered-window image (tiles.TileLayout, 4-lag groups for the 3xTF32 kernel, 8 for
-    bf16): every candidate sits in exactly one tile row, and decoding the slabs (tile row,
-    group_col + lag offset, natural -> storage column) gives exactly the CSR's nonzero
-    entries with float32 weights; the remaining slab entries are 0."""
+    fp16 / bf16; compact bisected tiles, tiles of aligned 8-candidate runs, tiles of 256
+    consecutive candidates): every candidate sits in exactly one tile row, and decoding the
+    slabs (tile row, group_col + lag offset, natural -> storage column) gives exactly the
+    CSR's nonzero entries with float32 weights; the remaining slab entries are 0."""
     from paper_2306_08514_b200 import tiles
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
@@ -285,7 +287,15 @@ def test_tile_layout_holds_the_csr(golden_scene, group):
     for tag in keep_tags(g):
         sp = sparse_from_golden(g, tag)
         j = int(np.asarray(sp.row_splits).shape[0] - 1)
-        lay = tiles.TileLayout(sp, off, j, group=group)
+        lay = tiles.TileLayout(sp, off, j, group=group, runs=(mode == "runs"), contiguous=(mode == "contiguous"))
+        if mode == "contiguous":
+            assert_array_equal(lay.tile_rows.ravel()[:j], np.arange(j))
+        if mode == "runs":       # whole aligned runs of 8 candidates, in ascending tile rows
+            first = lay.tile_rows[:, ::8]
+            assert np.all(first[first >= 0] % 8 == 0)
+        # the valid rows of a tile are a prefix (the kernel's epilogue counts on it)
+        valid = lay.tile_rows >= 0
+        assert np.all(valid[:, :-1] >= valid[:, 1:])
         rows_used = lay.tile_rows[lay.tile_rows >= 0]
         assert_array_equal(np.sort(rows_used), np.arange(j))
         assert_array_equal(lay.tile_pos[lay.tile_rows[lay.tile_rows >= 0]], np.flatnonzero(lay.tile_rows.ravel() >= 0))
