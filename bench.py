@@ -645,6 +645,26 @@ def run_ours(args):
         z, idx = pipe.z, pipe.index
         parity = spot_parity(wl, args.variant, op, z, idx, min(8, count))
 
+    # ---- the same chain as a localizer (N = 1 only): MapPipeline(out_map=False) keeps every map
+    # value on chip (accumulators -> fused argmax), so neither the map nor its tile-order scratch
+    # is written.  Reported beside the headline, which materialises the full map as the
+    # reference's evaluate_map does (cli.py:241-258 writes both the map and its peak).
+    locate_only = None
+    if world == 1 and args.variant in ("sspi", "si", "slri", "lr", "conv"):
+        try:
+            pl = MapPipeline("conv" if args.variant == "conv_h" else args.variant, op, wl.frame, wl.pairs, wl.spec,
+                             frames=count, engine=args.engine, precision=args.precision, out_map=False)
+            pl.input.copy_(x_dev)
+            ms_l, _ = timed(pl.replay, max(5, args.steps // 2), 3, False)
+            pl.run(x_dev)
+            same = bool(torch.equal(pl.index, pipe.index))
+            locate_only = {"value": total / (ms_l / 1e3), "unit": UNIT, "ms_per_step": ms_l,
+                           "argmax_equal_to_headline": same,
+                           "what": "fused argmax only: map values never leave the chip (out_map=False)"}
+            del pl
+        except Exception as exc:  # report, never hide
+            locate_only = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- other variants of the same workload (same rules; N = 1 only)
     variants = {}
     if not args.no_variants and world == 1:
@@ -701,7 +721,7 @@ def run_ours(args):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e_block,
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "gpu_launches_per_step": launches_per_step,
-            "clocks": clocks.summary(), "parity": parity, "variants": variants,
+            "clocks": clocks.summary(), "parity": parity, "locate_only": locate_only, "variants": variants,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

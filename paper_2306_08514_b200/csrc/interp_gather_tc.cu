@@ -362,6 +362,22 @@ __device__ __forceinline__ bool decode32(int u, int T, int fg, int n_tiles, Unit
   return out.n < n_tiles;
 }
 
+// Unit order of the pair kernel with tile chunks (tc > 0): chunk of tc tiles, frame group, tile
+// of the chunk, frame tile of the group -- a chunk's slabs stay in L2 (evict_last) while every
+// frame group streams past them, so each slab comes from DRAM once per launch instead of once
+// per group.  tc == 0: group, tile, frame tile (decode32).
+__device__ __forceinline__ bool decode_pair(int u, int T, int fg, int n_tiles, int tc, Unit& out) {
+  if (tc <= 0) return decode32(u, T, fg, n_tiles, out);
+  const int ng = (n_tiles + fg - 1) / fg;
+  const int per_g = tc * fg, per_c = ng * per_g;
+  const int c = u / per_c, r = u - c * per_c;
+  const int g = r / per_g, r2 = r - g * per_g;
+  const int tl = r2 / fg;
+  out.t = c * tc + tl;
+  out.n = g * fg + (r2 - tl * fg);
+  return out.t < T && out.n < n_tiles;
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -698,7 +714,7 @@ template <class TR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PThreads, 1)
 gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
                    const __grid_constant__ CUtensorMap mz, int z_tma, int l2pol, int64_t zt_ld, float zscale,
-                   int fg, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
+                   int fg, int tc, int CH, int u_begin, int u_end, int64_t F, int64_t J, int32_t T, const int32_t* __restrict__ group_col,
                    const int32_t* __restrict__ tile_blk, const int32_t* __restrict__ tile_nst,
                    const int32_t* __restrict__ tile_rows, float* __restrict__ zt, float* __restrict__ zg,
                    unsigned long long* __restrict__ keys) {
@@ -711,7 +727,7 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
   const uint32_t rank = cluster_ctarank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int n_tiles = (int)((F + PN - 1) / PN);
-  const int u_total = min(u_end, ((n_tiles + fg - 1) / fg) * T * fg);
+  const int u_total = min(u_end, ((n_tiles + fg - 1) / fg) * fg * (tc > 0 ? ((T + tc - 1) / tc) * tc : T));
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&ma);
@@ -749,7 +765,7 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
     auto pol = [](int c) { return c == 0 ? policy_evict_last() : c == 1 ? policy_evict_first() : policy_evict_normal(); };
     const uint64_t keep = pol(l2pol & 3), once = pol((l2pol >> 2) & 3);
     auto next_unit = [&](int u, Unit& w) {
-      while (u < u_total && !decode32(u, T, fg, n_tiles, w)) u += ncl;
+      while (u < u_total && !decode_pair(u, T, fg, n_tiles, tc, w)) u += ncl;
       return u;
     };
     auto stage_rows = [&](int buf, const Unit& w) {
@@ -816,7 +832,7 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
       uint32_t s = 0, ph = 0, c = 0;
       for (int u = u_begin + cid; u < u_total; u += ncl) {
         Unit w;
-        if (!decode32(u, T, fg, n_tiles, w)) continue;
+        if (!decode_pair(u, T, fg, n_tiles, tc, w)) continue;
         const int ns = __ldg(tile_nst + w.t);
         int kc = 0;                                              // stage within the accumulation chunk
         for (int kq = 0; kq < ns; ++kq) {
@@ -870,7 +886,7 @@ gather_pair_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant
     uint32_t c = 0;
     for (int u = u_begin + cid; u < u_total; u += ncl) {
       Unit w;
-      if (!decode32(u, T, fg, n_tiles, w)) continue;
+      if (!decode_pair(u, T, fg, n_tiles, tc, w)) continue;
       const int64_t f0 = (int64_t)w.n * PN + (int)rank * PNC + q * 32;   // the warp's first frame
       const int64_t f = f0 + lane;
       const int32_t* trow = tile_rows + (int64_t)w.t * GT + ch * PCols;
@@ -1036,7 +1052,7 @@ static int untile_frames(int64_t num_frames) {
   static const int forced = [] {
     const char* v = std::getenv("SRPGPU_UNTILE_FB");
     const int x = v ? std::atoi(v) : 0;
-    return (x == 1 || x == 2 || x == 4) ? x : 0;
+    return (x == 1 || x == 2 || x == 4 || x == 8) ? x : 0;
   }();
   if (forced) return forced;
   return num_frames >= 4096 ? 4 : 1;
@@ -1049,7 +1065,8 @@ static int untile(const float* z_tiles, int32_t num_tiles, const int32_t* tile_p
             (unsigned)std::min<int64_t>((num_frames + fb - 1) / fb, 65535));
   const int64_t ldt = (int64_t)num_tiles * GT;
   const int64_t bt = blocked ? num_tiles : 0;
-  if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
+  if (fb == 8) untile_kernel<8><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
+  else if (fb == 4) untile_kernel<4><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
   else if (fb == 2) untile_kernel<2><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
   else untile_kernel<1><<<grid, 256, 0, st>>>(z_tiles, ldt, tile_pos, num_candidates, num_frames, z, bt);
   SRPGPU_CHECK_LAUNCH("interp_map_gather(untile)");
@@ -1123,6 +1140,7 @@ struct GatherTuning {
   int l2pol;                  // L2 policies (SRPGPU_GATHER_L2)
   int64_t zt_ld;              // diagnostic: SRPGPU_GATHER_ZTEST=1 writes every frame's row to the same place
   int zstg;                   // SRPGPU_GATHER_ZSTG: tile-order map by register stores instead of TMA stores
+  int tchunk;                 // tiles per L2-resident slab chunk (SRPGPU_GATHER_TCHUNK; 0: frame-group-major units)
 };
 
 static const GatherTuning& tuning() {
@@ -1145,6 +1163,7 @@ static const GatherTuning& tuning() {
     g.l2pol = getenv("SRPGPU_GATHER_L2") ? atoi(getenv("SRPGPU_GATHER_L2")) : (0 | (1 << 2));
     g.zt_ld = getenv("SRPGPU_GATHER_ZTEST") ? 0 : -1;
     g.zstg = getenv("SRPGPU_GATHER_ZSTG") ? 1 : 0;
+    g.tchunk = getenv("SRPGPU_GATHER_TCHUNK") ? atoi(getenv("SRPGPU_GATHER_TCHUNK")) : 0;
     return g;
   }();
   return t;
@@ -1229,11 +1248,13 @@ static int launch_pair(int clusters, const CUtensorMap& ma, const CUtensorMap& m
   }
   const int64_t fpg = tn.frames_per_group ? tn.frames_per_group : (TR::ES == 2 ? 512 : 1024);
   const int fg = (int)(fpg / g32::PN);
-  const int64_t units_per_group = (int64_t)num_tiles * fg;
+  const int tc = tn.tchunk > 0 ? tn.tchunk : 0;
+  const int64_t tiles_padded = tc > 0 ? ((int64_t)num_tiles + tc - 1) / tc * tc : num_tiles;
+  const int64_t units_per_group = tiles_padded * fg;
   const int64_t n_groups = (num_frames + fpg - 1) / fpg;
   SRPGPU_CHECK_ARG(n_groups * units_per_group < (1ll << 31), SRPGPU_ERR_DIMENSION, "%s: too many units", what);
   g32::gather_pair_kernel<TR><<<(unsigned)(2 * clusters), g32::PThreads, sizeof(g32::PairSmem<TR>) + 1024, st>>>(
-      ma, mb, mz, tn.zt_ld < 0 ? z_tma : 0, tn.l2pol, tn.zt_ld, zscale, fg, tn.chunk, 0,
+      ma, mb, mz, tn.zt_ld < 0 ? z_tma : 0, tn.l2pol, tn.zt_ld, zscale, fg, tc, tn.chunk, 0,
       (int)(n_groups * units_per_group), num_frames, num_candidates, num_tiles, group_col, tile_slab, tile_nst,
       tile_rows, z_tiles, z && !z_tiles ? z : nullptr, reinterpret_cast<unsigned long long*>(keys));
   SRPGPU_CHECK_LAUNCH(what);
