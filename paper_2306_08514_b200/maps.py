@@ -574,9 +574,18 @@ def uses_tc(variant: str, op, engine: str = "auto", frames: int | None = None) -
     return eng == "tc" or eng in TILE_ENGINES
 
 
+F16_MAX_HALF_LEN = 16384    # PHAT samples are bounded by 2(K-1): far inside fp16's 65504 up to here
+
+
+def phat_bounded(weighting: str, half_len: int) -> bool:
+    """Whether samples with this weighting and frame half-length K fit fp16 operands."""
+    return weighting == "phat" and int(half_len) <= F16_MAX_HALF_LEN
+
+
 def _bounded(samples) -> bool:
     """Kernel-produced PHAT samples (|xi| <= 2(K-1)): safe as fp16 hi / lo operands."""
-    return bool(getattr(samples, "phat", False))
+    spec = getattr(samples, "spec", None)
+    return bool(getattr(samples, "phat", False)) and int(getattr(spec, "half_len", 0) or 0) <= F16_MAX_HALF_LEN
 
 
 def _num_frames(samples) -> int:

@@ -66,7 +66,7 @@ class MapPipeline:
             return fused(self.op, self.input, self.frame, self.pairs, self.spec, rng,
                                            self.weighting, self.floor, argmax=True, out_map=self.out_map)
         if v in ("sspi", "si", "slri"):
-            eng = maps.map_engine(v, self.op, self.engine, self.frames, bounded=(self.weighting == "phat"))
+            eng = maps.map_engine(v, self.op, self.engine, self.frames, bounded=maps.phat_bounded(self.weighting, self.frame.half_len))
             xi = sampling.frames_to_samples(self.input, self.frame, self.pairs, self.spec, rng,
                                             self.weighting, self.floor, **maps.plane_args(eng))
             if v == "slri":
