@@ -129,7 +129,7 @@ def main():
         fit_s = time.perf_counter() - t0
         pipe = pipe_for("sspi", sp, f_main)
         ms = graph_ms(pipe, 10)
-        eng = "fused" if pipe.uses_fused_chain() else maps.map_engine("sspi", sp, "auto", f_main)
+        eng = "fused" if pipe.uses_fused_chain() else maps.map_engine("sspi", sp, "auto", f_main, bounded=True)
         row = {"sweep": "nnz", "nnz_per_cand_pair": q, "kept": int(sp.values.shape[0]), "frames": f_main,
                "ms_per_batch": ms, "maps_per_s": f_main / (ms / 1e3), "engine": eng,
                "host_fit_s": fit_s, **errors("sspi", sp, pipe)}
@@ -151,12 +151,12 @@ def main():
         for fb in batches:
             if fb > wl.num_frames:
                 continue
-            for eng in ("tc", "tile", "band", "auto"):
+            for eng in ("tc", "tile", "tile_f16", "band", "auto"):
                 pipe = pipe_for("sspi", sp, fb, eng)
                 ms = graph_ms(pipe, 10 if fb >= 1024 else 30)
                 row = {"sweep": "batch", "frames": fb, "ms_per_batch": ms, "maps_per_s": fb / (ms / 1e3),
                        "z_write_GBps": fb * j * 4 / (ms / 1e3) / 1e9, "engine": eng,
-                       "auto_picks": maps.map_engine("sspi", sp, "auto", fb)}
+                       "auto_picks": maps.map_engine("sspi", sp, "auto", fb, bounded=True)}
                 print(json.dumps(row), flush=True)
                 del pipe
                 torch.cuda.empty_cache()
