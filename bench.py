@@ -704,6 +704,22 @@ def run_ours(args):
             except Exception as exc:  # report, never hide
                 variants[v] = {"error": f"{type(exc).__name__}: {exc}"}
 
+        # the headline's operator on the 3xTF32 kernel (the engine unbounded samples take): the same
+        # map with tf32 split operands, for a like-for-like view of the fp16x3 headline
+        if eng == "tile_f16" and args.variant in ("sspi", "si"):
+            try:
+                pv = MapPipeline(args.variant, op, wl.frame, wl.pairs, wl.spec, frames=count, engine="tile")
+                pv.input.copy_(x_dev)
+                ms_v, _ = timed(pv.replay, max(5, args.steps // 2), 3, False)
+                pv.run(x_dev)
+                variants[f"{args.variant}_tf32x3"] = {
+                    "value": total / (ms_v / 1e3), "unit": UNIT, "ms_per_step": ms_v, "dtype": "tf32x3",
+                    "gpu_launches_per_step": pipe_launches(pv),
+                    "parity": spot_parity(wl, args.variant, op, pv.z, pv.index, min(8, count))}
+                del pv
+            except Exception as exc:  # report, never hide
+                variants[f"{args.variant}_tf32x3"] = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, args.variant, op, args.cpu_seconds)
