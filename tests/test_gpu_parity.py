@@ -398,6 +398,21 @@ def test_tile_map_stages_and_layouts(golden_scene, engine, monkeypatch):
         assert O.normalized_max_error(np_(zp[:, :j]), np_(z).astype(np.float64)).max() < 5e-6
 
 
+@pytest.mark.parametrize("engine", ["tile", "tile_f16"])
+def test_localizer_mode_keeps_the_argmax(golden_scene, engine):
+    """out_map=False (no map, no tile-order scratch, no untile pass: the bench's locate_only
+    line) returns the same per-frame argmax as the map-writing call, bit for bit."""
+    _, g = golden_scene
+    array, pairs, grid, frame, tdoa, spec = scene_objects(g)
+    sp = sparse_from_golden(g, keep_tags(g)[0])
+    x = torch.from_numpy(g["samples"].astype(np.float32)).cuda()
+    xi = s.frames_to_samples(x, frame, pairs, spec, **s.maps.plane_args(engine))
+    z, idx = s.sspi_map(sp, xi, argmax=True, engine=engine)
+    none, idx2 = s.sspi_map(sp, xi, argmax=True, out_map=False, engine=engine)
+    assert none is None and torch.equal(idx, idx2)
+    assert torch.equal(idx, torch.argmax(z, dim=1))          # the kernel's first-maximum rule
+
+
 def test_sspi_tile_and_row_kernels_agree(golden_scene):
     _, g = golden_scene
     array, pairs, grid, frame, tdoa, spec = scene_objects(g)
