@@ -20,6 +20,8 @@ tensor-core GEMM.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -319,8 +321,8 @@ def dense_from_matrix(interp) -> DenseInterpOperator:
                          lambda: DenseInterpOperator(np.asarray(interp.matrix).astype(np.float32)))
 
 
-import os as _os
-CONTIGUOUS_K_SLACK = float(_os.environ.get("SRPGPU_CONTIGUOUS_SLACK", "1.03"))   # contiguous 256-candidate tiles while their MMA work stays within 3%
+# contiguous 256-candidate tiles while their MMA work stays within 3% (SRPGPU_CONTIGUOUS_SLACK overrides)
+CONTIGUOUS_K_SLACK = float(os.environ.get("SRPGPU_CONTIGUOUS_SLACK", "1.03"))
 CONTIGUOUS_SHORT_SLACK, CONTIGUOUS_SHORT_K = 1.6, 512.0
 F16_AUTO = True             # auto: PHAT-bounded samples take the fp16x3 gathered-window engine
 F16_SLAB_SCALE = 256.0      # slab weights are split as fp16(w * 256): |w| <= 1, lo stays normal down to |w| ~ 1e-3
