@@ -379,23 +379,27 @@ def test_tile_map_stages_and_layouts(golden_scene, engine, monkeypatch):
     # the same operator on a grid padded with copies of its last rows to J % 8 == 0: bisected
     # sector runs (slack 0) and contiguous tiles (any slack) store straight into grid order
     j = int(np.asarray(sp.row_splits).shape[0] - 1)
-    pad = (-j) % 8 or 8
     splits = np.asarray(sp.row_splits)
     lo = int(splits[j - 1])
-    vals = np.concatenate([np.asarray(sp.values)] + [np.asarray(sp.values)[lo:]] * pad)
-    cols = np.concatenate([np.asarray(sp.col_indices)] + [np.asarray(sp.col_indices)[lo:]] * pad)
-    spl = np.concatenate([splits, splits[-1] + (np.arange(1, pad + 1) * (int(splits[j]) - lo))])
-    ref = O.sspi_map(vals, cols, spl, np_(xi.values).astype(np.float64))
-    for slack, contiguous in ((0.0, False), (1e9, True)):
-        monkeypatch.setattr(s.maps, "CONTIGUOUS_K_SLACK", slack)
-        monkeypatch.setattr(s.maps, "CONTIGUOUS_SHORT_SLACK", slack)
-        spp = s.SparseInterp(vals, cols, spl, int(sp.num_cols))
-        opp = s.maps.tile_from_sparse(spp, spec_offsets(spec), fmt=s.maps.TILE_ENGINES[engine])
-        assert opp.grid_order and opp.contiguous == contiguous
-        zp, ip = s.sspi_map(spp, xi, argmax=True, engine=engine)
-        assert_map_close(zp, ref)
-        assert_argmax_agrees(ip, ref)
-        assert O.normalized_max_error(np_(zp[:, :j]), np_(z).astype(np.float64)).max() < 5e-6
+    for mod in (8, 4):       # J % 8 == 0: runs or contiguous; J % 8 == 4: scratch or contiguous
+        pad = (-j) % 8 or 8
+        if mod == 4:
+            pad += 4
+        vals = np.concatenate([np.asarray(sp.values)] + [np.asarray(sp.values)[lo:]] * pad)
+        cols = np.concatenate([np.asarray(sp.col_indices)] + [np.asarray(sp.col_indices)[lo:]] * pad)
+        spl = np.concatenate([splits, splits[-1] + (np.arange(1, pad + 1) * (int(splits[j]) - lo))])
+        ref = O.sspi_map(vals, cols, spl, np_(xi.values).astype(np.float64))
+        for slack, contiguous in ((0.0, False), (1e9, True)):
+            monkeypatch.setattr(s.maps, "CONTIGUOUS_K_SLACK", slack)
+            monkeypatch.setattr(s.maps, "CONTIGUOUS_SHORT_SLACK", slack)
+            spp = s.SparseInterp(vals, cols, spl, int(sp.num_cols))
+            opp = s.maps.tile_from_sparse(spp, spec_offsets(spec), fmt=s.maps.TILE_ENGINES[engine])
+            assert opp.contiguous == contiguous and opp.grid_order == (contiguous or mod == 8)
+            zp, ip = s.sspi_map(spp, xi, argmax=True, engine=engine)
+            assert zp.shape[1] == j + pad
+            assert_map_close(zp, ref)
+            assert_argmax_agrees(ip, ref)
+            assert O.normalized_max_error(np_(zp[:, :j]), np_(z).astype(np.float64)).max() < 5e-6
 
 
 @pytest.mark.parametrize("engine", ["tile", "tile_f16"])
